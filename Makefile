@@ -1,0 +1,40 @@
+# Builds the B200 library (CUDA kernels + C ABI), the C++ drop-in host
+# library, the dfakit CLI and the test-only oracle.
+#   make            -> paper_2508_20735_b200/lib/libdfakit_b200.so, bin/dfakit, oracle/
+NVCC     ?= /usr/local/cuda/bin/nvcc
+CXX      ?= g++
+ARCH     := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude -Ipaper_2508_20735_b200/csrc \
+            --expt-relaxed-constexpr -Xptxas -v
+CXXFLAGS := -O2 -fPIC -std=c++20 -Iinclude -Wall -Wextra -Wno-unused-parameter
+PKG      := paper_2508_20735_b200
+CSRC     := $(PKG)/csrc
+BUILD    := build
+LIB      := $(PKG)/lib/libdfakit_b200.so
+CU_SRCS  := $(wildcard $(CSRC)/*.cu)
+CU_OBJS  := $(patsubst $(CSRC)/%.cu,$(BUILD)/%.o,$(CU_SRCS))
+HOST_SRCS:= $(wildcard $(CSRC)/host/*.cpp)
+HOST_OBJS:= $(patsubst $(CSRC)/host/%.cpp,$(BUILD)/host_%.o,$(HOST_SRCS))
+
+all: $(LIB) oracle
+
+$(BUILD)/%.o: $(CSRC)/%.cu $(wildcard $(CSRC)/*.cuh) include/dfakit_b200.h
+	@mkdir -p $(BUILD)
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(BUILD)/$*.ptxas.log || (cat $(BUILD)/$*.ptxas.log; false)
+
+$(BUILD)/host_%.o: $(CSRC)/host/%.cpp $(wildcard include/dfakit/*.hpp) include/dfakit_b200.h include/dfakit_b200.hpp
+	@mkdir -p $(BUILD)
+	$(CXX) $(CXXFLAGS) -c $< -o $@
+
+$(LIB): $(CU_OBJS) $(HOST_OBJS)
+	@mkdir -p $(PKG)/lib
+	$(NVCC) $(ARCH) -shared -o $@ $^ -Xcompiler -fPIC -lcudart_static -lpthread -ldl -lrt
+
+oracle:
+	$(MAKE) -s -C oracle
+
+clean:
+	rm -rf $(BUILD) $(PKG)/lib bin
+	$(MAKE) -s -C oracle clean
+
+.PHONY: all oracle clean

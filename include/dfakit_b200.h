@@ -1,0 +1,212 @@
+/*
+ * dfakit_b200.h -- C ABI of the B200-native DFA minimisation / equivalence
+ * library (libdfakit_b200.so).
+ *
+ * Plain pointers and sizes only.  Each entry point names the reference
+ * interface it replaces (/root/reference/proj/include/dfakit/...).  The C++
+ * drop-in API (include/dfakit/*.hpp, namespace dfakit) is a thin host layer
+ * over these calls; see INTEGRATION.md for the bindings.
+ *
+ * Memory conventions
+ *   - delta is letter-major: delta[a * n + q] = delta(q, a), exactly the
+ *     reference's `delta[a][q]` (dfa.hpp:22-24) laid out contiguously.
+ *   - accepting is one byte per state (0 / 1).
+ *   - `dfakit_*` calls take HOST buffers and copy them in and out;
+ *     `dfakit_*_device` calls take DEVICE pointers already resident in HBM and
+ *     run on the given CUDA stream (NULL = the context's stream).
+ *   - Block numbering of every returned partition is canonical: blocks are
+ *     numbered by first occurrence scanning states upwards (equivalently, by
+ *     the minimum state id of each block), the reference's
+ *     Partition::from_labels normal form (dfa.hpp:46-60).
+ *
+ * Errors: every call returns a dfakit_status; dfakit_last_error() returns a
+ * thread-local message for the last failure.  There is no CPU fallback: when
+ * no CUDA device is present calls return DFAKIT_E_NODEVICE.
+ */
+#ifndef DFAKIT_B200_H
+#define DFAKIT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DFAKIT_B200_ABI_VERSION 1
+#define DFAKIT_NO_STATE 0xffffffffu
+
+typedef enum {
+    DFAKIT_OK = 0,
+    DFAKIT_E_INVALID = -1,  /* std::invalid_argument in the reference          */
+    DFAKIT_E_RESOURCE = -2, /* dfakit::ResourceError (errors.hpp:21-24)         */
+    DFAKIT_E_CUDA = -3,     /* CUDA runtime failure                             */
+    DFAKIT_E_NODEVICE = -4  /* no CUDA device: the library refuses to run       */
+} dfakit_status;
+
+/* Same order as dfakit::Algorithm (minimize.hpp:9). */
+typedef enum {
+    DFAKIT_ALGO_MOORE = 0,
+    DFAKIT_ALGO_TRANS = 1,
+    DFAKIT_ALGO_NAIVE_PR = 2,
+    DFAKIT_ALGO_NAIVE_PR_FUSED = 3,
+    DFAKIT_ALGO_SORT_PR = 4,
+    DFAKIT_ALGO_TRANS_PR = 5
+} dfakit_algorithm;
+
+/* dfakit::ElectionPolicy (minimize.hpp:16-24). */
+typedef enum { DFAKIT_POLICY_MIN_INDEX = 0, DFAKIT_POLICY_ARBITRARY = 1 } dfakit_policy;
+
+/* dfakit::ExploreMode (equivalence.hpp:24). */
+typedef enum { DFAKIT_MODE_EQUIVALENCE = 0, DFAKIT_MODE_INCLUSION = 1, DFAKIT_MODE_FULL = 2 } dfakit_mode;
+
+/* dfakit::Verdict (equivalence.hpp:10). */
+typedef enum { DFAKIT_EQUIVALENT = 0, DFAKIT_INCLUDED = 1, DFAKIT_COUNTEREXAMPLE = 2 } dfakit_verdict;
+
+/* A DFA view (dfakit::Dfa, dfa.hpp:21-41) over caller-owned memory. */
+typedef struct {
+    uint32_t num_states;
+    uint32_t alphabet_size;
+    const uint32_t* delta;     /* alphabet_size * num_states, letter-major */
+    const uint8_t* accepting;  /* num_states                               */
+    int64_t initial;           /* -1 when absent                           */
+} dfakit_dfa;
+
+/* dfakit::RefinementReport (minimize.hpp:26-35) plus device statistics. */
+typedef struct {
+    uint32_t num_blocks;
+    uint32_t refining_iterations; /* passes that changed the partition       */
+    uint32_t closure_iterations;  /* trans / trans_pr only                   */
+    uint32_t algorithm;           /* dfakit_algorithm                        */
+    uint64_t passes;              /* passes executed incl. the confirming one */
+    uint64_t transitions_refined; /* n * k * passes (algorithmic work)       */
+    uint64_t states_sorted;       /* sum over passes of keys radix-sorted    */
+    uint32_t hash_collisions;     /* fingerprint collisions caught + re-run  */
+    uint32_t reserved;
+    double device_ms;             /* device time of the call (CUDA events)   */
+} dfakit_report;
+
+/* dfakit::ProductResult (equivalence.hpp:12-22). */
+typedef struct {
+    int32_t verdict;              /* dfakit_verdict */
+    uint32_t levels;
+    uint64_t explored_states;
+    uint32_t counterexample_len;  /* full length even when > capacity */
+    uint32_t reserved;
+    double device_ms;
+} dfakit_product;
+
+/* Options for the refinement calls. */
+typedef struct {
+    uint32_t policy;            /* dfakit_policy                                       */
+    uint32_t force_exact;       /* sort_pr: never use fingerprint keys (testing)       */
+    uint64_t seed;              /* ElectionPolicy::arbitrary seed                      */
+    uint64_t max_transitions;   /* trans_pr budget, minimize.hpp:41 (0 = default 2^28) */
+    uint64_t max_pair_nodes;    /* trans budget, minimize.hpp:38 (0 = default 2^16)    */
+    uint32_t fingerprint_bits;  /* sort_pr: 0 = 64; smaller values force collisions    */
+    uint32_t reserved;
+} dfakit_options;
+
+typedef struct dfakit_ctx dfakit_ctx;
+
+/* ---- context -------------------------------------------------------------- */
+int dfakit_abi_version(void);
+const char* dfakit_last_error(void);
+/* Number of CUDA devices visible (0 when none). */
+int dfakit_device_count(void);
+/* Creates a context bound to `device` with its own stream and memory pool. */
+dfakit_status dfakit_ctx_create(int device, dfakit_ctx** out);
+void dfakit_ctx_destroy(dfakit_ctx* ctx);
+/* The context's CUDA stream (cudaStream_t) as an opaque pointer. */
+void* dfakit_ctx_stream(dfakit_ctx* ctx);
+/* Number of kernels this context has launched so far. */
+uint64_t dfakit_ctx_kernel_launches(dfakit_ctx* ctx);
+/* Live kernel profiling: between begin and end every launch is bracketed by
+ * CUDA events on its stream.  end() writes per-kernel totals as JSON
+ * [{"name","launches","ms","bytes"}] where bytes are the algorithmic bytes
+ * annotated at the launch site ("roofline"). */
+dfakit_status dfakit_profile_begin(dfakit_ctx* ctx);
+dfakit_status dfakit_profile_end(dfakit_ctx* ctx, char* json, size_t cap);
+
+/* ---- minimisation: host buffers (minimize.hpp:46-85) ------------------------
+ * block_of: num_states entries, canonical numbering.  opts may be NULL.    */
+dfakit_status dfakit_minimize(dfakit_ctx* ctx, const dfakit_dfa* dfa, dfakit_algorithm algo,
+                              const dfakit_options* opts, uint32_t* block_of, dfakit_report* report);
+/* moore_minimize, minimize.hpp:46 (GPU signature refinement; same partition
+ * and pass count as Moore's sequential refinement). */
+dfakit_status dfakit_moore_minimize(dfakit_ctx* ctx, const dfakit_dfa* dfa, uint32_t* block_of,
+                                    dfakit_report* report);
+/* sort_pr, minimize.hpp:72 */
+dfakit_status dfakit_sort_pr(dfakit_ctx* ctx, const dfakit_dfa* dfa, uint32_t* block_of, dfakit_report* report);
+/* naive_pr, minimize.hpp:62 */
+dfakit_status dfakit_naive_pr(dfakit_ctx* ctx, const dfakit_dfa* dfa, uint32_t policy, uint64_t seed,
+                              uint32_t* block_of, dfakit_report* report);
+/* naive_pr_fused, minimize.hpp:66 */
+dfakit_status dfakit_naive_pr_fused(dfakit_ctx* ctx, const dfakit_dfa* dfa, uint32_t* block_of,
+                                    dfakit_report* report);
+/* trans_pr, minimize.hpp:82 */
+dfakit_status dfakit_trans_pr(dfakit_ctx* ctx, const dfakit_dfa* dfa, uint32_t policy, uint64_t seed,
+                              uint64_t max_transitions, uint32_t* block_of, dfakit_report* report);
+/* trans_minimize, minimize.hpp:55 (Cai-Haase pair-graph closure; small n).
+ * apart: optional num_states^2 bytes (row-major), may be NULL. */
+dfakit_status dfakit_trans_minimize(dfakit_ctx* ctx, const dfakit_dfa* dfa, uint64_t max_pair_nodes,
+                                    uint32_t* block_of, uint8_t* apart, dfakit_report* report);
+/* build_transitive_alphabet, minimize.hpp:77.  out_delta holds
+ * alphabet_size * (floor(log2 n) + 1) * n entries; *out_alphabet receives
+ * the new alphabet size.  Call with out_delta == NULL to query the size. */
+dfakit_status dfakit_build_transitive_alphabet(dfakit_ctx* ctx, const dfakit_dfa* dfa, uint64_t max_transitions,
+                                               uint32_t* out_delta, uint32_t* out_alphabet);
+
+/* ---- minimisation: device-resident ------------------------------------------
+ * dfa->delta / dfa->accepting and block_of are device pointers. */
+dfakit_status dfakit_minimize_device(dfakit_ctx* ctx, const dfakit_dfa* dfa, dfakit_algorithm algo,
+                                     const dfakit_options* opts, uint32_t* block_of, dfakit_report* report,
+                                     void* stream);
+
+/* ---- equivalence / inclusion (equivalence.hpp:37-50) -------------------------
+ * Naive Hopcroft-Karp: level-synchronous product BFS over a lock-free GPU
+ * hash set.  Records are ordered exactly like the reference's sequential
+ * insertion order, so verdict, explored_states, levels and the counterexample
+ * word are identical to the reference's.  letter_map maps letters of A to
+ * letters of B (NULL = positional).  counterexample receives up to
+ * counterexample_cap letter ids of A. */
+dfakit_status dfakit_explore_product(dfakit_ctx* ctx, const dfakit_dfa* a, const dfakit_dfa* b, dfakit_mode mode,
+                                     const uint32_t* letter_map, uint64_t max_visited, uint32_t* counterexample,
+                                     uint32_t counterexample_cap, dfakit_product* out);
+dfakit_status dfakit_check_equiv(dfakit_ctx* ctx, const dfakit_dfa* a, const dfakit_dfa* b, uint64_t max_visited,
+                                 uint32_t* counterexample, uint32_t counterexample_cap, dfakit_product* out);
+dfakit_status dfakit_check_inclusion(dfakit_ctx* ctx, const dfakit_dfa* a, const dfakit_dfa* b,
+                                     uint64_t max_visited, uint32_t* counterexample, uint32_t counterexample_cap,
+                                     dfakit_product* out);
+/* Device-resident product (a/b delta & accepting on the device). */
+dfakit_status dfakit_explore_product_device(dfakit_ctx* ctx, const dfakit_dfa* a, const dfakit_dfa* b,
+                                            dfakit_mode mode, const uint32_t* letter_map_host, uint64_t max_visited,
+                                            uint32_t* counterexample, uint32_t counterexample_cap,
+                                            dfakit_product* out, void* stream);
+/* Hopcroft-Karp with a GPU union-find (path-halving CAS) -- the paper's §6
+ * future work; equivalence only.  Verdict identical to check_equiv; the
+ * witness (when any) is a valid distinguishing word, explored_states counts
+ * the unions performed. */
+dfakit_status dfakit_check_equiv_uf(dfakit_ctx* ctx, const dfakit_dfa* a, const dfakit_dfa* b,
+                                    uint32_t* counterexample, uint32_t counterexample_cap, dfakit_product* out);
+dfakit_status dfakit_check_equiv_uf_device(dfakit_ctx* ctx, const dfakit_dfa* a, const dfakit_dfa* b,
+                                           uint32_t* counterexample, uint32_t counterexample_cap,
+                                           dfakit_product* out, void* stream);
+
+/* ---- device generators (bench inputs built in HBM) --------------------------- */
+/* Synthetic random DFA, same formula as oracle/oracle.c or_gen_synth. */
+dfakit_status dfakit_gen_synth_device(dfakit_ctx* ctx, uint32_t n, uint32_t k, uint64_t seed, uint32_t* delta,
+                                      uint8_t* accepting, void* stream);
+/* Unary chain q -> q+1 (last state loops and accepts). */
+dfakit_status dfakit_gen_chain_device(dfakit_ctx* ctx, uint32_t n, uint32_t* delta, uint8_t* accepting,
+                                      void* stream);
+/* Relabel states by a seeded bijection: out(perm(q)) = perm(in(q)).  Used to
+ * build a language-equal partner DFA for equivalence benchmarks. */
+dfakit_status dfakit_permute_states_device(dfakit_ctx* ctx, uint32_t n, uint32_t k, uint64_t seed,
+                                           const uint32_t* delta, const uint8_t* accepting, uint32_t* out_delta,
+                                           uint8_t* out_accepting, uint32_t* initial_out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DFAKIT_B200_H */

@@ -1,0 +1,106 @@
+// ctx.cu -- device context, error state and small readbacks.
+#include <cstring>
+
+#include "common.cuh"
+
+namespace dk {
+
+void note_launch(Ctx* ctx) {
+    if (ctx) ++ctx->launches;
+}
+
+void prof_begin_launch(Ctx* ctx, cudaStream_t s) {
+    if (!ctx || !ctx->profiling) return;
+    DK_CUDA(cudaEventCreate(&ctx->pending));
+    DK_CUDA(cudaEventRecord(ctx->pending, s));
+}
+
+void prof_end_launch(Ctx* ctx, cudaStream_t s, const char* name, double bytes) {
+    if (!ctx || !ctx->profiling || !ctx->pending) return;
+    cudaEvent_t b;
+    DK_CUDA(cudaEventCreate(&b));
+    DK_CUDA(cudaEventRecord(b, s));
+    ctx->prof.push_back(ProfRec{name, ctx->pending, b, bytes});
+    ctx->pending = nullptr;
+}
+
+// Per-kernel totals as a JSON array: [{"name", "launches", "ms", "bytes"}].
+std::string prof_collect(Ctx* ctx) {
+    struct Agg {
+        std::string name;
+        uint64_t launches = 0;
+        double ms = 0, bytes = 0;
+    };
+    std::vector<Agg> aggs;
+    for (auto& r : ctx->prof) {
+        DK_CUDA(cudaEventSynchronize(r.b));
+        float ms = 0;
+        DK_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+        Agg* g = nullptr;
+        for (auto& x : aggs)
+            if (x.name == r.name) g = &x;
+        if (!g) {
+            aggs.push_back(Agg{r.name});
+            g = &aggs.back();
+        }
+        ++g->launches;
+        g->ms += ms;
+        g->bytes += r.bytes;
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    ctx->prof.clear();
+    std::string out = "[";
+    char buf[512];
+    for (size_t i = 0; i < aggs.size(); ++i) {
+        snprintf(buf, sizeof buf, "%s{\"name\":\"%s\",\"launches\":%llu,\"ms\":%.6f,\"bytes\":%.0f}", i ? "," : "",
+                 aggs[i].name.c_str(), (unsigned long long)aggs[i].launches, aggs[i].ms, aggs[i].bytes);
+        out += buf;
+    }
+    return out + "]";
+}
+
+void read_words(Ctx* ctx, const void* dsrc, size_t bytes, void* hdst, cudaStream_t s) {
+    if (bytes > 64 * sizeof(uint64_t)) throw Error(DFAKIT_E_INVALID, "read_words: too large");
+    DK_CUDA(cudaMemcpyAsync(ctx->mailbox, dsrc, bytes, cudaMemcpyDeviceToHost, s));
+    DK_CUDA(cudaStreamSynchronize(s));
+    std::memcpy(hdst, ctx->mailbox, bytes);
+}
+
+Ctx* ctx_create(int device) {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+        cudaGetLastError();
+        throw Error(DFAKIT_E_NODEVICE, "no CUDA device available: the B200 library has no CPU fallback");
+    }
+    if (device < 0 || device >= count) throw Error(DFAKIT_E_INVALID, "device index out of range");
+    DK_CUDA(cudaSetDevice(device));
+    Ctx* c = new Ctx();
+    c->device = device;
+    DK_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+    DK_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    DK_CUDA(cudaMallocHost(reinterpret_cast<void**>(&c->mailbox), 64 * sizeof(uint64_t)));
+    DK_CUDA(cudaMalloc(reinterpret_cast<void**>(&c->dmailbox), 64 * sizeof(uint64_t)));
+    DK_CUDA(cudaEventCreate(&c->ev0));
+    DK_CUDA(cudaEventCreate(&c->ev1));
+    // keep freed pool memory around: repeated calls reuse it without cudaMalloc
+    cudaMemPool_t pool;
+    DK_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t threshold = ~0ull;
+    DK_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold));
+    return c;
+}
+
+void ctx_destroy(Ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->mailbox) cudaFreeHost(c->mailbox);
+    if (c->dmailbox) cudaFree(c->dmailbox);
+    if (c->ev0) cudaEventDestroy(c->ev0);
+    if (c->ev1) cudaEventDestroy(c->ev1);
+    if (c->stream && c->own_stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+}  // namespace dk

@@ -1,0 +1,347 @@
+// prims.cu -- scan, compaction and the LSD radix sort.
+//
+// Radix sort design (per 8-bit digit pass, reduce-then-scan):
+//   1. radix_hist:    each 256-thread CTA histograms a 4096-key tile in shared
+//                     memory; lanes holding the same digit are grouped with
+//                     __match_any_sync so one shared atomic is issued per
+//                     distinct digit per warp (warp-match histogram).  Counts
+//                     are written digit-major: counts[d * tiles + t].
+//   2. exclusive scan of the digit-major counts gives every (digit, tile) its
+//      global output offset.
+//   3. radix_scatter: the tile is re-read; each warp ranks its keys stably
+//      (match_any peers + popc of lower lanes + a per-warp running count),
+//      warp prefixes are combined per digit, keys are staged digit-sorted in
+//      shared memory and then written out with consecutive threads writing
+//      consecutive addresses of the same digit bucket (coalesced stores).
+#include "prims.cuh"
+
+namespace dk {
+
+// ---------------------------------------------------------------------------
+// block-level scan helpers (256 threads)
+// ---------------------------------------------------------------------------
+
+template <int THREADS>
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* total, uint32_t* warp_sums) {
+    constexpr int W = THREADS / 32;
+    const unsigned lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= (unsigned)o) x += y;
+    }
+    if (lane == 31) warp_sums[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        uint32_t s = lane < (unsigned)W ? warp_sums[lane] : 0u;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, s, o);
+            if (lane >= (unsigned)o) s += y;
+        }
+        if (lane < (unsigned)W) warp_sums[lane] = s;
+    }
+    __syncthreads();
+    uint32_t prefix = wid ? warp_sums[wid - 1] : 0u;
+    *total = warp_sums[W - 1];
+    __syncthreads();
+    return prefix + x - v;
+}
+
+// ---------------------------------------------------------------------------
+// exclusive scan
+// ---------------------------------------------------------------------------
+
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 8;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+__global__ void __launch_bounds__(kScanThreads) scan_reduce_kernel(const uint32_t* __restrict__ in, uint64_t n,
+                                                                   uint32_t* __restrict__ sums) {
+    __shared__ uint32_t ws[kScanThreads / 32];
+    const uint64_t base = (uint64_t)blockIdx.x * kScanTile;
+    uint32_t acc = 0;
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) {
+        uint64_t i = base + (uint64_t)j * kScanThreads + threadIdx.x;
+        if (i < n) acc += in[i];
+    }
+    uint32_t total;
+    block_exclusive_scan<kScanThreads>(acc, &total, ws);
+    if (threadIdx.x == 0) sums[blockIdx.x] = total;
+}
+
+__global__ void __launch_bounds__(kScanThreads) scan_tile_kernel(const uint32_t* __restrict__ in, uint64_t n,
+                                                                 uint32_t* __restrict__ out,
+                                                                 const uint32_t* __restrict__ tile_offsets,
+                                                                 uint32_t* __restrict__ total_dev) {
+    __shared__ uint32_t tile[kScanTile];
+    __shared__ uint32_t ws[kScanThreads / 32];
+    const uint64_t base = (uint64_t)blockIdx.x * kScanTile;
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) {
+        uint64_t i = base + (uint64_t)j * kScanThreads + threadIdx.x;
+        tile[j * kScanThreads + threadIdx.x] = i < n ? in[i] : 0u;
+    }
+    __syncthreads();
+    uint32_t local[kScanItems];
+    uint32_t acc = 0;
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) {
+        local[j] = tile[threadIdx.x * kScanItems + j];
+        acc += local[j];
+    }
+    uint32_t total;
+    uint32_t prefix = block_exclusive_scan<kScanThreads>(acc, &total, ws);
+    const uint32_t off = tile_offsets ? tile_offsets[blockIdx.x] : 0u;
+    prefix += off;
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) {
+        tile[threadIdx.x * kScanItems + j] = prefix;
+        prefix += local[j];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) {
+        uint64_t i = base + (uint64_t)j * kScanThreads + threadIdx.x;
+        if (i < n) out[i] = tile[j * kScanThreads + threadIdx.x];
+    }
+    if (total_dev && blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) *total_dev = off + total;
+}
+
+void exclusive_scan_u32(Ctx* ctx, const uint32_t* in, uint32_t* out, uint64_t n, uint32_t* total_dev,
+                        cudaStream_t s) {
+    if (n == 0) {
+        if (total_dev) DK_CUDA(cudaMemsetAsync(total_dev, 0, sizeof(uint32_t), s));
+        return;
+    }
+    const uint64_t tiles = (n + kScanTile - 1) / kScanTile;
+    if (tiles == 1) {
+        DK_LAUNCH(ctx, scan_tile_kernel, 1, kScanThreads, 0, s, in, n, out, nullptr, total_dev);
+        return;
+    }
+    DBuf<uint32_t> sums(tiles, s);
+    DK_LAUNCH(ctx, scan_reduce_kernel, (unsigned)tiles, kScanThreads, 0, s, in, n, sums.get());
+    exclusive_scan_u32(ctx, sums.get(), sums.get(), tiles, nullptr, s);
+    DK_LAUNCH(ctx, scan_tile_kernel, (unsigned)tiles, kScanThreads, 0, s, in, n, out, sums.get(), total_dev);
+}
+
+// ---------------------------------------------------------------------------
+// fill / iota / compaction
+// ---------------------------------------------------------------------------
+
+__global__ void fill_kernel(uint32_t* p, uint64_t n, uint32_t v) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        p[i] = v;
+}
+
+__global__ void iota_kernel(uint32_t* p, uint64_t n) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        p[i] = (uint32_t)i;
+}
+
+void fill_u32(Ctx* ctx, uint32_t* p, uint64_t n, uint32_t value, cudaStream_t s) {
+    if (n) DK_LAUNCH(ctx, fill_kernel, grid_for(n), kThreads, 0, s, p, n, value);
+}
+
+void iota_u32(Ctx* ctx, uint32_t* p, uint64_t n, cudaStream_t s) {
+    if (n) DK_LAUNCH(ctx, iota_kernel, grid_for(n), kThreads, 0, s, p, n);
+}
+
+__global__ void flag_to_u32_kernel(const uint8_t* __restrict__ f, uint64_t n, uint32_t* __restrict__ o) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        o[i] = f[i] ? 1u : 0u;
+}
+
+__global__ void compact_scatter_kernel(const uint32_t* __restrict__ in, const uint8_t* __restrict__ f, uint64_t n,
+                                       const uint32_t* __restrict__ pos, uint32_t* __restrict__ out) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        if (f[i]) out[pos[i]] = in[i];
+}
+
+uint32_t compact_u32(Ctx* ctx, const uint32_t* in, const uint8_t* flag, uint64_t n, uint32_t* out,
+                     uint32_t* scratch, cudaStream_t s) {
+    if (n == 0) return 0;
+    DK_LAUNCH(ctx, flag_to_u32_kernel, grid_for(n), kThreads, 0, s, flag, n, scratch);
+    exclusive_scan_u32(ctx, scratch, scratch, n, scratch + n, s);
+    DK_LAUNCH(ctx, compact_scatter_kernel, grid_for(n), kThreads, 0, s, in, flag, n, scratch, out);
+    uint32_t total = 0;
+    read_words(ctx, scratch + n, sizeof(uint32_t), &total, s);
+    return total;
+}
+
+// ---------------------------------------------------------------------------
+// canonical renumbering
+// ---------------------------------------------------------------------------
+
+__global__ void head_flags_kernel(const uint32_t* __restrict__ lab, uint64_t n, uint32_t* __restrict__ f) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        f[i] = lab[i] == (uint32_t)i ? 1u : 0u;
+}
+
+__global__ void relabel_kernel(const uint32_t* __restrict__ lab, uint64_t n, const uint32_t* __restrict__ dense,
+                               uint32_t* __restrict__ out) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = dense[lab[i]];
+}
+
+uint32_t canonical_from_min_labels(Ctx* ctx, const uint32_t* lab, uint64_t n, uint32_t* out, uint32_t* scratch,
+                                   cudaStream_t s) {
+    if (n == 0) return 0;
+    DK_LAUNCH(ctx, head_flags_kernel, grid_for(n), kThreads, 0, s, lab, n, scratch);
+    exclusive_scan_u32(ctx, scratch, scratch, n, scratch + n, s);
+    DK_LAUNCH(ctx, relabel_kernel, grid_for(n), kThreads, 0, s, lab, n, scratch, out);
+    uint32_t total = 0;
+    read_words(ctx, scratch + n, sizeof(uint32_t), &total, s);
+    return total;
+}
+
+// ---------------------------------------------------------------------------
+// radix sort
+// ---------------------------------------------------------------------------
+
+constexpr int kRadixBits = 8;
+constexpr int kRadix = 1 << kRadixBits;
+constexpr int kSortThreads = 256;
+constexpr int kSortWarps = kSortThreads / 32;
+constexpr int kSortItems = 16;
+constexpr int kSortTile = kSortThreads * kSortItems;  // 4096 keys
+constexpr int kWarpSpan = 32 * kSortItems;            // keys per warp segment
+
+__device__ __forceinline__ uint32_t digit_of(uint64_t key, uint32_t shift) {
+    return (uint32_t)(key >> shift) & (kRadix - 1);
+}
+
+__global__ void __launch_bounds__(kSortThreads) radix_hist_kernel(const uint64_t* __restrict__ keys, uint64_t m,
+                                                                  uint32_t shift, uint32_t tiles,
+                                                                  uint32_t* __restrict__ counts) {
+    __shared__ uint32_t hist[kRadix];
+    for (int d = threadIdx.x; d < kRadix; d += kSortThreads) hist[d] = 0;
+    __syncthreads();
+    const uint64_t base = (uint64_t)blockIdx.x * kSortTile;
+    const unsigned lane = threadIdx.x & 31u;
+#pragma unroll 4
+    for (int j = 0; j < kSortItems; ++j) {
+        uint64_t i = base + (uint64_t)j * kSortThreads + threadIdx.x;
+        bool valid = i < m;
+        unsigned vmask = __ballot_sync(0xffffffffu, valid);
+        if (valid) {
+            uint32_t d = digit_of(__ldcs(keys + i), shift);
+            unsigned peers = __match_any_sync(vmask, d);
+            if (lane == (unsigned)(__ffs(peers) - 1)) atomicAdd(&hist[d], (uint32_t)__popc(peers));
+        }
+    }
+    __syncthreads();
+    for (int d = threadIdx.x; d < kRadix; d += kSortThreads) counts[(uint64_t)d * tiles + blockIdx.x] = hist[d];
+}
+
+struct ScatterSmem {
+    uint64_t keys[kSortTile];
+    uint32_t vals[kSortTile];
+    uint32_t warp_hist[kSortWarps][kRadix];
+    uint32_t digit_start[kRadix];
+    uint32_t global_base[kRadix];
+    uint32_t ws[kSortWarps];
+};
+
+__global__ void __launch_bounds__(kSortThreads) radix_scatter_kernel(const uint64_t* __restrict__ keys_in,
+                                                                     const uint32_t* __restrict__ vals_in, uint64_t m,
+                                                                     uint32_t shift, uint32_t tiles,
+                                                                     const uint32_t* __restrict__ offsets,
+                                                                     uint64_t* __restrict__ keys_out,
+                                                                     uint32_t* __restrict__ vals_out) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    ScatterSmem& sm = *reinterpret_cast<ScatterSmem*>(smem_raw);
+    const unsigned lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < kSortWarps * kRadix; i += kSortThreads) (&sm.warp_hist[0][0])[i] = 0;
+    for (int d = threadIdx.x; d < kRadix; d += kSortThreads)
+        sm.global_base[d] = offsets[(uint64_t)d * tiles + blockIdx.x];
+    __syncthreads();
+
+    const uint64_t tile_base = (uint64_t)blockIdx.x * kSortTile;
+    const uint64_t seg = tile_base + (uint64_t)wid * kWarpSpan;
+    uint64_t key[kSortItems];
+    uint32_t val[kSortItems];
+    uint32_t rank[kSortItems];
+    const unsigned lt_mask = (1u << lane) - 1u;
+#pragma unroll
+    for (int j = 0; j < kSortItems; ++j) {
+        uint64_t i = seg + (uint64_t)j * 32 + lane;
+        bool valid = i < m;
+        key[j] = valid ? __ldcs(keys_in + i) : 0ull;
+        val[j] = valid ? __ldcs(vals_in + i) : 0u;
+        unsigned vmask = __ballot_sync(0xffffffffu, valid);
+        uint32_t d = digit_of(key[j], shift);
+        uint32_t r = 0;
+        unsigned peers = 0;
+        if (valid) {
+            peers = __match_any_sync(vmask, d);
+            r = sm.warp_hist[wid][d] + (uint32_t)__popc(peers & lt_mask);
+        }
+        __syncwarp();
+        if (valid && lane == (unsigned)(__ffs(peers) - 1)) sm.warp_hist[wid][d] += (uint32_t)__popc(peers);
+        __syncwarp();
+        rank[j] = valid ? r : kNone;
+    }
+    __syncthreads();
+    // per digit: exclusive prefix over warps, tile total, then scan over digits
+    uint32_t tile_count = 0;
+    {
+        const int d = threadIdx.x;  // kSortThreads == kRadix
+        uint32_t run = 0;
+#pragma unroll
+        for (int w = 0; w < kSortWarps; ++w) {
+            uint32_t c = sm.warp_hist[w][d];
+            sm.warp_hist[w][d] = run;
+            run += c;
+        }
+        uint32_t start = block_exclusive_scan<kSortThreads>(run, &tile_count, sm.ws);
+        sm.digit_start[d] = start;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kSortItems; ++j) {
+        if (rank[j] != kNone) {
+            uint32_t d = digit_of(key[j], shift);
+            uint32_t p = sm.digit_start[d] + sm.warp_hist[wid][d] + rank[j];
+            sm.keys[p] = key[j];
+            sm.vals[p] = val[j];
+        }
+    }
+    __syncthreads();
+    for (uint32_t p = threadIdx.x; p < tile_count; p += kSortThreads) {
+        uint64_t k = sm.keys[p];
+        uint32_t d = digit_of(k, shift);
+        uint64_t g = (uint64_t)sm.global_base[d] + (p - sm.digit_start[d]);
+        keys_out[g] = k;
+        vals_out[g] = sm.vals[p];
+    }
+}
+
+bool radix_sort_pairs(Ctx* ctx, RadixBuffers b, uint64_t m, uint32_t nbits, cudaStream_t s) {
+    static_assert(kSortThreads == kRadix, "one thread per digit in the tile scan");
+    DK_CUDA(cudaFuncSetAttribute(radix_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sizeof(ScatterSmem)));
+    if (m <= 1 || nbits == 0) return false;
+    if (m > 0xffffffffull) throw Error(DFAKIT_E_RESOURCE, "radix sort: more than 2^32 keys");
+    const uint32_t passes = (nbits + kRadixBits - 1) / kRadixBits;
+    const uint32_t tiles = (uint32_t)((m + kSortTile - 1) / kSortTile);
+    DBuf<uint32_t> counts((uint64_t)kRadix * tiles, s);
+    bool flipped = false;
+    for (uint32_t p = 0; p < passes; ++p) {
+        const uint32_t shift = p * kRadixBits;
+        const uint64_t* kin = flipped ? b.k1 : b.k0;
+        const uint32_t* vin = flipped ? b.v1 : b.v0;
+        uint64_t* kout = flipped ? b.k0 : b.k1;
+        uint32_t* vout = flipped ? b.v0 : b.v1;
+        DK_LAUNCH_B(ctx, 8.0 * m, radix_hist_kernel, tiles, kSortThreads, 0, s, kin, m, shift, tiles, counts.get());
+        exclusive_scan_u32(ctx, counts.get(), counts.get(), (uint64_t)kRadix * tiles, nullptr, s);
+        DK_LAUNCH_B(ctx, 24.0 * m, radix_scatter_kernel, tiles, kSortThreads, sizeof(ScatterSmem), s, kin, vin, m, shift, tiles,
+                  counts.get(), kout, vout);
+        flipped = !flipped;
+    }
+    return flipped;
+}
+
+}  // namespace dk

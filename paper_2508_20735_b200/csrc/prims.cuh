@@ -1,0 +1,42 @@
+// prims.cuh -- device-wide primitives used by every refinement path:
+// exclusive scan, stream compaction, and the LSD radix sort of
+// (64-bit key, 32-bit value) pairs with warp-match histograms.
+#pragma once
+
+#include "common.cuh"
+
+namespace dk {
+
+// out[i] = sum_{j<i} in[i]; optional *total_dev receives the full sum.
+// in and out may alias.  Works for any n (multi-level).
+void exclusive_scan_u32(Ctx* ctx, const uint32_t* in, uint32_t* out, uint64_t n, uint32_t* total_dev,
+                        cudaStream_t s);
+
+// Compacts in[i] where flag[i] != 0, preserving order.  Returns the count
+// (synchronises).  scratch must hold n+1 uint32.
+uint32_t compact_u32(Ctx* ctx, const uint32_t* in, const uint8_t* flag, uint64_t n, uint32_t* out,
+                     uint32_t* scratch, cudaStream_t s);
+
+// LSD radix sort on bits [0, nbits) of 64-bit keys with 32-bit values.
+// Stable.  Ping-pongs between (k0,v0) and (k1,v1); returns true when the
+// sorted data ended in (k1,v1).
+struct RadixBuffers {
+    uint64_t* k0;
+    uint32_t* v0;
+    uint64_t* k1;
+    uint32_t* v1;
+};
+bool radix_sort_pairs(Ctx* ctx, RadixBuffers b, uint64_t m, uint32_t nbits, cudaStream_t s);
+
+// Fills [0, n) with value.
+void fill_u32(Ctx* ctx, uint32_t* p, uint64_t n, uint32_t value, cudaStream_t s);
+void iota_u32(Ctx* ctx, uint32_t* p, uint64_t n, cudaStream_t s);
+
+// Canonical first-occurrence renumbering of min-state labels: every block's
+// label is its minimum member, so heads are states with lab[q] == q and the
+// dense id of a block is the number of heads before its label.
+// out may alias nothing; scratch holds n+1 uint32.  Returns the block count.
+uint32_t canonical_from_min_labels(Ctx* ctx, const uint32_t* lab, uint64_t n, uint32_t* out, uint32_t* scratch,
+                                   cudaStream_t s);
+
+}  // namespace dk

@@ -1,0 +1,69 @@
+// refine.cuh -- device entry points of the refinement and product engines.
+#pragma once
+
+#include "common.cuh"
+
+namespace dk {
+
+struct DevDfa {
+    uint32_t n = 0;
+    uint32_t k = 0;
+    const uint32_t* delta = nullptr;  // device, letter-major
+    const uint8_t* acc = nullptr;     // device
+    int64_t initial = -1;
+};
+
+struct RefineResult {
+    uint32_t num_blocks = 0;
+    uint32_t iters = 0;
+    uint32_t closure = 0;
+    uint64_t passes = 0;
+    uint64_t sorted = 0;
+    uint32_t collisions = 0;
+};
+
+struct SortOptions {
+    bool force_exact = false;
+    uint32_t fingerprint_bits = 64;
+};
+
+// All block_out arrays are device arrays of n entries, canonical numbering.
+RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uint32_t* block_out, cudaStream_t s);
+RefineResult naive_pr_device(Ctx* ctx, const DevDfa& d, int policy, uint64_t seed, uint32_t* block_out,
+                             cudaStream_t s);
+RefineResult naive_pr_fused_device(Ctx* ctx, const DevDfa& d, uint32_t* block_out, cudaStream_t s);
+uint32_t floor_log2_u32(uint32_t n);
+// out: k * (floor_log2(n)+1) * n entries (device)
+void transitive_alphabet_device(Ctx* ctx, const DevDfa& d, uint32_t* out, cudaStream_t s);
+RefineResult trans_pr_device(Ctx* ctx, const DevDfa& d, int policy, uint64_t seed, uint64_t max_transitions,
+                             uint32_t* block_out, cudaStream_t s);
+RefineResult trans_minimize_device(Ctx* ctx, const DevDfa& d, uint64_t max_pair_nodes, uint32_t* block_out,
+                                   uint8_t* apart_dev, cudaStream_t s);
+
+// Leader initialisation shared by naive/fused: min-index accepting and
+// rejecting leaders; returns false when F or Q\F is empty (one block).
+struct LeaderInfo {
+    uint32_t min_acc, min_rej, cnt_acc, cnt_rej;
+};
+LeaderInfo leader_info(Ctx* ctx, const DevDfa& d, cudaStream_t s);
+void init_leader_labels(Ctx* ctx, const DevDfa& d, const LeaderInfo& li, uint32_t* lab, cudaStream_t s);
+
+// product exploration
+struct ProductOut {
+    int32_t verdict = 0;
+    uint32_t levels = 0;
+    uint64_t explored = 0;
+    std::basic_string<uint32_t> word;
+};
+ProductOut explore_product_device(Ctx* ctx, const DevDfa& a, const DevDfa& b, int mode, const uint32_t* letter_map,
+                                  uint64_t max_visited, cudaStream_t s);
+ProductOut check_equiv_uf_device(Ctx* ctx, const DevDfa& a, const DevDfa& b, cudaStream_t s);
+
+// generators
+void gen_synth_device(Ctx* ctx, uint32_t n, uint32_t k, uint64_t seed, uint32_t* delta, uint8_t* acc,
+                      cudaStream_t s);
+void gen_chain_device(Ctx* ctx, uint32_t n, uint32_t* delta, uint8_t* acc, cudaStream_t s);
+uint32_t permute_states_device(Ctx* ctx, uint32_t n, uint32_t k, uint64_t seed, const uint32_t* delta,
+                               const uint8_t* acc, uint32_t* out_delta, uint8_t* out_acc, cudaStream_t s);
+
+}  // namespace dk

@@ -1,0 +1,194 @@
+"""GPU parity of the minimisers against the oracle and the reference's golden
+vectors.  Bar: bit-exact partitions (canonical numbering) and identical
+refining / closure pass counts.  For ElectionPolicy.arbitrary the winner
+sequence of the reference comes from its sequential mt19937_64 stream, so
+only the final partition is compared (winner independence, minimize.hpp:14)."""
+import random
+
+import numpy as np
+import pytest
+
+from conftest import digest, mkdfa
+
+pytestmark = pytest.mark.gpu
+
+ALGOS = {"moore": "moore_minimize", "sort": "sort_pr", "naive": "naive_pr", "naive-fused": "naive_pr_fused",
+         "transpr": "trans_pr"}
+
+
+def run(dk, algo, dfa, policy=None):
+    if algo == "naive":
+        return dk.naive_pr(dfa, policy or dk.ElectionPolicy.min_index())
+    if algo == "transpr":
+        return dk.trans_pr(dfa, policy or dk.ElectionPolicy.min_index())
+    if algo == "trans":
+        return dk.trans_minimize(dfa).report
+    return getattr(dk, ALGOS[algo])(dfa)
+
+
+def same(rep, want):
+    return (np.array_equal(rep.partition.block_of, want.blocks) and rep.partition.num_blocks == want.num_blocks
+            and rep.refining_iterations == want.refine_iters and rep.closure_iterations == want.closure_iters)
+
+
+def test_random_sweep_all_minimisers(dk, oracle):
+    """Acceptance criterion 1 shape: random DFAs n<=200, k<=4, every minimiser."""
+    g = random.Random(1000)
+    for i in range(250):
+        n, k, frac, s = g.randint(1, 200), g.randint(1, 4), g.randint(0, 10) / 10, g.getrandbits(64)
+        t = oracle.gen_random(n, k, frac, s)
+        dfa = mkdfa(dk, t)
+        for algo in ("moore", "sort", "naive", "naive-fused", "transpr") + (("trans",) if n <= 30 else ()):
+            want = oracle.minimize(algo, t[0], t[1])
+            got = run(dk, algo, dfa)
+            assert same(got, want), (i, algo, n, k, frac, s, got.refining_iterations, want.refine_iters)
+        moore = oracle.minimize("moore", t[0], t[1])
+        for seed in (1, 2, 3):
+            got = dk.naive_pr(dfa, dk.ElectionPolicy.arbitrary(seed))
+            assert np.array_equal(got.partition.block_of, moore.blocks)
+        got = dk.trans_pr(dfa, dk.ElectionPolicy.arbitrary(5))
+        assert np.array_equal(got.partition.block_of, moore.blocks)
+
+
+def test_golden_minimise_vectors(dk, oracle, golden):
+    for e in golden["minimize"]:
+        t = (oracle.gen_random(e["n"], e["k"], e["frac"], e["seed"]) if e["kind"] == "random"
+             else oracle.gen_family(e["family"], e["param"]))
+        dfa = mkdfa(dk, t)
+        n = t[0].shape[1]
+        for key, want in e["results"].items():
+            algo, _, pol = key.partition("@arbitrary")
+            if pol:
+                rep = run(dk, algo, dfa, dk.ElectionPolicy.arbitrary(int(pol)))
+            else:
+                rep = run(dk, algo, dfa)
+            blocks = [int(x) for x in rep.partition.block_of] if n <= 64 else digest(rep.partition.block_of)
+            assert blocks == want["blocks"], (e, key)
+            assert rep.partition.num_blocks == want["num_blocks"]
+            if not pol:
+                assert (rep.refining_iterations, rep.closure_iterations) == \
+                    (want["refine_iters"], want["closure_iters"]), (e, key)
+
+
+def test_bitsplitter_and_fibonacci_pass_counts(dk, oracle, golden):
+    """Acceptance criteria 2 and 3 (the reference's own observed values)."""
+    for n, want in golden["acceptance"]["bitsplit"].items():
+        dfa = mkdfa(dk, oracle.gen_family("bitsplit", int(n)))
+        for algo, iters in want.items():
+            rep = run(dk, algo, dfa)
+            assert rep.partition.num_blocks == 1 << int(n)
+            assert rep.refining_iterations == iters, (n, algo)
+    dfa = mkdfa(dk, oracle.gen_family("fib", 19))
+    for algo, iters in golden["acceptance"]["fib19"].items():
+        rep = run(dk, algo, dfa)
+        assert rep.partition.num_blocks == 6765 and rep.refining_iterations == iters, algo
+    rep = dk.naive_pr_fused(dfa)
+    assert rep.refining_iterations == golden["acceptance"]["fib19"]["naive"]
+
+
+def test_trans_minimize_matches_oracle(dk, oracle, golden):
+    for m, (nb, ri, ci) in golden["acceptance"]["trans_closure"].items():
+        res = dk.trans_minimize(mkdfa(dk, oracle.gen_family("fib", int(m))))
+        assert (res.report.partition.num_blocks, res.report.refining_iterations,
+                res.report.closure_iterations) == (nb, ri, ci)
+    g = random.Random(7)
+    for _ in range(20):
+        n, k, frac, s = g.randint(1, 25), g.randint(1, 3), g.randint(0, 10) / 10, g.getrandbits(64)
+        t = oracle.gen_random(n, k, frac, s)
+        res = dk.trans_minimize(mkdfa(dk, t))
+        assert np.array_equal(res.apart, oracle.trans_apart(t[0], t[1]).astype(bool))
+        assert same(res.report, oracle.minimize("trans", t[0], t[1]))
+
+
+def test_trans_minimize_budget_message(dk, oracle):
+    with pytest.raises(dk.ResourceError, match=r"7921.*MiB"):
+        dk.trans_minimize(mkdfa(dk, oracle.gen_family("fib", 10)), 1000)
+
+
+def test_transitive_alphabet(dk, oracle, golden):
+    for e in golden["transitive"]:
+        t = oracle.gen_random(e["n"], e["k"], e["frac"], e["seed"])
+        out = dk.build_transitive_alphabet(mkdfa(dk, t))
+        assert out.alphabet_size == e["k_out"] and digest(out.delta) == e["delta"]
+    chain = mkdfa(dk, oracle.gen_chain(10))
+    closed = dk.build_transitive_alphabet(chain)
+    assert closed.alphabet_size == 4 and closed.letter_names[3] == "a^8"
+    assert closed.delta[3][0] == 8 and closed.delta[3][1] == 9
+    with pytest.raises(dk.ResourceError):
+        dk.build_transitive_alphabet(mkdfa(dk, oracle.gen_family("fib", 10)), 100)
+    with pytest.raises(dk.ResourceError):
+        dk.trans_pr(mkdfa(dk, oracle.gen_family("fib", 10)), max_transitions=100)
+
+
+def test_edge_cases(dk):
+    one = dk.Dfa(np.zeros((1, 1), np.uint32), np.array([1], np.uint8), 0)
+    empty_alpha = dk.Dfa(np.zeros((0, 2), np.uint32), np.array([0, 1], np.uint8), None)
+    none_acc = dk.Dfa(np.array([[1, 2, 0]], np.uint32), np.zeros(3, np.uint8), 0)
+    all_acc = dk.Dfa(np.array([[1, 2, 0]], np.uint32), np.ones(3, np.uint8), 0)
+    cyc4 = dk.Dfa(np.array([[1, 2, 3, 0]], np.uint32), np.array([1, 1, 0, 0], np.uint8), None)
+    for f in (dk.moore_minimize, dk.sort_pr, dk.naive_pr, dk.naive_pr_fused, dk.trans_pr):
+        r = f(one)
+        assert r.partition.num_blocks == 1 and r.refining_iterations == 0
+        r = f(empty_alpha)
+        assert list(r.partition.block_of) == [0, 1] and r.refining_iterations == 0
+        for d in (none_acc, all_acc):
+            r = f(d)
+            assert r.partition.num_blocks == 1 and r.refining_iterations == 0
+    r = dk.sort_pr(cyc4)
+    assert r.partition.num_blocks == 4 and r.refining_iterations == 1
+    bad = dk.Dfa(np.array([[5, 1]], np.uint32), np.array([0, 1], np.uint8), None)
+    with pytest.raises(ValueError):
+        dk.sort_pr(bad)
+
+
+def test_sort_exact_paths_and_collision_recovery(dk, oracle):
+    """Packed, dense-packed, fingerprint, chunked-exact and forced-collision
+    paths all give the oracle's partition and pass count."""
+    g = random.Random(31)
+    for _ in range(12):
+        n, k, s = g.randint(500, 5000), g.randint(5, 12), g.getrandbits(64)
+        t = oracle.gen_random(n, k, 0.5, s)
+        want = oracle.minimize("moore", t[0], t[1])
+        dfa = mkdfa(dk, t)
+        for kw in ({}, {"force_exact": True}, {"fingerprint_bits": 6}):
+            rep = dk.sort_pr(dfa, **kw)
+            assert same(rep, want), kw
+        assert dk.sort_pr(dfa, fingerprint_bits=6).hash_collisions > 0
+
+
+@pytest.mark.slow
+def test_config0_random_1M_k2(dk, oracle):
+    """BASELINE configs[0]: random complete DFA, 1M states, |Sigma|=2."""
+    t = oracle.gen_random(1_000_000, 2, 0.5, 7)
+    want = oracle.minimize("moore", t[0], t[1])
+    rep = dk.sort_pr(mkdfa(dk, t))
+    assert same(rep, want)
+
+
+@pytest.mark.slow
+def test_config1_synth_10M_k10(dk, oracle):
+    """BASELINE configs[1] size: 10M states x 10 letters = 100M transitions."""
+    t = oracle.gen_synth(10_000_000, 10, 1)
+    want = oracle.minimize("moore", t[0], t[1])
+    dfa = mkdfa(dk, t)
+    rep = dk.sort_pr(dfa)
+    assert same(rep, want)
+    # the partition is a congruence: successors of block-mates are block-mates
+    blk = rep.partition.block_of
+    first = np.full(rep.partition.num_blocks, -1, np.int64)
+    order = np.arange(blk.size)
+    first[blk[::-1]] = order[::-1]
+    rep_of = first[blk]
+    for a in range(t[0].shape[0]):
+        assert np.array_equal(blk[t[0][a]], blk[t[0][a][rep_of]])
+
+
+@pytest.mark.slow
+def test_config2_chain_with_closure(dk, oracle):
+    """BASELINE configs[2]: chain DFA with partial transitive closure."""
+    for n in (1000, 100_000):
+        t = oracle.gen_chain(n)
+        want = oracle.minimize("transpr", t[0], t[1])
+        rep = dk.trans_pr(mkdfa(dk, t))
+        assert same(rep, want)
+        assert rep.partition.num_blocks == n
