@@ -16,7 +16,7 @@ CU_OBJS  := $(patsubst $(CSRC)/%.cu,$(BUILD)/%.o,$(CU_SRCS))
 HOST_SRCS:= $(wildcard $(CSRC)/host/*.cpp)
 HOST_OBJS:= $(patsubst $(CSRC)/host/%.cpp,$(BUILD)/host_%.o,$(HOST_SRCS))
 
-all: $(LIB) oracle
+all: $(LIB) bin/dfakit oracle
 
 $(BUILD)/%.o: $(CSRC)/%.cu $(wildcard $(CSRC)/*.cuh) include/dfakit_b200.h
 	@mkdir -p $(BUILD)
@@ -29,6 +29,10 @@ $(BUILD)/host_%.o: $(CSRC)/host/%.cpp $(wildcard include/dfakit/*.hpp) include/d
 $(LIB): $(CU_OBJS) $(HOST_OBJS)
 	@mkdir -p $(PKG)/lib
 	$(NVCC) $(ARCH) -shared -o $@ $^ -Xcompiler -fPIC -lcudart_static -lpthread -ldl -lrt
+
+bin/dfakit: $(CSRC)/cli/dfakit_cli.cpp $(LIB) include/dfakit_b200.hpp
+	@mkdir -p bin
+	$(CXX) $(CXXFLAGS) -o $@ $< -L$(PKG)/lib -ldfakit_b200 -Wl,-rpath,'$$ORIGIN/../$(PKG)/lib' -lpthread
 
 oracle:
 	$(MAKE) -s -C oracle

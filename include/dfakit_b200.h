@@ -4,8 +4,9 @@
  *
  * Plain pointers and sizes only.  Each entry point names the reference
  * interface it replaces (/root/reference/proj/include/dfakit/...).  The C++
- * drop-in API (include/dfakit/*.hpp, namespace dfakit) is a thin host layer
- * over these calls; see INTEGRATION.md for the bindings.
+ * drop-in API (include/dfakit_b200.hpp, reached through the reference header
+ * names under include/dfakit/, namespace dfakit) is a thin host layer over
+ * these calls; see INTEGRATION.md for the bindings.
  *
  * Memory conventions
  *   - delta is letter-major: delta[a * n + q] = delta(q, a), exactly the

@@ -186,6 +186,23 @@ __global__ void relabel_kernel(const uint32_t* __restrict__ lab, uint64_t n, con
         out[i] = dense[lab[i]];
 }
 
+__global__ void label_min_kernel(const uint32_t* __restrict__ lab, uint64_t n, uint32_t* __restrict__ minof) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        atomicMin(&minof[lab[i]], (uint32_t)i);
+}
+
+__global__ void to_min_label_kernel(uint32_t* __restrict__ lab, uint64_t n, const uint32_t* __restrict__ minof) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        lab[i] = minof[lab[i]];
+}
+
+void min_state_labels(Ctx* ctx, uint32_t* lab, uint64_t n, uint32_t* scratch, cudaStream_t s) {
+    if (n == 0) return;
+    fill_u32(ctx, scratch, n, kNone, s);
+    DK_LAUNCH(ctx, label_min_kernel, grid_for(n), kThreads, 0, s, lab, n, scratch);
+    DK_LAUNCH(ctx, to_min_label_kernel, grid_for(n), kThreads, 0, s, lab, n, scratch);
+}
+
 uint32_t canonical_from_min_labels(Ctx* ctx, const uint32_t* lab, uint64_t n, uint32_t* out, uint32_t* scratch,
                                    cudaStream_t s) {
     if (n == 0) return 0;

@@ -39,4 +39,8 @@ void iota_u32(Ctx* ctx, uint32_t* p, uint64_t n, cudaStream_t s);
 uint32_t canonical_from_min_labels(Ctx* ctx, const uint32_t* lab, uint64_t n, uint32_t* out, uint32_t* scratch,
                                    cudaStream_t s);
 
+// Rewrites arbitrary block labels (label values < n) in place so every
+// block is labelled by its minimum member.  scratch holds n uint32.
+void min_state_labels(Ctx* ctx, uint32_t* lab, uint64_t n, uint32_t* scratch, cudaStream_t s);
+
 }  // namespace dk

@@ -176,6 +176,8 @@ RefineResult naive_pr_device(Ctx* ctx, const DevDfa& d, int policy, uint64_t see
         ++res.iters;
         DK_LAUNCH(ctx, follow_kernel, grid_for(c), kThreads, 0, s, split.get(), c, lab.get(), slot.get(), pr);
     }
+    // min_index leaders are always block minima; arbitrary winners are not
+    if (policy != DFAKIT_POLICY_MIN_INDEX) min_state_labels(ctx, lab.get(), n, scratch.get(), s);
     res.num_blocks = canonical_from_min_labels(ctx, lab.get(), n, block_out, scratch.get(), s);
     return res;
 }
