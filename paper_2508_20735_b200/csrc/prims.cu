@@ -21,33 +21,6 @@ namespace dk {
 // block-level scan helpers (256 threads)
 // ---------------------------------------------------------------------------
 
-template <int THREADS>
-__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* total, uint32_t* warp_sums) {
-    constexpr int W = THREADS / 32;
-    const unsigned lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
-    uint32_t x = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= (unsigned)o) x += y;
-    }
-    if (lane == 31) warp_sums[wid] = x;
-    __syncthreads();
-    if (wid == 0) {
-        uint32_t s = lane < (unsigned)W ? warp_sums[lane] : 0u;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            uint32_t y = __shfl_up_sync(0xffffffffu, s, o);
-            if (lane >= (unsigned)o) s += y;
-        }
-        if (lane < (unsigned)W) warp_sums[lane] = s;
-    }
-    __syncthreads();
-    uint32_t prefix = wid ? warp_sums[wid - 1] : 0u;
-    *total = warp_sums[W - 1];
-    __syncthreads();
-    return prefix + x - v;
-}
 
 // ---------------------------------------------------------------------------
 // exclusive scan
@@ -157,7 +130,7 @@ __global__ void flag_to_u32_kernel(const uint8_t* __restrict__ f, uint64_t n, ui
 __global__ void compact_scatter_kernel(const uint32_t* __restrict__ in, const uint8_t* __restrict__ f, uint64_t n,
                                        const uint32_t* __restrict__ pos, uint32_t* __restrict__ out) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-        if (f[i]) out[pos[i]] = in[i];
+        if (f[i]) out[pos[i]] = in ? in[i] : (uint32_t)i;
 }
 
 uint32_t compact_u32(Ctx* ctx, const uint32_t* in, const uint8_t* flag, uint64_t n, uint32_t* out,
@@ -237,18 +210,16 @@ __global__ void __launch_bounds__(kSortThreads) radix_hist_kernel(const uint64_t
     for (int d = threadIdx.x; d < kRadix; d += kSortThreads) hist[d] = 0;
     __syncthreads();
     const uint64_t base = (uint64_t)blockIdx.x * kSortTile;
-    const unsigned lane = threadIdx.x & 31u;
-#pragma unroll 4
+    // issue every load of the tile before counting (16 independent loads in flight)
+    uint32_t dig[kSortItems];
+#pragma unroll
     for (int j = 0; j < kSortItems; ++j) {
-        uint64_t i = base + (uint64_t)j * kSortThreads + threadIdx.x;
-        bool valid = i < m;
-        unsigned vmask = __ballot_sync(0xffffffffu, valid);
-        if (valid) {
-            uint32_t d = digit_of(__ldcs(keys + i), shift);
-            unsigned peers = __match_any_sync(vmask, d);
-            if (lane == (unsigned)(__ffs(peers) - 1)) atomicAdd(&hist[d], (uint32_t)__popc(peers));
-        }
+        const uint64_t i = base + (uint64_t)j * kSortThreads + threadIdx.x;
+        dig[j] = i < m ? digit_of(__ldcs(keys + i), shift) : kNone;
     }
+#pragma unroll
+    for (int j = 0; j < kSortItems; ++j)
+        if (dig[j] != kNone) atomicAdd(&hist[dig[j]], 1u);
     __syncthreads();
     for (int d = threadIdx.x; d < kRadix; d += kSortThreads) counts[(uint64_t)d * tiles + blockIdx.x] = hist[d];
 }
@@ -283,11 +254,15 @@ __global__ void __launch_bounds__(kSortThreads) radix_scatter_kernel(const uint6
     uint32_t rank[kSortItems];
     const unsigned lt_mask = (1u << lane) - 1u;
 #pragma unroll
+    for (int j = 0; j < kSortItems; ++j) {  // all loads first: 32 independent loads in flight
+        const uint64_t i = seg + (uint64_t)j * 32 + lane;
+        key[j] = i < m ? __ldcs(keys_in + i) : 0ull;
+        val[j] = i < m ? __ldcs(vals_in + i) : 0u;
+    }
+#pragma unroll
     for (int j = 0; j < kSortItems; ++j) {
         uint64_t i = seg + (uint64_t)j * 32 + lane;
         bool valid = i < m;
-        key[j] = valid ? __ldcs(keys_in + i) : 0ull;
-        val[j] = valid ? __ldcs(vals_in + i) : 0u;
         unsigned vmask = __ballot_sync(0xffffffffu, valid);
         uint32_t d = digit_of(key[j], shift);
         uint32_t r = 0;
@@ -336,29 +311,34 @@ __global__ void __launch_bounds__(kSortThreads) radix_scatter_kernel(const uint6
     }
 }
 
-bool radix_sort_pairs(Ctx* ctx, RadixBuffers b, uint64_t m, uint32_t nbits, cudaStream_t s) {
+bool radix_sort_pairs_range(Ctx* ctx, RadixBuffers b, uint64_t m, uint32_t bit_lo, uint32_t bit_hi,
+                            cudaStream_t s) {
     static_assert(kSortThreads == kRadix, "one thread per digit in the tile scan");
     DK_CUDA(cudaFuncSetAttribute(radix_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)sizeof(ScatterSmem)));
-    if (m <= 1 || nbits == 0) return false;
+    if (m <= 1 || bit_hi <= bit_lo) return false;
     if (m > 0xffffffffull) throw Error(DFAKIT_E_RESOURCE, "radix sort: more than 2^32 keys");
-    const uint32_t passes = (nbits + kRadixBits - 1) / kRadixBits;
+    const uint32_t passes = (bit_hi - bit_lo + kRadixBits - 1) / kRadixBits;
     const uint32_t tiles = (uint32_t)((m + kSortTile - 1) / kSortTile);
     DBuf<uint32_t> counts((uint64_t)kRadix * tiles, s);
     bool flipped = false;
     for (uint32_t p = 0; p < passes; ++p) {
-        const uint32_t shift = p * kRadixBits;
+        const uint32_t shift = bit_lo + p * kRadixBits;
         const uint64_t* kin = flipped ? b.k1 : b.k0;
         const uint32_t* vin = flipped ? b.v1 : b.v0;
         uint64_t* kout = flipped ? b.k0 : b.k1;
         uint32_t* vout = flipped ? b.v0 : b.v1;
         DK_LAUNCH_B(ctx, 8.0 * m, radix_hist_kernel, tiles, kSortThreads, 0, s, kin, m, shift, tiles, counts.get());
         exclusive_scan_u32(ctx, counts.get(), counts.get(), (uint64_t)kRadix * tiles, nullptr, s);
-        DK_LAUNCH_B(ctx, 24.0 * m, radix_scatter_kernel, tiles, kSortThreads, sizeof(ScatterSmem), s, kin, vin, m, shift, tiles,
-                  counts.get(), kout, vout);
+        DK_LAUNCH_B(ctx, 24.0 * m, radix_scatter_kernel, tiles, kSortThreads, sizeof(ScatterSmem), s, kin, vin, m,
+                    shift, tiles, counts.get(), kout, vout);
         flipped = !flipped;
     }
     return flipped;
+}
+
+bool radix_sort_pairs(Ctx* ctx, RadixBuffers b, uint64_t m, uint32_t nbits, cudaStream_t s) {
+    return radix_sort_pairs_range(ctx, b, m, 0, nbits, s);
 }
 
 }  // namespace dk

@@ -7,13 +7,44 @@
 
 namespace dk {
 
+// Block-wide exclusive scan of one value per thread (THREADS a multiple of
+// 32, <= 1024); *total receives the block sum.  warp_sums: THREADS/32 words
+// of shared memory.  Contains __syncthreads: call from every thread.
+template <int THREADS>
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* total, uint32_t* warp_sums) {
+    constexpr int W = THREADS / 32;
+    const unsigned lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= (unsigned)o) x += y;
+    }
+    if (lane == 31) warp_sums[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        uint32_t s = lane < (unsigned)W ? warp_sums[lane] : 0u;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, s, o);
+            if (lane >= (unsigned)o) s += y;
+        }
+        if (lane < (unsigned)W) warp_sums[lane] = s;
+    }
+    __syncthreads();
+    uint32_t prefix = wid ? warp_sums[wid - 1] : 0u;
+    *total = warp_sums[W - 1];
+    __syncthreads();
+    return prefix + x - v;
+}
+
 // out[i] = sum_{j<i} in[i]; optional *total_dev receives the full sum.
 // in and out may alias.  Works for any n (multi-level).
 void exclusive_scan_u32(Ctx* ctx, const uint32_t* in, uint32_t* out, uint64_t n, uint32_t* total_dev,
                         cudaStream_t s);
 
-// Compacts in[i] where flag[i] != 0, preserving order.  Returns the count
-// (synchronises).  scratch must hold n+1 uint32.
+// Compacts in[i] where flag[i] != 0, preserving order (in == nullptr means
+// in[i] = i).  Returns the count (synchronises).  scratch holds n+1 uint32.
 uint32_t compact_u32(Ctx* ctx, const uint32_t* in, const uint8_t* flag, uint64_t n, uint32_t* out,
                      uint32_t* scratch, cudaStream_t s);
 
@@ -27,6 +58,9 @@ struct RadixBuffers {
     uint32_t* v1;
 };
 bool radix_sort_pairs(Ctx* ctx, RadixBuffers b, uint64_t m, uint32_t nbits, cudaStream_t s);
+// Same, on the bit range [bit_lo, bit_hi) only (8-bit digits from bit_lo up).
+bool radix_sort_pairs_range(Ctx* ctx, RadixBuffers b, uint64_t m, uint32_t bit_lo, uint32_t bit_hi,
+                            cudaStream_t s);
 
 // Fills [0, n) with value.
 void fill_u32(Ctx* ctx, uint32_t* p, uint64_t n, uint32_t value, cudaStream_t s);
