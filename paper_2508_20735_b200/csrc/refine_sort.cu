@@ -393,6 +393,198 @@ __global__ void __launch_bounds__(kSegThreads) segment_refine_kernel(
     }
 }
 
+// ---- warp-per-bucket variant (buckets of <= 256 keys) --------------------------------
+//
+// Same algorithm as segment_refine_kernel, one warp per MSD bucket, with a
+// private 6.6 KB shared-memory slice: no block-wide barriers, 32 warps per
+// SM.  Survivors are written inside the bucket's own index range and the
+// per-bucket counts are scanned afterwards (no contended atomics).
+
+constexpr int kWarpCap = 256;
+constexpr int kWarpChunks = kWarpCap / 32;
+constexpr int kWarpsPerCta = 8;
+
+struct WarpSlice {
+    unsigned long long k[2][kWarpCap];
+    uint32_t v[2][kWarpCap];
+    uint32_t hist[256];
+    uint32_t run_start[kWarpCap + 1];
+};
+
+struct BucketStats {
+    uint32_t runs, ablocks, survivors, pad;
+};
+
+__global__ void __launch_bounds__(kWarpsPerCta * 32) bucket_refine_kernel(
+    const unsigned long long* __restrict__ keys, const uint32_t* __restrict__ vals,
+    const uint32_t* __restrict__ bucket_start, uint32_t buckets, uint64_t m, uint32_t low_bits,
+    const uint32_t* __restrict__ delta, uint32_t n, uint32_t k, int fingerprint, const uint32_t* __restrict__ lab_in,
+    uint32_t* __restrict__ lab_out, uint32_t* __restrict__ tmp_list, BucketStats* __restrict__ stats,
+    IterCounters* __restrict__ ctr) {
+    extern __shared__ __align__(16) unsigned char warp_raw[];
+    const unsigned lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+    WarpSlice& ws = reinterpret_cast<WarpSlice*>(warp_raw)[wid];
+    const unsigned lt_mask = (1u << lane) - 1u;
+    bool clash = false;
+    for (uint32_t bkt = blockIdx.x * kWarpsPerCta + wid; bkt < buckets; bkt += gridDim.x * kWarpsPerCta) {
+        const uint32_t s0 = bucket_start[bkt];
+        const uint32_t len = (bkt + 1 < buckets ? bucket_start[bkt + 1] : (uint32_t)m) - s0;
+        if (len == 0) {
+            if (lane == 0) stats[bkt] = BucketStats{0, 0, 0, 0};
+            continue;
+        }
+        const uint32_t nch = (len + 31) / 32;
+#pragma unroll
+        for (int c = 0; c < kWarpChunks; ++c) {
+            const uint32_t i = c * 32 + lane;
+            if (i < len) {
+                ws.k[0][i] = __ldcs(keys + s0 + i);
+                ws.v[0][i] = __ldcs(vals + s0 + i);
+            }
+        }
+        __syncwarp();
+        int cur = 0;
+        for (uint32_t shift = 0; shift < low_bits; shift += 8) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) ws.hist[lane * 8 + j] = 0;
+            __syncwarp();
+            uint32_t rank[kWarpChunks];
+#pragma unroll
+            for (int c = 0; c < kWarpChunks; ++c) {
+                rank[c] = 0;
+                if ((uint32_t)c < nch) {
+                    const uint32_t i = c * 32 + lane;
+                    const bool valid = i < len;
+                    const unsigned vmask = __ballot_sync(0xffffffffu, valid);
+                    const uint32_t d = valid ? (uint32_t)(ws.k[cur][i] >> shift) & 255u : 0u;
+                    unsigned peers = 0;
+                    if (valid) {
+                        peers = __match_any_sync(vmask, d);
+                        rank[c] = ws.hist[d] + (uint32_t)__popc(peers & lt_mask);
+                    }
+                    __syncwarp();
+                    if (valid && lane == (unsigned)(__ffs(peers) - 1)) ws.hist[d] += (uint32_t)__popc(peers);
+                    __syncwarp();
+                }
+            }
+            // exclusive scan of the 256 digit counts: 8 consecutive digits per lane
+            uint32_t cnt[8], local = 0;
+            bool all_one = false;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                cnt[j] = ws.hist[lane * 8 + j];
+                all_one |= cnt[j] == len;
+                local += cnt[j];
+            }
+            uint32_t incl = local;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= (unsigned)o) incl += y;
+            }
+            uint32_t start = incl - local;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                ws.hist[lane * 8 + j] = start;
+                start += cnt[j];
+            }
+            const bool skip = __any_sync(0xffffffffu, all_one);  // one digit holds every key
+            __syncwarp();
+            if (!skip) {
+#pragma unroll
+                for (int c = 0; c < kWarpChunks; ++c) {
+                    const uint32_t i = c * 32 + lane;
+                    if ((uint32_t)c < nch && i < len) {
+                        const unsigned long long key = ws.k[cur][i];
+                        const uint32_t p = ws.hist[(uint32_t)(key >> shift) & 255u] + rank[c];
+                        ws.k[cur ^ 1][p] = key;
+                        ws.v[cur ^ 1][p] = ws.v[cur][i];
+                    }
+                }
+                __syncwarp();
+                cur ^= 1;
+            }
+        }
+        const unsigned long long* K = ws.k[cur];
+        const uint32_t* V = ws.v[cur];
+        // runs
+        uint32_t R = 0;
+        for (uint32_t c = 0; c < nch; ++c) {
+            const uint32_t i = c * 32 + lane;
+            const bool head = i < len && (i == 0 || K[i] != K[i - 1]);
+            const unsigned hm = __ballot_sync(0xffffffffu, head);
+            if (head) ws.run_start[R + __popc(hm & lt_mask)] = i;
+            R += __popc(hm);
+        }
+        if (lane == 0) ws.run_start[R] = len;
+        __syncwarp();
+        uint32_t r = 0, surv = 0, ablk = 0;
+        for (uint32_t c = 0; c < nch; ++c) {
+            const uint32_t i = c * 32 + lane;
+            const bool valid = i < len;
+            const bool head = valid && (i == 0 || K[i] != K[i - 1]);
+            // run index of element i: heads at or before i
+            const unsigned hm = __ballot_sync(0xffffffffu, head);
+            const uint32_t ri = r + __popc(hm & (lt_mask | (1u << lane))) - 1;
+            r += __popc(hm);
+            bool multi = false;
+            if (valid) {
+                const uint32_t s = ws.run_start[ri], e = ws.run_start[ri + 1];
+                multi = e - s >= 2;
+                lab_out[V[i]] = V[s];
+                if (fingerprint && !head && !same_tuple(V[i], V[i - 1], delta, n, k, lab_in)) clash = true;
+            }
+            const unsigned mm = __ballot_sync(0xffffffffu, multi);
+            if (multi) tmp_list[s0 + surv + __popc(mm & lt_mask)] = V[i];
+            surv += __popc(mm);
+            ablk += __popc(__ballot_sync(0xffffffffu, multi && head));
+        }
+        if (lane == 0) stats[bkt] = BucketStats{R, ablk, surv, 0};
+        __syncwarp();
+    }
+    if (__any_sync(0xffffffffu, clash) && lane == 0) atomicOr(&ctr->collision, 1u);
+}
+
+// single-CTA totals and exclusive scan of per-bucket survivor counts
+__global__ void __launch_bounds__(1024) bucket_totals_kernel(BucketStats* __restrict__ stats, uint32_t buckets,
+                                                             uint32_t* __restrict__ surv_off,
+                                                             IterCounters* __restrict__ ctr) {
+    __shared__ uint32_t wsum[32];
+    const uint32_t per = (buckets + 1023) / 1024;
+    const uint32_t b0 = threadIdx.x * per;
+    uint32_t runs = 0, ablk = 0, surv = 0;
+    for (uint32_t b = b0; b < b0 + per && b < buckets; ++b) {
+        runs += stats[b].runs;
+        ablk += stats[b].ablocks;
+        surv += stats[b].survivors;
+    }
+    uint32_t tot;
+    uint32_t off = block_exclusive_scan<1024>(surv, &tot, wsum);
+    for (uint32_t b = b0; b < b0 + per && b < buckets; ++b) {
+        surv_off[b] = off;
+        off += stats[b].survivors;
+    }
+    runs = __reduce_add_sync(0xffffffffu, runs);
+    ablk = __reduce_add_sync(0xffffffffu, ablk);
+    if ((threadIdx.x & 31u) == 0) {
+        atomicAdd(&ctr->runs, runs);
+        atomicAdd(&ctr->active_blocks, ablk);
+    }
+    if (threadIdx.x == 0) ctr->active_states = tot;
+}
+
+// move every bucket's survivors (stored at the bucket's own range) to the
+// compacted active list; one warp per bucket, coalesced
+__global__ void bucket_gather_kernel(const uint32_t* __restrict__ tmp_list, const uint32_t* __restrict__ bucket_start,
+                                     const BucketStats* __restrict__ stats, const uint32_t* __restrict__ surv_off,
+                                     uint32_t buckets, uint32_t* __restrict__ new_list) {
+    const unsigned lane = threadIdx.x & 31u;
+    for (uint32_t b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < buckets; b += (gridDim.x * blockDim.x) >> 5) {
+        const uint32_t cnt = stats[b].survivors, src = bucket_start[b], dst = surv_off[b];
+        for (uint32_t i = lane; i < cnt; i += 32) new_list[dst + i] = tmp_list[src + i];
+    }
+}
+
 // ---- global strategy kernels ---------------------------------------------------------
 
 __global__ void run_heads_kernel(const uint64_t* __restrict__ keys, uint64_t m, uint32_t* __restrict__ heads) {
@@ -456,6 +648,7 @@ __global__ void gather_dense_kernel(const uint32_t* __restrict__ list, uint64_t 
 struct Workspace {
     DBuf<uint32_t> lab, lab2, list0, list1, vals0, vals1, heads, pos, run_start, scratch, dense, cur, tmin, tcnt;
     DBuf<uint32_t> buckets, gstart;
+    DBuf<BucketStats> stats;
     DBuf<uint64_t> keys0, keys1;
     DBuf<uint8_t> keep;
     DBuf<IterCounters> ctr;
@@ -501,6 +694,8 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
                                  (int)sizeof(SegSmem)));
     DK_CUDA(cudaFuncSetAttribute(sig_table_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)(2u << kSmemTableBits) * 4));
+    DK_CUDA(cudaFuncSetAttribute(bucket_refine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(kWarpsPerCta * sizeof(WarpSlice))));
 
     // initial partition {F, Q\F} with min-state labels
     LeaderInfo li = leader_info(ctx, d, s);
@@ -604,6 +799,47 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
                 DK_LAUNCH(ctx, prefix_count_kernel, g, kThreads, 0, s, (const unsigned long long*)skeys, m, shift,
                           w.buckets.get());
                 exclusive_scan_u32(ctx, w.buckets.get(), w.buckets.get(), nb, nullptr, s);
+                // largest bucket: warp-per-bucket refinement when every bucket fits a warp slice
+                if (w.gstart.n < (uint64_t)nb + 1) w.gstart.alloc((uint64_t)nb + 1, s);
+                DK_LAUNCH(ctx, group_bounds_kernel, grid_for(nb), kThreads, 0, s, w.buckets.get(), nb, 1u, nb, m,
+                          w.gstart.get(), w.ctr.get());
+                read_words(ctx, w.ctr.get(), sizeof(c), &c, s);
+                if (c.max_group <= (uint32_t)kWarpCap) {
+                    if (w.stats.n < nb) w.stats.alloc(nb, s);
+                    uint32_t* dst = (list == list_buf) ? list_alt : list_buf;
+                    DK_CUDA(cudaMemcpyAsync(w.lab2.get(), w.lab.get(), (size_t)n * 4, cudaMemcpyDeviceToDevice, s));
+                    const unsigned bg =
+                        (unsigned)std::min<uint64_t>((nb + kWarpsPerCta - 1) / kWarpsPerCta, (uint64_t)ctx->num_sms * 12);
+                    DK_LAUNCH_B(ctx, 16.0 * m, bucket_refine_kernel, bg, kWarpsPerCta * 32,
+                                kWarpsPerCta * sizeof(WarpSlice), s, (const unsigned long long*)skeys, svals,
+                                w.buckets.get(), nb, m, shift, d.delta, n, k, (int)fingerprint, w.lab.get(),
+                                w.lab2.get(), w.pos.get(), w.stats.get(), w.ctr.get());
+                    DK_LAUNCH(ctx, bucket_totals_kernel, 1, 1024, 0, s, w.stats.get(), nb, w.run_start.get(),
+                              w.ctr.get());
+                    DK_LAUNCH(ctx, bucket_gather_kernel, grid_for((uint64_t)nb * 32), kThreads, 0, s, w.pos.get(),
+                              w.buckets.get(), w.stats.get(), w.run_start.get(), nb, dst);
+                    res.sorted += m;
+                    read_words(ctx, w.ctr.get(), sizeof(c), &c, s);
+                    if (fingerprint && c.collision) {
+                        ++res.collisions;
+                        ++collisions_this_pass;
+                        --res.passes;
+                        salt = mix64(salt + 0x1234567ull);
+                        continue;
+                    }
+                    collisions_this_pass = 0;
+                    const uint32_t newB = B - A + c.runs;
+                    if (newB == B) break;  // fixed point (reference l.411)
+                    ++res.iters;
+                    B = newB;
+                    A = c.active_blocks;
+                    std::swap(w.lab, w.lab2);
+                    m = c.active_states;
+                    list = dst;
+                    if (dst == list_alt) std::swap(list_buf, list_alt);
+                    continue;
+                }
+                DK_CUDA(cudaMemsetAsync(&w.ctr.get()->max_group, 0, sizeof(uint32_t), s));
                 const uint64_t mean = m / nb;
                 const uint32_t per_group = (uint32_t)std::max<uint64_t>(
                     1, std::min<uint64_t>(nb, (kSegCap / 2) / std::max<uint64_t>(mean, 1)));

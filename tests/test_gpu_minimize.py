@@ -159,6 +159,32 @@ def test_sort_exact_paths_and_collision_recovery(dk, oracle):
     assert collisions > 0, "the 6-bit fingerprint hook never produced a collision"
 
 
+def copies(t, c):
+    """c language-equal copies of a DFA, copy j stepping into copy j+1:
+    every equivalence class has c members spread over the state space."""
+    delta, acc, _ = t
+    k, n0 = delta.shape
+    out = np.empty((k, n0 * c), np.uint32)
+    for j in range(c):
+        out[:, j * n0:(j + 1) * n0] = delta + ((j + 1) % c) * n0
+    return out, np.tile(acc, c), 0
+
+
+def test_grouping_strategies(dk, oracle):
+    """Large equivalence classes push fingerprint passes through the warp,
+    CTA-group and global-fallback grouping strategies; all must agree with
+    the oracle."""
+    for n0, c, k in ((2000, 50, 8), (40, 1500, 8), (20, 6000, 8), (3000, 3, 12)):
+        base = oracle.gen_random(n0, k, 0.5, n0 * 7 + c)
+        t = copies(base, c)
+        want = oracle.minimize("moore", t[0], t[1])
+        dfa = mkdfa(dk, t)
+        for kw in ({}, {"fingerprint_bits": 6}, {"force_exact": True}):
+            assert same(dk.sort_pr(dfa, **kw), want), (n0, c, k, kw)
+        for algo in ("naive", "naive-fused"):
+            assert same(run(dk, algo, dfa), oracle.minimize(algo, t[0], t[1])), (n0, c, algo)
+
+
 @pytest.mark.slow
 def test_config0_random_1M_k2(dk, oracle):
     """BASELINE configs[0]: random complete DFA, 1M states, |Sigma|=2."""
