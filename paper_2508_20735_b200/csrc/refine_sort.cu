@@ -411,26 +411,23 @@ struct WarpSlice {
     uint32_t run_start[kWarpCap + 1];
 };
 
-struct BucketStats {
-    uint32_t runs, ablocks, survivors, pad;
-};
-
 __global__ void __launch_bounds__(kWarpsPerCta * 32) bucket_refine_kernel(
     const unsigned long long* __restrict__ keys, const uint32_t* __restrict__ vals,
     const uint32_t* __restrict__ bucket_start, uint32_t buckets, uint64_t m, uint32_t low_bits,
     const uint32_t* __restrict__ delta, uint32_t n, uint32_t k, int fingerprint, const uint32_t* __restrict__ lab_in,
-    uint32_t* __restrict__ lab_out, uint32_t* __restrict__ tmp_list, BucketStats* __restrict__ stats,
+    uint32_t* __restrict__ lab_out, uint32_t* __restrict__ tmp_list, uint32_t* __restrict__ surv_count,
     IterCounters* __restrict__ ctr) {
     extern __shared__ __align__(16) unsigned char warp_raw[];
     const unsigned lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
     WarpSlice& ws = reinterpret_cast<WarpSlice*>(warp_raw)[wid];
     const unsigned lt_mask = (1u << lane) - 1u;
     bool clash = false;
+    uint32_t runs_total = 0, ablk_total = 0;
     for (uint32_t bkt = blockIdx.x * kWarpsPerCta + wid; bkt < buckets; bkt += gridDim.x * kWarpsPerCta) {
         const uint32_t s0 = bucket_start[bkt];
         const uint32_t len = (bkt + 1 < buckets ? bucket_start[bkt + 1] : (uint32_t)m) - s0;
         if (len == 0) {
-            if (lane == 0) stats[bkt] = BucketStats{0, 0, 0, 0};
+            if (lane == 0) surv_count[bkt] = 0;
             continue;
         }
         const uint32_t nch = (len + 31) / 32;
@@ -539,48 +536,27 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) bucket_refine_kernel(
             surv += __popc(mm);
             ablk += __popc(__ballot_sync(0xffffffffu, multi && head));
         }
-        if (lane == 0) stats[bkt] = BucketStats{R, ablk, surv, 0};
+        if (lane == 0) surv_count[bkt] = surv;
+        runs_total += R;
+        ablk_total += ablk;
         __syncwarp();
     }
     if (__any_sync(0xffffffffu, clash) && lane == 0) atomicOr(&ctr->collision, 1u);
-}
-
-// single-CTA totals and exclusive scan of per-bucket survivor counts
-__global__ void __launch_bounds__(1024) bucket_totals_kernel(BucketStats* __restrict__ stats, uint32_t buckets,
-                                                             uint32_t* __restrict__ surv_off,
-                                                             IterCounters* __restrict__ ctr) {
-    __shared__ uint32_t wsum[32];
-    const uint32_t per = (buckets + 1023) / 1024;
-    const uint32_t b0 = threadIdx.x * per;
-    uint32_t runs = 0, ablk = 0, surv = 0;
-    for (uint32_t b = b0; b < b0 + per && b < buckets; ++b) {
-        runs += stats[b].runs;
-        ablk += stats[b].ablocks;
-        surv += stats[b].survivors;
+    // one atomic per warp and counter (lane 0 holds the warp's totals)
+    if (lane == 0) {
+        if (runs_total) atomicAdd(&ctr->runs, runs_total);
+        if (ablk_total) atomicAdd(&ctr->active_blocks, ablk_total);
     }
-    uint32_t tot;
-    uint32_t off = block_exclusive_scan<1024>(surv, &tot, wsum);
-    for (uint32_t b = b0; b < b0 + per && b < buckets; ++b) {
-        surv_off[b] = off;
-        off += stats[b].survivors;
-    }
-    runs = __reduce_add_sync(0xffffffffu, runs);
-    ablk = __reduce_add_sync(0xffffffffu, ablk);
-    if ((threadIdx.x & 31u) == 0) {
-        atomicAdd(&ctr->runs, runs);
-        atomicAdd(&ctr->active_blocks, ablk);
-    }
-    if (threadIdx.x == 0) ctr->active_states = tot;
 }
 
 // move every bucket's survivors (stored at the bucket's own range) to the
 // compacted active list; one warp per bucket, coalesced
 __global__ void bucket_gather_kernel(const uint32_t* __restrict__ tmp_list, const uint32_t* __restrict__ bucket_start,
-                                     const BucketStats* __restrict__ stats, const uint32_t* __restrict__ surv_off,
+                                     const uint32_t* __restrict__ surv_count, const uint32_t* __restrict__ surv_off,
                                      uint32_t buckets, uint32_t* __restrict__ new_list) {
     const unsigned lane = threadIdx.x & 31u;
     for (uint32_t b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < buckets; b += (gridDim.x * blockDim.x) >> 5) {
-        const uint32_t cnt = stats[b].survivors, src = bucket_start[b], dst = surv_off[b];
+        const uint32_t cnt = surv_count[b], src = bucket_start[b], dst = surv_off[b];
         for (uint32_t i = lane; i < cnt; i += 32) new_list[dst + i] = tmp_list[src + i];
     }
 }
@@ -647,8 +623,8 @@ __global__ void gather_dense_kernel(const uint32_t* __restrict__ list, uint64_t 
 
 struct Workspace {
     DBuf<uint32_t> lab, lab2, list0, list1, vals0, vals1, heads, pos, run_start, scratch, dense, cur, tmin, tcnt;
-    DBuf<uint32_t> buckets, gstart;
-    DBuf<BucketStats> stats;
+    DBuf<uint32_t> buckets, gstart, surv_off;
+    DBuf<uint32_t> stats;  // per-bucket survivor counts
     DBuf<uint64_t> keys0, keys1;
     DBuf<uint8_t> keep;
     DBuf<IterCounters> ctr;
@@ -805,7 +781,10 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
                           w.gstart.get(), w.ctr.get());
                 read_words(ctx, w.ctr.get(), sizeof(c), &c, s);
                 if (c.max_group <= (uint32_t)kWarpCap) {
-                    if (w.stats.n < nb) w.stats.alloc(nb, s);
+                    if (w.stats.n < nb) {
+                        w.stats.alloc(nb, s);
+                        w.surv_off.alloc(nb, s);
+                    }
                     uint32_t* dst = (list == list_buf) ? list_alt : list_buf;
                     DK_CUDA(cudaMemcpyAsync(w.lab2.get(), w.lab.get(), (size_t)n * 4, cudaMemcpyDeviceToDevice, s));
                     const unsigned bg =
@@ -814,10 +793,9 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
                                 kWarpsPerCta * sizeof(WarpSlice), s, (const unsigned long long*)skeys, svals,
                                 w.buckets.get(), nb, m, shift, d.delta, n, k, (int)fingerprint, w.lab.get(),
                                 w.lab2.get(), w.pos.get(), w.stats.get(), w.ctr.get());
-                    DK_LAUNCH(ctx, bucket_totals_kernel, 1, 1024, 0, s, w.stats.get(), nb, w.run_start.get(),
-                              w.ctr.get());
+                    exclusive_scan_u32(ctx, w.stats.get(), w.surv_off.get(), nb, &w.ctr.get()->active_states, s);
                     DK_LAUNCH(ctx, bucket_gather_kernel, grid_for((uint64_t)nb * 32), kThreads, 0, s, w.pos.get(),
-                              w.buckets.get(), w.stats.get(), w.run_start.get(), nb, dst);
+                              w.buckets.get(), w.stats.get(), w.surv_off.get(), nb, dst);
                     res.sorted += m;
                     read_words(ctx, w.ctr.get(), sizeof(c), &c, s);
                     if (fingerprint && c.collision) {
