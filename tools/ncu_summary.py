@@ -43,7 +43,7 @@ SCALE = {"dur_us": {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3},
 
 def short(name):
     name = name.split("(")[0]
-    for p in ("dk::<unnamed>::", "dk::", "<unnamed>::", "(anonymous namespace)::"):
+    for p in ("dk::<unnamed>::", "dk::", "<unnamed>::", "unnamed>::", "(anonymous namespace)::"):
         name = name.replace(p, "")
     return name.split("<")[0] if "<" in name and name.index("<") > 0 else name
 
