@@ -160,11 +160,20 @@ def _report(rep: CReport, blocks: np.ndarray, algo: Algorithm) -> RefinementRepo
 
 def minimize(dfa: Dfa, algo: Algorithm, policy: ElectionPolicy = ElectionPolicy.min_index(), *,
              max_transitions: int = K_DEFAULT_MAX_TRANSITIONS, max_pair_nodes: int = K_DEFAULT_MAX_PAIR_NODES,
-             force_exact: bool = False, fingerprint_bits: int = 64, ctx: Optional[Context] = None) -> RefinementReport:
-    """Generic entry (dfakit_minimize); the named functions below call it."""
+             force_exact: bool = False, fingerprint_bits: int = 64, grouping: str = "auto",
+             ctx: Optional[Context] = None) -> RefinementReport:
+    """Generic entry (dfakit_minimize); the named functions below call it.
+
+    sort_pr knobs (testing / comparison): force_exact never uses fingerprint
+    keys, fingerprint_bits < 64 forces collisions, grouping="radix_sort"
+    groups keys with the full LSD radix sort of the literal Alg. 4 instead of
+    the counting-table / radix-bucket hashing default."""
     view = dfa.c_view()
     blocks = np.zeros(max(dfa.num_states, 1), np.uint32)
-    opts = COptions(policy.kind, int(force_exact), policy.seed, max_transitions, max_pair_nodes, fingerprint_bits, 0)
+    if grouping not in ("auto", "radix_sort"):
+        raise ValueError(f"grouping must be 'auto' or 'radix_sort', not {grouping!r}")
+    opts = COptions(policy.kind, int(force_exact), policy.seed, max_transitions, max_pair_nodes, fingerprint_bits,
+                    int(grouping == "radix_sort"))
     rep = CReport()
     check(lib.dfakit_minimize(_ctx(ctx).handle, C.byref(view), int(algo), C.byref(opts), blocks.ctypes.data,
                               C.byref(rep)))

@@ -55,7 +55,7 @@ class CProduct(C.Structure):
 class COptions(C.Structure):
     _fields_ = [("policy", C.c_uint32), ("force_exact", C.c_uint32), ("seed", C.c_uint64),
                 ("max_transitions", C.c_uint64), ("max_pair_nodes", C.c_uint64), ("fingerprint_bits", C.c_uint32),
-                ("reserved", C.c_uint32)]
+                ("grouping", C.c_uint32)]
 
 
 _P = C.POINTER

@@ -114,6 +114,7 @@ dk::RefineResult run_algo(dk::Ctx* c, const dk::DevDfa& v, dfakit_algorithm algo
             dk::SortOptions so;
             so.force_exact = o->force_exact != 0;
             so.fingerprint_bits = o->fingerprint_bits ? o->fingerprint_bits : 64;
+            so.grouping = o->grouping;
             return dk::sort_pr_device(c, v, so, block_out, s);
         }
         case DFAKIT_ALGO_NAIVE_PR:

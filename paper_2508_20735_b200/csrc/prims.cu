@@ -145,6 +145,146 @@ uint32_t compact_u32(Ctx* ctx, const uint32_t* in, const uint8_t* flag, uint64_t
 }
 
 // ---------------------------------------------------------------------------
+// tiled compaction / head scan: per-tile counts, one-CTA scan of the tile
+// counts, then an apply pass that re-reads its tile (coalesced), scans it in
+// shared memory and writes coalesced.  Three launches, no inter-CTA spinning.
+// ---------------------------------------------------------------------------
+
+constexpr int kCpThreads = 256;
+constexpr int kCpItems = 16;
+constexpr int kCpTile = kCpThreads * kCpItems;
+
+template <bool HEADS>
+__device__ __forceinline__ uint32_t elem_flag(const uint32_t* __restrict__ lab, const uint8_t* __restrict__ flag,
+                                              uint64_t i) {
+    if (HEADS) return lab[i] == (uint32_t)i ? 1u : 0u;
+    return flag[i] != 0 ? 1u : 0u;
+}
+
+template <bool HEADS>
+__global__ void __launch_bounds__(kCpThreads) tile_count_kernel(const uint32_t* __restrict__ lab,
+                                                                const uint8_t* __restrict__ flag, uint64_t n,
+                                                                uint32_t* __restrict__ sums) {
+    __shared__ uint32_t ws[kCpThreads / 32];
+    const uint64_t base = (uint64_t)blockIdx.x * kCpTile;
+    uint32_t c = 0;
+#pragma unroll
+    for (int j = 0; j < kCpItems; ++j) {
+        const uint64_t i = base + (uint64_t)j * kCpThreads + threadIdx.x;
+        if (i < n) c += elem_flag<HEADS>(lab, flag, i);
+    }
+    c = __reduce_add_sync(0xffffffffu, c);
+    if ((threadIdx.x & 31u) == 0) ws[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t t = 0;
+#pragma unroll
+        for (int w = 0; w < kCpThreads / 32; ++w) t += ws[w];
+        sums[blockIdx.x] = t;
+    }
+}
+
+// exclusive scan of `tiles` counts in place by one CTA; total -> *total
+__global__ void __launch_bounds__(1024) scan_counts_kernel(uint32_t* __restrict__ sums, uint32_t tiles,
+                                                           uint32_t* __restrict__ total) {
+    __shared__ uint32_t ws[32];
+    uint32_t carry = 0;
+    for (uint32_t b = 0; b < tiles; b += 1024) {
+        const uint32_t i = b + threadIdx.x;
+        const uint32_t v = i < tiles ? sums[i] : 0u;
+        uint32_t tot;
+        const uint32_t e = block_exclusive_scan<1024>(v, &tot, ws);
+        if (i < tiles) sums[i] = carry + e;
+        carry += tot;
+    }
+    if (threadIdx.x == 0 && total) *total = carry;
+}
+
+struct CompactSmem {
+    uint32_t v[kCpTile];  // coalesced input staging, then the tile's selected values / positions
+    uint8_t f[kCpTile];
+    uint32_t ws[kCpThreads / 32];
+};
+
+// HEADS: pos[i] = offset + #heads before i in the tile.  Else: compaction.
+template <bool HEADS>
+__global__ void __launch_bounds__(kCpThreads) tile_apply_kernel(const uint32_t* __restrict__ lab,
+                                                                const uint8_t* __restrict__ flag,
+                                                                const uint32_t* __restrict__ in, uint64_t n,
+                                                                const uint32_t* __restrict__ offs,
+                                                                uint32_t* __restrict__ out) {
+    __shared__ CompactSmem sm;
+    const unsigned tid = threadIdx.x;
+    const uint64_t base = (uint64_t)blockIdx.x * kCpTile;
+#pragma unroll
+    for (int j = 0; j < kCpItems; ++j) {
+        const uint64_t i = base + (uint64_t)j * kCpThreads + tid;
+        const bool ok = i < n;
+        sm.f[j * kCpThreads + tid] = ok ? (uint8_t)elem_flag<HEADS>(lab, flag, i) : 0;
+        if (!HEADS) sm.v[j * kCpThreads + tid] = ok ? (in ? __ldcs(in + i) : (uint32_t)i) : 0u;
+    }
+    __syncthreads();
+    uint32_t c = 0;
+    uint8_t f[kCpItems];
+    uint32_t v[kCpItems];
+#pragma unroll
+    for (int j = 0; j < kCpItems; ++j) {
+        f[j] = sm.f[tid * kCpItems + j];
+        if (!HEADS) v[j] = sm.v[tid * kCpItems + j];
+        c += f[j];
+    }
+    uint32_t agg;
+    uint32_t o = block_exclusive_scan<kCpThreads>(c, &agg, sm.ws);  // ends with a barrier
+    const uint32_t off = offs[blockIdx.x];
+    if (HEADS) {
+        o += off;
+#pragma unroll
+        for (int j = 0; j < kCpItems; ++j) {
+            sm.v[tid * kCpItems + j] = o;
+            o += f[j];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < kCpItems; ++j) {
+            const uint64_t i = base + (uint64_t)j * kCpThreads + tid;
+            if (i < n) out[i] = sm.v[j * kCpThreads + tid];
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < kCpItems; ++j)
+            if (f[j]) sm.v[o++] = v[j];
+        __syncthreads();
+        for (uint32_t i = tid; i < agg; i += kCpThreads) out[(uint64_t)off + i] = sm.v[i];
+    }
+}
+
+template <bool HEADS>
+void tiled_scan(Ctx* ctx, const uint32_t* lab, const uint8_t* flag, const uint32_t* in, uint64_t n, uint32_t* out,
+                uint32_t* total_dev, cudaStream_t s) {
+    if (n == 0) {
+        DK_CUDA(cudaMemsetAsync(total_dev, 0, sizeof(uint32_t), s));
+        return;
+    }
+    const uint64_t tiles = (n + kCpTile - 1) / kCpTile;
+    if (tiles > 0xffffffffull) throw Error(DFAKIT_E_RESOURCE, "scan: too many tiles");
+    DBuf<uint32_t> sums(tiles, s);
+    const double eb = HEADS ? 4.0 : 1.0;
+    DK_LAUNCH_B(ctx, eb * n, tile_count_kernel<HEADS>, (unsigned)tiles, kCpThreads, 0, s, lab, flag, n, sums.get());
+    DK_LAUNCH(ctx, scan_counts_kernel, 1, 1024, 0, s, sums.get(), (uint32_t)tiles, total_dev);
+    DK_LAUNCH_B(ctx, HEADS ? 8.0 * n : (double)n * (1.0 + (in ? 4.0 : 0.0)), tile_apply_kernel<HEADS>,
+                (unsigned)tiles, kCpThreads, 0, s, lab, flag, in, n, sums.get(), out);
+}
+
+void compact_flags(Ctx* ctx, const uint32_t* in, const uint8_t* flag, uint64_t n, uint32_t* out,
+                   uint32_t* count_dev, cudaStream_t s) {
+    tiled_scan<false>(ctx, nullptr, flag, in, n, out, count_dev, s);
+}
+
+void head_scan(Ctx* ctx, const uint32_t* lab, uint64_t n, uint32_t* pos, uint32_t* total_dev, cudaStream_t s) {
+    tiled_scan<true>(ctx, lab, nullptr, nullptr, n, pos, total_dev, s);
+}
+
+// ---------------------------------------------------------------------------
 // canonical renumbering
 // ---------------------------------------------------------------------------
 
@@ -176,11 +316,34 @@ void min_state_labels(Ctx* ctx, uint32_t* lab, uint64_t n, uint32_t* scratch, cu
     DK_LAUNCH(ctx, to_min_label_kernel, grid_for(n), kThreads, 0, s, lab, n, scratch);
 }
 
+template <typename T>
+__global__ void relabel_narrow_kernel(const uint32_t* __restrict__ lab, uint64_t n, const uint32_t* __restrict__ dense,
+                                      T* __restrict__ out) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = (T)dense[lab[i]];
+}
+
+uint32_t dense_labels(Ctx* ctx, const uint32_t* lab, uint64_t n, void* out, int bytes, uint32_t* scratch,
+                      cudaStream_t s) {
+    if (n == 0) return 0;
+    head_scan(ctx, lab, n, scratch, scratch + n, s);
+    if (bytes == 1)
+        DK_LAUNCH(ctx, relabel_narrow_kernel<uint8_t>, grid_for(n), kThreads, 0, s, lab, n, scratch,
+                  static_cast<uint8_t*>(out));
+    else if (bytes == 2)
+        DK_LAUNCH(ctx, relabel_narrow_kernel<uint16_t>, grid_for(n), kThreads, 0, s, lab, n, scratch,
+                  static_cast<uint16_t*>(out));
+    else
+        DK_LAUNCH(ctx, relabel_kernel, grid_for(n), kThreads, 0, s, lab, n, scratch, static_cast<uint32_t*>(out));
+    uint32_t total = 0;
+    read_words(ctx, scratch + n, sizeof(uint32_t), &total, s);
+    return total;
+}
+
 uint32_t canonical_from_min_labels(Ctx* ctx, const uint32_t* lab, uint64_t n, uint32_t* out, uint32_t* scratch,
                                    cudaStream_t s) {
     if (n == 0) return 0;
-    DK_LAUNCH(ctx, head_flags_kernel, grid_for(n), kThreads, 0, s, lab, n, scratch);
-    exclusive_scan_u32(ctx, scratch, scratch, n, scratch + n, s);
+    head_scan(ctx, lab, n, scratch, scratch + n, s);
     DK_LAUNCH(ctx, relabel_kernel, grid_for(n), kThreads, 0, s, lab, n, scratch, out);
     uint32_t total = 0;
     read_words(ctx, scratch + n, sizeof(uint32_t), &total, s);

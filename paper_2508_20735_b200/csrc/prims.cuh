@@ -62,6 +62,18 @@ bool radix_sort_pairs(Ctx* ctx, RadixBuffers b, uint64_t m, uint32_t nbits, cuda
 bool radix_sort_pairs_range(Ctx* ctx, RadixBuffers b, uint64_t m, uint32_t bit_lo, uint32_t bit_hi,
                             cudaStream_t s);
 
+// Single-pass stream compaction (decoupled look-back, one launch):
+// out[j] = in ? in[i] : i for the j-th i with flag[i] != 0, order preserved.
+// *count_dev receives the count.  Returns nothing (no host sync).
+void compact_flags(Ctx* ctx, const uint32_t* in, const uint8_t* flag, uint64_t n, uint32_t* out,
+                   uint32_t* count_dev, cudaStream_t s);
+
+// Dense first-occurrence block ids of min-state labels written in the
+// narrowest type that holds them: bytes = 1, 2 or 4 (uint8/uint16/uint32).
+// Returns the block count (synchronises).  scratch holds n+1 uint32.
+uint32_t dense_labels(Ctx* ctx, const uint32_t* lab, uint64_t n, void* out, int bytes, uint32_t* scratch,
+                      cudaStream_t s);
+
 // Fills [0, n) with value.
 void fill_u32(Ctx* ctx, uint32_t* p, uint64_t n, uint32_t value, cudaStream_t s);
 void iota_u32(Ctx* ctx, uint32_t* p, uint64_t n, cudaStream_t s);

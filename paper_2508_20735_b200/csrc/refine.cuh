@@ -25,6 +25,7 @@ struct RefineResult {
 struct SortOptions {
     bool force_exact = false;
     uint32_t fingerprint_bits = 64;
+    uint32_t grouping = 0;  // 0 = auto (table / bucket hashing), 1 = LSD radix sort (literal Alg. 4)
 };
 
 // All block_out arrays are device arrays of n entries, canonical numbering.

@@ -152,7 +152,8 @@ def test_sort_exact_paths_and_collision_recovery(dk, oracle):
         t = oracle.gen_random(n, k, frac, s)
         want = oracle.minimize("moore", t[0], t[1])
         dfa = mkdfa(dk, t)
-        for kw in ({}, {"force_exact": True}, {"fingerprint_bits": 6}):
+        for kw in ({}, {"force_exact": True}, {"fingerprint_bits": 6}, {"grouping": "radix_sort"},
+                   {"grouping": "radix_sort", "fingerprint_bits": 6}):
             rep = dk.sort_pr(dfa, **kw)
             assert same(rep, want), kw
             collisions += rep.hash_collisions
@@ -171,15 +172,15 @@ def copies(t, c):
 
 
 def test_grouping_strategies(dk, oracle):
-    """Large equivalence classes push fingerprint passes through the warp,
-    CTA-group and global-fallback grouping strategies; all must agree with
-    the oracle."""
+    """Large equivalence classes push passes through the counting table, the
+    radix-bucket shared-memory hashing, the overflow (global table) fallback
+    and the radix-sort grouping; all must agree with the oracle."""
     for n0, c, k in ((2000, 50, 8), (40, 1500, 8), (20, 6000, 8), (3000, 3, 12)):
         base = oracle.gen_random(n0, k, 0.5, n0 * 7 + c)
         t = copies(base, c)
         want = oracle.minimize("moore", t[0], t[1])
         dfa = mkdfa(dk, t)
-        for kw in ({}, {"fingerprint_bits": 6}, {"force_exact": True}):
+        for kw in ({}, {"fingerprint_bits": 6}, {"force_exact": True}, {"grouping": "radix_sort"}):
             assert same(dk.sort_pr(dfa, **kw), want), (n0, c, k, kw)
         for algo in ("naive", "naive-fused"):
             assert same(run(dk, algo, dfa), oracle.minimize(algo, t[0], t[1])), (n0, c, algo)
