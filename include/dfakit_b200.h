@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define DFAKIT_B200_ABI_VERSION 1
+#define DFAKIT_B200_ABI_VERSION 2
 #define DFAKIT_NO_STATE 0xffffffffu
 
 typedef enum {
@@ -196,6 +196,68 @@ dfakit_status dfakit_check_equiv_uf(dfakit_ctx* ctx, const dfakit_dfa* a, const 
 dfakit_status dfakit_check_equiv_uf_device(dfakit_ctx* ctx, const dfakit_dfa* a, const dfakit_dfa* b,
                                            uint32_t* counterexample, uint32_t counterexample_cap,
                                            dfakit_product* out, void* stream);
+
+/* ---- sharded sort_pr (multi-GPU) ---------------------------------------------
+ * Pass-level primitives of the sharded engine; the pass loop and the
+ * collectives (NCCL all-to-all / allgather / allreduce through
+ * torch.distributed) live in paper_2508_20735_b200/sharded.py.  States are
+ * sharded in contiguous ranges [lo, hi); delta, accepting and the block-label
+ * array `lab` (min-state labels, padded to world * shard entries) are
+ * replicated on every rank.  Pointers are device pointers; `counters` is a
+ * device uint32[4] = {runs, active blocks, active states, collision}.  Send /
+ * receive entries are 16 bytes {hkey lo, hkey hi, state, 0}.  The plan is
+ * the same on every rank (it depends on global counts only). */
+typedef enum {
+    DFAKIT_PLAN_TABLE = 0,       /* packed keys <= 20 bits: allreduced counting table      */
+    DFAKIT_PLAN_PACKED = 1,      /* packed exact 64-bit keys: all-to-all + owner grouping   */
+    DFAKIT_PLAN_FINGERPRINT = 2, /* 64-bit fingerprints, groups verified tuple by tuple     */
+    DFAKIT_PLAN_CHUNKED = 3      /* exact letter chunks (single-GPU engine only)            */
+} dfakit_plan_strategy;
+
+typedef struct {
+    uint32_t strategy;      /* dfakit_plan_strategy                                   */
+    uint32_t field_bits;    /* packed keys: bits per field                            */
+    uint32_t key_bits;      /* packed key width; 64 for fingerprints                  */
+    uint32_t keylab_bytes;  /* 0: gather min-state labels; 1/2/4: dense block ids     */
+} dfakit_pass_plan;
+
+/* Key plan of one sort_pr pass (host only; no device needed). */
+dfakit_status dfakit_plan_pass(uint32_t num_states, uint32_t alphabet_size, uint32_t num_blocks,
+                               uint64_t active_states, uint32_t collisions, uint32_t force_exact,
+                               dfakit_pass_plan* out);
+/* Initial partition {F, Q\F}: full `lab`, survivor flags act[lo, hi), global counts. */
+dfakit_status dfakit_shard_init(dfakit_ctx* ctx, const dfakit_dfa* dfa, uint32_t lo, uint32_t hi, uint32_t* lab,
+                                uint8_t* act, uint32_t* num_blocks, uint32_t* active_blocks,
+                                uint64_t* active_states, void* stream);
+/* Dense block ids of `lab` in plan->keylab_bytes-wide entries (no-op when 0). */
+dfakit_status dfakit_shard_keylab(dfakit_ctx* ctx, const uint32_t* lab, uint32_t n, const dfakit_pass_plan* plan,
+                                  void* keylab, void* stream);
+/* Table passes: keys of the m local active states in `list`, local (min, count)
+ * table of 2^key_bits entries (caller allreduces MIN / SUM), then apply. */
+dfakit_status dfakit_shard_table_signature(dfakit_ctx* ctx, const dfakit_dfa* dfa, const void* keylab,
+                                           const dfakit_pass_plan* plan, const uint32_t* list, uint64_t m,
+                                           uint32_t* keys32, uint32_t* tmin, uint32_t* tcnt, void* stream);
+dfakit_status dfakit_shard_table_apply(dfakit_ctx* ctx, const uint32_t* list, const uint32_t* keys32, uint64_t m,
+                                       const uint32_t* tmin, const uint32_t* tcnt, uint32_t* lab, uint8_t* act,
+                                       uint32_t* counters, void* stream);
+/* Wide passes: keys of the local active states partitioned by owner rank into
+ * send_entries (m entries, destination-contiguous); send_counts[world]. */
+dfakit_status dfakit_shard_partition(dfakit_ctx* ctx, const dfakit_dfa* dfa, const void* keylab,
+                                     const dfakit_pass_plan* plan, uint64_t salt, const uint32_t* list, uint64_t m,
+                                     uint32_t world, void* send_entries, uint32_t* send_counts, void* stream);
+/* Owner side: groups the received entries; results[i] = new label | survivor << 31. */
+dfakit_status dfakit_shard_group(dfakit_ctx* ctx, const dfakit_dfa* dfa, const uint32_t* lab,
+                                 const dfakit_pass_plan* plan, const void* recv_entries, uint64_t count,
+                                 uint32_t* results, uint32_t* counters, void* stream);
+/* Home side: returned results applied to lab / act of the sent states. */
+dfakit_status dfakit_shard_apply(dfakit_ctx* ctx, const void* send_entries, const uint32_t* results, uint64_t count,
+                                 uint32_t* lab, uint8_t* act, void* stream);
+/* Next local active list: states q in [lo, hi) with act[q] != 0, increasing. */
+dfakit_status dfakit_shard_compact(dfakit_ctx* ctx, const uint8_t* act, uint32_t lo, uint32_t hi, uint32_t* list,
+                                   uint32_t* count, void* stream);
+/* Canonical first-occurrence numbering of min-state labels. */
+dfakit_status dfakit_shard_canonical(dfakit_ctx* ctx, const uint32_t* lab, uint32_t n, uint32_t* block_of,
+                                     uint32_t* num_blocks, void* stream);
 
 /* ---- device generators (bench inputs built in HBM) --------------------------- */
 /* Synthetic random DFA, same formula as oracle/oracle.c or_gen_synth. */

@@ -58,7 +58,13 @@ class COptions(C.Structure):
                 ("grouping", C.c_uint32)]
 
 
+class CPassPlan(C.Structure):
+    _fields_ = [("strategy", C.c_uint32), ("field_bits", C.c_uint32), ("key_bits", C.c_uint32),
+                ("keylab_bytes", C.c_uint32)]
+
+
 _P = C.POINTER
+_V = C.c_void_p
 _sig = {
     "dfakit_abi_version": (C.c_int, []),
     "dfakit_last_error": (C.c_char_p, []),
@@ -97,6 +103,20 @@ _sig = {
     "dfakit_gen_chain_device": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p]),
     "dfakit_permute_states_device": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint64, C.c_void_p,
                                                C.c_void_p, C.c_void_p, C.c_void_p, _P(C.c_uint32), C.c_void_p]),
+    # sharded sort_pr primitives (sharded.py)
+    "dfakit_plan_pass": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint32, C.c_uint32,
+                                   _P(CPassPlan)]),
+    "dfakit_shard_init": (C.c_int, [_V, _P(CDfa), C.c_uint32, C.c_uint32, _V, _V, _P(C.c_uint32), _P(C.c_uint32),
+                                    _P(C.c_uint64), _V]),
+    "dfakit_shard_keylab": (C.c_int, [_V, _V, C.c_uint32, _P(CPassPlan), _V, _V]),
+    "dfakit_shard_table_signature": (C.c_int, [_V, _P(CDfa), _V, _P(CPassPlan), _V, C.c_uint64, _V, _V, _V, _V]),
+    "dfakit_shard_table_apply": (C.c_int, [_V, _V, _V, C.c_uint64, _V, _V, _V, _V, _V, _V]),
+    "dfakit_shard_partition": (C.c_int, [_V, _P(CDfa), _V, _P(CPassPlan), C.c_uint64, _V, C.c_uint64, C.c_uint32,
+                                         _V, _V, _V]),
+    "dfakit_shard_group": (C.c_int, [_V, _P(CDfa), _V, _P(CPassPlan), _V, C.c_uint64, _V, _V, _V]),
+    "dfakit_shard_apply": (C.c_int, [_V, _V, _V, C.c_uint64, _V, _V, _V]),
+    "dfakit_shard_compact": (C.c_int, [_V, _V, C.c_uint32, C.c_uint32, _V, _V, _V]),
+    "dfakit_shard_canonical": (C.c_int, [_V, _V, C.c_uint32, _V, _P(C.c_uint32), _V]),
 }
 EXPORTS = tuple(_sig)
 for _name, (_res, _args) in _sig.items():

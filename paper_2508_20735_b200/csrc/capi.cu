@@ -204,6 +204,26 @@ void product_host(dfakit_ctx* ctx, const dfakit_dfa* a, const dfakit_dfa* b, dfa
 
 }  // namespace
 
+namespace {
+dk::PassPlan plan_in(const dfakit_pass_plan* p) {
+    if (!p) throw dk::Error(DFAKIT_E_INVALID, "null plan");
+    dk::PassPlan q;
+    q.strategy = p->strategy;
+    q.field_bits = p->field_bits;
+    q.key_bits = p->key_bits;
+    q.keylab_bytes = p->keylab_bytes;
+    return q;
+}
+template <typename F>
+dfakit_status on_device(dfakit_ctx* ctx, void* stream, F&& f) {
+    return guard([&] {
+        if (!ctx) throw dk::Error(DFAKIT_E_INVALID, "null context");
+        DK_CUDA(cudaSetDevice(ctx->c->device));
+        f(ctx->c, stream ? (cudaStream_t)stream : ctx->c->stream);
+    });
+}
+}  // namespace
+
 extern "C" {
 
 int dfakit_abi_version(void) { return DFAKIT_B200_ABI_VERSION; }
@@ -429,6 +449,108 @@ dfakit_status dfakit_permute_states_device(dfakit_ctx* ctx, uint32_t n, uint32_t
         uint32_t init = dk::permute_states_device(ctx->c, n, k, seed, delta, accepting, out_delta, out_accepting,
                                                   stream ? (cudaStream_t)stream : ctx->c->stream);
         if (initial_out) *initial_out = init;
+    });
+}
+
+// ---- sharded sort_pr primitives ------------------------------------------------
+
+dfakit_status dfakit_plan_pass(uint32_t num_states, uint32_t alphabet_size, uint32_t num_blocks,
+                               uint64_t active_states, uint32_t collisions, uint32_t force_exact,
+                               dfakit_pass_plan* out) {
+    return guard([&] {
+        if (!out) throw dk::Error(DFAKIT_E_INVALID, "null plan");
+        const dk::PassPlan p = dk::plan_pass(num_states, alphabet_size, num_blocks, active_states, collisions,
+                                             force_exact != 0);
+        *out = dfakit_pass_plan{p.strategy, p.field_bits, p.key_bits, p.keylab_bytes};
+    });
+}
+
+
+dfakit_status dfakit_shard_init(dfakit_ctx* ctx, const dfakit_dfa* dfa, uint32_t lo, uint32_t hi, uint32_t* lab,
+                                uint8_t* act, uint32_t* num_blocks, uint32_t* active_blocks,
+                                uint64_t* active_states, void* stream) {
+    return on_device(ctx, stream, [&](dk::Ctx* c, cudaStream_t s) {
+        check_view(dfa, "shard_init");
+        if (lo > hi || hi > dfa->num_states) throw dk::Error(DFAKIT_E_INVALID, "shard_init: bad state range");
+        const dk::ShardInit r = dk::shard_init(c, device_view(dfa), lo, hi, lab, act, s);
+        if (num_blocks) *num_blocks = r.num_blocks;
+        if (active_blocks) *active_blocks = r.active_blocks;
+        if (active_states) *active_states = r.active_states;
+    });
+}
+
+dfakit_status dfakit_shard_keylab(dfakit_ctx* ctx, const uint32_t* lab, uint32_t n, const dfakit_pass_plan* plan,
+                                  void* keylab, void* stream) {
+    return on_device(ctx, stream, [&](dk::Ctx* c, cudaStream_t s) {
+        const dk::PassPlan p = plan_in(plan);
+        if (!p.keylab_bytes || !n) return;
+        dk::DBuf<uint32_t> scratch((uint64_t)n + 1, s);
+        dk::shard_keylab(c, lab, n, p, keylab, scratch.get(), s);
+    });
+}
+
+dfakit_status dfakit_shard_table_signature(dfakit_ctx* ctx, const dfakit_dfa* dfa, const void* keylab,
+                                           const dfakit_pass_plan* plan, const uint32_t* list, uint64_t m,
+                                           uint32_t* keys32, uint32_t* tmin, uint32_t* tcnt, void* stream) {
+    return on_device(ctx, stream, [&](dk::Ctx* c, cudaStream_t s) {
+        check_view(dfa, "shard_table_signature");
+        const dk::PassPlan p = plan_in(plan);
+        if (p.strategy != dk::kPlanTable || p.key_bits > 20)
+            throw dk::Error(DFAKIT_E_INVALID, "shard_table_signature: not a table plan");
+        dk::shard_table_signature(c, device_view(dfa), keylab, p, list, m, keys32, tmin, tcnt, s);
+    });
+}
+
+dfakit_status dfakit_shard_table_apply(dfakit_ctx* ctx, const uint32_t* list, const uint32_t* keys32, uint64_t m,
+                                       const uint32_t* tmin, const uint32_t* tcnt, uint32_t* lab, uint8_t* act,
+                                       uint32_t* counters, void* stream) {
+    return on_device(ctx, stream, [&](dk::Ctx* c, cudaStream_t s) {
+        dk::shard_table_apply(c, list, keys32, m, tmin, tcnt, lab, act, counters, s);
+    });
+}
+
+dfakit_status dfakit_shard_partition(dfakit_ctx* ctx, const dfakit_dfa* dfa, const void* keylab,
+                                     const dfakit_pass_plan* plan, uint64_t salt, const uint32_t* list, uint64_t m,
+                                     uint32_t world, void* send_entries, uint32_t* send_counts, void* stream) {
+    return on_device(ctx, stream, [&](dk::Ctx* c, cudaStream_t s) {
+        check_view(dfa, "shard_partition");
+        const dk::PassPlan p = plan_in(plan);
+        if (p.strategy != dk::kPlanPacked && p.strategy != dk::kPlanFingerprint)
+            throw dk::Error(DFAKIT_E_INVALID, "shard_partition: plan is not packed / fingerprint");
+        dk::shard_sig_partition(c, device_view(dfa), keylab, p, salt, list, m, world,
+                                static_cast<uint4*>(send_entries), send_counts, s);
+    });
+}
+
+dfakit_status dfakit_shard_group(dfakit_ctx* ctx, const dfakit_dfa* dfa, const uint32_t* lab,
+                                 const dfakit_pass_plan* plan, const void* recv_entries, uint64_t count,
+                                 uint32_t* results, uint32_t* counters, void* stream) {
+    return on_device(ctx, stream, [&](dk::Ctx* c, cudaStream_t s) {
+        check_view(dfa, "shard_group");
+        if (dfa->num_states > 0x7fffffffu) throw dk::Error(DFAKIT_E_INVALID, "shard_group: more than 2^31 states");
+        dk::shard_group(c, device_view(dfa), lab, plan_in(plan), static_cast<const uint4*>(recv_entries), count,
+                        results, counters, s);
+    });
+}
+
+dfakit_status dfakit_shard_apply(dfakit_ctx* ctx, const void* send_entries, const uint32_t* results, uint64_t count,
+                                 uint32_t* lab, uint8_t* act, void* stream) {
+    return on_device(ctx, stream, [&](dk::Ctx* c, cudaStream_t s) {
+        dk::shard_apply(c, static_cast<const uint4*>(send_entries), results, count, lab, act, s);
+    });
+}
+
+dfakit_status dfakit_shard_compact(dfakit_ctx* ctx, const uint8_t* act, uint32_t lo, uint32_t hi, uint32_t* list,
+                                   uint32_t* count, void* stream) {
+    return on_device(ctx, stream, [&](dk::Ctx* c, cudaStream_t s) { dk::shard_compact(c, act, lo, hi, list, count, s); });
+}
+
+dfakit_status dfakit_shard_canonical(dfakit_ctx* ctx, const uint32_t* lab, uint32_t n, uint32_t* block_of,
+                                     uint32_t* num_blocks, void* stream) {
+    return on_device(ctx, stream, [&](dk::Ctx* c, cudaStream_t s) {
+        dk::DBuf<uint32_t> scratch((uint64_t)n + 1, s);
+        const uint32_t b = dk::canonical_from_min_labels(c, lab, n, block_of, scratch.get(), s);
+        if (num_blocks) *num_blocks = b;
     });
 }
 

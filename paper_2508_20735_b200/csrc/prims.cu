@@ -212,7 +212,7 @@ __global__ void __launch_bounds__(kCpThreads) tile_apply_kernel(const uint32_t* 
                                                                 const uint8_t* __restrict__ flag,
                                                                 const uint32_t* __restrict__ in, uint64_t n,
                                                                 const uint32_t* __restrict__ offs,
-                                                                uint32_t* __restrict__ out) {
+                                                                uint32_t* __restrict__ out, uint32_t id_base) {
     __shared__ CompactSmem sm;
     const unsigned tid = threadIdx.x;
     const uint64_t base = (uint64_t)blockIdx.x * kCpTile;
@@ -221,7 +221,7 @@ __global__ void __launch_bounds__(kCpThreads) tile_apply_kernel(const uint32_t* 
         const uint64_t i = base + (uint64_t)j * kCpThreads + tid;
         const bool ok = i < n;
         sm.f[j * kCpThreads + tid] = ok ? (uint8_t)elem_flag<HEADS>(lab, flag, i) : 0;
-        if (!HEADS) sm.v[j * kCpThreads + tid] = ok ? (in ? __ldcs(in + i) : (uint32_t)i) : 0u;
+        if (!HEADS) sm.v[j * kCpThreads + tid] = ok ? (in ? __ldcs(in + i) : id_base + (uint32_t)i) : 0u;
     }
     __syncthreads();
     uint32_t c = 0;
@@ -260,7 +260,7 @@ __global__ void __launch_bounds__(kCpThreads) tile_apply_kernel(const uint32_t* 
 
 template <bool HEADS>
 void tiled_scan(Ctx* ctx, const uint32_t* lab, const uint8_t* flag, const uint32_t* in, uint64_t n, uint32_t* out,
-                uint32_t* total_dev, cudaStream_t s) {
+                uint32_t* total_dev, cudaStream_t s, uint32_t id_base = 0) {
     if (n == 0) {
         DK_CUDA(cudaMemsetAsync(total_dev, 0, sizeof(uint32_t), s));
         return;
@@ -272,12 +272,12 @@ void tiled_scan(Ctx* ctx, const uint32_t* lab, const uint8_t* flag, const uint32
     DK_LAUNCH_B(ctx, eb * n, tile_count_kernel<HEADS>, (unsigned)tiles, kCpThreads, 0, s, lab, flag, n, sums.get());
     DK_LAUNCH(ctx, scan_counts_kernel, 1, 1024, 0, s, sums.get(), (uint32_t)tiles, total_dev);
     DK_LAUNCH_B(ctx, HEADS ? 8.0 * n : (double)n * (1.0 + (in ? 4.0 : 0.0)), tile_apply_kernel<HEADS>,
-                (unsigned)tiles, kCpThreads, 0, s, lab, flag, in, n, sums.get(), out);
+                (unsigned)tiles, kCpThreads, 0, s, lab, flag, in, n, sums.get(), out, id_base);
 }
 
 void compact_flags(Ctx* ctx, const uint32_t* in, const uint8_t* flag, uint64_t n, uint32_t* out,
-                   uint32_t* count_dev, cudaStream_t s) {
-    tiled_scan<false>(ctx, nullptr, flag, in, n, out, count_dev, s);
+                   uint32_t* count_dev, cudaStream_t s, uint32_t id_base) {
+    tiled_scan<false>(ctx, nullptr, flag, in, n, out, count_dev, s, id_base);
 }
 
 void head_scan(Ctx* ctx, const uint32_t* lab, uint64_t n, uint32_t* pos, uint32_t* total_dev, cudaStream_t s) {

@@ -63,10 +63,11 @@ bool radix_sort_pairs_range(Ctx* ctx, RadixBuffers b, uint64_t m, uint32_t bit_l
                             cudaStream_t s);
 
 // Single-pass stream compaction (decoupled look-back, one launch):
-// out[j] = in ? in[i] : i for the j-th i with flag[i] != 0, order preserved.
+// out[j] = in ? in[i] : id_base + i for the j-th i with flag[i] != 0, order
+// preserved.
 // *count_dev receives the count.  Returns nothing (no host sync).
 void compact_flags(Ctx* ctx, const uint32_t* in, const uint8_t* flag, uint64_t n, uint32_t* out,
-                   uint32_t* count_dev, cudaStream_t s);
+                   uint32_t* count_dev, cudaStream_t s, uint32_t id_base = 0);
 
 // Dense first-occurrence block ids of min-state labels written in the
 // narrowest type that holds them: bytes = 1, 2 or 4 (uint8/uint16/uint32).

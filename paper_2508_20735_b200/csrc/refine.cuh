@@ -28,6 +28,40 @@ struct SortOptions {
     uint32_t grouping = 0;  // 0 = auto (table / bucket hashing), 1 = LSD radix sort (literal Alg. 4)
 };
 
+// Key plan of one sortPR pass (see plan_pass in refine_sort.cu).
+enum : uint32_t { kPlanTable = 0, kPlanPacked = 1, kPlanFingerprint = 2, kPlanChunked = 3 };
+struct PassPlan {
+    uint32_t strategy = kPlanTable;
+    uint32_t field_bits = 0;    // packed keys: bits per field
+    uint32_t key_bits = 0;      // packed key width (64 for fingerprints)
+    uint32_t keylab_bytes = 0;  // 0: gather min-state labels; 1/2/4: dense block ids of that width
+};
+PassPlan plan_pass(uint32_t n, uint32_t k, uint32_t B, uint64_t m, uint32_t collisions, bool force_exact);
+
+// Sharded sortPR primitives (refine_sort.cu; driven by sharded.py).
+// counters: device uint32[4] = {runs, active blocks, active states, collision}.
+struct ShardInit {
+    uint32_t num_blocks, active_blocks;
+    uint64_t active_states;
+};
+ShardInit shard_init(Ctx* ctx, const DevDfa& d, uint32_t lo, uint32_t hi, uint32_t* lab, uint8_t* act,
+                     cudaStream_t s);
+void shard_keylab(Ctx* ctx, const uint32_t* lab, uint32_t n, const PassPlan& plan, void* out, uint32_t* scratch,
+                  cudaStream_t s);
+void shard_table_signature(Ctx* ctx, const DevDfa& d, const void* keylab, const PassPlan& plan, const uint32_t* list,
+                           uint64_t m, uint32_t* keys32, uint32_t* tmin, uint32_t* tcnt, cudaStream_t s);
+void shard_table_apply(Ctx* ctx, const uint32_t* list, const uint32_t* keys32, uint64_t m, const uint32_t* tmin,
+                       const uint32_t* tcnt, uint32_t* lab, uint8_t* act, uint32_t* counters, cudaStream_t s);
+void shard_sig_partition(Ctx* ctx, const DevDfa& d, const void* keylab, const PassPlan& plan, uint64_t salt,
+                         const uint32_t* list, uint64_t m, uint32_t world, uint4* send, uint32_t* send_counts,
+                         cudaStream_t s);
+void shard_group(Ctx* ctx, const DevDfa& d, const uint32_t* lab, const PassPlan& plan, const uint4* recv,
+                 uint64_t count, uint32_t* results, uint32_t* counters, cudaStream_t s);
+void shard_apply(Ctx* ctx, const uint4* send, const uint32_t* results, uint64_t count, uint32_t* lab, uint8_t* act,
+                 cudaStream_t s);
+void shard_compact(Ctx* ctx, const uint8_t* act, uint32_t lo, uint32_t hi, uint32_t* list, uint32_t* count_dev,
+                   cudaStream_t s);
+
 // All block_out arrays are device arrays of n entries, canonical numbering.
 RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uint32_t* block_out, cudaStream_t s);
 RefineResult naive_pr_device(Ctx* ctx, const DevDfa& d, int policy, uint64_t seed, uint32_t* block_out,

@@ -250,6 +250,7 @@ __global__ void __launch_bounds__(kThreads) table_apply_kernel(const uint32_t* _
                                                                const uint32_t* __restrict__ tmin,
                                                                const uint32_t* __restrict__ tcnt,
                                                                uint32_t* __restrict__ lab, uint8_t* __restrict__ keep,
+                                                               uint8_t* __restrict__ act,
                                                                IterCounters* __restrict__ ctr) {
     uint32_t heads = 0, ablk = 0, surv = 0;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
@@ -258,7 +259,8 @@ __global__ void __launch_bounds__(kThreads) table_apply_kernel(const uint32_t* _
         const uint32_t rep = tmin[key];
         const bool multi = tcnt[key] >= 2;
         lab[q] = rep;
-        keep[i] = multi;
+        if (keep) keep[i] = multi;
+        if (act) act[q] = multi;
         heads += rep == q;
         ablk += (rep == q) && multi;
         surv += multi;
@@ -273,6 +275,8 @@ constexpr int kGrpItems = 8;
 constexpr uint32_t kGrpCap = kGrpThreads * kGrpItems;  // bucket capacity (slots per bucket)
 constexpr uint32_t kGrpSlots = 2 * kGrpCap;            // shared hash table (load <= 1/2)
 constexpr unsigned long long kEmptyKey = ~0ull;         // a real ~0 key takes the extra slot
+constexpr uint32_t kBucketShift = 20;                   // bucket = hkey bits [20, 20 + D): slots use the low
+                                                        // bits, the sharded engine's owner rank the top 32
 
 __device__ __forceinline__ bool same_tuple(uint32_t q, uint32_t r, const uint32_t* __restrict__ delta, uint32_t n,
                                            uint32_t k, const uint32_t* __restrict__ lab) {
@@ -286,11 +290,42 @@ __device__ __forceinline__ bool same_tuple(uint32_t q, uint32_t r, const uint32_
 
 // Bucket entries are 16 bytes {hkey lo, hkey hi, state, 0}: one vector
 // store per append (a scattered 8 + 4 byte pair costs two L1 wavefronts).
-__device__ __forceinline__ void st_entry(uint4* p, unsigned long long hk, uint32_t q) {
-    *p = make_uint4((uint32_t)hk, (uint32_t)(hk >> 32), q, 0u);
+__device__ __forceinline__ void st_entry(uint4* p, unsigned long long hk, uint32_t q, uint32_t idx) {
+    *p = make_uint4((uint32_t)hk, (uint32_t)(hk >> 32), q, idx);
 }
 __device__ __forceinline__ unsigned long long entry_key(const uint4& e) {
     return ((unsigned long long)e.y << 32) | e.x;
+}
+
+// Appends {hk, q, idx} to bucket (hk >> kBucketShift) & (nb - 1): lanes of a
+// warp hitting the same bucket share one cursor atomic.  Past the bucket's
+// kGrpCap slots the entry goes to the overflow region at nb * kGrpCap.
+__device__ __forceinline__ void bucket_append(unsigned long long hk, uint32_t q, uint32_t idx, uint32_t nb,
+                                              uint32_t* __restrict__ bcnt, uint4* __restrict__ bent,
+                                              IterCounters* __restrict__ ctr) {
+    const unsigned lane = threadIdx.x & 31u;
+    const unsigned lt = (1u << lane) - 1u;
+    const uint32_t b = (uint32_t)(hk >> kBucketShift) & (nb - 1);
+    const unsigned act = __activemask();
+    const unsigned peers = __match_any_sync(act, b);
+    const unsigned leader = __ffs(peers) - 1;
+    uint32_t base = 0;
+    if (lane == leader) base = atomicAdd(&bcnt[b], (uint32_t)__popc(peers));
+    base = __shfl_sync(act, base, leader);
+    const uint32_t pos = base + (uint32_t)__popc(peers & lt);
+    uint64_t slot;
+    const bool over = pos >= kGrpCap;
+    const unsigned om = __ballot_sync(act, over);
+    if (over) {
+        const unsigned ol = __ffs(om) - 1;
+        uint32_t obase = 0;
+        if (lane == ol) obase = atomicAdd(&ctr->overflow, (uint32_t)__popc(om));
+        obase = __shfl_sync(om, obase, ol);
+        slot = (uint64_t)nb * kGrpCap + obase + (uint32_t)__popc(om & lt);
+    } else {
+        slot = (uint64_t)b * kGrpCap + pos;
+    }
+    st_entry(bent + slot, hk, q, idx);
 }
 
 // Signature + fused radix partition: (hkey, state) appended to bucket
@@ -299,37 +334,15 @@ __device__ __forceinline__ unsigned long long entry_key(const uint4& e) {
 template <typename LT>
 __global__ void __launch_bounds__(kThreads) sig_bucket_kernel(const uint32_t* __restrict__ list, uint64_t m,
                                                               const uint32_t* __restrict__ delta, uint32_t n,
-                                                              const LT* __restrict__ lab, SigParams p, uint32_t shift,
+                                                              const LT* __restrict__ lab, SigParams p,
                                                               uint32_t nb, uint32_t* __restrict__ bcnt,
                                                               uint4* __restrict__ bent,
                                                               IterCounters* __restrict__ ctr) {
-    const unsigned lane = threadIdx.x & 31u;
-    const unsigned lt = (1u << lane) - 1u;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t q = list ? list[i] : (uint32_t)i;
         const uint64_t key = tuple_key<LT>(q, (uint32_t)lab[q], delta, n, lab, p);
         const unsigned long long hk = p.kind == kKeyPacked ? mix64(key) : key;
-        const uint32_t b = (uint32_t)(hk >> shift);
-        const unsigned act = __activemask();
-        const unsigned peers = __match_any_sync(act, b);
-        const unsigned leader = __ffs(peers) - 1;
-        uint32_t base = 0;
-        if (lane == leader) base = atomicAdd(&bcnt[b], (uint32_t)__popc(peers));
-        base = __shfl_sync(act, base, leader);
-        const uint32_t pos = base + (uint32_t)__popc(peers & lt);
-        uint64_t slot;
-        const bool over = pos >= kGrpCap;
-        const unsigned om = __ballot_sync(act, over);
-        if (over) {
-            const unsigned ol = __ffs(om) - 1;
-            uint32_t obase = 0;
-            if (lane == ol) obase = atomicAdd(&ctr->overflow, (uint32_t)__popc(om));
-            obase = __shfl_sync(om, obase, ol);
-            slot = (uint64_t)nb * kGrpCap + obase + (uint32_t)__popc(om & lt);
-        } else {
-            slot = (uint64_t)b * kGrpCap + pos;
-        }
-        st_entry(bent + slot, hk, q);
+        bucket_append(hk, q, 0u, nb, bcnt, bent, ctr);
     }
 }
 
@@ -349,10 +362,14 @@ struct GroupOut {
     uint8_t* act;      // state_order: survivor flag per state
     uint32_t* rep_slot;
     uint8_t* keep_slot;
+    uint32_t* res;     // sharded engine: res[entry index] = rep | multi << 31
 };
 
-__device__ __forceinline__ void emit(const GroupOut& o, uint64_t slot, uint32_t q, uint32_t r, bool multi) {
-    if (o.direct) {
+__device__ __forceinline__ void emit(const GroupOut& o, uint64_t slot, uint32_t q, uint32_t r, bool multi,
+                                     uint32_t idx) {
+    if (o.res) {
+        o.res[idx] = r | (multi ? 0x80000000u : 0u);
+    } else if (o.direct) {
         o.lab[q] = r;
         if (o.state_order) o.act[q] = multi;
         else o.keep_slot[slot] = multi;
@@ -385,7 +402,7 @@ __global__ void __launch_bounds__(kGrpThreads) bucket_group_kernel(
         __syncthreads();
         const uint64_t s0 = (uint64_t)b * kGrpCap;
         unsigned long long hk[kGrpItems];
-        uint32_t q[kGrpItems], slot[kGrpItems];
+        uint32_t q[kGrpItems], slot[kGrpItems], ix[kGrpItems];
 #pragma unroll
         for (int j = 0; j < kGrpItems; ++j) {
             const uint32_t idx = j * kGrpThreads + tid;
@@ -393,6 +410,7 @@ __global__ void __launch_bounds__(kGrpThreads) bucket_group_kernel(
                 const uint4 e = __ldcs(bent + s0 + idx);
                 hk[j] = entry_key(e);
                 q[j] = e.z;
+                ix[j] = e.w;
             }
         }
 #pragma unroll
@@ -432,7 +450,7 @@ __global__ void __launch_bounds__(kGrpThreads) bucket_group_kernel(
                 ablk += head && multi;
                 surv += multi;
                 if (fingerprint && !head && !same_tuple(q[j], r, delta, n, k, lab_in)) clash = true;
-                emit(o, s0 + idx, q[j], r, multi);
+                emit(o, s0 + idx, q[j], r, multi, ix[j]);
             }
         }
         __syncthreads();
@@ -502,14 +520,15 @@ __global__ void __launch_bounds__(kThreads) ghash_out_kernel(
     for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
          e += (uint64_t)gridDim.x * blockDim.x) {
         if (!fallback_elem(e, bcnt, nb, ovf)) continue;
-        const uint32_t s = gslot[e], q = bent[e].z;
+        const uint4 ent = bent[e];
+        const uint32_t s = gslot[e], q = ent.z;
         const uint32_t r = grep[s];
         const bool multi = gmul[s] != 0, head = r == q;
         heads += head;
         ablk += head && multi;
         surv += multi;
         if (fingerprint && !head && !same_tuple(q, r, delta, n, k, lab_in)) clash = true;
-        emit(o, e, q, r, multi);
+        emit(o, e, q, r, multi, ent.w);
     }
     if (__syncthreads_or(clash) && threadIdx.x == 0) atomicOr(&ctr->collision, 1u);
     flush_counters<kThreads>(heads, ablk, surv, &ctr->runs, &ctr->active_blocks, &ctr->active_states);
@@ -564,12 +583,23 @@ __global__ void run_starts_kernel(const uint32_t* __restrict__ heads, const uint
     }
 }
 
-// The sort is stable and every list is increasing within a block, so a
-// run's first element is its minimum state.
+// run minimum (lists need not be increasing: bucket passes emit survivors
+// in bucket order); consecutive elements of one run elect first per warp
+__global__ void run_min_kernel(const uint32_t* __restrict__ heads, const uint32_t* __restrict__ pos,
+                               const uint32_t* __restrict__ vals, uint64_t m, uint32_t* __restrict__ rmin) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t r = pos[i] + heads[i] - 1;
+        const unsigned peers = __match_any_sync(__activemask(), r);
+        const uint32_t mq = __reduce_min_sync(peers, vals[i]);
+        if ((threadIdx.x & 31u) == (unsigned)(__ffs(peers) - 1)) atomicMin(&rmin[r], mq);
+    }
+}
+
 __global__ void __launch_bounds__(kThreads) run_apply_kernel(const uint32_t* __restrict__ heads,
                                                              const uint32_t* __restrict__ pos,
                                                              const uint32_t* __restrict__ vals, uint64_t m,
                                                              const uint32_t* __restrict__ run_start,
+                                                             const uint32_t* __restrict__ rmin,
                                                              uint32_t* __restrict__ lab, uint8_t* __restrict__ keep,
                                                              IterCounters* __restrict__ ctr) {
     uint32_t ablk = 0, surv = 0;
@@ -577,7 +607,7 @@ __global__ void __launch_bounds__(kThreads) run_apply_kernel(const uint32_t* __r
         const uint32_t r = pos[i] + heads[i] - 1;
         const uint32_t s = run_start[r], e = run_start[r + 1];
         const bool multi = (e - s) >= 2;
-        lab[vals[i]] = vals[s];
+        lab[vals[i]] = rmin[r];
         keep[i] = multi;
         ablk += multi && heads[i];
         surv += multi;
@@ -645,6 +675,45 @@ void init_leader_labels(Ctx* ctx, const DevDfa& d, const LeaderInfo& li, uint32_
     DK_LAUNCH(ctx, init_labels_kernel, grid_for(d.n), kThreads, 0, s, d.acc, d.n, li.min_acc, li.min_rej, lab);
 }
 
+// Key choice of one pass (shared by the single-GPU and the sharded engine):
+// min-state labels when they pack, dense block ids (in the narrowest type)
+// when only those pack or when they make the counting table possible on a
+// large pass -- the dense relabelling is O(n), so it is avoided on small
+// late passes -- else fingerprints (narrow dense gathers on large passes),
+// else (force_exact / three collisions in one pass) exact letter chunks.
+PassPlan plan_pass(uint32_t n, uint32_t k, uint32_t B, uint64_t m, uint32_t collisions, bool force_exact) {
+    PassPlan p;
+    const uint32_t label_bits = bits_for(n ? n - 1 : 0);
+    const uint32_t dense_bits = bits_for(B ? B - 1 : 0);
+    const uint64_t k1 = (uint64_t)k + 1;
+    const bool big_pass = m >= (uint64_t)n / 16;
+    auto narrow = [](uint32_t bits) { return bits <= 8 ? 1u : bits <= 16 ? 2u : 4u; };
+    if (k1 * label_bits <= kTableBits) {
+        p.strategy = kPlanTable;
+        p.field_bits = label_bits;
+    } else if (k1 * dense_bits <= kTableBits && big_pass) {
+        p.strategy = kPlanTable;
+        p.field_bits = dense_bits;
+        p.keylab_bytes = narrow(dense_bits);
+    } else if (k1 * label_bits <= 64) {
+        p.strategy = kPlanPacked;
+        p.field_bits = label_bits;
+    } else if (k1 * dense_bits <= 64) {
+        p.strategy = k1 * dense_bits <= kTableBits ? kPlanTable : kPlanPacked;
+        p.field_bits = dense_bits;
+        p.keylab_bytes = narrow(dense_bits);
+    } else if (!force_exact && collisions < 3) {
+        p.strategy = kPlanFingerprint;
+        if (dense_bits <= 16 && big_pass) p.keylab_bytes = narrow(dense_bits);
+    } else {
+        p.strategy = kPlanChunked;
+        p.field_bits = dense_bits;
+        p.keylab_bytes = 4;
+    }
+    p.key_bits = p.strategy == kPlanFingerprint ? 64u : (uint32_t)(k1 * p.field_bits);
+    return p;
+}
+
 RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uint32_t* block_out, cudaStream_t s) {
     RefineResult res;
     const uint32_t n = d.n, k = d.k;
@@ -681,13 +750,11 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
         list = list_buf;
     }
 
-    const uint32_t label_bits = bits_for(n - 1);
     uint64_t salt = 0x5eed5eed5eedull;
     const uint64_t fp_mask = o.fingerprint_bits >= 64 ? ~0ull : ((1ull << o.fingerprint_bits) - 1ull);
     uint32_t collisions_this_pass = 0;
 
-    auto dense_keylab = [&](uint32_t dense_bits) -> KeyLab {
-        const int bytes = dense_bits <= 8 ? 1 : dense_bits <= 16 ? 2 : 4;
+    auto dense_keylab = [&](int bytes) -> KeyLab {
         void* p;
         if (bytes == 1) {
             if (!w.dense8.get()) w.dense8.alloc(n, s);
@@ -705,28 +772,14 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
 
     while (m > 0) {
         ++res.passes;
-        const uint32_t dense_bits = bits_for(B ? B - 1 : 0);
-        bool fingerprint = false, chunked = false;
-        uint32_t field_bits = 0;
+        const PassPlan plan = plan_pass(n, k, B, m, collisions_this_pass, o.force_exact);
+        const bool fingerprint = plan.strategy == kPlanFingerprint, chunked = plan.strategy == kPlanChunked;
+        const uint32_t field_bits = plan.field_bits;
         KeyLab kl{w.lab.get(), 4};
-        if ((uint64_t)(k + 1) * label_bits <= 64 && (k + 1) * label_bits <= kTableBits) {
-            field_bits = label_bits;
-        } else if ((uint64_t)(k + 1) * dense_bits <= 64) {
-            field_bits = dense_bits;
-            kl = dense_keylab(dense_bits);
-        } else if ((uint64_t)(k + 1) * label_bits <= 64) {
-            field_bits = label_bits;
-        } else if (!o.force_exact && collisions_this_pass < 3) {
-            fingerprint = true;
-            if (dense_bits <= 16) kl = dense_keylab(dense_bits);  // narrower gathers
-        } else {
-            chunked = true;
-            field_bits = dense_bits;
-            kl = dense_keylab(32);
-        }
+        if (plan.keylab_bytes) kl = dense_keylab(plan.keylab_bytes);
         DK_CUDA(cudaMemsetAsync(dctr, 0, sizeof(IterCounters), s));
         const unsigned g = grid_for(m);
-        const uint32_t nbits = fingerprint ? 64u : (k + 1) * field_bits;
+        const uint32_t nbits = plan.key_bits;
         SigParams p{};
         p.kind = fingerprint ? kKeyFingerprint : kKeyPacked;
         p.a0 = 0;
@@ -739,7 +792,7 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
         uint32_t* dst = (list == list_buf) ? list_alt : list_buf;
         bool listed = false;  // survivors already compacted into dst
 
-        if (!chunked && nbits <= kTableBits && o.grouping != 1) {
+        if (plan.strategy == kPlanTable && o.grouping != 1) {
             // ---- table strategy
             const uint64_t tsize = 1ull << nbits;
             if (w.tmin.n < tsize) {
@@ -759,7 +812,7 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
                             w.tcnt.get());
             });
             DK_LAUNCH_B(ctx, (double)m * (9.0 + 2 * list_b), table_apply_kernel, g, kThreads, 0, s, list,
-                        w.heads.get(), m, w.tmin.get(), w.tcnt.get(), w.lab.get(), w.keep.get(), dctr);
+                        w.heads.get(), m, w.tmin.get(), w.tcnt.get(), w.lab.get(), w.keep.get(), nullptr, dctr);
             compact_flags(ctx, list, w.keep.get(), m, dst, &dctr->listed, s);
             listed = true;
             read_words(ctx, dctr, sizeof(c), &c, s);
@@ -797,10 +850,10 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
                 // algorithmic HBM bytes: delta rows (+ list), (hkey, state) out, the key-label array once
                 DK_LAUNCH_B(ctx, (double)m * (4.0 * k + 12.0 + list_b) + (double)kl.bytes * n, sig_bucket_kernel,
                             grid_for(m, kThreads, (unsigned)ctx->num_sms * 8u), kThreads, 0, s, list, m, d.delta, n,
-                            lab, p, 64u - D, nb, w.bcnt.get(), w.bent.get(), dctr);
+                            lab, p, nb, w.bcnt.get(), w.bent.get(), dctr);
             });
             GroupOut go{direct ? 1 : 0, state_order ? 1 : 0, out_lab, w.act.get(),
-                        direct ? nullptr : w.rep_slot.get(), w.keep_slot.get()};
+                        direct ? nullptr : w.rep_slot.get(), w.keep_slot.get(), nullptr};
             const unsigned gg = (unsigned)std::min<uint64_t>(nb, (uint64_t)ctx->num_sms * 4);
             // algorithmic HBM bytes: (hkey, state) in, label + survivor flag out
             DK_LAUNCH_B(ctx, (double)m * (16.0 + 4.0 + 1.0 + (direct ? 0.0 : 4.0)), bucket_group_kernel, gg,
@@ -932,8 +985,10 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
             DK_LAUNCH(ctx, run_heads_kernel, g, kThreads, 0, s, skeys, m, w.heads.get());
             exclusive_scan_u32(ctx, w.heads.get(), w.pos.get(), m, &dctr->runs, s);
             DK_LAUNCH(ctx, run_starts_kernel, g, kThreads, 0, s, w.heads.get(), w.pos.get(), m, w.run_start.get());
+            DK_CUDA(cudaMemsetAsync(w.scratch.get(), 0xff, m * sizeof(uint32_t), s));
+            DK_LAUNCH(ctx, run_min_kernel, g, kThreads, 0, s, w.heads.get(), w.pos.get(), svals, m, w.scratch.get());
             DK_LAUNCH_B(ctx, 25.0 * m, run_apply_kernel, g, kThreads, 0, s, w.heads.get(), w.pos.get(), svals, m,
-                        w.run_start.get(), w.lab.get(), w.keep.get(), dctr);
+                        w.run_start.get(), w.scratch.get(), w.lab.get(), w.keep.get(), dctr);
             // surviving active states in sorted order (runs grouped, increasing
             // state order inside each run)
             compact_flags(ctx, svals, w.keep.get(), m, dst, &dctr->listed, s);
@@ -955,6 +1010,268 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
     }
     res.num_blocks = canonical_from_min_labels(ctx, w.lab.get(), n, block_out, w.scratch.get(), s);
     return res;
+}
+
+// ==========================================================================
+// Sharded sortPR primitives (paper_2508_20735_b200/sharded.py drives them).
+//
+// States are sharded in contiguous ranges; delta and the block-label array
+// are replicated (delta read-only, labels allgathered after every pass).  A
+// pass on rank r: keys of its active states are partitioned by owner rank
+// (top 32 hash bits, multiply-shift), exchanged with one all-to-all, grouped
+// at the owner in shared-memory buckets (the owner can verify fingerprint
+// tuples of any state: delta and labels are replicated), and the per-entry
+// results (new label | survivor bit) travel back by the reverse all-to-all.
+// Counting-table passes allreduce the (min, count) table instead.
+// ==========================================================================
+
+namespace {
+
+constexpr int kPartThreads = 256;
+constexpr int kPartItems = 16;
+constexpr int kMaxWorld = 64;
+
+__device__ __forceinline__ uint32_t owner_of(unsigned long long hk, uint32_t world) {
+    return (uint32_t)(((hk >> 32) * (unsigned long long)world) >> 32);
+}
+
+// entries {hk, state, dest} in list order + per-destination counts
+template <typename LT>
+__global__ void __launch_bounds__(kThreads) sig_entries_kernel(const uint32_t* __restrict__ list, uint64_t m,
+                                                               const uint32_t* __restrict__ delta, uint32_t n,
+                                                               const LT* __restrict__ lab, SigParams p,
+                                                               uint32_t world, uint4* __restrict__ tmp,
+                                                               uint32_t* __restrict__ counts) {
+    __shared__ uint32_t cnt[kMaxWorld];
+    for (uint32_t d = threadIdx.x; d < world; d += blockDim.x) cnt[d] = 0;
+    __syncthreads();
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t q = list ? list[i] : (uint32_t)i;
+        const uint64_t key = tuple_key<LT>(q, (uint32_t)lab[q], delta, n, lab, p);
+        const unsigned long long hk = p.kind == kKeyPacked ? mix64(key) : key;
+        const uint32_t d = owner_of(hk, world);
+        tmp[i] = make_uint4((uint32_t)hk, (uint32_t)(hk >> 32), q, d);
+        const unsigned peers = __match_any_sync(__activemask(), d);
+        if ((threadIdx.x & 31u) == (unsigned)(__ffs(peers) - 1)) atomicAdd(&cnt[d], (uint32_t)__popc(peers));
+    }
+    __syncthreads();
+    for (uint32_t d = threadIdx.x; d < world; d += blockDim.x)
+        if (cnt[d]) atomicAdd(&counts[d], cnt[d]);
+}
+
+__global__ void dest_offsets_kernel(const uint32_t* __restrict__ counts, uint32_t world, uint32_t* __restrict__ cur) {
+    if (threadIdx.x == 0) {
+        uint32_t o = 0;
+        for (uint32_t d = 0; d < world; ++d) {
+            cur[d] = o;
+            o += counts[d];
+        }
+    }
+}
+
+// tile of 4096 entries -> destination-contiguous send buffer; one global
+// cursor atomic per (CTA, destination)
+__global__ void __launch_bounds__(kPartThreads) partition_kernel(const uint4* __restrict__ tmp, uint64_t m,
+                                                                 uint32_t world, uint32_t* __restrict__ cur,
+                                                                 uint4* __restrict__ send) {
+    __shared__ uint32_t cnt[kMaxWorld], gbase[kMaxWorld];
+    const unsigned lane = threadIdx.x & 31u, lt = (1u << lane) - 1u;
+    for (uint32_t d = threadIdx.x; d < world; d += blockDim.x) cnt[d] = 0;
+    __syncthreads();
+    const uint64_t base = (uint64_t)blockIdx.x * kPartThreads * kPartItems;
+    uint4 e[kPartItems];
+    uint32_t pos[kPartItems];
+#pragma unroll
+    for (int j = 0; j < kPartItems; ++j) {
+        const uint64_t i = base + (uint64_t)j * kPartThreads + threadIdx.x;
+        if (i < m) e[j] = __ldcs(tmp + i);
+    }
+#pragma unroll
+    for (int j = 0; j < kPartItems; ++j) {
+        const uint64_t i = base + (uint64_t)j * kPartThreads + threadIdx.x;
+        const bool ok = i < m;
+        const unsigned act = __ballot_sync(0xffffffffu, ok);
+        if (ok) {
+            const unsigned peers = __match_any_sync(act, e[j].w);
+            const unsigned leader = __ffs(peers) - 1;
+            uint32_t b = 0;
+            if (lane == leader) b = atomicAdd(&cnt[e[j].w], (uint32_t)__popc(peers));
+            b = __shfl_sync(act, b, leader);
+            pos[j] = b + (uint32_t)__popc(peers & lt);
+        }
+    }
+    __syncthreads();
+    for (uint32_t d = threadIdx.x; d < world; d += blockDim.x) gbase[d] = cnt[d] ? atomicAdd(&cur[d], cnt[d]) : 0u;
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kPartItems; ++j) {
+        const uint64_t i = base + (uint64_t)j * kPartThreads + threadIdx.x;
+        if (i < m) send[gbase[e[j].w] + pos[j]] = make_uint4(e[j].x, e[j].y, e[j].z, 0u);
+    }
+}
+
+// received entries -> owner-side buckets; entry index kept in .w
+__global__ void entry_bucket_kernel(const uint4* __restrict__ recv, uint64_t count, uint32_t nb,
+                                    uint32_t* __restrict__ bcnt, uint4* __restrict__ bent,
+                                    IterCounters* __restrict__ ctr) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint4 e = __ldcs(recv + i);
+        bucket_append(entry_key(e), e.z, (uint32_t)i, nb, bcnt, bent, ctr);
+    }
+}
+
+__global__ void shard_apply_kernel(const uint4* __restrict__ send, const uint32_t* __restrict__ res, uint64_t count,
+                                   uint32_t* __restrict__ lab, uint8_t* __restrict__ act) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t q = send[i].z, r = res[i];
+        lab[q] = r & 0x7fffffffu;
+        act[q] = (uint8_t)(r >> 31);
+    }
+}
+
+__global__ void init_act_range_kernel(const uint8_t* __restrict__ acc, uint32_t lo, uint32_t hi, uint8_t keep_acc,
+                                      uint8_t keep_rej, uint8_t* __restrict__ act) {
+    for (uint32_t q = lo + blockIdx.x * blockDim.x + threadIdx.x; q < hi; q += gridDim.x * blockDim.x)
+        act[q] = acc[q] ? keep_acc : keep_rej;
+}
+
+SigParams sig_params(const PassPlan& plan, uint32_t k, uint64_t salt) {
+    SigParams p{};
+    p.kind = plan.strategy == kPlanFingerprint ? kKeyFingerprint : kKeyPacked;
+    p.a0 = 0;
+    p.a1 = k;
+    p.field_bits = plan.field_bits;
+    p.salt = salt;
+    p.fp_mask = ~0ull;
+    return p;
+}
+
+}  // namespace
+
+ShardInit shard_init(Ctx* ctx, const DevDfa& d, uint32_t lo, uint32_t hi, uint32_t* lab, uint8_t* act,
+                     cudaStream_t s) {
+    ShardInit r{};
+    if (d.n == 0) return r;
+    LeaderInfo li = leader_info(ctx, d, s);
+    init_leader_labels(ctx, d, li, lab, s);
+    r.num_blocks = (li.min_acc != kNone) + (li.min_rej != kNone);
+    r.active_blocks = (li.cnt_acc >= 2) + (li.cnt_rej >= 2);
+    r.active_states = (li.cnt_acc >= 2 ? li.cnt_acc : 0) + (li.cnt_rej >= 2 ? li.cnt_rej : 0);
+    if (hi > lo)
+        DK_LAUNCH(ctx, init_act_range_kernel, grid_for(hi - lo), kThreads, 0, s, d.acc, lo, hi,
+                  (uint8_t)(li.cnt_acc >= 2), (uint8_t)(li.cnt_rej >= 2), act);
+    return r;
+}
+
+void shard_keylab(Ctx* ctx, const uint32_t* lab, uint32_t n, const PassPlan& plan, void* out, uint32_t* scratch,
+                  cudaStream_t s) {
+    if (plan.keylab_bytes) dense_labels(ctx, lab, n, out, (int)plan.keylab_bytes, scratch, s);
+}
+
+void shard_table_signature(Ctx* ctx, const DevDfa& d, const void* keylab, const PassPlan& plan, const uint32_t* list,
+                           uint64_t m, uint32_t* keys32, uint32_t* tmin, uint32_t* tcnt, cudaStream_t s) {
+    const uint32_t nbits = plan.key_bits;
+    const uint64_t tsize = 1ull << nbits;
+    DK_CUDA(cudaMemsetAsync(tmin, 0xff, tsize * 4, s));
+    DK_CUDA(cudaMemsetAsync(tcnt, 0, tsize * 4, s));
+    if (m == 0) return;
+    const bool local = nbits <= kSmemTableBits;
+    const size_t smem = local ? (size_t)(2u << nbits) * 4 : 0;
+    const int smem_table = (int)(2u << kSmemTableBits) * 4;
+    const unsigned tg = (unsigned)std::min<uint64_t>((m + 511) / 512, (uint64_t)ctx->num_sms * 3);
+    const SigParams p = sig_params(plan, d.k, 0);
+    with_lab_type(KeyLab{keylab, plan.keylab_bytes ? (int)plan.keylab_bytes : 4}, [&](auto lab) {
+        using LT = std::remove_const_t<std::remove_pointer_t<decltype(lab)>>;
+        DK_CUDA(cudaFuncSetAttribute(sig_table_kernel<LT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_table));
+        DK_LAUNCH_B(ctx, (double)m * (8.0 + 4.0 * d.k), sig_table_kernel<LT>, tg, 512, smem, s, list, m, d.delta,
+                    d.n, lab, p, nbits, keys32, tmin, tcnt);
+    });
+}
+
+void shard_table_apply(Ctx* ctx, const uint32_t* list, const uint32_t* keys32, uint64_t m, const uint32_t* tmin,
+                       const uint32_t* tcnt, uint32_t* lab, uint8_t* act, uint32_t* counters, cudaStream_t s) {
+    DK_CUDA(cudaMemsetAsync(counters, 0, 4 * sizeof(uint32_t), s));
+    if (m == 0) return;
+    DK_LAUNCH_B(ctx, (double)m * 13.0, table_apply_kernel, grid_for(m), kThreads, 0, s, list, keys32, m, tmin, tcnt,
+                lab, nullptr, act, reinterpret_cast<IterCounters*>(counters));
+}
+
+void shard_sig_partition(Ctx* ctx, const DevDfa& d, const void* keylab, const PassPlan& plan, uint64_t salt,
+                         const uint32_t* list, uint64_t m, uint32_t world, uint4* send, uint32_t* send_counts,
+                         cudaStream_t s) {
+    if (world == 0 || world > (uint32_t)kMaxWorld) throw Error(DFAKIT_E_INVALID, "shard: world size out of range");
+    DK_CUDA(cudaMemsetAsync(send_counts, 0, world * 4, s));
+    if (m == 0) return;
+    DBuf<uint4> tmp(m, s);
+    DBuf<uint32_t> cur(world, s);
+    const SigParams p = sig_params(plan, d.k, salt);
+    with_lab_type(KeyLab{keylab, plan.keylab_bytes ? (int)plan.keylab_bytes : 4}, [&](auto lab) {
+        DK_LAUNCH_B(ctx, (double)m * (4.0 * d.k + 20.0), sig_entries_kernel, grid_for(m, kThreads,
+                    (unsigned)ctx->num_sms * 8u), kThreads, 0, s, list, m, d.delta, d.n, lab, p, world, tmp.get(),
+                    send_counts);
+    });
+    DK_LAUNCH(ctx, dest_offsets_kernel, 1, 32, 0, s, send_counts, world, cur.get());
+    const uint64_t tiles = (m + kPartThreads * kPartItems - 1) / (kPartThreads * kPartItems);
+    DK_LAUNCH_B(ctx, 32.0 * m, partition_kernel, (unsigned)tiles, kPartThreads, 0, s, tmp.get(), m, world, cur.get(),
+                send);
+}
+
+void shard_group(Ctx* ctx, const DevDfa& d, const uint32_t* lab, const PassPlan& plan, const uint4* recv,
+                 uint64_t count, uint32_t* results, uint32_t* counters, cudaStream_t s) {
+    IterCounters* dctr = reinterpret_cast<IterCounters*>(ctx->dmailbox) + 4;
+    DK_CUDA(cudaMemsetAsync(dctr, 0, sizeof(IterCounters), s));
+    if (count) {
+        uint32_t D = 1;
+        while (D < 24 && ((uint64_t)1 << D) * (kGrpCap * 3 / 4) < count) ++D;
+        const uint32_t nb = 1u << D;
+        const uint64_t bspace = (uint64_t)nb * kGrpCap, espace = bspace + count;
+        DBuf<uint32_t> bcnt(nb, s);
+        DBuf<uint4> bent(espace, s);
+        DK_CUDA(cudaMemsetAsync(bcnt.get(), 0, (size_t)nb * 4, s));
+        DK_LAUNCH_B(ctx, 32.0 * count, entry_bucket_kernel, grid_for(count), kThreads, 0, s, recv, count, nb,
+                    bcnt.get(), bent.get(), dctr);
+        const int fp = plan.strategy == kPlanFingerprint ? 1 : 0;
+        GroupOut go{0, 0, nullptr, nullptr, nullptr, nullptr, results};
+        DK_CUDA(cudaFuncSetAttribute(bucket_group_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sizeof(GroupSmem)));
+        const unsigned gg = (unsigned)std::min<uint64_t>(nb, (uint64_t)ctx->num_sms * 4);
+        DK_LAUNCH_B(ctx, 20.0 * count, bucket_group_kernel, gg, kGrpThreads, sizeof(GroupSmem), s, bcnt.get(), nb,
+                    bent.get(), fp, d.delta, d.n, d.k, lab, go, dctr);
+        IterCounters c{};
+        read_words(ctx, dctr, sizeof(c), &c, s);
+        if (c.overflow) {
+            uint64_t T = 2;
+            while (T < 2 * count) T <<= 1;
+            DBuf<unsigned long long> gkey(T + 1, s);
+            DBuf<uint32_t> grep(T + 1, s), gslot(espace, s);
+            DBuf<uint8_t> gmul(T + 1, s);
+            DK_CUDA(cudaMemsetAsync(gkey.get(), 0xff, (T + 1) * 8, s));
+            DK_CUDA(cudaMemsetAsync(grep.get(), 0xff, (T + 1) * 4, s));
+            DK_CUDA(cudaMemsetAsync(gmul.get(), 0, T + 1, s));
+            const unsigned eg = grid_for(bspace + c.overflow);
+            DK_LAUNCH(ctx, ghash_insert_kernel, eg, kThreads, 0, s, bcnt.get(), nb, c.overflow, bent.get(), T,
+                      gkey.get(), grep.get(), gslot.get());
+            DK_LAUNCH(ctx, ghash_multi_kernel, eg, kThreads, 0, s, bcnt.get(), nb, c.overflow, bent.get(), grep.get(),
+                      gslot.get(), gmul.get());
+            DK_LAUNCH(ctx, ghash_out_kernel, eg, kThreads, 0, s, bcnt.get(), nb, c.overflow, bent.get(), grep.get(),
+                      gslot.get(), gmul.get(), fp, d.delta, d.n, d.k, lab, go, dctr);
+        }
+    }
+    DK_CUDA(cudaMemcpyAsync(counters, dctr, 4 * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+}
+
+void shard_apply(Ctx* ctx, const uint4* send, const uint32_t* results, uint64_t count, uint32_t* lab, uint8_t* act,
+                 cudaStream_t s) {
+    if (count)
+        DK_LAUNCH_B(ctx, 25.0 * count, shard_apply_kernel, grid_for(count), kThreads, 0, s, send, results, count, lab,
+                    act);
+}
+
+void shard_compact(Ctx* ctx, const uint8_t* act, uint32_t lo, uint32_t hi, uint32_t* list, uint32_t* count_dev,
+                   cudaStream_t s) {
+    compact_flags(ctx, nullptr, act + lo, hi > lo ? hi - lo : 0, list, count_dev, s, lo);
 }
 
 }  // namespace dk

@@ -1,0 +1,123 @@
+"""Sharded sort_pr on the GPU: the sm_100a shard primitives (CudaShardOps,
+C ABI) under the sharded driver, against the oracle -- identical canonical
+partition and refining-pass count.  World size 1 runs over NCCL; world size
+2 runs two ranks on the one available GPU over gloo with host-staged
+collectives (the NCCL path is the same driver with device tensors)."""
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+
+CASES = [
+    ("random", 300, 2, 0.5, 11),
+    ("random", 5000, 3, 0.5, 12),
+    ("random", 4000, 6, 0.9, 13),
+    ("random", 20000, 10, 0.5, 14),
+    ("copies", 400, 8, 0.5, 15),
+    ("family", 7, 0, 0.0, 0),
+    ("family", 12, 0, 0.0, 1),
+    ("synth", 1_000_000, 10, 0.0, 3),
+]
+
+
+def make_case(case):
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle
+    o = pyoracle.COracle()
+    kind, n, k, frac, seed = case
+    if kind == "random":
+        d, a, _ = o.gen_random(n, k, frac, seed)
+    elif kind == "synth":
+        d, a, _ = o.gen_synth(n, k, seed)
+    elif kind == "copies":
+        base, acc0, _ = o.gen_random(n, k, frac, seed)
+        c = 30
+        d = np.empty((k, n * c), np.uint32)
+        for j in range(c):
+            d[:, j * n:(j + 1) * n] = base + ((j + 1) % c) * n
+        a = np.tile(acc0, c)
+    else:
+        d, a, _ = o.gen_family("bitsplit" if seed == 0 else "fib", n)
+    return d, a, o.minimize("moore", d, a)
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def run_cases(comm, dk, sharded):
+    ctx = dk.Context(0)
+    out = []
+    for case in CASES:
+        d, a, want = make_case(case)
+        k, n = d.shape
+        delta = torch.from_numpy(np.ascontiguousarray(d).view(np.int32).reshape(-1)).cuda()
+        acc = torch.from_numpy(np.ascontiguousarray(a)).cuda()
+        ops = sharded.CudaShardOps(ctx, delta, acc, n, k)
+        blocks, rep = sharded.sort_pr_sharded(ops, comm, n, k)
+        got = blocks.cpu().numpy().view(np.uint32)
+        out.append((case, bool(np.array_equal(got, want.blocks)), rep.num_blocks == want.num_blocks,
+                    rep.refining_iterations, want.refine_iters, rep.table_passes, rep.passes))
+    return out
+
+
+def check(rows):
+    for case, same, nb, got, want, *_ in rows:
+        assert same and nb and got == want, (case, got, want)
+    assert any(tp > 0 for *_a, tp, p in rows) and any(p > tp for *_a, tp, p in rows)
+
+
+def test_sharded_world1_nccl(dk):
+    from paper_2508_20735_b200 import sharded
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = str(free_port())
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        check(run_cases(sharded.TorchComm(), dk, sharded))
+    finally:
+        dist.destroy_process_group()
+
+
+def worker(rank, world, port, q):
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        sys.path.insert(0, ROOT)
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        import paper_2508_20735_b200 as dk
+        from paper_2508_20735_b200 import sharded
+        q.put((rank, run_cases(sharded.TorchComm(stage_cpu=True), dk, sharded)))
+        dist.destroy_process_group()
+    except Exception:
+        import traceback
+        q.put((rank, "ERROR " + traceback.format_exc()))
+
+
+def test_sharded_world2_one_gpu(dk):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=900) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    for r in range(2):
+        assert not isinstance(res[r], str), res[r]
+        check(res[r])

@@ -41,7 +41,7 @@ def test_python_mirror_binds_every_export(dk):
 
 
 def test_abi_version(dk):
-    assert dk.lib.dfakit_abi_version() == 1
+    assert dk.lib.dfakit_abi_version() == 2
 
 
 def test_library_carries_sm100a_code(dk):
@@ -72,3 +72,19 @@ def test_dfa_validation_and_letter_mapping(dk):
     with pytest.raises(ValueError):
         dk._letter_mapping(a, dk.Dfa(np.zeros((3, 1), np.uint32), np.zeros(1, np.uint8), 0),
                            dk.ExploreOptions())
+
+
+def test_pass_planner_host_only(dk):
+    """dfakit_plan_pass needs no device: the key plan of the bench workload's
+    passes (10M states, |Sigma| = 10) and of the small-key regimes."""
+    from paper_2508_20735_b200.sharded import plan_pass, PLAN_TABLE, PLAN_PACKED, PLAN_FINGERPRINT
+    p = plan_pass(10_000_000, 10, 2, 10_000_000)
+    assert (p.strategy, p.field_bits, p.key_bits, p.keylab_bytes) == (PLAN_TABLE, 1, 11, 1)
+    p = plan_pass(10_000_000, 10, 2000, 10_000_000)
+    assert (p.strategy, p.key_bits, p.keylab_bytes) == (PLAN_FINGERPRINT, 64, 2)
+    p = plan_pass(10_000_000, 10, 2000, 1000)           # small late pass: no O(n) relabel
+    assert (p.strategy, p.keylab_bytes) == (PLAN_FINGERPRINT, 0)
+    p = plan_pass(1000, 1, 10, 1000)                    # min-state labels pack into 20 bits
+    assert (p.strategy, p.field_bits, p.keylab_bytes) == (PLAN_TABLE, 10, 0)
+    p = plan_pass(5000, 3, 100, 5000)                   # 52-bit packed keys
+    assert (p.strategy, p.key_bits) == (PLAN_PACKED, 52)
