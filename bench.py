@@ -8,13 +8,16 @@ Default workload (BASELINE.json configs[1]): 10M states x |Sigma| = 10 =
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
-N > 1 (torchrun): every rank minimises its own independent 100M-transition
-DFA (independent objects, no data-path collective; "scaling": "weak"); the
-step time is the max over ranks.
+N = 1: the single-GPU engine (dfakit_minimize_device).  N > 1 (torchrun, one
+rank per GPU, NCCL): the sharded engine (paper_2508_20735_b200/sharded.py)
+on ONE automaton of N x 10M states (weak scaling: 100M transitions per GPU;
+N = 8 is the 800M-transition neighbourhood of configs[4]); per pass the
+label slices are allgathered and the wide-key entries exchanged all-to-all
+over NVLink; the step time is the max over ranks.
 
 --impl reference times the reference's own CPU sort_pr (oracle/_ref, the
 unmodified reference sources compiled in place) on a bounded sample of the
-same workload, rank 0 only.
+same workload, one independent minimisation per host core, rank 0 only.
 """
 from __future__ import annotations
 
@@ -22,6 +25,7 @@ import argparse
 import ctypes as C
 import json
 import os
+import socket
 import sys
 import threading
 import time
@@ -41,7 +45,8 @@ def parse_args():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["b200", "reference"], default="b200")
-    p.add_argument("--states", type=int, default=10_000_000)
+    p.add_argument("--engine", choices=["auto", "single", "sharded"], default="auto")
+    p.add_argument("--states", type=int, default=10_000_000, help="states per GPU")
     p.add_argument("--alphabet", type=int, default=10)
     p.add_argument("--seed", type=int, default=1)
     p.add_argument("--no-extras", action="store_true", help="skip the secondary configs")
@@ -56,8 +61,9 @@ def dist_env():
     return rank, world, local
 
 
-def workload_name(n, k):
-    return f"sort_pr random DFA {n // 1_000_000}M states x |Sigma|={k} ({n * k // 1_000_000}M transitions)"
+def workload_name(n, k, world=1):
+    s = f"sort_pr random DFA {n / 1e6:g}M states x |Sigma|={k} ({n * k / 1e6:g}M transitions)"
+    return s + (f", sharded over {world} GPUs" if world > 1 else "")
 
 
 # --------------------------------------------------------------------------
@@ -125,18 +131,19 @@ def measured_peaks():
 
 
 def ncu_traffic(kernel: str):
-    """dram bytes per launch of `kernel` from the committed ncu --set full summary."""
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full summary."""
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(path) as f:
             j = json.load(f)
-        return j["kernels"][kernel]["dram_bytes_per_launch"]
+        k = j["kernels"][kernel]
+        return {"dram_bytes_per_launch": k["dram_bytes_per_launch"], "source": f"profiles/ncu_summary.json ({j['tag']})"}
     except Exception:
         return None
 
 
 # --------------------------------------------------------------------------
-# CPU baseline: the reference's own sort_pr (oracle/_ref) on a bounded sample
+# CPU side: the reference's own sort_pr (oracle/_ref) on bounded samples
 # --------------------------------------------------------------------------
 
 def reference_sample(n: int, k: int, seed: int):
@@ -144,13 +151,11 @@ def reference_sample(n: int, k: int, seed: int):
     import pyoracle
     try:
         lib = pyoracle.RefLib()
-        kind = "reference"
     except Exception:
         lib = pyoracle.COracle()
-        kind = "port"
     gen = pyoracle.COracle()
     d, a, _ = gen.gen_synth(n, k, seed)
-    return lib, kind, d, a
+    return lib, d, a
 
 
 def time_reference_once(lib, d, a):
@@ -158,44 +163,59 @@ def time_reference_once(lib, d, a):
     r = lib.minimize("sort", d, a, want_blocks=False) if lib.kind == "reference" else lib.minimize("sort", d, a)
     dt = time.perf_counter() - t0
     n, k = d.shape[1], d.shape[0]
-    return n * k * (r.refine_iters + 1) / dt, dt, r
+    return n * k * (r.refine_iters + 1), dt, r
 
 
 def cpu_baseline(k: int, seed: int, budget_s: float = 20.0):
+    """Single-threaded reference on one sample grown toward ~budget/6 s."""
     n = 250_000
-    lib, kind, d, a = reference_sample(n, k, seed)
-    v, dt, r = time_reference_once(lib, d, a)
-    # grow the sample toward ~budget/2 seconds of reference work
+    lib, d, a = reference_sample(n, k, seed)
+    work, dt, r = time_reference_once(lib, d, a)
     while dt < budget_s / 6 and n < 4_000_000:
         n *= 2
-        lib, kind, d, a = reference_sample(n, k, seed)
-        v, dt, r = time_reference_once(lib, d, a)
-    return {"value": v, "unit": UNIT, "cores": 1, "kind": kind,
+        lib, d, a = reference_sample(n, k, seed)
+        work, dt, r = time_reference_once(lib, d, a)
+    return {"value": work / dt, "unit": UNIT, "cores": 1, "kind": lib.kind,
             "sample": f"reference sort_pr on synth DFA {n} states x |Sigma|={k} (same generator), "
-                      f"{r.refine_iters + 1} passes, {dt:.2f} s, single-threaded (the reference is sequential)"}
+                      f"{r.refine_iters + 1} passes, {dt:.2f} s, one thread (the reference is sequential)"}
+
+
+def _ref_worker(args):
+    n, k, seed, reps = args
+    lib, d, a = reference_sample(n, k, seed)
+    out = []
+    for _ in range(reps):
+        out.append(time_reference_once(lib, d, a)[:2])
+    return lib.kind, out
 
 
 def run_reference_arm(args, rank, world):
+    """The reference sort_pr is sequential: every host core minimises its own
+    1M-state sample of the workload concurrently; value = all transitions
+    refined / wall time of the timed steps."""
     if rank != 0:
         return
+    import multiprocessing as mp
     k = args.alphabet
     n = min(args.states, 1_000_000)
-    lib, kind, d, a = reference_sample(n, k, args.seed)
-    for _ in range(args.warmup):
-        time_reference_once(lib, d, a)
-    vals, secs = [], 0.0
-    for _ in range(args.steps):
-        v, dt, r = time_reference_once(lib, d, a)
-        vals.append(v)
-        secs += dt
-    value = float(np.mean(vals))
+    cores = max(1, min(len(os.sched_getaffinity(0)), 64))
+    with mp.get_context("fork").Pool(cores) as pool:
+        pool.map(_ref_worker, [(n, k, args.seed + c, max(1, args.warmup)) for c in range(cores)])
+        t0 = time.perf_counter()
+        res = pool.map(_ref_worker, [(n, k, args.seed + c, args.steps) for c in range(cores)])
+        wall = time.perf_counter() - t0
+    kind = res[0][0]
+    work = sum(w for _, runs in res for w, _ in runs)
+    value = work / wall
+    passes = int(round(res[0][1][0][0] / (n * k)))
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1000 * secs / args.steps, "higher_is_better": True,
+            "warmup": args.warmup, "ms_per_step": 1000 * wall / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic", "impl": "reference",
-            "config": {"workload": workload_name(args.states, k), "sample_states": n, "alphabet": k,
-                       "passes": r.refine_iters + 1},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": kind,
-                             "sample": f"reference sort_pr on synth DFA {n} states x |Sigma|={k} per step"},
+            "config": {"workload": workload_name(args.states * max(1, args.gpus), k, args.gpus), "sample_states": n,
+                       "alphabet": k, "passes": passes, "cores": cores},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+                             "sample": f"reference sort_pr, one {n}-state x |Sigma|={k} synth DFA per core per step "
+                                       f"({cores} concurrent processes)"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -204,136 +224,208 @@ def run_reference_arm(args, rank, world):
 # B200 arm
 # --------------------------------------------------------------------------
 
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def profile_kernels(nat, ctx, run, steps):
+    """Live per-kernel profile (CUDA events around every library launch on
+    its stream) over `steps` repetitions of `run`."""
+    nat.check(nat.lib.dfakit_profile_begin(ctx.handle))
+    for _ in range(steps):
+        run()
+    buf = C.create_string_buffer(1 << 16)
+    nat.check(nat.lib.dfakit_profile_end(ctx.handle, buf, len(buf)))
+    kernels = json.loads(buf.value.decode())
+    kernels.sort(key=lambda x: -x["ms"])
+    return kernels
+
+
+def roofline_of(kernels, steps, gather_peak, n):
+    top = kernels[0]
+    peak, peak_src = measured_peaks()
+    achieved = top["bytes"] / (top["ms"] / 1000.0) / 1e9 if top["ms"] > 0 else 0.0
+    prof_ms = sum(x["ms"] for x in kernels)
+    g = [x for x in kernels if x.get("units")]
+    gather = None
+    if g and gather_peak:
+        gk = g[0]
+        rate = gk["units"] / (gk["ms"] / 1000.0)
+        gather = {"kernel": gk["name"], "achieved_gathers_per_s": rate, "peak_gathers_per_s": gather_peak,
+                  "frac": rate / gather_peak,
+                  "peak_source": f"dfakit_calibrate_gather: random 32-bit gathers from an {n}-entry table, "
+                                 "every SM busy, measured in this run",
+                  "all_gather_kernels": [{"name": x["name"], "gathers_per_s": x["units"] / (x["ms"] / 1000.0),
+                                          "frac": x["units"] / (x["ms"] / 1000.0) / gather_peak} for x in g]}
+    return {"bound": "hbm", "kernel": top["name"], "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": ncu_traffic(top["name"]),
+            "algorithmic_bytes_per_launch": top["bytes"] / max(top["launches"], 1),
+            "avg_launch_ms": top["ms"] / max(top["launches"], 1), "share_of_step": top["ms"] / prof_ms,
+            "peak_source": peak_src,
+            "binding_resource": "L1TEX/L2 line rate of the random block-label gathers (one 128-byte line per "
+                                "lane); see gather_roofline and profiles/",
+            "gather_roofline": gather,
+            "kernels": [{"name": x["name"], "ms_per_step": x["ms"] / steps, "launches_per_step": x["launches"] / steps,
+                         "GBps": (x["bytes"] / (x["ms"] / 1000.0) / 1e9) if x["ms"] > 0 and x["bytes"] else None}
+                        for x in kernels[:10]]}
+
+
 def run_b200(args, rank, world, local):
     import torch
     import paper_2508_20735_b200 as dk
     from paper_2508_20735_b200 import _native as nat
+    from paper_2508_20735_b200 import sharded
 
     torch.cuda.set_device(local)
-    if world > 1:
-        import torch.distributed as dist
+    engine = args.engine if args.engine != "auto" else ("single" if world == 1 else "sharded")
+    import torch.distributed as dist
+    if world > 1 or engine == "sharded":
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", str(free_port()))
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        use_dist = True
     else:
-        dist = None
+        use_dist = False
 
     def barrier():
-        if dist is not None:
+        if use_dist:
             dist.barrier()
 
     def max_over_ranks(x: float) -> float:
-        if dist is None:
+        if not use_dist:
             return x
         t = torch.tensor([x], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
     ctx = dk.Context(local)
-    stream = torch.cuda.ExternalStream(ctx.stream)
-    n, k = args.states, args.alphabet
+    lib_stream = torch.cuda.ExternalStream(ctx.stream)
+    k = args.alphabet
+    n = args.states * (world if engine == "sharded" else 1)
     delta = torch.empty(k * n, dtype=torch.int32, device="cuda")
     acc = torch.empty(n, dtype=torch.uint8, device="cuda")
     blocks = torch.empty(n, dtype=torch.int32, device="cuda")
-    nat.check(nat.lib.dfakit_gen_synth_device(ctx.handle, n, k, args.seed + rank, delta.data_ptr(), acc.data_ptr(),
-                                              ctx.stream))
+    # the same automaton on every rank (replicated input of the sharded engine);
+    # the single-GPU engine's replicas minimise their own seeds
+    gseed = args.seed if engine == "sharded" else args.seed + rank
+    nat.check(nat.lib.dfakit_gen_synth_device(ctx.handle, n, k, gseed, delta.data_ptr(), acc.data_ptr(), ctx.stream))
     torch.cuda.synchronize()
-    view = nat.CDfa(n, k, delta.data_ptr(), acc.data_ptr(), -1)
     opts = nat.COptions(0, 0, 0, 0, 0, 64, 0)
     rep = nat.CReport()
+    state = {}
 
-    def step():
-        nat.check(nat.lib.dfakit_minimize_device(ctx.handle, C.byref(view), int(dk.Algorithm.sort_pr), C.byref(opts),
-                                                 blocks.data_ptr(), C.byref(rep), ctx.stream))
+    if engine == "single":
+        view = nat.CDfa(n, k, delta.data_ptr(), acc.data_ptr(), -1)
+
+        def step():
+            nat.check(nat.lib.dfakit_minimize_device(ctx.handle, C.byref(view), int(dk.Algorithm.sort_pr),
+                                                     C.byref(opts), blocks.data_ptr(), C.byref(rep), ctx.stream))
+            state["passes"], state["iters"], state["blocks"] = int(rep.passes), int(rep.refining_iterations), \
+                int(rep.num_blocks)
+    else:
+        comm = sharded.TorchComm()
+        ops = sharded.CudaShardOps(ctx, delta, acc, n, k)
+
+        def step():
+            b, r = sharded.sort_pr_sharded(ops, comm, n, k)
+            state["passes"], state["iters"], state["blocks"] = r.passes, r.refining_iterations, r.num_blocks
+            state["exchanged"] = r.exchanged_entries
+            state["out"] = b
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     launches0 = ctx.kernel_launches
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    timing_stream = lib_stream if engine == "single" else torch.cuda.current_stream()
     barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clocks:
-        ev0.record(stream)
+        ev0.record(timing_stream)
         for _ in range(args.steps):
             step()
-        ev1.record(stream)
+        ev1.record(timing_stream)
         ev1.synchronize()
     torch.cuda.synchronize()
     barrier()
-    launches = ctx.kernel_launches - launches0
+    launches = (ctx.kernel_launches - launches0)
     ms_total = max_over_ranks(ev0.elapsed_time(ev1))
     ms_step = ms_total / args.steps
-    passes = int(rep.passes)
-    transitions = n * k * passes
-    value = transitions * world / (ms_step / 1000.0)
+    passes = state["passes"]
+    transitions = n * k * passes  # the whole automaton's transitions, every pass
+    value = transitions * (world if engine == "single" else 1) / (ms_step / 1000.0)
 
-    # live per-kernel profile (event-bracketed launches on the library stream)
-    # of the same steps, for the roofline of the dominant kernel
-    nat.check(nat.lib.dfakit_profile_begin(ctx.handle))
-    for _ in range(args.steps):
-        step()
-    buf = C.create_string_buffer(1 << 16)
-    nat.check(nat.lib.dfakit_profile_end(ctx.handle, buf, len(buf)))
-    kernels = json.loads(buf.value.decode())
-    kernels.sort(key=lambda x: -x["ms"])
-    top = kernels[0]
-    peak, peak_src = measured_peaks()
-    achieved = top["bytes"] / (top["ms"] / 1000.0) / 1e9 if top["ms"] > 0 else 0.0
-    prof_ms = sum(x["ms"] for x in kernels)
-    roofline = {"bound": "hbm", "kernel": top["name"], "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": ncu_traffic(top["name"]),
-                "algorithmic_bytes_per_launch": top["bytes"] / max(top["launches"], 1),
-                "avg_launch_ms": top["ms"] / max(top["launches"], 1), "share_of_step": top["ms"] / prof_ms,
-                "peak_source": peak_src,
-                "kernels": [{"name": x["name"], "ms_per_step": x["ms"] / args.steps,
-                             "launches_per_step": x["launches"] / args.steps,
-                             "GBps": (x["bytes"] / (x["ms"] / 1000.0) / 1e9) if x["ms"] > 0 and x["bytes"] else None}
-                            for x in kernels[:8]]}
+    # measured ceiling of the random label gathers, then the live per-kernel profile
+    gather_peak = C.c_double(0)
+    nat.check(nat.lib.dfakit_calibrate_gather(ctx.handle, n, 4, 200_000_000, C.byref(gather_peak)))
+    kernels = profile_kernels(nat, ctx, step, args.steps)
+    roofline = roofline_of(kernels, args.steps, gather_peak.value, n)
 
-    # end to end through the public host-buffer API (H2D + compute + D2H)
+    # end to end through the public API with host buffers (H2D + compute + D2H)
     h_delta = torch.empty(k * n, dtype=torch.int32, pin_memory=True)
     h_acc = torch.empty(n, dtype=torch.uint8, pin_memory=True)
     h_blocks = torch.empty(n, dtype=torch.int32, pin_memory=True)
     h_delta.copy_(delta.cpu())
     h_acc.copy_(acc.cpu())
-    hview = nat.CDfa(n, k, h_delta.data_ptr(), h_acc.data_ptr(), -1)
+    if engine == "single":
+        hview = nat.CDfa(n, k, h_delta.data_ptr(), h_acc.data_ptr(), -1)
 
-    def e2e_step():
-        nat.check(nat.lib.dfakit_minimize(ctx.handle, C.byref(hview), int(dk.Algorithm.sort_pr), C.byref(opts),
-                                          h_blocks.data_ptr(), C.byref(rep)))
-
+        def e2e_step():
+            nat.check(nat.lib.dfakit_minimize(ctx.handle, C.byref(hview), int(dk.Algorithm.sort_pr), C.byref(opts),
+                                              h_blocks.data_ptr(), C.byref(rep)))
+        h2d, d2h, api = 4 * k * n + n, 4 * n, "dfakit_minimize (host buffers, pinned)"
+    else:
+        def e2e_step():
+            delta.copy_(h_delta, non_blocking=True)
+            acc.copy_(h_acc, non_blocking=True)
+            step()
+            if rank == 0:
+                h_blocks.copy_(state["out"], non_blocking=True)
+            torch.cuda.synchronize()
+        h2d, d2h, api = 4 * k * n + n, 4 * n if rank == 0 else 0, "sharded.sort_pr_sharded (inputs copied from pinned host memory on every rank)"
     for _ in range(max(1, args.warmup)):
         e2e_step()
     barrier()
     t0 = time.perf_counter()
     for _ in range(args.steps):
         e2e_step()
+    torch.cuda.synchronize()
     e2e_s = max_over_ranks(time.perf_counter() - t0) / args.steps
-    e2e = {"value": transitions * world / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 4 * k * n + n,
-           "d2h_bytes_per_step": 4 * n, "ms_per_step": e2e_s * 1000.0,
-           "api": "dfakit_minimize (host buffers, pinned)"}
+    e2e_transitions = transitions * (world if engine == "single" else 1)
+    e2e = {"value": e2e_transitions / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+           "ms_per_step": e2e_s * 1000.0, "api": api}
 
+    cfg = {"workload": workload_name(n, k, world if engine == "sharded" else 1), "states": n, "alphabet": k,
+           "transitions": n * k, "algorithm": "sort_pr", "engine": engine, "passes": passes,
+           "refining_iterations": state["iters"], "num_blocks": state["blocks"], "wall_ms_to_minimal_dfa": ms_step,
+           "l2": f"inputs larger than L2 (delta {4 * k * n / 1e6:.0f} MB per rank > 126 MB L2)",
+           "parallelism": (f"sharded x{world} (NCCL all-to-all + label allgather per pass)" if engine == "sharded"
+                           else (f"replicas x{world}" if world > 1 else "single GPU"))}
+    if engine == "sharded":
+        cfg["entries_exchanged_per_step_rank0"] = state.get("exchanged", 0)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "config": {"workload": workload_name(n, k), "states": n, "alphabet": k, "transitions": n * k,
-                       "algorithm": "sort_pr", "passes": passes, "refining_iterations": int(rep.refining_iterations),
-                       "num_blocks": int(rep.num_blocks), "wall_ms_to_minimal_dfa": ms_step,
-                       "states_sorted_per_step": int(rep.states_sorted),
-                       "l2": "inputs larger than L2 (delta 400 MB per rank > 126 MB L2)",
-                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
-            "roofline": roofline, "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks.summary()}
+            "vs_baseline": None, "dtype": "u32", "data": "synthetic", "config": cfg, "roofline": roofline, "e2e": e2e,
+            "gpu_launches": int(launches), "clocks": clocks.summary()}
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(k, args.seed)
     if rank == 0 and world == 1 and not args.no_extras:
-        line["extra"] = extras(dk, nat, ctx, torch)
+        line["extra"] = extras(dk, nat, ctx, torch, sharded, args)
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if dist is not None:
+    if use_dist:
         dist.destroy_process_group()
 
 
-def extras(dk, nat, ctx, torch):
+def extras(dk, nat, ctx, torch, sharded, args):
     """Secondary BASELINE configs, device-resident, timed with CUDA events."""
     out = {}
 
@@ -346,6 +438,42 @@ def extras(dk, nat, ctx, torch):
         torch.cuda.synchronize()
         return (time.perf_counter() - t0) / reps, r
 
+    def minimize(view, algo, b, opts=None):
+        rep = nat.CReport()
+        opts = opts or nat.COptions(0, 0, 0, 1 << 40, 0, 64, 0)
+
+        def f():
+            nat.check(nat.lib.dfakit_minimize_device(ctx.handle, C.byref(view), int(dk.Algorithm[algo]),
+                                                     C.byref(opts), b.data_ptr(), C.byref(rep), ctx.stream))
+            return rep
+        return f
+
+    # configs[1] at full size: the literal Alg. 4 grouping (full LSD radix sort
+    # of the keys + adjacent difference + scan) beside the default
+    n, k = args.states, args.alphabet
+    d = torch.empty(k * n, dtype=torch.int32, device="cuda")
+    a = torch.empty(n, dtype=torch.uint8, device="cuda")
+    b = torch.empty(n, dtype=torch.int32, device="cuda")
+    nat.check(nat.lib.dfakit_gen_synth_device(ctx.handle, n, k, args.seed, d.data_ptr(), a.data_ptr(), ctx.stream))
+    view = nat.CDfa(n, k, d.data_ptr(), a.data_ptr(), -1)
+    s, r = timed(minimize(view, "sort_pr", b, nat.COptions(0, 0, 0, 0, 0, 64, 1)), 3)
+    out["sort_pr_radix_sort_grouping_10M_k10"] = {"ms": s * 1000, "passes": int(r.passes),
+                                                  "transitions_per_s": n * k * int(r.passes) / s}
+    # the sharded engine at world size 1 (its per-pass exchange logic, no peers)
+    import torch.distributed as dist
+    own_pg = not dist.is_initialized()
+    if own_pg:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ["MASTER_PORT"] = str(free_port())
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", ctx.device))
+    comm = sharded.TorchComm()
+    ops = sharded.CudaShardOps(ctx, d, a, n, k)
+    s, (bl, rr) = timed(lambda: sharded.sort_pr_sharded(ops, comm, n, k), 3)
+    out["sort_pr_sharded_engine_world1_10M_k10"] = {"ms": s * 1000, "passes": rr.passes,
+                                                    "transitions_per_s": n * k * rr.passes / s}
+    if own_pg:
+        dist.destroy_process_group()
+    del d, a, b
     # configs[1]: sort vs naive splitting (naive needs ~0.4 n passes on random
     # DFAs, so it is measured on a 100K-state instance)
     n, k = 100_000, 10
@@ -355,15 +483,7 @@ def extras(dk, nat, ctx, torch):
     nat.check(nat.lib.dfakit_gen_synth_device(ctx.handle, n, k, 7, d.data_ptr(), a.data_ptr(), ctx.stream))
     view = nat.CDfa(n, k, d.data_ptr(), a.data_ptr(), -1)
     for algo in ("sort_pr", "naive_pr", "naive_pr_fused"):
-        rep = nat.CReport()
-        opts = nat.COptions(0, 0, 0, 0, 0, 64, 0)
-
-        def f():
-            nat.check(nat.lib.dfakit_minimize_device(ctx.handle, C.byref(view), int(dk.Algorithm[algo]),
-                                                     C.byref(opts), b.data_ptr(), C.byref(rep), ctx.stream))
-            return rep
-
-        s, r = timed(f, 2)
+        s, r = timed(minimize(view, algo, b), 2)
         out[f"{algo}_100K_k10"] = {"ms": s * 1000, "passes": int(r.passes), "blocks": int(r.num_blocks),
                                    "transitions_per_s": n * k * int(r.passes) / s}
     # configs[2]: chain DFA (n-pass worst case) with partial transitive closure
@@ -373,17 +493,9 @@ def extras(dk, nat, ctx, torch):
     b = torch.empty(n, dtype=torch.int32, device="cuda")
     nat.check(nat.lib.dfakit_gen_chain_device(ctx.handle, n, d.data_ptr(), a.data_ptr(), ctx.stream))
     view = nat.CDfa(n, 1, d.data_ptr(), a.data_ptr(), 0)
-    rep = nat.CReport()
-    opts = nat.COptions(0, 0, 0, 1 << 40, 0, 64, 0)
-
-    def g():
-        nat.check(nat.lib.dfakit_minimize_device(ctx.handle, C.byref(view), int(dk.Algorithm.trans_pr),
-                                                 C.byref(opts), b.data_ptr(), C.byref(rep), ctx.stream))
-        return rep
-
-    s, r = timed(g, 2)
-    out["trans_pr_chain_10M"] = {"ms": s * 1000, "passes": int(r.passes), "closure_iterations": int(r.closure_iterations),
-                                 "blocks": int(r.num_blocks)}
+    s, r = timed(minimize(view, "trans_pr", b), 2)
+    out["trans_pr_chain_10M"] = {"ms": s * 1000, "passes": int(r.passes),
+                                 "closure_iterations": int(r.closure_iterations), "blocks": int(r.num_blocks)}
     # configs[3]: equivalence / inclusion of two 10M-state DFAs
     n, k = 10_000_000, 2
     d = torch.empty(k * n, dtype=torch.int32, device="cuda")
@@ -398,18 +510,18 @@ def extras(dk, nat, ctx, torch):
     va = nat.CDfa(n, k, d.data_ptr(), a.data_ptr(), 0)
     vb = nat.CDfa(n, k, d2.data_ptr(), a2.data_ptr(), int(init2.value))
     cex = np.zeros(1 << 16, np.uint32)
-    for name, fn in (("naive_hk", nat.lib.dfakit_explore_product_device),):
+    for mode, name in ((0, "equivalence"), (1, "inclusion")):
         res = nat.CProduct()
 
         def h():
-            nat.check(fn(ctx.handle, C.byref(va), C.byref(vb), 0, None, 1 << 32, cex.ctypes.data, len(cex),
-                         C.byref(res), ctx.stream))
+            nat.check(nat.lib.dfakit_explore_product_device(ctx.handle, C.byref(va), C.byref(vb), mode, None, 1 << 32,
+                                                            cex.ctypes.data, len(cex), C.byref(res), ctx.stream))
             return res
 
         s, r = timed(h, 1)
-        out[f"equiv_{name}_10M_equal"] = {"ms": s * 1000, "verdict": int(r.verdict),
-                                          "explored_pairs": int(r.explored_states), "levels": int(r.levels),
-                                          "pairs_per_s": int(r.explored_states) * k / s}
+        out[f"{name}_naive_hk_10M_equal"] = {"ms": s * 1000, "verdict": int(r.verdict),
+                                             "explored_pairs": int(r.explored_states), "levels": int(r.levels),
+                                             "pairs_per_s": int(r.explored_states) / s}
     res = nat.CProduct()
 
     def u():
@@ -419,11 +531,14 @@ def extras(dk, nat, ctx, torch):
 
     s, r = timed(u, 1)
     out["equiv_union_find_10M_equal"] = {"ms": s * 1000, "verdict": int(r.verdict), "unions": int(r.explored_states),
-                                         "levels": int(r.levels)}
+                                         "levels": int(r.levels), "pairs_per_s": int(r.explored_states) / s}
     return out
 
 
 def main():
+    # one JSON line on stdout: keep NCCL's version banner off it
+    if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
+        os.environ["NCCL_DEBUG"] = "WARN"
     args = parse_args()
     rank, world, local = dist_env()
     if args.impl == "reference":

@@ -259,6 +259,14 @@ dfakit_status dfakit_shard_compact(dfakit_ctx* ctx, const uint8_t* act, uint32_t
 dfakit_status dfakit_shard_canonical(dfakit_ctx* ctx, const uint32_t* lab, uint32_t n, uint32_t* block_of,
                                      uint32_t* num_blocks, void* stream);
 
+/* ---- calibration ---------------------------------------------------------------
+ * Measured ceiling of the signature kernels' random block-label gathers:
+ * independent random gathers of elem_bytes (1, 2, 4) from a table of
+ * table_words entries (L2-resident as far as it fits), every SM busy.
+ * *gathers_per_s receives the rate (used by bench.py as the gather roofline). */
+dfakit_status dfakit_calibrate_gather(dfakit_ctx* ctx, uint64_t table_words, uint32_t elem_bytes, uint64_t gathers,
+                                      double* gathers_per_s);
+
 /* ---- device generators (bench inputs built in HBM) --------------------------- */
 /* Synthetic random DFA, same formula as oracle/oracle.c or_gen_synth. */
 dfakit_status dfakit_gen_synth_device(dfakit_ctx* ctx, uint32_t n, uint32_t k, uint64_t seed, uint32_t* delta,

@@ -103,6 +103,7 @@ _sig = {
     "dfakit_gen_chain_device": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p]),
     "dfakit_permute_states_device": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint64, C.c_void_p,
                                                C.c_void_p, C.c_void_p, C.c_void_p, _P(C.c_uint32), C.c_void_p]),
+    "dfakit_calibrate_gather": (C.c_int, [_V, C.c_uint64, C.c_uint32, C.c_uint64, _P(C.c_double)]),
     # sharded sort_pr primitives (sharded.py)
     "dfakit_plan_pass": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint32, C.c_uint32,
                                    _P(CPassPlan)]),

@@ -452,6 +452,16 @@ dfakit_status dfakit_permute_states_device(dfakit_ctx* ctx, uint32_t n, uint32_t
     });
 }
 
+dfakit_status dfakit_calibrate_gather(dfakit_ctx* ctx, uint64_t table_words, uint32_t elem_bytes, uint64_t gathers,
+                                      double* gathers_per_s) {
+    return on_device(ctx, nullptr, [&](dk::Ctx* c, cudaStream_t s) {
+        if (elem_bytes != 1 && elem_bytes != 2 && elem_bytes != 4)
+            throw dk::Error(DFAKIT_E_INVALID, "calibrate_gather: elem_bytes must be 1, 2 or 4");
+        const double r = dk::calibrate_gather(c, table_words ? table_words : 1, elem_bytes, gathers, s, nullptr);
+        if (gathers_per_s) *gathers_per_s = r;
+    });
+}
+
 // ---- sharded sort_pr primitives ------------------------------------------------
 
 dfakit_status dfakit_plan_pass(uint32_t num_states, uint32_t alphabet_size, uint32_t num_blocks,

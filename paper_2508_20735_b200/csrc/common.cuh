@@ -37,9 +37,11 @@ struct Ctx;
 // bytes (the minimum the kernel must move), used for the roofline.
 void note_launch(Ctx* ctx);
 void prof_begin_launch(Ctx* ctx, cudaStream_t s);
-void prof_end_launch(Ctx* ctx, cudaStream_t s, const char* name, double bytes);
+void prof_end_launch(Ctx* ctx, cudaStream_t s, const char* name, double bytes, double units);
 
-#define DK_LAUNCH_B(ctx, bytes, kernel, grid, block, smem, stream, ...)                                  \
+// DK_LAUNCH_BU also annotates work units (the random label gathers of the
+// signature kernels), for the gather roofline.
+#define DK_LAUNCH_BU(ctx, bytes, units, kernel, grid, block, smem, stream, ...)                          \
     do {                                                                                                 \
         ::dk::prof_begin_launch(ctx, stream);                                                            \
         kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);                                      \
@@ -47,8 +49,11 @@ void prof_end_launch(Ctx* ctx, cudaStream_t s, const char* name, double bytes);
         cudaError_t e_ = cudaGetLastError();                                                             \
         if (e_ != cudaSuccess)                                                                           \
             throw ::dk::Error(DFAKIT_E_CUDA, std::string(#kernel) + " launch: " + cudaGetErrorString(e_)); \
-        ::dk::prof_end_launch(ctx, stream, #kernel, (double)(bytes));                                    \
+        ::dk::prof_end_launch(ctx, stream, #kernel, (double)(bytes), (double)(units));                   \
     } while (0)
+
+#define DK_LAUNCH_B(ctx, bytes, kernel, grid, block, smem, stream, ...) \
+    DK_LAUNCH_BU(ctx, bytes, 0, kernel, grid, block, smem, stream, __VA_ARGS__)
 
 #define DK_LAUNCH(ctx, kernel, grid, block, smem, stream, ...) \
     DK_LAUNCH_B(ctx, 0, kernel, grid, block, smem, stream, __VA_ARGS__)
@@ -56,7 +61,7 @@ void prof_end_launch(Ctx* ctx, cudaStream_t s, const char* name, double bytes);
 struct ProfRec {
     const char* name;
     cudaEvent_t a, b;
-    double bytes;
+    double bytes, units;
 };
 
 // Device context: one device, one stream, a stream-ordered pool, a pinned

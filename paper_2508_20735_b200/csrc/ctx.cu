@@ -15,12 +15,12 @@ void prof_begin_launch(Ctx* ctx, cudaStream_t s) {
     DK_CUDA(cudaEventRecord(ctx->pending, s));
 }
 
-void prof_end_launch(Ctx* ctx, cudaStream_t s, const char* name, double bytes) {
+void prof_end_launch(Ctx* ctx, cudaStream_t s, const char* name, double bytes, double units) {
     if (!ctx || !ctx->profiling || !ctx->pending) return;
     cudaEvent_t b;
     DK_CUDA(cudaEventCreate(&b));
     DK_CUDA(cudaEventRecord(b, s));
-    ctx->prof.push_back(ProfRec{name, ctx->pending, b, bytes});
+    ctx->prof.push_back(ProfRec{name, ctx->pending, b, bytes, units});
     ctx->pending = nullptr;
 }
 
@@ -29,7 +29,7 @@ std::string prof_collect(Ctx* ctx) {
     struct Agg {
         std::string name;
         uint64_t launches = 0;
-        double ms = 0, bytes = 0;
+        double ms = 0, bytes = 0, units = 0;
     };
     std::vector<Agg> aggs;
     for (auto& r : ctx->prof) {
@@ -46,6 +46,7 @@ std::string prof_collect(Ctx* ctx) {
         ++g->launches;
         g->ms += ms;
         g->bytes += r.bytes;
+        g->units += r.units;
         cudaEventDestroy(r.a);
         cudaEventDestroy(r.b);
     }
@@ -53,8 +54,9 @@ std::string prof_collect(Ctx* ctx) {
     std::string out = "[";
     char buf[512];
     for (size_t i = 0; i < aggs.size(); ++i) {
-        snprintf(buf, sizeof buf, "%s{\"name\":\"%s\",\"launches\":%llu,\"ms\":%.6f,\"bytes\":%.0f}", i ? "," : "",
-                 aggs[i].name.c_str(), (unsigned long long)aggs[i].launches, aggs[i].ms, aggs[i].bytes);
+        snprintf(buf, sizeof buf, "%s{\"name\":\"%s\",\"launches\":%llu,\"ms\":%.6f,\"bytes\":%.0f,\"units\":%.0f}",
+                 i ? "," : "", aggs[i].name.c_str(), (unsigned long long)aggs[i].launches, aggs[i].ms, aggs[i].bytes,
+                 aggs[i].units);
         out += buf;
     }
     return out + "]";

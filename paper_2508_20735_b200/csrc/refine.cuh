@@ -94,6 +94,10 @@ ProductOut explore_product_device(Ctx* ctx, const DevDfa& a, const DevDfa& b, in
                                   uint64_t max_visited, cudaStream_t s);
 ProductOut check_equiv_uf_device(Ctx* ctx, const DevDfa& a, const DevDfa& b, cudaStream_t s);
 
+// measured random-gather rate (gathers/s) from a table of table_words entries
+double calibrate_gather(Ctx* ctx, uint64_t table_words, uint32_t elem_bytes, uint64_t gathers, cudaStream_t s,
+                        float* ms_out);
+
 // generators
 void gen_synth_device(Ctx* ctx, uint32_t n, uint32_t k, uint64_t seed, uint32_t* delta, uint8_t* acc,
                       cudaStream_t s);

@@ -807,7 +807,8 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
             const unsigned tg = (unsigned)std::min<uint64_t>((m + 511) / 512, (uint64_t)ctx->num_sms * 3);
             with_lab_type(kl, [&](auto lab) {
                 // algorithmic HBM bytes: delta rows + key out (+ list), the key-label array once
-                DK_LAUNCH_B(ctx, (double)m * (4.0 + 4.0 * k + list_b) + (double)kl.bytes * n, sig_table_kernel, tg,
+                DK_LAUNCH_BU(ctx, (double)m * (4.0 + 4.0 * k + list_b) + (double)kl.bytes * n, (double)m * k,
+                             sig_table_kernel, tg,
                             512, smem, s, list, m, d.delta, n, lab, p, nbits, w.heads.get(), w.tmin.get(),
                             w.tcnt.get());
             });
@@ -848,7 +849,8 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
             if (!state_order) DK_CUDA(cudaMemsetAsync(w.keep_slot.get(), 0, espace, s));
             with_lab_type(kl, [&](auto lab) {
                 // algorithmic HBM bytes: delta rows (+ list), (hkey, state) out, the key-label array once
-                DK_LAUNCH_B(ctx, (double)m * (4.0 * k + 12.0 + list_b) + (double)kl.bytes * n, sig_bucket_kernel,
+                DK_LAUNCH_BU(ctx, (double)m * (4.0 * k + 16.0 + list_b) + (double)kl.bytes * n, (double)m * k,
+                             sig_bucket_kernel,
                             grid_for(m, kThreads, (unsigned)ctx->num_sms * 8u), kThreads, 0, s, list, m, d.delta, n,
                             lab, p, nb, w.bcnt.get(), w.bent.get(), dctr);
             });
@@ -926,8 +928,8 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
             uint32_t* svals = w.vals0.get();
             if (!chunked) {
                 with_lab_type(kl, [&](auto lab) {
-                    DK_LAUNCH_B(ctx, (double)m * (12.0 + 4.0 * k + list_b) + (double)kl.bytes * n,
-                                signature_kernel, g, kThreads, 0, s, list, m, d.delta, n, lab, nullptr, p,
+                    DK_LAUNCH_BU(ctx, (double)m * (12.0 + 4.0 * k + list_b) + (double)kl.bytes * n, (double)m * k,
+                                 signature_kernel, g, kThreads, 0, s, list, m, d.delta, n, lab, nullptr, p,
                                 w.keys0.get(), w.vals0.get());
                 });
                 if (radix_sort_pairs(ctx, rb, m, nbits, s)) {
@@ -1185,7 +1187,7 @@ void shard_table_signature(Ctx* ctx, const DevDfa& d, const void* keylab, const 
     with_lab_type(KeyLab{keylab, plan.keylab_bytes ? (int)plan.keylab_bytes : 4}, [&](auto lab) {
         using LT = std::remove_const_t<std::remove_pointer_t<decltype(lab)>>;
         DK_CUDA(cudaFuncSetAttribute(sig_table_kernel<LT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_table));
-        DK_LAUNCH_B(ctx, (double)m * (8.0 + 4.0 * d.k), sig_table_kernel<LT>, tg, 512, smem, s, list, m, d.delta,
+        DK_LAUNCH_BU(ctx, (double)m * (8.0 + 4.0 * d.k), (double)m * d.k, sig_table_kernel<LT>, tg, 512, smem, s, list, m, d.delta,
                     d.n, lab, p, nbits, keys32, tmin, tcnt);
     });
 }
@@ -1208,7 +1210,7 @@ void shard_sig_partition(Ctx* ctx, const DevDfa& d, const void* keylab, const Pa
     DBuf<uint32_t> cur(world, s);
     const SigParams p = sig_params(plan, d.k, salt);
     with_lab_type(KeyLab{keylab, plan.keylab_bytes ? (int)plan.keylab_bytes : 4}, [&](auto lab) {
-        DK_LAUNCH_B(ctx, (double)m * (4.0 * d.k + 20.0), sig_entries_kernel, grid_for(m, kThreads,
+        DK_LAUNCH_BU(ctx, (double)m * (4.0 * d.k + 20.0), (double)m * d.k, sig_entries_kernel, grid_for(m, kThreads,
                     (unsigned)ctx->num_sms * 8u), kThreads, 0, s, list, m, d.delta, d.n, lab, p, world, tmp.get(),
                     send_counts);
     });
