@@ -7,4 +7,4 @@ timeout -s KILL 300 python bench.py --steps 10 --warmup 3 --no-extras --no-cpu-b
 timeout -s KILL 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python tools/profile_step.py --reps 2 > gpurun_out/launches.log 2>&1
 K=${PROF_KERNELS:-'regex:sig_table_kernel|sig_bucket_kernel|bucket_group_kernel|table_apply_kernel|compact_flags_kernel|slot_apply_kernel'}
 timeout -s KILL 600 ncu --set full --clock-control none --import-source on -k "$K" -c 12 \
-  -o gpurun_out/prof_full -f python tools/profile_step.py --reps 2 > gpurun_out/prof_full.log 2>&1; echo "ncu rc=$?" >> gpurun_out/prof_full.log
+  -o /tmp/prof_full -f python tools/profile_step.py --reps 2 > gpurun_out/prof_full.log 2>&1; echo "ncu rc=$?" >> gpurun_out/prof_full.log; cp /tmp/prof_full.ncu-rep gpurun_out/

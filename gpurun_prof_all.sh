@@ -1,0 +1,22 @@
+#!/bin/bash
+# ncu --set full of every kernel family (1 GPU).  Reports stay in /tmp on the
+# box; their raw pages come back as CSV (the merge limit is 64 MiB).
+cd "$GRAFT_REPO_ROOT"
+mkdir -p gpurun_out /tmp/prof
+run() {  # name regex count skip workload-args...
+  local name=$1 re=$2 cnt=$3 skip=$4; shift 4
+  timeout -s KILL 600 ncu --set full --clock-control none --import-source on -k "regex:$re" -s $skip -c $cnt \
+    -o /tmp/prof/$name -f python tools/profile_step.py "$@" > gpurun_out/prof_$name.log 2>&1
+  echo "$name rc=$?" >> gpurun_out/prof_all.log
+  ncu -i /tmp/prof/$name.ncu-rep --page raw --csv > gpurun_out/prof_$name.csv 2>/dev/null
+}
+run sort 'sig_table_kernel|sig_bucket_kernel|bucket_group_kernel|table_apply_kernel|tile_apply_kernel|tile_count_kernel|dense2_kernel|relabel_kernel|leader_info_kernel|init_labels_kernel' 12 0 --workload synth --reps 1
+cp /tmp/prof/sort.ncu-rep gpurun_out/prof_sort.ncu-rep
+run radix 'signature_kernel|radix_hist_kernel|radix_scatter_kernel|run_heads_kernel|run_apply_kernel|run_min_kernel|verify_runs_kernel' 14 0 --workload radix --reps 1
+run naive 'elect_kernel|follow_kernel|fused_kernel' 6 0 --workload naive
+run chain 'double_kernel|elect_kernel|follow_kernel' 8 0 --workload chain --reps 1
+run equiv 'expand_kernel|winner_flags_kernel|emit_kernel|uf_expand_kernel|uf_seed_kernel|resolve_all_kernel|reinsert_kernel' 12 75 --workload equiv
+run sharded 'sig_entries_kernel|partition_kernel|entry_bucket_kernel|shard_apply_kernel|bucket_group_kernel' 10 0 --workload sharded --reps 1
+run trans 'trans_' 6 0 --workload trans --reps 1
+run calib 'gather_probe_kernel' 2 0 --workload calib
+du -sh gpurun_out >> gpurun_out/prof_all.log

@@ -200,9 +200,14 @@ __global__ void __launch_bounds__(1024) scan_counts_kernel(uint32_t* __restrict_
     if (threadIdx.x == 0 && total) *total = carry;
 }
 
+// Shared staging is skewed by one word per 32 (sk(p) = p + p / 32): the
+// coalesced fill writes element j*256 + t, the scan reads 16 consecutive
+// elements per thread -- unskewed that read is a 16-way bank conflict.
+__device__ __forceinline__ uint32_t sk(uint32_t p) { return p + (p >> 5); }
+
 struct CompactSmem {
-    uint32_t v[kCpTile];  // coalesced input staging, then the tile's selected values / positions
-    uint8_t f[kCpTile];
+    uint32_t v[kCpTile + kCpTile / 32];  // staged values, then selected values / positions
+    uint32_t f[kCpTile + kCpTile / 32];  // staged flags
     uint32_t ws[kCpThreads / 32];
 };
 
@@ -218,19 +223,20 @@ __global__ void __launch_bounds__(kCpThreads) tile_apply_kernel(const uint32_t* 
     const uint64_t base = (uint64_t)blockIdx.x * kCpTile;
 #pragma unroll
     for (int j = 0; j < kCpItems; ++j) {
-        const uint64_t i = base + (uint64_t)j * kCpThreads + tid;
+        const uint32_t p = j * kCpThreads + tid;
+        const uint64_t i = base + p;
         const bool ok = i < n;
-        sm.f[j * kCpThreads + tid] = ok ? (uint8_t)elem_flag<HEADS>(lab, flag, i) : 0;
-        if (!HEADS) sm.v[j * kCpThreads + tid] = ok ? (in ? __ldcs(in + i) : id_base + (uint32_t)i) : 0u;
+        sm.f[sk(p)] = ok ? elem_flag<HEADS>(lab, flag, i) : 0u;
+        if (!HEADS) sm.v[sk(p)] = ok ? (in ? __ldcs(in + i) : id_base + (uint32_t)i) : 0u;
     }
     __syncthreads();
     uint32_t c = 0;
-    uint8_t f[kCpItems];
+    uint32_t f[kCpItems];
     uint32_t v[kCpItems];
 #pragma unroll
     for (int j = 0; j < kCpItems; ++j) {
-        f[j] = sm.f[tid * kCpItems + j];
-        if (!HEADS) v[j] = sm.v[tid * kCpItems + j];
+        f[j] = sm.f[sk(tid * kCpItems + j)];
+        if (!HEADS) v[j] = sm.v[sk(tid * kCpItems + j)];
         c += f[j];
     }
     uint32_t agg;
@@ -240,21 +246,22 @@ __global__ void __launch_bounds__(kCpThreads) tile_apply_kernel(const uint32_t* 
         o += off;
 #pragma unroll
         for (int j = 0; j < kCpItems; ++j) {
-            sm.v[tid * kCpItems + j] = o;
+            sm.v[sk(tid * kCpItems + j)] = o;
             o += f[j];
         }
         __syncthreads();
 #pragma unroll
         for (int j = 0; j < kCpItems; ++j) {
-            const uint64_t i = base + (uint64_t)j * kCpThreads + tid;
-            if (i < n) out[i] = sm.v[j * kCpThreads + tid];
+            const uint32_t p = j * kCpThreads + tid;
+            const uint64_t i = base + p;
+            if (i < n) out[i] = sm.v[sk(p)];
         }
     } else {
 #pragma unroll
         for (int j = 0; j < kCpItems; ++j)
-            if (f[j]) sm.v[o++] = v[j];
+            if (f[j]) sm.v[sk(o++)] = v[j];
         __syncthreads();
-        for (uint32_t i = tid; i < agg; i += kCpThreads) out[(uint64_t)off + i] = sm.v[i];
+        for (uint32_t i = tid; i < agg; i += kCpThreads) out[(uint64_t)off + i] = sm.v[sk(i)];
     }
 }
 

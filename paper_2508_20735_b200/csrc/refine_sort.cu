@@ -251,6 +251,9 @@ __global__ void __launch_bounds__(kThreads) table_apply_kernel(const uint32_t* _
                                                                const uint32_t* __restrict__ tcnt,
                                                                uint32_t* __restrict__ lab, uint8_t* __restrict__ keep,
                                                                uint8_t* __restrict__ act,
+                                                               const uint32_t* __restrict__ rank,
+                                                               uint16_t* __restrict__ next16,
+                                                               uint32_t* __restrict__ next32,
                                                                IterCounters* __restrict__ ctr) {
     uint32_t heads = 0, ablk = 0, surv = 0;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
@@ -259,6 +262,8 @@ __global__ void __launch_bounds__(kThreads) table_apply_kernel(const uint32_t* _
         const uint32_t rep = tmin[key];
         const bool multi = tcnt[key] >= 2;
         lab[q] = rep;
+        if (next16) next16[q] = (uint16_t)rank[key];
+        if (next32) next32[q] = rank[key];
         if (keep) keep[i] = multi;
         if (act) act[q] = multi;
         heads += rep == q;
@@ -266,6 +271,18 @@ __global__ void __launch_bounds__(kThreads) table_apply_kernel(const uint32_t* _
         surv += multi;
     }
     flush_counters<kThreads>(heads, ablk, surv, &ctr->runs, &ctr->active_blocks, &ctr->active_states);
+}
+
+__global__ void table_occupied_kernel(const uint32_t* __restrict__ tcnt, uint32_t tsize, uint32_t* __restrict__ occ) {
+    for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < tsize; e += gridDim.x * blockDim.x)
+        occ[e] = tcnt[e] ? 1u : 0u;
+}
+
+// dense ids of a two-block partition: the block of state 0 is block 0
+__global__ void dense2_kernel(const uint32_t* __restrict__ lab, uint32_t n, uint8_t* __restrict__ out) {
+    const uint32_t l0 = lab[0];
+    for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x)
+        out[q] = lab[q] != l0;
 }
 
 // ---- bucket strategy -----------------------------------------------------------------
@@ -601,6 +618,7 @@ __global__ void __launch_bounds__(kThreads) run_apply_kernel(const uint32_t* __r
                                                              const uint32_t* __restrict__ run_start,
                                                              const uint32_t* __restrict__ rmin,
                                                              uint32_t* __restrict__ lab, uint8_t* __restrict__ keep,
+                                                             uint8_t* __restrict__ act,
                                                              IterCounters* __restrict__ ctr) {
     uint32_t ablk = 0, surv = 0;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
@@ -609,6 +627,7 @@ __global__ void __launch_bounds__(kThreads) run_apply_kernel(const uint32_t* __r
         const bool multi = (e - s) >= 2;
         lab[vals[i]] = rmin[r];
         keep[i] = multi;
+        if (act) act[vals[i]] = multi;
         ablk += multi && heads[i];
         surv += multi;
     }
@@ -630,7 +649,8 @@ __global__ void gather_dense_kernel(const uint32_t* __restrict__ list, uint64_t 
 }
 
 struct Workspace {
-    DBuf<uint32_t> lab, lab2, list0, list1, vals0, vals1, heads, pos, run_start, scratch, cur, tmin, tcnt;
+    DBuf<uint32_t> lab, lab2, list0, list1, vals0, vals1, heads, pos, run_start, scratch, cur, tmin, tcnt, trank, next32;
+    DBuf<uint16_t> next16;
     DBuf<uint32_t> dense32;
     DBuf<uint8_t> dense8;
     DBuf<uint16_t> dense16;
@@ -751,6 +771,8 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
     }
 
     uint64_t salt = 0x5eed5eed5eedull;
+    bool next_valid = false;  // next16 / next32 hold compact block ids of the current partition
+    uint32_t prev_nbits = 0;
     const uint64_t fp_mask = o.fingerprint_bits >= 64 ? ~0ull : ((1ull << o.fingerprint_bits) - 1ull);
     uint32_t collisions_this_pass = 0;
 
@@ -776,7 +798,18 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
         const bool fingerprint = plan.strategy == kPlanFingerprint, chunked = plan.strategy == kPlanChunked;
         const uint32_t field_bits = plan.field_bits;
         KeyLab kl{w.lab.get(), 4};
-        if (plan.keylab_bytes) kl = dense_keylab(plan.keylab_bytes);
+        if (plan.keylab_bytes) {
+            if (next_valid && plan.strategy != kPlanChunked) {
+                kl = w.next16.get() && prev_nbits <= 16 ? KeyLab{w.next16.get(), 2} : KeyLab{w.next32.get(), 4};
+            } else if (B <= 2 && plan.strategy != kPlanChunked) {
+                if (!w.dense8.get()) w.dense8.alloc(n, s);
+                DK_LAUNCH(ctx, dense2_kernel, grid_for(n), kThreads, 0, s, w.lab.get(), n, w.dense8.get());
+                kl = KeyLab{w.dense8.get(), 1};
+            } else {
+                kl = dense_keylab(plan.keylab_bytes);
+            }
+        }
+        next_valid = false;
         DK_CUDA(cudaMemsetAsync(dctr, 0, sizeof(IterCounters), s));
         const unsigned g = grid_for(m);
         const uint32_t nbits = plan.key_bits;
@@ -812,8 +845,24 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
                             512, smem, s, list, m, d.delta, n, lab, p, nbits, w.heads.get(), w.tmin.get(),
                             w.tcnt.get());
             });
+            // a table pass over every state sees every block of the next
+            // partition as one table key: the ranks of the occupied entries
+            // are compact block ids, the next pass's key labels (no O(n) scan)
+            const bool full = list == nullptr;
+            if (full) {
+                if (w.trank.n < tsize) w.trank.alloc(tsize, s);
+                DK_LAUNCH(ctx, table_occupied_kernel, grid_for(tsize), kThreads, 0, s, w.tcnt.get(), (uint32_t)tsize,
+                          w.trank.get());
+                exclusive_scan_u32(ctx, w.trank.get(), w.trank.get(), tsize, nullptr, s);
+                if (nbits <= 16 && !w.next16.get()) w.next16.alloc(n, s);
+                if (nbits > 16 && !w.next32.get()) w.next32.alloc(n, s);
+            }
             DK_LAUNCH_B(ctx, (double)m * (9.0 + 2 * list_b), table_apply_kernel, g, kThreads, 0, s, list,
-                        w.heads.get(), m, w.tmin.get(), w.tcnt.get(), w.lab.get(), w.keep.get(), nullptr, dctr);
+                        w.heads.get(), m, w.tmin.get(), w.tcnt.get(), w.lab.get(), w.keep.get(), nullptr,
+                        full ? w.trank.get() : nullptr, full && nbits <= 16 ? w.next16.get() : nullptr,
+                        full && nbits > 16 ? w.next32.get() : nullptr, dctr);
+            next_valid = full;
+            prev_nbits = nbits;
             compact_flags(ctx, list, w.keep.get(), m, dst, &dctr->listed, s);
             listed = true;
             read_words(ctx, dctr, sizeof(c), &c, s);
@@ -989,11 +1038,18 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
             DK_LAUNCH(ctx, run_starts_kernel, g, kThreads, 0, s, w.heads.get(), w.pos.get(), m, w.run_start.get());
             DK_CUDA(cudaMemsetAsync(w.scratch.get(), 0xff, m * sizeof(uint32_t), s));
             DK_LAUNCH(ctx, run_min_kernel, g, kThreads, 0, s, w.heads.get(), w.pos.get(), svals, m, w.scratch.get());
+            // big passes flag survivors per state so the next list is increasing
+            // (coalesced delta rows); small ones keep the sorted order
+            const bool state_order = m >= (uint64_t)n / 16;
+            if (state_order) {
+                if (!w.act.get()) w.act.alloc(n, s);
+                DK_CUDA(cudaMemsetAsync(w.act.get(), 0, n, s));
+            }
             DK_LAUNCH_B(ctx, 25.0 * m, run_apply_kernel, g, kThreads, 0, s, w.heads.get(), w.pos.get(), svals, m,
-                        w.run_start.get(), w.scratch.get(), w.lab.get(), w.keep.get(), dctr);
-            // surviving active states in sorted order (runs grouped, increasing
-            // state order inside each run)
-            compact_flags(ctx, svals, w.keep.get(), m, dst, &dctr->listed, s);
+                        w.run_start.get(), w.scratch.get(), w.lab.get(), w.keep.get(),
+                        state_order ? w.act.get() : nullptr, dctr);
+            if (state_order) compact_flags(ctx, nullptr, w.act.get(), n, dst, &dctr->listed, s);
+            else compact_flags(ctx, svals, w.keep.get(), m, dst, &dctr->listed, s);
             listed = true;
             read_words(ctx, dctr, sizeof(c), &c, s);
         }
@@ -1197,7 +1253,7 @@ void shard_table_apply(Ctx* ctx, const uint32_t* list, const uint32_t* keys32, u
     DK_CUDA(cudaMemsetAsync(counters, 0, 4 * sizeof(uint32_t), s));
     if (m == 0) return;
     DK_LAUNCH_B(ctx, (double)m * 13.0, table_apply_kernel, grid_for(m), kThreads, 0, s, list, keys32, m, tmin, tcnt,
-                lab, nullptr, act, reinterpret_cast<IterCounters*>(counters));
+                lab, nullptr, act, nullptr, nullptr, nullptr, reinterpret_cast<IterCounters*>(counters));
 }
 
 void shard_sig_partition(Ctx* ctx, const DevDfa& d, const void* keylab, const PassPlan& plan, uint64_t salt,
