@@ -14,7 +14,8 @@
  *   - accepting is one byte per state (0 / 1).
  *   - `dfakit_*` calls take HOST buffers and copy them in and out;
  *     `dfakit_*_device` calls take DEVICE pointers already resident in HBM and
- *     run on the given CUDA stream (NULL = the context's stream).
+ *     run on the given CUDA stream (NULL = the context's stream; pass
+ *     cudaStreamLegacy, (void*)1, for the legacy default stream).
  *   - Block numbering of every returned partition is canonical: blocks are
  *     numbered by first occurrence scanning states upwards (equivalently, by
  *     the minimum state id of each block), the reference's
@@ -229,22 +230,31 @@ dfakit_status dfakit_plan_pass(uint32_t num_states, uint32_t alphabet_size, uint
 dfakit_status dfakit_shard_init(dfakit_ctx* ctx, const dfakit_dfa* dfa, uint32_t lo, uint32_t hi, uint32_t* lab,
                                 uint8_t* act, uint32_t* num_blocks, uint32_t* active_blocks,
                                 uint64_t* active_states, void* stream);
-/* Dense block ids of `lab` in plan->keylab_bytes-wide entries (no-op when 0). */
-dfakit_status dfakit_shard_keylab(dfakit_ctx* ctx, const uint32_t* lab, uint32_t n, const dfakit_pass_plan* plan,
-                                  void* keylab, void* stream);
-/* Table passes: keys of the m local active states in `list`, local (min, count)
- * table of 2^key_bits entries (caller allreduces MIN / SUM), then apply. */
+/* Dense block ids of `lab` (num_blocks blocks) in plan->keylab_bytes-wide
+ * entries (no-op when 0). */
+dfakit_status dfakit_shard_keylab(dfakit_ctx* ctx, const uint32_t* lab, uint32_t n, uint32_t num_blocks,
+                                  const dfakit_pass_plan* plan, void* keylab, void* stream);
+/* `list` == NULL everywhere below: the m active states are list_base,
+ * list_base + 1, ... (a shard whose states are all active).
+ * Table passes: keys of the m local active states in `list`, local (min, count)
+ * table of 2^key_bits entries (caller allreduces MIN / SUM), then apply.
+ * next_keylab (optional; uint16 when key_bits <= 16, else uint32, indexed by
+ * state): compact block ids of the new partition for the local states -- valid
+ * as the next pass's key labels when this pass covered every state. */
 dfakit_status dfakit_shard_table_signature(dfakit_ctx* ctx, const dfakit_dfa* dfa, const void* keylab,
-                                           const dfakit_pass_plan* plan, const uint32_t* list, uint64_t m,
-                                           uint32_t* keys32, uint32_t* tmin, uint32_t* tcnt, void* stream);
-dfakit_status dfakit_shard_table_apply(dfakit_ctx* ctx, const uint32_t* list, const uint32_t* keys32, uint64_t m,
-                                       const uint32_t* tmin, const uint32_t* tcnt, uint32_t* lab, uint8_t* act,
+                                           const dfakit_pass_plan* plan, const uint32_t* list, uint32_t list_base,
+                                           uint64_t m, uint32_t* keys32, uint32_t* tmin, uint32_t* tcnt,
+                                           void* stream);
+dfakit_status dfakit_shard_table_apply(dfakit_ctx* ctx, const dfakit_pass_plan* plan, const uint32_t* list,
+                                       uint32_t list_base, const uint32_t* keys32, uint64_t m, const uint32_t* tmin,
+                                       const uint32_t* tcnt, uint32_t* lab, uint8_t* act, void* next_keylab,
                                        uint32_t* counters, void* stream);
 /* Wide passes: keys of the local active states partitioned by owner rank into
  * send_entries (m entries, destination-contiguous); send_counts[world]. */
 dfakit_status dfakit_shard_partition(dfakit_ctx* ctx, const dfakit_dfa* dfa, const void* keylab,
-                                     const dfakit_pass_plan* plan, uint64_t salt, const uint32_t* list, uint64_t m,
-                                     uint32_t world, void* send_entries, uint32_t* send_counts, void* stream);
+                                     const dfakit_pass_plan* plan, uint64_t salt, const uint32_t* list,
+                                     uint32_t list_base, uint64_t m, uint32_t world, void* send_entries,
+                                     uint32_t* send_counts, void* stream);
 /* Owner side: groups the received entries; results[i] = new label | survivor << 31. */
 dfakit_status dfakit_shard_group(dfakit_ctx* ctx, const dfakit_dfa* dfa, const uint32_t* lab,
                                  const dfakit_pass_plan* plan, const void* recv_entries, uint64_t count,

@@ -109,11 +109,13 @@ _sig = {
                                    _P(CPassPlan)]),
     "dfakit_shard_init": (C.c_int, [_V, _P(CDfa), C.c_uint32, C.c_uint32, _V, _V, _P(C.c_uint32), _P(C.c_uint32),
                                     _P(C.c_uint64), _V]),
-    "dfakit_shard_keylab": (C.c_int, [_V, _V, C.c_uint32, _P(CPassPlan), _V, _V]),
-    "dfakit_shard_table_signature": (C.c_int, [_V, _P(CDfa), _V, _P(CPassPlan), _V, C.c_uint64, _V, _V, _V, _V]),
-    "dfakit_shard_table_apply": (C.c_int, [_V, _V, _V, C.c_uint64, _V, _V, _V, _V, _V, _V]),
-    "dfakit_shard_partition": (C.c_int, [_V, _P(CDfa), _V, _P(CPassPlan), C.c_uint64, _V, C.c_uint64, C.c_uint32,
-                                         _V, _V, _V]),
+    "dfakit_shard_keylab": (C.c_int, [_V, _V, C.c_uint32, C.c_uint32, _P(CPassPlan), _V, _V]),
+    "dfakit_shard_table_signature": (C.c_int, [_V, _P(CDfa), _V, _P(CPassPlan), _V, C.c_uint32, C.c_uint64, _V, _V,
+                                               _V, _V]),
+    "dfakit_shard_table_apply": (C.c_int, [_V, _P(CPassPlan), _V, C.c_uint32, _V, C.c_uint64, _V, _V, _V, _V, _V,
+                                           _V, _V]),
+    "dfakit_shard_partition": (C.c_int, [_V, _P(CDfa), _V, _P(CPassPlan), C.c_uint64, _V, C.c_uint32, C.c_uint64,
+                                         C.c_uint32, _V, _V, _V]),
     "dfakit_shard_group": (C.c_int, [_V, _P(CDfa), _V, _P(CPassPlan), _V, C.c_uint64, _V, _V, _V]),
     "dfakit_shard_apply": (C.c_int, [_V, _V, _V, C.c_uint64, _V, _V, _V]),
     "dfakit_shard_compact": (C.c_int, [_V, _V, C.c_uint32, C.c_uint32, _V, _V, _V]),

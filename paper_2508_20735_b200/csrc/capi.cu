@@ -489,45 +489,49 @@ dfakit_status dfakit_shard_init(dfakit_ctx* ctx, const dfakit_dfa* dfa, uint32_t
     });
 }
 
-dfakit_status dfakit_shard_keylab(dfakit_ctx* ctx, const uint32_t* lab, uint32_t n, const dfakit_pass_plan* plan,
-                                  void* keylab, void* stream) {
+dfakit_status dfakit_shard_keylab(dfakit_ctx* ctx, const uint32_t* lab, uint32_t n, uint32_t num_blocks,
+                                  const dfakit_pass_plan* plan, void* keylab, void* stream) {
     return on_device(ctx, stream, [&](dk::Ctx* c, cudaStream_t s) {
         const dk::PassPlan p = plan_in(plan);
         if (!p.keylab_bytes || !n) return;
-        dk::DBuf<uint32_t> scratch((uint64_t)n + 1, s);
-        dk::shard_keylab(c, lab, n, p, keylab, scratch.get(), s);
+        dk::DBuf<uint32_t> scratch(num_blocks <= 2 ? 1 : (uint64_t)n + 1, s);
+        dk::shard_keylab(c, lab, n, num_blocks, p, keylab, scratch.get(), s);
     });
 }
 
 dfakit_status dfakit_shard_table_signature(dfakit_ctx* ctx, const dfakit_dfa* dfa, const void* keylab,
-                                           const dfakit_pass_plan* plan, const uint32_t* list, uint64_t m,
-                                           uint32_t* keys32, uint32_t* tmin, uint32_t* tcnt, void* stream) {
+                                           const dfakit_pass_plan* plan, const uint32_t* list, uint32_t list_base,
+                                           uint64_t m, uint32_t* keys32, uint32_t* tmin, uint32_t* tcnt,
+                                           void* stream) {
     return on_device(ctx, stream, [&](dk::Ctx* c, cudaStream_t s) {
         check_view(dfa, "shard_table_signature");
         const dk::PassPlan p = plan_in(plan);
         if (p.strategy != dk::kPlanTable || p.key_bits > 20)
             throw dk::Error(DFAKIT_E_INVALID, "shard_table_signature: not a table plan");
-        dk::shard_table_signature(c, device_view(dfa), keylab, p, list, m, keys32, tmin, tcnt, s);
+        dk::shard_table_signature(c, device_view(dfa), keylab, p, list, list_base, m, keys32, tmin, tcnt, s);
     });
 }
 
-dfakit_status dfakit_shard_table_apply(dfakit_ctx* ctx, const uint32_t* list, const uint32_t* keys32, uint64_t m,
-                                       const uint32_t* tmin, const uint32_t* tcnt, uint32_t* lab, uint8_t* act,
+dfakit_status dfakit_shard_table_apply(dfakit_ctx* ctx, const dfakit_pass_plan* plan, const uint32_t* list,
+                                       uint32_t list_base, const uint32_t* keys32, uint64_t m, const uint32_t* tmin,
+                                       const uint32_t* tcnt, uint32_t* lab, uint8_t* act, void* next_keylab,
                                        uint32_t* counters, void* stream) {
     return on_device(ctx, stream, [&](dk::Ctx* c, cudaStream_t s) {
-        dk::shard_table_apply(c, list, keys32, m, tmin, tcnt, lab, act, counters, s);
+        dk::shard_table_apply(c, plan_in(plan), list, list_base, keys32, m, tmin, tcnt, lab, act, next_keylab,
+                              counters, s);
     });
 }
 
 dfakit_status dfakit_shard_partition(dfakit_ctx* ctx, const dfakit_dfa* dfa, const void* keylab,
-                                     const dfakit_pass_plan* plan, uint64_t salt, const uint32_t* list, uint64_t m,
-                                     uint32_t world, void* send_entries, uint32_t* send_counts, void* stream) {
+                                     const dfakit_pass_plan* plan, uint64_t salt, const uint32_t* list,
+                                     uint32_t list_base, uint64_t m, uint32_t world, void* send_entries,
+                                     uint32_t* send_counts, void* stream) {
     return on_device(ctx, stream, [&](dk::Ctx* c, cudaStream_t s) {
         check_view(dfa, "shard_partition");
         const dk::PassPlan p = plan_in(plan);
         if (p.strategy != dk::kPlanPacked && p.strategy != dk::kPlanFingerprint)
             throw dk::Error(DFAKIT_E_INVALID, "shard_partition: plan is not packed / fingerprint");
-        dk::shard_sig_partition(c, device_view(dfa), keylab, p, salt, list, m, world,
+        dk::shard_sig_partition(c, device_view(dfa), keylab, p, salt, list, list_base, m, world,
                                 static_cast<uint4*>(send_entries), send_counts, s);
     });
 }

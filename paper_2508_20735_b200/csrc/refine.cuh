@@ -46,15 +46,18 @@ struct ShardInit {
 };
 ShardInit shard_init(Ctx* ctx, const DevDfa& d, uint32_t lo, uint32_t hi, uint32_t* lab, uint8_t* act,
                      cudaStream_t s);
-void shard_keylab(Ctx* ctx, const uint32_t* lab, uint32_t n, const PassPlan& plan, void* out, uint32_t* scratch,
-                  cudaStream_t s);
+void shard_keylab(Ctx* ctx, const uint32_t* lab, uint32_t n, uint32_t num_blocks, const PassPlan& plan, void* out,
+                  uint32_t* scratch, cudaStream_t s);
+// list == nullptr: the active states are list_base .. list_base + m - 1
 void shard_table_signature(Ctx* ctx, const DevDfa& d, const void* keylab, const PassPlan& plan, const uint32_t* list,
-                           uint64_t m, uint32_t* keys32, uint32_t* tmin, uint32_t* tcnt, cudaStream_t s);
-void shard_table_apply(Ctx* ctx, const uint32_t* list, const uint32_t* keys32, uint64_t m, const uint32_t* tmin,
-                       const uint32_t* tcnt, uint32_t* lab, uint8_t* act, uint32_t* counters, cudaStream_t s);
+                           uint32_t list_base, uint64_t m, uint32_t* keys32, uint32_t* tmin, uint32_t* tcnt,
+                           cudaStream_t s);
+void shard_table_apply(Ctx* ctx, const PassPlan& plan, const uint32_t* list, uint32_t list_base,
+                       const uint32_t* keys32, uint64_t m, const uint32_t* tmin, const uint32_t* tcnt, uint32_t* lab,
+                       uint8_t* act, void* next_keylab, uint32_t* counters, cudaStream_t s);
 void shard_sig_partition(Ctx* ctx, const DevDfa& d, const void* keylab, const PassPlan& plan, uint64_t salt,
-                         const uint32_t* list, uint64_t m, uint32_t world, uint4* send, uint32_t* send_counts,
-                         cudaStream_t s);
+                         const uint32_t* list, uint32_t list_base, uint64_t m, uint32_t world, uint4* send,
+                         uint32_t* send_counts, cudaStream_t s);
 void shard_group(Ctx* ctx, const DevDfa& d, const uint32_t* lab, const PassPlan& plan, const uint4* recv,
                  uint64_t count, uint32_t* results, uint32_t* counters, cudaStream_t s);
 void shard_apply(Ctx* ctx, const uint4* send, const uint32_t* results, uint64_t count, uint32_t* lab, uint8_t* act,

@@ -123,6 +123,7 @@ struct SigParams {
     uint32_t field_bits;  // packed: bits per successor field
     uint64_t salt;        // fingerprint salt
     uint64_t fp_mask;     // fingerprint mask (testing hook)
+    uint32_t q0;          // list == nullptr: the active states are q0, q0 + 1, ...
 };
 
 __device__ __forceinline__ uint64_t fp_step(uint64_t h, uint32_t x) {
@@ -165,7 +166,7 @@ __global__ void __launch_bounds__(kThreads) signature_kernel(const uint32_t* __r
                                                              const uint32_t* __restrict__ head, SigParams p,
                                                              uint64_t* __restrict__ keys, uint32_t* __restrict__ vals) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t q = list ? list[i] : (uint32_t)i;
+        const uint32_t q = list ? list[i] : p.q0 + (uint32_t)i;
         keys[i] = tuple_key<LT>(q, head ? head[i] : (uint32_t)lab[q], delta, n, lab, p);
         vals[i] = q;
     }
@@ -194,7 +195,7 @@ __global__ void __launch_bounds__(512) sig_table_kernel(const uint32_t* __restri
         __syncthreads();
     }
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t q = list ? list[i] : (uint32_t)i;
+        const uint32_t q = list ? list[i] : p.q0 + (uint32_t)i;
         const uint32_t key = (uint32_t)tuple_key<LT>(q, (uint32_t)lab[q], delta, n, lab, p);
         keys32[i] = key;
         const unsigned peers = __match_any_sync(__activemask(), key);
@@ -253,12 +254,12 @@ __global__ void __launch_bounds__(kThreads) table_apply_kernel(const uint32_t* _
                                                                uint8_t* __restrict__ act,
                                                                const uint32_t* __restrict__ rank,
                                                                uint16_t* __restrict__ next16,
-                                                               uint32_t* __restrict__ next32,
+                                                               uint32_t* __restrict__ next32, uint32_t q0,
                                                                IterCounters* __restrict__ ctr) {
     uint32_t heads = 0, ablk = 0, surv = 0;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t key = keys32[i];
-        const uint32_t q = list ? list[i] : (uint32_t)i;
+        const uint32_t q = list ? list[i] : q0 + (uint32_t)i;
         const uint32_t rep = tmin[key];
         const bool multi = tcnt[key] >= 2;
         lab[q] = rep;
@@ -356,7 +357,7 @@ __global__ void __launch_bounds__(kThreads) sig_bucket_kernel(const uint32_t* __
                                                               uint4* __restrict__ bent,
                                                               IterCounters* __restrict__ ctr) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t q = list ? list[i] : (uint32_t)i;
+        const uint32_t q = list ? list[i] : p.q0 + (uint32_t)i;
         const uint64_t key = tuple_key<LT>(q, (uint32_t)lab[q], delta, n, lab, p);
         const unsigned long long hk = p.kind == kKeyPacked ? mix64(key) : key;
         bucket_append(hk, q, 0u, nb, bcnt, bent, ctr);
@@ -860,7 +861,7 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
             DK_LAUNCH_B(ctx, (double)m * (9.0 + 2 * list_b), table_apply_kernel, g, kThreads, 0, s, list,
                         w.heads.get(), m, w.tmin.get(), w.tcnt.get(), w.lab.get(), w.keep.get(), nullptr,
                         full ? w.trank.get() : nullptr, full && nbits <= 16 ? w.next16.get() : nullptr,
-                        full && nbits > 16 ? w.next32.get() : nullptr, dctr);
+                        full && nbits > 16 ? w.next32.get() : nullptr, 0u, dctr);
             next_valid = full;
             prev_nbits = nbits;
             compact_flags(ctx, list, w.keep.get(), m, dst, &dctr->listed, s);
@@ -1104,7 +1105,7 @@ __global__ void __launch_bounds__(kThreads) sig_entries_kernel(const uint32_t* _
     for (uint32_t d = threadIdx.x; d < world; d += blockDim.x) cnt[d] = 0;
     __syncthreads();
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t q = list ? list[i] : (uint32_t)i;
+        const uint32_t q = list ? list[i] : p.q0 + (uint32_t)i;
         const uint64_t key = tuple_key<LT>(q, (uint32_t)lab[q], delta, n, lab, p);
         const unsigned long long hk = p.kind == kKeyPacked ? mix64(key) : key;
         const uint32_t d = owner_of(hk, world);
@@ -1223,13 +1224,18 @@ ShardInit shard_init(Ctx* ctx, const DevDfa& d, uint32_t lo, uint32_t hi, uint32
     return r;
 }
 
-void shard_keylab(Ctx* ctx, const uint32_t* lab, uint32_t n, const PassPlan& plan, void* out, uint32_t* scratch,
-                  cudaStream_t s) {
-    if (plan.keylab_bytes) dense_labels(ctx, lab, n, out, (int)plan.keylab_bytes, scratch, s);
+void shard_keylab(Ctx* ctx, const uint32_t* lab, uint32_t n, uint32_t num_blocks, const PassPlan& plan, void* out,
+                  uint32_t* scratch, cudaStream_t s) {
+    if (!plan.keylab_bytes) return;
+    if (num_blocks <= 2 && plan.keylab_bytes == 1)  // two blocks: no scan
+        DK_LAUNCH(ctx, dense2_kernel, grid_for(n), kThreads, 0, s, lab, n, static_cast<uint8_t*>(out));
+    else
+        dense_labels(ctx, lab, n, out, (int)plan.keylab_bytes, scratch, s);
 }
 
 void shard_table_signature(Ctx* ctx, const DevDfa& d, const void* keylab, const PassPlan& plan, const uint32_t* list,
-                           uint64_t m, uint32_t* keys32, uint32_t* tmin, uint32_t* tcnt, cudaStream_t s) {
+                           uint32_t list_base, uint64_t m, uint32_t* keys32, uint32_t* tmin, uint32_t* tcnt,
+                           cudaStream_t s) {
     const uint32_t nbits = plan.key_bits;
     const uint64_t tsize = 1ull << nbits;
     DK_CUDA(cudaMemsetAsync(tmin, 0xff, tsize * 4, s));
@@ -1239,7 +1245,8 @@ void shard_table_signature(Ctx* ctx, const DevDfa& d, const void* keylab, const 
     const size_t smem = local ? (size_t)(2u << nbits) * 4 : 0;
     const int smem_table = (int)(2u << kSmemTableBits) * 4;
     const unsigned tg = (unsigned)std::min<uint64_t>((m + 511) / 512, (uint64_t)ctx->num_sms * 3);
-    const SigParams p = sig_params(plan, d.k, 0);
+    SigParams p = sig_params(plan, d.k, 0);
+    p.q0 = list_base;
     with_lab_type(KeyLab{keylab, plan.keylab_bytes ? (int)plan.keylab_bytes : 4}, [&](auto lab) {
         using LT = std::remove_const_t<std::remove_pointer_t<decltype(lab)>>;
         DK_CUDA(cudaFuncSetAttribute(sig_table_kernel<LT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_table));
@@ -1248,23 +1255,37 @@ void shard_table_signature(Ctx* ctx, const DevDfa& d, const void* keylab, const 
     });
 }
 
-void shard_table_apply(Ctx* ctx, const uint32_t* list, const uint32_t* keys32, uint64_t m, const uint32_t* tmin,
-                       const uint32_t* tcnt, uint32_t* lab, uint8_t* act, uint32_t* counters, cudaStream_t s) {
+void shard_table_apply(Ctx* ctx, const PassPlan& plan, const uint32_t* list, uint32_t list_base,
+                       const uint32_t* keys32, uint64_t m, const uint32_t* tmin, const uint32_t* tcnt, uint32_t* lab,
+                       uint8_t* act, void* next_keylab, uint32_t* counters, cudaStream_t s) {
     DK_CUDA(cudaMemsetAsync(counters, 0, 4 * sizeof(uint32_t), s));
     if (m == 0) return;
+    // ranks of the occupied entries of the (allreduced, identical) table:
+    // compact block ids of the next partition when the pass covered every state
+    DBuf<uint32_t> rank;
+    const uint32_t tsize = 1u << plan.key_bits;
+    if (next_keylab) {
+        rank.alloc(tsize, s);
+        DK_LAUNCH(ctx, table_occupied_kernel, grid_for(tsize), kThreads, 0, s, tcnt, tsize, rank.get());
+        exclusive_scan_u32(ctx, rank.get(), rank.get(), tsize, nullptr, s);
+    }
+    const bool narrow = plan.key_bits <= 16;
     DK_LAUNCH_B(ctx, (double)m * 13.0, table_apply_kernel, grid_for(m), kThreads, 0, s, list, keys32, m, tmin, tcnt,
-                lab, nullptr, act, nullptr, nullptr, nullptr, reinterpret_cast<IterCounters*>(counters));
+                lab, nullptr, act, rank.get(), next_keylab && narrow ? static_cast<uint16_t*>(next_keylab) : nullptr,
+                next_keylab && !narrow ? static_cast<uint32_t*>(next_keylab) : nullptr, list_base,
+                reinterpret_cast<IterCounters*>(counters));
 }
 
 void shard_sig_partition(Ctx* ctx, const DevDfa& d, const void* keylab, const PassPlan& plan, uint64_t salt,
-                         const uint32_t* list, uint64_t m, uint32_t world, uint4* send, uint32_t* send_counts,
-                         cudaStream_t s) {
+                         const uint32_t* list, uint32_t list_base, uint64_t m, uint32_t world, uint4* send,
+                         uint32_t* send_counts, cudaStream_t s) {
     if (world == 0 || world > (uint32_t)kMaxWorld) throw Error(DFAKIT_E_INVALID, "shard: world size out of range");
     DK_CUDA(cudaMemsetAsync(send_counts, 0, world * 4, s));
     if (m == 0) return;
     DBuf<uint4> tmp(m, s);
     DBuf<uint32_t> cur(world, s);
-    const SigParams p = sig_params(plan, d.k, salt);
+    SigParams p = sig_params(plan, d.k, salt);
+    p.q0 = list_base;
     with_lab_type(KeyLab{keylab, plan.keylab_bytes ? (int)plan.keylab_bytes : 4}, [&](auto lab) {
         DK_LAUNCH_BU(ctx, (double)m * (4.0 * d.k + 20.0), (double)m * d.k, sig_entries_kernel, grid_for(m, kThreads,
                     (unsigned)ctx->num_sms * 8u), kThreads, 0, s, list, m, d.delta, d.n, lab, p, world, tmp.get(),

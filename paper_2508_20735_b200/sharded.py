@@ -119,15 +119,19 @@ class TorchComm:
         return out.to(send.device) if self.stage_cpu else out
 
     def allgather_slices_(self, full, shard: int):
-        """full[r*shard:(r+1)*shard] of every rank r -> full on every rank."""
+        """full[r*shard:(r+1)*shard] of every rank r -> full on every rank
+        (on byte views: int16 / uint8 label arrays travel on every backend)."""
+        import torch
         h = self._host(full)
-        mine = h[self.rank * shard:(self.rank + 1) * shard].clone()
+        es = h.element_size()
+        h8 = h.view(torch.uint8)
+        mine = h8[self.rank * shard * es:(self.rank + 1) * shard * es].clone()
         if self.backend == "nccl":
-            self.dist.all_gather_into_tensor(h, mine, group=self.group)
+            self.dist.all_gather_into_tensor(h8, mine, group=self.group)
         else:
-            parts = list(h.split(shard))
+            parts = list(h8.split(shard * es))
             self.dist.all_gather(parts, mine, group=self.group)
-            h.copy_(__import__("torch").cat(parts))
+            h8.copy_(torch.cat(parts))
         if h is not full:
             full.copy_(h)
         return full
@@ -147,8 +151,15 @@ class CudaShardOps:
         self.n, self.k = n, k
         self.device = delta.device if k else acc.device
         self.view = _CDfa(n, k, delta.data_ptr() if k else None, acc.data_ptr(), -1)
-        self.stream = ctx.stream
         self._scratch = {}
+
+    @property
+    def stream(self):
+        """every primitive runs on torch's current stream: collectives and
+        kernels are ordered without cross-stream waits"""
+        # 0 (torch's default stream) would mean "the context's stream" at the
+        # C ABI: pass cudaStreamLegacy, the same NULL stream, explicitly
+        return self.torch.cuda.current_stream(self.device).cuda_stream or 1
 
     # buffers reused across passes
     def _buf(self, name, count, dtype):
@@ -158,67 +169,48 @@ class CudaShardOps:
             self._scratch[name] = b
         return b[:count]
 
-    def _sync(self):
-        self.torch.cuda.current_stream(self.device).wait_stream(self._torch_stream())
-
-    def _torch_stream(self):
-        return self.torch.cuda.ExternalStream(self.stream, device=self.device)
-
-    def _ready(self):
-        """library stream waits for torch's current stream (collectives, fills)."""
-        self._torch_stream().wait_stream(self.torch.cuda.current_stream(self.device))
-
     def init(self, lab, act, lo, hi):
         B, A, M = C.c_uint32(), C.c_uint32(), C.c_uint64()
-        self._ready()
         check(lib.dfakit_shard_init(self.ctx.handle, C.byref(self.view), lo, hi, lab.data_ptr(), act.data_ptr(),
                                     C.byref(B), C.byref(A), C.byref(M), self.stream))
-        self._sync()
         return int(B.value), int(A.value), int(M.value)
 
-    def keylab(self, lab, plan):
+    def keylab(self, lab, plan, num_blocks):
         if not plan.keylab_bytes:
             return lab
         dt = {1: self.torch.uint8, 2: self.torch.int16, 4: self.torch.int32}[plan.keylab_bytes]
         out = self._buf(f"keylab{plan.keylab_bytes}", self.n, dt)
-        self._ready()
-        check(lib.dfakit_shard_keylab(self.ctx.handle, lab.data_ptr(), self.n, C.byref(plan), out.data_ptr(),
-                                      self.stream))
-        self._sync()
+        check(lib.dfakit_shard_keylab(self.ctx.handle, lab.data_ptr(), self.n, num_blocks, C.byref(plan),
+                                      out.data_ptr(), self.stream))
         return out
 
-    def table_signature(self, keylab, plan, lst, m):
+    def table_signature(self, keylab, plan, lst, m, base=0):
         t = self.torch
         tsize = 1 << plan.key_bits
         keys32 = self._buf("keys32", m, t.int32)
         tmin = t.empty(tsize, dtype=t.int32, device=self.device)
         tcnt = t.empty(tsize, dtype=t.int32, device=self.device)
-        self._ready()
         check(lib.dfakit_shard_table_signature(self.ctx.handle, C.byref(self.view), keylab.data_ptr(), C.byref(plan),
-                                               lst.data_ptr(), m, keys32.data_ptr(), tmin.data_ptr(),
+                                               _ptr(lst), base, m, keys32.data_ptr(), tmin.data_ptr(),
                                                tcnt.data_ptr(), self.stream))
-        self._sync()
         return keys32, tmin, tcnt
 
-    def table_apply(self, lst, keys32, m, tmin, tcnt, lab, act):
+    def table_apply(self, plan, lst, keys32, m, tmin, tcnt, lab, act, next_keylab=None, base=0):
         ctr = self.torch.empty(4, dtype=self.torch.int32, device=self.device)
-        self._ready()
-        check(lib.dfakit_shard_table_apply(self.ctx.handle, lst.data_ptr(), keys32.data_ptr(), m, tmin.data_ptr(),
-                                           tcnt.data_ptr(), lab.data_ptr(), act.data_ptr(), ctr.data_ptr(),
-                                           self.stream))
-        self._sync()
+        check(lib.dfakit_shard_table_apply(self.ctx.handle, C.byref(plan), _ptr(lst), base, keys32.data_ptr(), m,
+                                           tmin.data_ptr(), tcnt.data_ptr(), lab.data_ptr(), act.data_ptr(),
+                                           next_keylab.data_ptr() if next_keylab is not None else None,
+                                           ctr.data_ptr(), self.stream))
         return ctr
 
-    def partition(self, keylab, plan, salt, lst, m, world):
+    def partition(self, keylab, plan, salt, lst, m, world, base=0):
         t = self.torch
         send = self._buf("send", 4 * m, t.int32).view(-1, 4) if m else t.empty((0, 4), dtype=t.int32,
                                                                                    device=self.device)
         counts = t.empty(world, dtype=t.int32, device=self.device)
-        self._ready()
         check(lib.dfakit_shard_partition(self.ctx.handle, C.byref(self.view), keylab.data_ptr(), C.byref(plan),
-                                         salt, lst.data_ptr(), m, world, send.data_ptr() if m else None,
+                                         salt, _ptr(lst), base, m, world, send.data_ptr() if m else None,
                                          counts.data_ptr(), self.stream))
-        self._sync()
         return send, counts
 
     def group(self, lab, plan, recv):
@@ -226,39 +218,36 @@ class CudaShardOps:
         cnt = recv.shape[0]
         res = self._buf("res", cnt, t.int32)
         ctr = t.empty(4, dtype=t.int32, device=self.device)
-        self._ready()
         check(lib.dfakit_shard_group(self.ctx.handle, C.byref(self.view), lab.data_ptr(), C.byref(plan),
                                      recv.data_ptr() if cnt else None, cnt, res.data_ptr(), ctr.data_ptr(),
                                      self.stream))
-        self._sync()
         return res, ctr
 
     def apply(self, send, results, lab, act):
-        self._ready()
         check(lib.dfakit_shard_apply(self.ctx.handle, send.data_ptr() if send.shape[0] else None,
                                      results.data_ptr(), send.shape[0], lab.data_ptr(), act.data_ptr(), self.stream))
-        self._sync()
 
     def compact(self, act, lo, hi):
         t = self.torch
         lst = t.empty(max(hi - lo, 1), dtype=t.int32, device=self.device)
         cnt = t.zeros(1, dtype=t.int32, device=self.device)
-        self._ready()
         check(lib.dfakit_shard_compact(self.ctx.handle, act.data_ptr(), lo, hi, lst.data_ptr(), cnt.data_ptr(),
                                        self.stream))
-        self._sync()
         m = int(cnt.item())
-        return lst[:m].clone(), m
+        # a shard whose states are all active travels as the identity range
+        return (None if m == hi - lo else lst[:m]), m
 
     def canonical(self, lab):
         t = self.torch
         out = t.empty(max(self.n, 1), dtype=t.int32, device=self.device)
         nb = C.c_uint32()
-        self._ready()
         check(lib.dfakit_shard_canonical(self.ctx.handle, lab.data_ptr(), self.n, out.data_ptr(), C.byref(nb),
                                          self.stream))
-        self._sync()
         return out[: self.n], int(nb.value)
+
+
+def _ptr(t):
+    return None if t is None else t.data_ptr()
 
 
 def sort_pr_sharded(ops, comm, n: int, k: int, max_collision_retries: int = 16):
@@ -277,21 +266,32 @@ def sort_pr_sharded(ops, comm, n: int, k: int, max_collision_retries: int = 16):
     B, A, m_total = ops.init(lab, act, lo, hi)
     lst, m = ops.compact(act, lo, hi)
     salt, strikes = _SALT0, 0
+    carried = None  # (key labels of the current partition, bytes): ranks of a full table pass
     while m_total > 0:
         rep.passes += 1
         plan = plan_pass(n, k, B, m_total, min(strikes, 2))
-        keylab = ops.keylab(lab, plan)
+        if plan.keylab_bytes and carried is not None:
+            keylab, plan.keylab_bytes = carried
+        else:
+            keylab = ops.keylab(lab, plan, B)
+        carried = None
+        next_kl = None
         if plan.strategy == PLAN_TABLE:
             rep.table_passes += 1
-            keys32, tmin, tcnt = ops.table_signature(keylab, plan, lst, m)
+            keys32, tmin, tcnt = ops.table_signature(keylab, plan, lst, m, base=lo)
             comm.allreduce_(tmin, "min")
             comm.allreduce_(tcnt, "sum")
             act[lo:hi].zero_()
-            ctr = ops.table_apply(lst, keys32, m, tmin, tcnt, lab, act).to(torch.int64)
+            if m_total == n:
+                # every block of the next partition is one table key: the
+                # ranks of the occupied entries are its compact block ids
+                next_kl = torch.zeros(world * shard, dtype=torch.int16 if plan.key_bits <= 16 else torch.int32,
+                                      device=dev)
+            ctr = ops.table_apply(plan, lst, keys32, m, tmin, tcnt, lab, act, next_kl, base=lo).to(torch.int64)
             comm.allreduce_(ctr, "sum")
             runs, ablk, surv, _ = (int(x) for x in ctr.tolist())
         else:
-            send, counts = ops.partition(keylab, plan, salt, lst, m, world)
+            send, counts = ops.partition(keylab, plan, salt, lst, m, world, base=lo)
             send_counts = counts.to(torch.int64).cpu().tolist()
             recv_counts = comm.all_to_all_counts(counts).cpu().tolist()
             recv = comm.all_to_all_v(send, send_counts, recv_counts)
@@ -322,6 +322,9 @@ def sort_pr_sharded(ops, comm, n: int, k: int, max_collision_retries: int = 16):
         rep.refining_iterations += 1
         B, A, m_total = new_b, ablk, surv
         comm.allgather_slices_(lab, shard)
+        if next_kl is not None:
+            comm.allgather_slices_(next_kl, shard)
+            carried = (next_kl, next_kl.element_size())
         lst, m = ops.compact(act, lo, hi)
     blocks, nb = ops.canonical(lab)
     rep.num_blocks = nb

@@ -47,7 +47,7 @@ class NumpyShardOps:
         B = int(ia.size > 0) + int(ir.size > 0)
         return B, int(keep_a) + int(keep_r), (ia.size if keep_a else 0) + (ir.size if keep_r else 0)
 
-    def keylab(self, lab, plan):
+    def keylab(self, lab, plan, num_blocks):
         if not plan.keylab_bytes:
             return lab
         L = u32(lab)[: self.n]
@@ -56,7 +56,8 @@ class NumpyShardOps:
         return torch.from_numpy(pos[L].astype(np.uint32).view(np.int32))
 
     def _tuples(self, keylab, qs):
-        L = u32(keylab) if keylab.dtype == torch.int32 else keylab.numpy()
+        L = {torch.int32: lambda t: u32(t), torch.int16: lambda t: t.numpy().view(np.uint16)}.get(
+            keylab.dtype, lambda t: t.numpy())(keylab)
         L = L[: self.n].astype(np.uint64)
         return L[qs], [L[self.delta[a][qs]] for a in range(self.k)]
 
@@ -74,8 +75,12 @@ class NumpyShardOps:
             key = (key << fb) | s
         return key
 
-    def table_signature(self, keylab, plan, lst, m):
-        qs = u32(lst)[:m]
+    @staticmethod
+    def _states(lst, m, base):
+        return np.arange(base, base + m, dtype=np.uint32) if lst is None else u32(lst)[:m]
+
+    def table_signature(self, keylab, plan, lst, m, base=0):
+        qs = self._states(lst, m, base)
         keys = self._keys(keylab, plan, 0, qs).astype(np.int64)
         tsize = 1 << plan.key_bits
         tmin = np.full(tsize, 0xFFFFFFFF, np.uint64)
@@ -86,18 +91,23 @@ class NumpyShardOps:
                 torch.from_numpy(tmin.astype(np.uint32).view(np.int32)),
                 torch.from_numpy(tcnt.astype(np.int32)))
 
-    def table_apply(self, lst, keys32, m, tmin, tcnt, lab, act):
-        qs = u32(lst)[:m]
+    def table_apply(self, plan, lst, keys32, m, tmin, tcnt, lab, act, next_keylab=None, base=0):
+        qs = self._states(lst, m, base)
         keys = u32(keys32)[:m].astype(np.int64)
         rep = u32(tmin)[keys]
         multi = tcnt.numpy()[keys] >= 2
+        if next_keylab is not None:
+            occ = (tcnt.numpy() > 0).astype(np.int64)
+            rank = np.cumsum(occ) - occ
+            nk = next_keylab.numpy().view(np.uint16 if next_keylab.dtype == torch.int16 else np.uint32)
+            nk[qs] = rank[keys]
         u32(lab)[qs] = rep
         act.numpy()[qs] = multi
         heads = rep == qs
         return torch.tensor([heads.sum(), (heads & multi).sum(), multi.sum(), 0], dtype=torch.int32)
 
-    def partition(self, keylab, plan, salt, lst, m, world):
-        qs = u32(lst)[:m]
+    def partition(self, keylab, plan, salt, lst, m, world, base=0):
+        qs = self._states(lst, m, base)
         key = self._keys(keylab, plan, salt, qs)
         hk = key if plan.strategy == 2 else mix64(key)
         dest = ((hk >> np.uint64(32)) * np.uint64(world)) >> np.uint64(32)
@@ -145,6 +155,8 @@ class NumpyShardOps:
 
     def compact(self, act, lo, hi):
         idx = (np.flatnonzero(act.numpy()[lo:hi]) + lo).astype(np.uint32)
+        if idx.size == hi - lo:
+            return None, int(idx.size)
         return torch.from_numpy(idx.view(np.int32).copy()), int(idx.size)
 
     def canonical(self, lab):
