@@ -9,8 +9,12 @@
 // reference's min_index policy exactly, so pass counts match bit for bit.
 // arbitrary(seed) uses a seeded per-pass bijection of q as priority (a
 // deterministic model of the CRCW arbitrary winner).
+#include <cooperative_groups.h>
+
 #include "prims.cuh"
 #include "refine.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace dk {
 
@@ -35,50 +39,17 @@ struct Prio {
     }
 };
 
-uint32_t inverse_odd(uint32_t a) {  // a * inv == 1 (mod 2^32), Newton iteration
+__host__ __device__ uint32_t inverse_odd(uint32_t a) {  // a * inv == 1 (mod 2^32), Newton iteration
     uint32_t x = a;
     for (int i = 0; i < 5; ++i) x *= 2u - a * x;
     return x;
 }
 
-Prio make_prio(int policy, uint64_t seed, uint64_t pass) {
+__host__ __device__ Prio make_prio(int policy, uint64_t seed, uint64_t pass) {
     if (policy == DFAKIT_POLICY_MIN_INDEX) return {0u, 1u, 1u, 1u};
     uint64_t h = mix64(seed * 0x9E3779B97F4A7C15ull + pass);
     uint32_t mul = (uint32_t)(h >> 32) | 1u;
     return {(uint32_t)h, mul, inverse_odd(mul), 0u};
-}
-
-// Alg. 2 l.9-11: split test against the leader + election.
-__global__ void __launch_bounds__(kThreads) elect_kernel(const uint32_t* __restrict__ delta, uint32_t n, uint32_t k,
-                                                         const uint32_t* __restrict__ lab,
-                                                         unsigned long long* __restrict__ slot, uint32_t epoch, Prio pr,
-                                                         uint32_t* __restrict__ split_list,
-                                                         uint32_t* __restrict__ split_count) {
-    for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
-        const uint32_t L = lab[q];
-        bool split = false;
-        if (L != q) {
-            for (uint32_t a = 0; a < k; ++a) {
-                const uint32_t* row = delta + (uint64_t)a * n;
-                if (lab[ld_stream(row + q)] != lab[row[L]]) {
-                    split = true;
-                    break;
-                }
-            }
-        }
-        if (split) atomicMin(&slot[L], ((unsigned long long)epoch << 32) | pr.enc(q));
-        uint32_t at = warp_append(split_count, split);
-        if (split) split_list[at] = q;
-    }
-}
-
-// Alg. 2 l.12-14: every split state follows its block's elected leader.
-__global__ void follow_kernel(const uint32_t* __restrict__ split_list, uint32_t cnt, uint32_t* __restrict__ lab,
-                              const unsigned long long* __restrict__ slot, Prio pr) {
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
-        const uint32_t q = split_list[i];
-        lab[q] = pr.dec((uint32_t)slot[lab[q]]);
-    }
 }
 
 // Alg. 3: election and reassignment in one pass.  Reads the pass-start
@@ -89,38 +60,122 @@ __device__ __forceinline__ uint32_t resolve(uint32_t v, const unsigned long long
     return (v & kPending) ? (uint32_t)prev_slot[v & ~kPending] : v;
 }
 
-__global__ void __launch_bounds__(kThreads) fused_kernel(const uint32_t* __restrict__ delta, uint32_t n, uint32_t k,
-                                                         const uint32_t* __restrict__ cur, uint32_t* __restrict__ next,
-                                                         const unsigned long long* __restrict__ prev_slot,
-                                                         unsigned long long* __restrict__ slot, uint32_t epoch,
-                                                         uint32_t* __restrict__ split_count) {
-    for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
-        const uint32_t L = resolve(cur[q], prev_slot);
-        bool split = false;
-        if (L != q) {
-            for (uint32_t a = 0; a < k; ++a) {
-                const uint32_t* row = delta + (uint64_t)a * n;
-                if (resolve(cur[ld_stream(row + q)], prev_slot) != resolve(cur[row[L]], prev_slot)) {
-                    split = true;
-                    break;
-                }
-            }
-        }
-        if (split) {
-            atomicMin(&slot[L], ((unsigned long long)epoch << 32) | q);
-            next[q] = kPending | L;
-        } else {
-            next[q] = L;
-        }
-        unsigned sm = __ballot_sync(__activemask(), split);
-        if (sm && (threadIdx.x & 31u) == (unsigned)(__ffs(sm) - 1)) atomicAdd(split_count, (uint32_t)__popc(sm));
-    }
-}
-
 __global__ void resolve_all_kernel(uint32_t* __restrict__ lab, uint32_t n,
                                    const unsigned long long* __restrict__ prev_slot) {
     for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x)
         lab[q] = resolve(lab[q], prev_slot);
+}
+
+// ---- persistent variants ---------------------------------------------------------
+//
+// The whole refinement in ONE cooperative launch: every CTA is resident, the
+// passes are separated by grid-wide barriers and the split count is read
+// from global memory by every thread, so a pass costs two barriers instead
+// of a host round trip (memset + launch + readback + launch).  Counters are
+// double-buffered by pass parity; the CTA that resets the next pass's counter
+// does so while nobody reads it.
+
+struct PersistOut {
+    uint32_t passes, iters;
+};
+
+// Alg. 2 (naive_pr): elect, barrier, follow, barrier.
+__global__ void __launch_bounds__(kThreads) naive_persistent_kernel(const uint32_t* __restrict__ delta, uint32_t n,
+                                                                    uint32_t k, uint32_t* __restrict__ lab,
+                                                                    unsigned long long* __restrict__ slot,
+                                                                    uint32_t* __restrict__ split_list,
+                                                                    uint32_t* __restrict__ cnt, int policy,
+                                                                    uint64_t seed, PersistOut* __restrict__ out) {
+    cg::grid_group grid = cg::this_grid();
+    const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
+    uint64_t pass = 0;
+    for (;; ++pass) {
+        const Prio pr = make_prio(policy, seed, pass);
+        const uint32_t epoch = 0xffffffffu - (uint32_t)pass;
+        uint32_t* c = cnt + (pass & 1);
+        for (uint32_t q = tid; q < n; q += stride) {
+            const uint32_t L = lab[q];
+            bool split = false;
+            if (L != q) {
+                for (uint32_t a = 0; a < k; ++a) {
+                    const uint32_t* row = delta + (uint64_t)a * n;
+                    if (lab[ld_stream(row + q)] != lab[row[L]]) {
+                        split = true;
+                        break;
+                    }
+                }
+            }
+            if (split) atomicMin(&slot[L], ((unsigned long long)epoch << 32) | pr.enc(q));
+            const uint32_t at = warp_append(c, split);
+            if (split) split_list[at] = q;
+        }
+        grid.sync();
+        const uint32_t total = *(volatile uint32_t*)c;
+        if (total == 0) break;
+        if (tid == 0) cnt[(pass + 1) & 1] = 0;
+        for (uint32_t i = tid; i < total; i += stride) {
+            const uint32_t q = split_list[i];
+            lab[q] = pr.dec((uint32_t)slot[lab[q]]);
+        }
+        grid.sync();
+    }
+    if (tid == 0) *out = PersistOut{(uint32_t)(pass + 1), (uint32_t)pass};
+}
+
+// Alg. 3 (naive_pr_fused): one barrier per pass; labels ping-pong.  cnt: 3 words.
+__global__ void __launch_bounds__(kThreads) fused_persistent_kernel(const uint32_t* __restrict__ delta, uint32_t n,
+                                                                    uint32_t k, uint32_t* __restrict__ lab0,
+                                                                    uint32_t* __restrict__ lab1,
+                                                                    unsigned long long* __restrict__ slot0,
+                                                                    unsigned long long* __restrict__ slot1,
+                                                                    uint32_t* __restrict__ cnt,
+                                                                    PersistOut* __restrict__ out) {
+    cg::grid_group grid = cg::this_grid();
+    const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
+    uint64_t pass = 0;
+    for (;; ++pass) {
+        const uint32_t* cur = (pass & 1) ? lab1 : lab0;
+        uint32_t* next = (pass & 1) ? lab0 : lab1;
+        const unsigned long long* prev_slot = (pass & 1) ? slot0 : slot1;
+        unsigned long long* slot = (pass & 1) ? slot1 : slot0;
+        const uint32_t epoch = 0xffffffffu - (uint32_t)pass;
+        // three counters: the one of pass p - 1 may still be read by threads
+        // leaving barrier p - 1; the one of pass p - 2 is free
+        uint32_t* c = cnt + (pass % 3);
+        if (tid == 0) cnt[(pass + 1) % 3] = 0;
+        for (uint32_t q = tid; q < n; q += stride) {
+            const uint32_t L = resolve(cur[q], prev_slot);
+            bool split = false;
+            if (L != q) {
+                for (uint32_t a = 0; a < k; ++a) {
+                    const uint32_t* row = delta + (uint64_t)a * n;
+                    if (resolve(cur[ld_stream(row + q)], prev_slot) != resolve(cur[row[L]], prev_slot)) {
+                        split = true;
+                        break;
+                    }
+                }
+            }
+            if (split) {
+                atomicMin(&slot[L], ((unsigned long long)epoch << 32) | q);
+                next[q] = kPending | L;
+            } else {
+                next[q] = L;
+            }
+            const unsigned sm = __ballot_sync(__activemask(), split);
+            if (sm && (threadIdx.x & 31u) == (unsigned)(__ffs(sm) - 1)) atomicAdd(c, (uint32_t)__popc(sm));
+        }
+        grid.sync();
+        if (*(volatile uint32_t*)c == 0) break;
+    }
+    if (tid == 0) *out = PersistOut{(uint32_t)(pass + 1), (uint32_t)pass};
+}
+
+unsigned coop_grid(Ctx* ctx, const void* kernel, uint32_t n) {
+    int per_sm = 0;
+    DK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, 0));
+    if (per_sm < 1) throw Error(DFAKIT_E_RESOURCE, "cooperative kernel does not fit an SM");
+    const uint64_t need = ((uint64_t)n + kThreads - 1) / kThreads;
+    return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(need, (uint64_t)per_sm * ctx->num_sms));
 }
 
 // Alg. 5 l.7: delta^T(q, a^(2^i)) = delta^T(delta^T(q, a^(2^(i-1))), a^(2^(i-1)))
@@ -159,22 +214,31 @@ RefineResult naive_pr_device(Ctx* ctx, const DevDfa& d, int policy, uint64_t see
     RefineResult res;
     DBuf<uint32_t> lab(n, s), split(n, s), scratch((uint64_t)n + 1, s);
     DBuf<unsigned long long> slot(n, s);
-    DBuf<uint32_t> cnt(1, s);
+    DBuf<uint32_t> cnt(2, s);
+    DBuf<PersistOut> out(1, s);
     DK_CUDA(cudaMemsetAsync(slot.get(), 0xff, (size_t)n * sizeof(unsigned long long), s));
+    DK_CUDA(cudaMemsetAsync(cnt.get(), 0, 2 * sizeof(uint32_t), s));
     init_leader_labels(ctx, d, li, lab.get(), s);
-    const unsigned g = grid_for(n);
-    for (uint64_t pass = 0;; ++pass) {
-        ++res.passes;
-        const Prio pr = make_prio(policy, seed, pass);
-        const uint32_t epoch = 0xffffffffu - (uint32_t)pass;
-        DK_CUDA(cudaMemsetAsync(cnt.get(), 0, sizeof(uint32_t), s));
-        DK_LAUNCH_B(ctx, (8.0 + 8.0 * d.k) * n, elect_kernel, g, kThreads, 0, s, d.delta, n, d.k, lab.get(), slot.get(), epoch, pr, split.get(),
-                  cnt.get());
-        uint32_t c = 0;
-        read_words(ctx, cnt.get(), sizeof(c), &c, s);
-        if (c == 0) break;
-        ++res.iters;
-        DK_LAUNCH(ctx, follow_kernel, grid_for(c), kThreads, 0, s, split.get(), c, lab.get(), slot.get(), pr);
+    {
+        const unsigned g = coop_grid(ctx, (const void*)naive_persistent_kernel, n);
+        const uint32_t* delta = d.delta;
+        uint32_t k = d.k;
+        uint32_t* labp = lab.get();
+        unsigned long long* slotp = slot.get();
+        uint32_t* splitp = split.get();
+        uint32_t* cntp = cnt.get();
+        PersistOut* outp = out.get();
+        uint32_t nn = n;
+        void* args[] = {(void*)&delta, (void*)&nn, (void*)&k, (void*)&labp, (void*)&slotp, (void*)&splitp,
+                        (void*)&cntp, (void*)&policy, (void*)&seed, (void*)&outp};
+        prof_begin_launch(ctx, s);
+        DK_CUDA(cudaLaunchCooperativeKernel((const void*)naive_persistent_kernel, g, kThreads, args, 0, s));
+        note_launch(ctx);
+        prof_end_launch(ctx, s, "naive_persistent_kernel", 0, 0);
+        PersistOut o{};
+        read_words(ctx, out.get(), sizeof(o), &o, s);
+        res.passes = o.passes;
+        res.iters = o.iters;
     }
     // min_index leaders are always block minima; arbitrary winners are not
     if (policy != DFAKIT_POLICY_MIN_INDEX) min_state_labels(ctx, lab.get(), n, scratch.get(), s);
@@ -191,27 +255,36 @@ RefineResult naive_pr_fused_device(Ctx* ctx, const DevDfa& d, uint32_t* block_ou
     RefineResult res;
     DBuf<uint32_t> lab0(n, s), lab1(n, s), scratch((uint64_t)n + 1, s);
     DBuf<unsigned long long> slot0(n, s), slot1(n, s);
-    DBuf<uint32_t> cnt(1, s);
+    DBuf<uint32_t> cnt(3, s);
+    DBuf<PersistOut> out(1, s);
     DK_CUDA(cudaMemsetAsync(slot0.get(), 0xff, (size_t)n * sizeof(unsigned long long), s));
     DK_CUDA(cudaMemsetAsync(slot1.get(), 0xff, (size_t)n * sizeof(unsigned long long), s));
+    DK_CUDA(cudaMemsetAsync(cnt.get(), 0, 3 * sizeof(uint32_t), s));
     init_leader_labels(ctx, d, li, lab0.get(), s);
-    uint32_t *cur = lab0.get(), *next = lab1.get();
-    unsigned long long *prev_slot = slot1.get(), *slot = slot0.get();
-    const unsigned g = grid_for(n);
-    for (uint64_t pass = 0;; ++pass) {
-        ++res.passes;
-        const uint32_t epoch = 0xffffffffu - (uint32_t)pass;
-        DK_CUDA(cudaMemsetAsync(cnt.get(), 0, sizeof(uint32_t), s));
-        DK_LAUNCH_B(ctx, (12.0 + 8.0 * d.k) * n, fused_kernel, g, kThreads, 0, s, d.delta, n, d.k, cur, next, prev_slot, slot, epoch, cnt.get());
-        uint32_t c = 0;
-        read_words(ctx, cnt.get(), sizeof(c), &c, s);
-        std::swap(cur, next);
-        std::swap(prev_slot, slot);
-        if (c == 0) break;
-        ++res.iters;
+    PersistOut o{};
+    {
+        const unsigned g = coop_grid(ctx, (const void*)fused_persistent_kernel, n);
+        const uint32_t* delta = d.delta;
+        uint32_t k = d.k, nn = n;
+        uint32_t *l0 = lab0.get(), *l1 = lab1.get(), *cntp = cnt.get();
+        unsigned long long *s0 = slot0.get(), *s1 = slot1.get();
+        PersistOut* outp = out.get();
+        void* args[] = {(void*)&delta, (void*)&nn, (void*)&k, (void*)&l0, (void*)&l1, (void*)&s0, (void*)&s1,
+                        (void*)&cntp, (void*)&outp};
+        prof_begin_launch(ctx, s);
+        DK_CUDA(cudaLaunchCooperativeKernel((const void*)fused_persistent_kernel, g, kThreads, args, 0, s));
+        note_launch(ctx);
+        prof_end_launch(ctx, s, "fused_persistent_kernel", 0, 0);
+        read_words(ctx, out.get(), sizeof(o), &o, s);
+        res.passes = o.passes;
+        res.iters = o.iters;
     }
+    // pass p read (lab, slot) index p & 1 and wrote index (p + 1) & 1; the
+    // last pass is o.passes - 1
+    uint32_t* cur = ((o.passes - 1) & 1) ? lab0.get() : lab1.get();
+    unsigned long long* prev_slot = ((o.passes - 1) & 1) ? slot1.get() : slot0.get();
     // the confirming pass wrote no pending labels; resolve defensively
-    DK_LAUNCH(ctx, resolve_all_kernel, g, kThreads, 0, s, cur, n, prev_slot);
+    DK_LAUNCH(ctx, resolve_all_kernel, grid_for(n), kThreads, 0, s, cur, n, prev_slot);
     res.num_blocks = canonical_from_min_labels(ctx, cur, n, block_out, scratch.get(), s);
     return res;
 }
