@@ -45,7 +45,8 @@ def parse_args():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["b200", "reference"], default="b200")
-    p.add_argument("--engine", choices=["auto", "single", "sharded"], default="auto")
+    p.add_argument("--engine", choices=["auto", "single", "sharded", "sharded-py"], default="auto",
+                   help="auto: single-GPU engine at N = 1, the native (C++ / NCCL) sharded engine at N > 1")
     p.add_argument("--states", type=int, default=10_000_000, help="states per GPU")
     p.add_argument("--alphabet", type=int, default=10)
     p.add_argument("--seed", type=int, default=1)
@@ -283,7 +284,7 @@ def run_b200(args, rank, world, local):
     torch.cuda.set_device(local)
     engine = args.engine if args.engine != "auto" else ("single" if world == 1 else "sharded")
     import torch.distributed as dist
-    if world > 1 or engine == "sharded":
+    if world > 1 or engine.startswith("sharded"):
         if world == 1:
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
             os.environ.setdefault("MASTER_PORT", str(free_port()))
@@ -308,13 +309,14 @@ def run_b200(args, rank, world, local):
     ctx = dk.Context(local)
     lib_stream = torch.cuda.ExternalStream(ctx.stream)
     k = args.alphabet
-    n = args.states * (world if engine == "sharded" else 1)
+    sharded_engine = engine.startswith("sharded")
+    n = args.states * (world if sharded_engine else 1)
     delta = torch.empty(k * n, dtype=torch.int32, device="cuda")
     acc = torch.empty(n, dtype=torch.uint8, device="cuda")
     blocks = torch.empty(n, dtype=torch.int32, device="cuda")
     # the same automaton on every rank (replicated input of the sharded engine);
     # the single-GPU engine's replicas minimise their own seeds
-    gseed = args.seed if engine == "sharded" else args.seed + rank
+    gseed = args.seed if sharded_engine else args.seed + rank
     nat.check(nat.lib.dfakit_gen_synth_device(ctx.handle, n, k, gseed, delta.data_ptr(), acc.data_ptr(), ctx.stream))
     torch.cuda.synchronize()
     opts = nat.COptions(0, 0, 0, 0, 0, 64, 0)
@@ -329,6 +331,14 @@ def run_b200(args, rank, world, local):
                                                      C.byref(opts), blocks.data_ptr(), C.byref(rep), ctx.stream))
             state["passes"], state["iters"], state["blocks"] = int(rep.passes), int(rep.refining_iterations), \
                 int(rep.num_blocks)
+    elif engine == "sharded":
+        ncomm = sharded.NativeComm(ctx)
+
+        def step():
+            b, r = sharded.sort_pr_sharded_native(ctx, ncomm, delta, acc, n, k, out=blocks)
+            state["passes"], state["iters"], state["blocks"] = r.passes, r.refining_iterations, r.num_blocks
+            state["exchanged"] = r.exchanged_entries
+            state["out"] = b
     else:
         comm = sharded.TorchComm()
         ops = sharded.CudaShardOps(ctx, delta, acc, n, k)
@@ -360,7 +370,7 @@ def run_b200(args, rank, world, local):
     ms_step = ms_total / args.steps
     passes = state["passes"]
     transitions = n * k * passes  # the whole automaton's transitions, every pass
-    value = transitions * (world if engine == "single" else 1) / (ms_step / 1000.0)
+    value = transitions * (1 if sharded_engine else world) / (ms_step / 1000.0)
 
     # measured ceiling of the random label gathers, then the live per-kernel profile
     gather_peak = C.c_double(0)
@@ -389,7 +399,8 @@ def run_b200(args, rank, world, local):
             if rank == 0:
                 h_blocks.copy_(state["out"], non_blocking=True)
             torch.cuda.synchronize()
-        h2d, d2h, api = 4 * k * n + n, 4 * n if rank == 0 else 0, "sharded.sort_pr_sharded (inputs copied from pinned host memory on every rank)"
+        h2d, d2h, api = 4 * k * n + n, 4 * n if rank == 0 else 0, \
+            f"sharded engine ({engine}; inputs copied from pinned host memory on every rank)"
     for _ in range(max(1, args.warmup)):
         e2e_step()
     barrier()
@@ -398,18 +409,26 @@ def run_b200(args, rank, world, local):
         e2e_step()
     torch.cuda.synchronize()
     e2e_s = max_over_ranks(time.perf_counter() - t0) / args.steps
-    e2e_transitions = transitions * (world if engine == "single" else 1)
+    e2e_transitions = transitions * (1 if sharded_engine else world)
     e2e = {"value": e2e_transitions / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
            "ms_per_step": e2e_s * 1000.0, "api": api}
 
-    cfg = {"workload": workload_name(n, k, world if engine == "sharded" else 1), "states": n, "alphabet": k,
+    cfg = {"workload": workload_name(n, k, world if sharded_engine else 1), "states": n, "alphabet": k,
            "transitions": n * k, "algorithm": "sort_pr", "engine": engine, "passes": passes,
            "refining_iterations": state["iters"], "num_blocks": state["blocks"], "wall_ms_to_minimal_dfa": ms_step,
            "l2": f"inputs larger than L2 (delta {4 * k * n / 1e6:.0f} MB per rank > 126 MB L2)",
-           "parallelism": (f"sharded x{world} (NCCL all-to-all + label allgather per pass)" if engine == "sharded"
+           "parallelism": (f"sharded x{world} (NCCL all-to-all + label allgather per pass)" if sharded_engine
                            else (f"replicas x{world}" if world > 1 else "single GPU"))}
-    if engine == "sharded":
-        cfg["entries_exchanged_per_step_rank0"] = state.get("exchanged", 0)
+    if sharded_engine:
+        ex = state.get("exchanged", 0)
+        # per rank and step over NVLink: 16 B out + 4 B back per exchanged entry,
+        # plus the label allgather (4 B per state and pass, all but the own slice)
+        nv_bytes = 20 * ex + 4 * n * (world - 1) / world * max(state["iters"], 1)
+        cfg["entries_exchanged_per_step_rank0"] = ex
+        if world > 1:
+            cfg["nvlink"] = {"bytes_per_rank_per_step": nv_bytes, "GBps_per_rank": nv_bytes / (ms_step / 1000.0) / 1e9,
+                             "peak_GBps": 770.0, "frac": nv_bytes / (ms_step / 1000.0) / 1e9 / 770.0,
+                             "peak_source": "B200_PROFILING.md measured peer copy per direction"}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u32", "data": "synthetic", "config": cfg, "roofline": roofline, "e2e": e2e,
@@ -459,7 +478,7 @@ def extras(dk, nat, ctx, torch, sharded, args):
     s, r = timed(minimize(view, "sort_pr", b, nat.COptions(0, 0, 0, 0, 0, 64, 1)), 3)
     out["sort_pr_radix_sort_grouping_10M_k10"] = {"ms": s * 1000, "passes": int(r.passes),
                                                   "transitions_per_s": n * k * int(r.passes) / s}
-    # the sharded engine at world size 1 (its per-pass exchange logic, no peers)
+    # the sharded engines at world size 1 (their per-pass exchange logic, no peers)
     import torch.distributed as dist
     own_pg = not dist.is_initialized()
     if own_pg:
@@ -469,8 +488,13 @@ def extras(dk, nat, ctx, torch, sharded, args):
     comm = sharded.TorchComm()
     ops = sharded.CudaShardOps(ctx, d, a, n, k)
     s, (bl, rr) = timed(lambda: sharded.sort_pr_sharded(ops, comm, n, k), 3)
-    out["sort_pr_sharded_engine_world1_10M_k10"] = {"ms": s * 1000, "passes": rr.passes,
+    out["sort_pr_sharded_py_world1_10M_k10"] = {"ms": s * 1000, "passes": rr.passes,
+                                                "transitions_per_s": n * k * rr.passes / s}
+    ncomm = sharded.NativeComm(ctx)
+    s, (bl, rr) = timed(lambda: sharded.sort_pr_sharded_native(ctx, ncomm, d, a, n, k, out=b), 3)
+    out["sort_pr_sharded_native_world1_10M_k10"] = {"ms": s * 1000, "passes": rr.passes,
                                                     "transitions_per_s": n * k * rr.passes / s}
+    ncomm.close()
     if own_pg:
         dist.destroy_process_group()
     del d, a, b

@@ -269,6 +269,21 @@ dfakit_status dfakit_shard_compact(dfakit_ctx* ctx, const uint8_t* act, uint32_t
 dfakit_status dfakit_shard_canonical(dfakit_ctx* ctx, const uint32_t* lab, uint32_t n, uint32_t* block_of,
                                      uint32_t* num_blocks, void* stream);
 
+/* Native sharded driver: the same pass loop in C++ with NCCL collectives on
+ * the caller's stream (NCCL resolved with dlopen; DFAKIT_E_RESOURCE when no
+ * libnccl.so.2 is found).  Rank 0 calls dfakit_comm_unique_id and shares the
+ * 128 bytes with every rank out of band (e.g. a torch.distributed
+ * broadcast); every rank then calls dfakit_comm_init and
+ * dfakit_sort_pr_sharded with the full automaton resident on its device.
+ * block_of (device, n entries) receives the canonical partition on every
+ * rank; exchanged (optional) the entries this rank sent. */
+typedef struct dfakit_comm dfakit_comm;
+dfakit_status dfakit_comm_unique_id(uint8_t* id128);
+dfakit_status dfakit_comm_init(dfakit_ctx* ctx, const uint8_t* id128, int world, int rank, dfakit_comm** out);
+void dfakit_comm_destroy(dfakit_comm* comm);
+dfakit_status dfakit_sort_pr_sharded(dfakit_ctx* ctx, dfakit_comm* comm, const dfakit_dfa* dfa, uint32_t* block_of,
+                                     dfakit_report* report, uint64_t* exchanged, void* stream);
+
 /* ---- calibration ---------------------------------------------------------------
  * Measured ceiling of the signature kernels' random block-label gathers:
  * independent random gathers of elem_bytes (1, 2, 4) from a table of

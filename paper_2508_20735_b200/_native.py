@@ -104,6 +104,10 @@ _sig = {
     "dfakit_permute_states_device": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint64, C.c_void_p,
                                                C.c_void_p, C.c_void_p, C.c_void_p, _P(C.c_uint32), C.c_void_p]),
     "dfakit_calibrate_gather": (C.c_int, [_V, C.c_uint64, C.c_uint32, C.c_uint64, _P(C.c_double)]),
+    "dfakit_comm_unique_id": (C.c_int, [_V]),
+    "dfakit_comm_init": (C.c_int, [_V, _V, C.c_int, C.c_int, _P(C.c_void_p)]),
+    "dfakit_comm_destroy": (None, [_V]),
+    "dfakit_sort_pr_sharded": (C.c_int, [_V, _V, _P(CDfa), _V, _P(CReport), _P(C.c_uint64), _V]),
     # sharded sort_pr primitives (sharded.py)
     "dfakit_plan_pass": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint32, C.c_uint32,
                                    _P(CPassPlan)]),

@@ -20,6 +20,10 @@ struct dfakit_ctx {
     dk::Ctx* c;
 };
 
+struct dfakit_comm {
+    dk::NcclComm* c;
+};
+
 namespace {
 
 thread_local std::string g_last_error;
@@ -449,6 +453,43 @@ dfakit_status dfakit_permute_states_device(dfakit_ctx* ctx, uint32_t n, uint32_t
         uint32_t init = dk::permute_states_device(ctx->c, n, k, seed, delta, accepting, out_delta, out_accepting,
                                                   stream ? (cudaStream_t)stream : ctx->c->stream);
         if (initial_out) *initial_out = init;
+    });
+}
+
+dfakit_status dfakit_comm_unique_id(uint8_t* id128) {
+    return guard([&] {
+        if (!id128) throw dk::Error(DFAKIT_E_INVALID, "null id");
+        dk::nccl_unique_id(id128);
+    });
+}
+
+dfakit_status dfakit_comm_init(dfakit_ctx* ctx, const uint8_t* id128, int world, int rank, dfakit_comm** out) {
+    return on_device(ctx, nullptr, [&](dk::Ctx* c, cudaStream_t) {
+        if (!id128 || !out) throw dk::Error(DFAKIT_E_INVALID, "null argument");
+        *out = nullptr;
+        dk::NcclComm* nc = dk::nccl_comm_init(c, id128, world, rank);
+        *out = new dfakit_comm{nc};
+    });
+}
+
+void dfakit_comm_destroy(dfakit_comm* comm) {
+    if (!comm) return;
+    dk::nccl_comm_destroy(comm->c);
+    delete comm;
+}
+
+dfakit_status dfakit_sort_pr_sharded(dfakit_ctx* ctx, dfakit_comm* comm, const dfakit_dfa* dfa, uint32_t* block_of,
+                                     dfakit_report* report, uint64_t* exchanged, void* stream) {
+    return on_device(ctx, stream, [&](dk::Ctx* c, cudaStream_t s) {
+        if (!comm) throw dk::Error(DFAKIT_E_INVALID, "null communicator");
+        check_view(dfa, "sort_pr_sharded");
+        DK_CUDA(cudaEventRecord(c->ev0, s));
+        const dk::RefineResult rr = dk::sort_pr_sharded_device(c, comm->c, device_view(dfa), block_of, s, exchanged);
+        DK_CUDA(cudaEventRecord(c->ev1, s));
+        DK_CUDA(cudaEventSynchronize(c->ev1));
+        float ms = 0;
+        DK_CUDA(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+        fill_report(report, rr, DFAKIT_ALGO_SORT_PR, dfa->num_states, dfa->alphabet_size, ms);
     });
 }
 

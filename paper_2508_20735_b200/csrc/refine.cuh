@@ -65,6 +65,14 @@ void shard_apply(Ctx* ctx, const uint4* send, const uint32_t* results, uint64_t 
 void shard_compact(Ctx* ctx, const uint8_t* act, uint32_t lo, uint32_t hi, uint32_t* list, uint32_t* count_dev,
                    cudaStream_t s);
 
+// Native sharded driver over NCCL (shard_driver.cu).
+struct NcclComm;
+void nccl_unique_id(uint8_t out[128]);
+NcclComm* nccl_comm_init(Ctx* ctx, const uint8_t id[128], int world, int rank);
+void nccl_comm_destroy(NcclComm* c);
+RefineResult sort_pr_sharded_device(Ctx* ctx, NcclComm* comm, const DevDfa& d, uint32_t* block_out, cudaStream_t s,
+                                    uint64_t* exchanged);
+
 // All block_out arrays are device arrays of n entries, canonical numbering.
 RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uint32_t* block_out, cudaStream_t s);
 RefineResult naive_pr_device(Ctx* ctx, const DevDfa& d, int policy, uint64_t seed, uint32_t* block_out,

@@ -79,6 +79,38 @@ struct PersistOut {
     uint32_t passes, iters;
 };
 
+// Does q differ from its leader L on some letter?  Loads of a chunk of 8
+// letters are issued together (delta rows of q and L, then the labels), so
+// a thread waits on two memory latencies per chunk, not per letter; the
+// early exit is per chunk.  lab_of maps a stored label to the current one.
+template <typename F>
+__device__ __forceinline__ bool differs_from_leader(uint32_t q, uint32_t L, const uint32_t* __restrict__ delta,
+                                                    uint32_t n, uint32_t k, const uint32_t* lab, F lab_of) {
+    constexpr int C = 8;
+    for (uint32_t a = 0; a < k; a += C) {
+        uint32_t tq[C], tl[C];
+#pragma unroll
+        for (int j = 0; j < C; ++j)
+            if (a + j < k) {
+                const uint32_t* row = delta + (uint64_t)(a + j) * n;
+                tq[j] = ld_stream(row + q);
+                tl[j] = row[L];
+            }
+#pragma unroll
+        for (int j = 0; j < C; ++j)
+            if (a + j < k) {
+                tq[j] = lab[tq[j]];
+                tl[j] = lab[tl[j]];
+            }
+        bool diff = false;
+#pragma unroll
+        for (int j = 0; j < C; ++j)
+            if (a + j < k) diff |= lab_of(tq[j]) != lab_of(tl[j]);
+        if (diff) return true;
+    }
+    return false;
+}
+
 // Alg. 2 (naive_pr): elect, barrier, follow, barrier.
 __global__ void __launch_bounds__(kThreads) naive_persistent_kernel(const uint32_t* __restrict__ delta, uint32_t n,
                                                                     uint32_t k, uint32_t* __restrict__ lab,
@@ -95,16 +127,7 @@ __global__ void __launch_bounds__(kThreads) naive_persistent_kernel(const uint32
         uint32_t* c = cnt + (pass & 1);
         for (uint32_t q = tid; q < n; q += stride) {
             const uint32_t L = lab[q];
-            bool split = false;
-            if (L != q) {
-                for (uint32_t a = 0; a < k; ++a) {
-                    const uint32_t* row = delta + (uint64_t)a * n;
-                    if (lab[ld_stream(row + q)] != lab[row[L]]) {
-                        split = true;
-                        break;
-                    }
-                }
-            }
+            const bool split = L != q && differs_from_leader(q, L, delta, n, k, lab, [](uint32_t v) { return v; });
             if (split) atomicMin(&slot[L], ((unsigned long long)epoch << 32) | pr.enc(q));
             const uint32_t at = warp_append(c, split);
             if (split) split_list[at] = q;
@@ -145,16 +168,8 @@ __global__ void __launch_bounds__(kThreads) fused_persistent_kernel(const uint32
         if (tid == 0) cnt[(pass + 1) % 3] = 0;
         for (uint32_t q = tid; q < n; q += stride) {
             const uint32_t L = resolve(cur[q], prev_slot);
-            bool split = false;
-            if (L != q) {
-                for (uint32_t a = 0; a < k; ++a) {
-                    const uint32_t* row = delta + (uint64_t)a * n;
-                    if (resolve(cur[ld_stream(row + q)], prev_slot) != resolve(cur[row[L]], prev_slot)) {
-                        split = true;
-                        break;
-                    }
-                }
-            }
+            const bool split = L != q && differs_from_leader(q, L, delta, n, k, cur,
+                                                             [&](uint32_t v) { return resolve(v, prev_slot); });
             if (split) {
                 atomicMin(&slot[L], ((unsigned long long)epoch << 32) | q);
                 next[q] = kPending | L;
@@ -174,8 +189,11 @@ unsigned coop_grid(Ctx* ctx, const void* kernel, uint32_t n) {
     int per_sm = 0;
     DK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, 0));
     if (per_sm < 1) throw Error(DFAKIT_E_RESOURCE, "cooperative kernel does not fit an SM");
+    // a grid barrier costs more with more CTAs: small automata (many cheap
+    // passes) run one CTA per SM, large ones fill every SM
     const uint64_t need = ((uint64_t)n + kThreads - 1) / kThreads;
-    return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(need, (uint64_t)per_sm * ctx->num_sms));
+    const uint64_t cap = n <= (1u << 22) ? (uint64_t)ctx->num_sms : (uint64_t)per_sm * ctx->num_sms;
+    return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(need, cap));
 }
 
 // Alg. 5 l.7: delta^T(q, a^(2^i)) = delta^T(delta^T(q, a^(2^(i-1))), a^(2^(i-1)))

@@ -1,0 +1,297 @@
+// shard_driver.cu -- the sharded sortPR pass loop in C++ over NCCL.
+//
+// Same protocol as paper_2508_20735_b200/sharded.py (whose gloo CPU tests pin
+// it), driven natively: one process per GPU, the shard primitives of
+// refine_sort.cu on the caller's stream, NCCL collectives on the same
+// stream.  Per pass:
+//   table plans:  local (min, count) table -> ncclAllReduce MIN / SUM ->
+//                 relabel own states (+ ranks as next key labels when the
+//                 pass covered every state);
+//   wide plans:   entries partitioned by owner -> grouped ncclSend/ncclRecv
+//                 (16 B per active state) -> owner groups -> counters
+//                 allreduced (collision => every rank retries with a new
+//                 salt) -> results back (4 B per entry) -> apply;
+//   then ncclAllGather of the label slices (the per-pass block-ID
+//   allgather) and the next local active list.
+// NCCL is resolved with dlopen at first use (the library has no link-time
+// NCCL dependency; a process that already loaded NCCL, e.g. through torch,
+// shares that copy).
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+
+#include "prims.cuh"
+#include "refine.cuh"
+
+namespace dk {
+
+namespace {
+
+struct NcclApi {
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*);
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int);
+    ncclResult_t (*CommDestroy)(ncclComm_t);
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t);
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t);
+    ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+    ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+    ncclResult_t (*GroupStart)();
+    ncclResult_t (*GroupEnd)();
+    const char* (*GetErrorString)(ncclResult_t);
+};
+
+const NcclApi& nccl() {
+    static NcclApi api{};
+    static std::string err;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            err = "libnccl.so.2 not found";
+            return;
+        }
+        auto sym = [&](const char* n) {
+            void* p = dlsym(h, n);
+            if (!p) err = std::string("NCCL symbol missing: ") + n;
+            return p;
+        };
+        api.GetUniqueId = (decltype(api.GetUniqueId))sym("ncclGetUniqueId");
+        api.CommInitRank = (decltype(api.CommInitRank))sym("ncclCommInitRank");
+        api.CommDestroy = (decltype(api.CommDestroy))sym("ncclCommDestroy");
+        api.AllReduce = (decltype(api.AllReduce))sym("ncclAllReduce");
+        api.AllGather = (decltype(api.AllGather))sym("ncclAllGather");
+        api.Send = (decltype(api.Send))sym("ncclSend");
+        api.Recv = (decltype(api.Recv))sym("ncclRecv");
+        api.GroupStart = (decltype(api.GroupStart))sym("ncclGroupStart");
+        api.GroupEnd = (decltype(api.GroupEnd))sym("ncclGroupEnd");
+        api.GetErrorString = (decltype(api.GetErrorString))sym("ncclGetErrorString");
+    });
+    if (!err.empty()) throw Error(DFAKIT_E_RESOURCE, err);
+    return api;
+}
+
+void nccl_check(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess) throw Error(DFAKIT_E_CUDA, std::string(what) + ": " + nccl().GetErrorString(r));
+}
+
+uint64_t mix64_host(uint64_t z) { return mix64(z); }
+
+// one grouped send/recv round: element_bytes-sized elements, counts per peer
+void all_to_all_v(const NcclApi& api, ncclComm_t comm, int world, const void* send,
+                  const std::vector<uint64_t>& scount, void* recv, const std::vector<uint64_t>& rcount,
+                  size_t element_bytes, cudaStream_t s) {
+    nccl_check(api.GroupStart(), "ncclGroupStart");
+    uint64_t so = 0, ro = 0;
+    for (int r = 0; r < world; ++r) {
+        if (scount[r])
+            nccl_check(api.Send(static_cast<const char*>(send) + so * element_bytes, scount[r] * element_bytes,
+                                ncclUint8, r, comm, s),
+                       "ncclSend");
+        if (rcount[r])
+            nccl_check(api.Recv(static_cast<char*>(recv) + ro * element_bytes, rcount[r] * element_bytes, ncclUint8,
+                                r, comm, s),
+                       "ncclRecv");
+        so += scount[r];
+        ro += rcount[r];
+    }
+    nccl_check(api.GroupEnd(), "ncclGroupEnd");
+}
+
+}  // namespace
+
+struct NcclComm {
+    ncclComm_t comm = nullptr;
+    int world = 1, rank = 0;
+};
+
+void nccl_unique_id(uint8_t out[128]) {
+    ncclUniqueId id;
+    nccl_check(nccl().GetUniqueId(&id), "ncclGetUniqueId");
+    static_assert(sizeof(id) == 128, "NCCL unique id size");
+    std::memcpy(out, &id, sizeof(id));
+}
+
+NcclComm* nccl_comm_init(Ctx* ctx, const uint8_t id[128], int world, int rank) {
+    if (world < 1 || rank < 0 || rank >= world) throw Error(DFAKIT_E_INVALID, "comm_init: bad rank / world");
+    DK_CUDA(cudaSetDevice(ctx->device));
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, sizeof(uid));
+    NcclComm* c = new NcclComm();
+    c->world = world;
+    c->rank = rank;
+    const ncclResult_t r = nccl().CommInitRank(&c->comm, world, uid, rank);
+    if (r != ncclSuccess) {
+        delete c;
+        nccl_check(r, "ncclCommInitRank");
+    }
+    return c;
+}
+
+void nccl_comm_destroy(NcclComm* c) {
+    if (!c) return;
+    if (c->comm) nccl().CommDestroy(c->comm);
+    delete c;
+}
+
+RefineResult sort_pr_sharded_device(Ctx* ctx, NcclComm* cm, const DevDfa& d, uint32_t* block_out, cudaStream_t s,
+                                    uint64_t* exchanged) {
+    const NcclApi& api = nccl();
+    RefineResult res;
+    const uint32_t n = d.n, k = d.k;
+    const int world = cm->world, rank = cm->rank;
+    if (n == 0) return res;
+    if (n > 0x7fffffffu) throw Error(DFAKIT_E_INVALID, "sharded sort_pr: at most 2^31 - 1 states");
+    const uint32_t shard = (uint32_t)(((uint64_t)n + world - 1) / world);
+    const uint32_t lo = std::min<uint64_t>(n, (uint64_t)rank * shard);
+    const uint32_t hi = std::min<uint64_t>(n, (uint64_t)(rank + 1) * shard);
+    DBuf<uint32_t> lab((uint64_t)world * shard, s), list(std::max(1u, hi - lo), s), scratch((uint64_t)n + 1, s);
+    DBuf<uint8_t> act(n, s);
+    DBuf<uint32_t> dctr(8, s), counts(world, s), keys32;
+    DBuf<uint8_t> kl8;
+    DBuf<uint16_t> kl16, next16;
+    DBuf<uint32_t> kl32, next32, tmin, tcnt, results, back;
+    DBuf<uint4> send, recv;
+    uint32_t* hmail = reinterpret_cast<uint32_t*>(ctx->mailbox);
+    auto read_u32 = [&](const uint32_t* p, size_t count, uint32_t* out) {
+        read_words(ctx, p, count * sizeof(uint32_t), out, s);
+    };
+    (void)hmail;
+
+    const ShardInit si = shard_init(ctx, d, lo, hi, lab.get(), act.get(), s);
+    uint32_t B = si.num_blocks, A = si.active_blocks;
+    uint64_t m_total = si.active_states;
+    uint32_t m = 0;
+    auto compact = [&] {
+        shard_compact(ctx, act.get(), lo, hi, list.get(), dctr.get() + 4, s);
+        read_u32(dctr.get() + 4, 1, &m);
+    };
+    compact();
+    uint64_t salt = 0x5EED5EED5EEDull;
+    uint32_t strikes = 0;
+    const void* carried = nullptr;  // key labels of the current partition (ranks of a full table pass)
+    uint32_t carried_bytes = 0;
+    uint64_t sent = 0;
+    while (m_total > 0) {
+        ++res.passes;
+        PassPlan plan = plan_pass(n, k, B, m_total, std::min(strikes, 2u), false);
+        if (plan.strategy == kPlanChunked) {  // sharded: fingerprints with fresh salts instead
+            plan.strategy = kPlanFingerprint;
+            plan.field_bits = 0;
+            plan.key_bits = 64;
+            plan.keylab_bytes = 0;
+        }
+        const uint32_t* lst = m == hi - lo ? nullptr : list.get();
+        const void* keylab = lab.get();
+        if (plan.keylab_bytes) {
+            if (carried) {
+                keylab = carried;
+                plan.keylab_bytes = carried_bytes;
+            } else {
+                void* out;
+                if (plan.keylab_bytes == 1) {
+                    if (!kl8.get()) kl8.alloc(n, s);
+                    out = kl8.get();
+                } else if (plan.keylab_bytes == 2) {
+                    if (!kl16.get()) kl16.alloc(n, s);
+                    out = kl16.get();
+                } else {
+                    if (!kl32.get()) kl32.alloc(n, s);
+                    out = kl32.get();
+                }
+                shard_keylab(ctx, lab.get(), n, B, plan, out, scratch.get(), s);
+                keylab = out;
+            }
+        }
+        carried = nullptr;
+        void* next_kl = nullptr;
+        uint32_t ctr[4];
+        if (plan.strategy == kPlanTable) {
+            const uint64_t tsize = 1ull << plan.key_bits;
+            if (tmin.n < tsize) {
+                tmin.alloc(tsize, s);
+                tcnt.alloc(tsize, s);
+            }
+            if (keys32.n < std::max(1u, m)) keys32.alloc(std::max(1u, hi - lo), s);
+            shard_table_signature(ctx, d, keylab, plan, lst, lo, m, keys32.get(), tmin.get(), tcnt.get(), s);
+            nccl_check(api.AllReduce(tmin.get(), tmin.get(), tsize, ncclUint32, ncclMin, cm->comm, s), "allreduce");
+            nccl_check(api.AllReduce(tcnt.get(), tcnt.get(), tsize, ncclUint32, ncclSum, cm->comm, s), "allreduce");
+            if (hi > lo) DK_CUDA(cudaMemsetAsync(act.get() + lo, 0, hi - lo, s));
+            if (m_total == n) {
+                // every block of the next partition is one table key
+                if (plan.key_bits <= 16) {
+                    if (!next16.get()) next16.alloc((uint64_t)world * shard, s);
+                    next_kl = next16.get();
+                } else {
+                    if (!next32.get()) next32.alloc((uint64_t)world * shard, s);
+                    next_kl = next32.get();
+                }
+            }
+            shard_table_apply(ctx, plan, lst, lo, keys32.get(), m, tmin.get(), tcnt.get(), lab.get(), act.get(),
+                              next_kl, dctr.get(), s);
+            nccl_check(api.AllReduce(dctr.get(), dctr.get(), 4, ncclUint32, ncclSum, cm->comm, s), "allreduce");
+            read_u32(dctr.get(), 4, ctr);
+        } else {
+            if (send.n < std::max(1u, m)) send.alloc(std::max(1u, hi - lo), s);
+            shard_sig_partition(ctx, d, keylab, plan, salt, lst, lo, m, (uint32_t)world, send.get(), counts.get(), s);
+            std::vector<uint32_t> sc32(world), rc32(world);
+            read_u32(counts.get(), world, sc32.data());
+            std::vector<uint64_t> scount(world), rcount(world), ones(world, 1);
+            for (int r = 0; r < world; ++r) scount[r] = sc32[r];
+            // counts: one word to every peer
+            DBuf<uint32_t> rc(world, s);
+            all_to_all_v(api, cm->comm, world, counts.get(), ones, rc.get(), ones, sizeof(uint32_t), s);
+            read_u32(rc.get(), world, rc32.data());
+            uint64_t rtotal = 0;
+            for (int r = 0; r < world; ++r) rtotal += (rcount[r] = rc32[r]);
+            if (recv.n < std::max<uint64_t>(1, rtotal)) recv.alloc(std::max<uint64_t>(1, rtotal) * 5 / 4, s);
+            all_to_all_v(api, cm->comm, world, send.get(), scount, recv.get(), rcount, sizeof(uint4), s);
+            sent += m;
+            if (results.n < std::max<uint64_t>(1, rtotal)) results.alloc(std::max<uint64_t>(1, rtotal) * 5 / 4, s);
+            shard_group(ctx, d, lab.get(), plan, recv.get(), rtotal, results.get(), dctr.get(), s);
+            nccl_check(api.AllReduce(dctr.get(), dctr.get(), 4, ncclUint32, ncclSum, cm->comm, s), "allreduce");
+            read_u32(dctr.get(), 4, ctr);
+            if (ctr[3]) {
+                // verified fingerprint collision on some owner: nothing applied
+                ++res.collisions;
+                --res.passes;
+                if (++strikes > 16) throw Error(DFAKIT_E_RESOURCE, "sharded sort_pr: repeated fingerprint collisions");
+                salt = mix64_host(salt + 0x1234567ull);
+                continue;
+            }
+            if (B - A + ctr[0] == B) break;  // fixed point (reference l.411)
+            if (back.n < std::max(1u, m)) back.alloc(std::max(1u, hi - lo), s);
+            all_to_all_v(api, cm->comm, world, results.get(), rcount, back.get(), scount, sizeof(uint32_t), s);
+            if (hi > lo) DK_CUDA(cudaMemsetAsync(act.get() + lo, 0, hi - lo, s));
+            shard_apply(ctx, send.get(), back.get(), m, lab.get(), act.get(), s);
+        }
+        strikes = 0;
+        const uint32_t newB = B - A + ctr[0];
+        if (newB == B) break;  // fixed point
+        ++res.iters;
+        B = newB;
+        A = ctr[1];
+        m_total = ctr[2];
+        nccl_check(api.AllGather(lab.get() + (uint64_t)rank * shard, lab.get(), shard * sizeof(uint32_t), ncclUint8,
+                                 cm->comm, s),
+                   "allgather");
+        if (next_kl) {
+            const size_t es = plan.key_bits <= 16 ? 2 : 4;
+            nccl_check(api.AllGather(static_cast<char*>(next_kl) + (uint64_t)rank * shard * es, next_kl, shard * es,
+                                     ncclUint8, cm->comm, s),
+                       "allgather");
+            carried = next_kl;
+            carried_bytes = (uint32_t)es;
+        }
+        compact();
+    }
+    res.num_blocks = canonical_from_min_labels(ctx, lab.get(), n, block_out, scratch.get(), s);
+    if (exchanged) *exchanged = sent;
+    return res;
+}
+
+}  // namespace dk

@@ -329,3 +329,54 @@ def sort_pr_sharded(ops, comm, n: int, k: int, max_collision_retries: int = 16):
     blocks, nb = ops.canonical(lab)
     rep.num_blocks = nb
     return blocks, rep
+
+
+class NativeComm:
+    """An NCCL communicator owned by the library (dfakit_comm_init): rank 0's
+    NCCL unique id travels to the other ranks by a torch.distributed
+    broadcast; the pass loop then runs in C++ (dfakit_sort_pr_sharded)."""
+
+    def __init__(self, ctx: Context, group=None):
+        import torch
+        import torch.distributed as dist
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        uid = torch.zeros(128, dtype=torch.uint8)
+        if self.rank == 0:
+            check(lib.dfakit_comm_unique_id(uid.data_ptr()))
+        t = uid.cuda() if dist.get_backend(group) == "nccl" else uid
+        dist.broadcast(t, src=0, group=group)
+        uid = t.cpu().contiguous()
+        h = C.c_void_p()
+        check(lib.dfakit_comm_init(ctx.handle, uid.data_ptr(), self.world, self.rank, C.byref(h)))
+        self.handle = h
+
+    def close(self):
+        if self.handle:
+            lib.dfakit_comm_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def sort_pr_sharded_native(ctx: Context, comm: NativeComm, delta, acc, n: int, k: int, out=None):
+    """The sharded pass loop in C++ over NCCL (same protocol as
+    sort_pr_sharded).  delta / acc: full automaton on this rank's device.
+    Returns (block_of tensor, ShardReport)."""
+    import torch
+    from ._native import CReport
+    dev = acc.device
+    if out is None:
+        out = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    view = _CDfa(n, k, delta.data_ptr() if k else None, acc.data_ptr(), -1)
+    rep = CReport()
+    sent = C.c_uint64()
+    stream = torch.cuda.current_stream(dev).cuda_stream or 1
+    check(lib.dfakit_sort_pr_sharded(ctx.handle, comm.handle, C.byref(view), out.data_ptr(), C.byref(rep),
+                                     C.byref(sent), stream))
+    r = ShardReport(int(rep.num_blocks), int(rep.refining_iterations), int(rep.passes), int(rep.hash_collisions),
+                    int(sent.value), 0)
+    return out[:n], r

@@ -92,6 +92,29 @@ def test_sharded_world1_nccl(dk):
         dist.destroy_process_group()
 
 
+def test_sharded_native_driver_world1(dk):
+    """The C++ pass loop over NCCL (dfakit_sort_pr_sharded), world size 1."""
+    from paper_2508_20735_b200 import sharded
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = str(free_port())
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        ctx = dk.Context(0)
+        comm = sharded.NativeComm(ctx)
+        for case in CASES:
+            d, a, want = make_case(case)
+            k, n = d.shape
+            delta = torch.from_numpy(np.ascontiguousarray(d).view(np.int32).reshape(-1)).cuda()
+            acc = torch.from_numpy(np.ascontiguousarray(a)).cuda()
+            blocks, rep = sharded.sort_pr_sharded_native(ctx, comm, delta, acc, n, k)
+            got = blocks.cpu().numpy().view(np.uint32)
+            assert np.array_equal(got, want.blocks) and rep.num_blocks == want.num_blocks, case
+            assert rep.refining_iterations == want.refine_iters, (case, rep.refining_iterations, want.refine_iters)
+        comm.close()
+    finally:
+        dist.destroy_process_group()
+
+
 def worker(rank, world, port, q):
     try:
         os.environ["MASTER_ADDR"] = "127.0.0.1"
