@@ -177,7 +177,7 @@ __global__ void __launch_bounds__(kThreads) signature_kernel(const uint32_t* __r
 // step 1: signature + table of (run minimum, run size), in shared memory
 // when <= 13 bits; equal keys of a warp are combined first (match_any)
 template <typename LT>
-__global__ void __launch_bounds__(512) sig_table_kernel(const uint32_t* __restrict__ list, uint64_t m,
+__global__ void __launch_bounds__(512, 3) sig_table_kernel(const uint32_t* __restrict__ list, uint64_t m,
                                                         const uint32_t* __restrict__ delta, uint32_t n,
                                                         const LT* __restrict__ lab, SigParams p, uint32_t nbits,
                                                         uint32_t* __restrict__ keys32, uint32_t* __restrict__ tmin,
@@ -350,7 +350,7 @@ __device__ __forceinline__ void bucket_append(unsigned long long hk, uint32_t q,
 // hkey >> shift.  Slots b*cap .. b*cap+cap-1; the excess goes to the
 // overflow region at nb*cap (counted in ctr->overflow).
 template <typename LT>
-__global__ void __launch_bounds__(kThreads) sig_bucket_kernel(const uint32_t* __restrict__ list, uint64_t m,
+__global__ void __launch_bounds__(kThreads, 5) sig_bucket_kernel(const uint32_t* __restrict__ list, uint64_t m,
                                                               const uint32_t* __restrict__ delta, uint32_t n,
                                                               const LT* __restrict__ lab, SigParams p,
                                                               uint32_t nb, uint32_t* __restrict__ bcnt,
