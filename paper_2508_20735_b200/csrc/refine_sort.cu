@@ -135,23 +135,23 @@ __device__ __forceinline__ uint64_t fp_step(uint64_t h, uint32_t x) {
 // and all gathers before the first use, so a thread keeps up to 16
 // independent loads in flight (the loop-carried version serialised two
 // memory latencies per letter).
-constexpr int kLetterChunk = 16;
+constexpr int kLetterChunk = 16;  // default; the counting-table kernel runs best with 8
 
-template <typename LT>
+template <typename LT, int CH = kLetterChunk>
 __device__ __forceinline__ uint64_t tuple_key(uint32_t q, uint32_t lead, const uint32_t* __restrict__ delta,
                                               uint32_t n, const LT* __restrict__ lab, const SigParams& p) {
     const bool packed = p.kind == kKeyPacked;
     uint64_t key = packed ? (uint64_t)lead : fp_step(p.salt, lead);
-    for (uint32_t a = p.a0; a < p.a1; a += kLetterChunk) {
-        uint32_t t[kLetterChunk];
+    for (uint32_t a = p.a0; a < p.a1; a += CH) {
+        uint32_t t[CH];
 #pragma unroll
-        for (int j = 0; j < kLetterChunk; ++j)
+        for (int j = 0; j < CH; ++j)
             if (a + j < p.a1) t[j] = ld_stream(delta + (uint64_t)(a + j) * n + q);
 #pragma unroll
-        for (int j = 0; j < kLetterChunk; ++j)
+        for (int j = 0; j < CH; ++j)
             if (a + j < p.a1) t[j] = (uint32_t)lab[t[j]];
 #pragma unroll
-        for (int j = 0; j < kLetterChunk; ++j)
+        for (int j = 0; j < CH; ++j)
             if (a + j < p.a1) key = packed ? (key << p.field_bits) | t[j] : fp_step(key + a + j, t[j]);
     }
     return packed ? key : key & p.fp_mask;
@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(512, 3) sig_table_kernel(const uint32_t* __res
     }
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t q = list ? list[i] : p.q0 + (uint32_t)i;
-        const uint32_t key = (uint32_t)tuple_key<LT>(q, (uint32_t)lab[q], delta, n, lab, p);
+        const uint32_t key = (uint32_t)tuple_key<LT, 8>(q, (uint32_t)lab[q], delta, n, lab, p);
         keys32[i] = key;
         const unsigned peers = __match_any_sync(__activemask(), key);
         const uint32_t mq = __reduce_min_sync(peers, q);
@@ -266,7 +266,7 @@ __global__ void __launch_bounds__(kThreads) table_apply_kernel(const uint32_t* _
         if (next16) next16[q] = (uint16_t)rank[key];
         if (next32) next32[q] = rank[key];
         if (keep) keep[i] = multi;
-        if (act) act[q] = multi;
+        if (act && multi) act[q] = 1;  // act zeroed by the caller
         heads += rep == q;
         ablk += (rep == q) && multi;
         surv += multi;
@@ -389,8 +389,11 @@ __device__ __forceinline__ void emit(const GroupOut& o, uint64_t slot, uint32_t 
         o.res[idx] = r | (multi ? 0x80000000u : 0u);
     } else if (o.direct) {
         o.lab[q] = r;
-        if (o.state_order) o.act[q] = multi;
-        else o.keep_slot[slot] = multi;
+        if (o.state_order) {
+            if (multi) o.act[q] = 1;  // act was zeroed: only survivors are written
+        } else {
+            o.keep_slot[slot] = multi;
+        }
     } else {
         o.rep_slot[slot] = r;
         o.keep_slot[slot] = multi;
@@ -1186,7 +1189,7 @@ __global__ void shard_apply_kernel(const uint4* __restrict__ send, const uint32_
          i += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t q = send[i].z, r = res[i];
         lab[q] = r & 0x7fffffffu;
-        act[q] = (uint8_t)(r >> 31);
+        if (r >> 31) act[q] = 1;  // act zeroed by the caller
     }
 }
 
