@@ -236,6 +236,231 @@ __global__ void __launch_bounds__(kThreads) uf_expand_kernel(Rec rec, uint64_t w
     }
 }
 
+// ---- persistent BFS ------------------------------------------------------------
+//
+// All levels of the product BFS in one cooperative launch.  Per level:
+// expand (find-or-insert + discoverer atomicMin), barrier, winner counts
+// over contiguous item chunks (one per CTA), barrier, emit: each CTA's chunk
+// in item order at its prefix of the counts (block-scanned tiles), so the
+// records land in exactly the order the per-level kernels produce --
+// barrier, then every thread reads the level's total and first failure.
+// The kernel returns to the host only when the table / record store must
+// grow or the exploration ends.
+
+enum : uint32_t { kBfsRunning = 0, kBfsDone = 1, kBfsGrow = 2, kBfsFail = 3, kBfsBudget = 4 };
+
+struct BfsState {
+    unsigned long long wb, we;
+    unsigned long long first_fail_all;  // FULL mode: first failing record (~0 if none)
+    uint32_t levels, status;
+    uint32_t fail_rec;                  // failing record (kBfsFail)
+    uint32_t pad;
+    uint32_t fail[3];                   // per level (mod 3): first failing emit position
+};
+
+struct BfsArgs {
+    Rec rec;
+    uint64_t rec_cap;
+    Slot* table;
+    uint64_t cap;  // slots (power of two)
+    uint32_t* item_slot;
+    uint64_t item_cap;
+    uint32_t* cta_cnt;
+    const uint32_t *da, *db, *to_b;
+    uint32_t na, nb, k;
+    const uint8_t *acc_a, *acc_b;
+    int mode;
+    uint64_t max_visited;
+    BfsState* st;
+};
+
+__device__ __forceinline__ bool item_wins(const Slot* __restrict__ table, const uint32_t* __restrict__ item_slot,
+                                          uint64_t wb, uint64_t t, uint32_t k) {
+    const uint32_t s = item_slot[t];
+    if (s == kNone) return false;
+    const unsigned long long disc = ((unsigned long long)(wb + t / k + 1) << 32) | (uint32_t)(t % k);
+    return __ldcg(&table[s].disc) == disc;
+}
+
+__global__ void __launch_bounds__(kThreads) bfs_persistent_kernel(BfsArgs A) {
+    cg::grid_group grid = cg::this_grid();
+    auto tile = cg::tiled_partition<kTile>(cg::this_thread_block());
+    __shared__ uint32_t ws[kThreads / 32];
+    __shared__ uint32_t red[kThreads / 32];
+    BfsState* st = A.st;
+    uint64_t wb = st->wb, we = st->we;
+    uint32_t levels = st->levels;
+    unsigned long long first_fail_all = st->first_fail_all;
+    uint32_t status = kBfsDone;
+    const uint64_t mask = A.cap - 1;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t gtid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    while (wb < we) {
+        const uint64_t items = (we - wb) * A.k;
+        if (items > A.item_cap || we + items > A.rec_cap || 2 * (we + items) + 64 > A.cap) {
+            status = kBfsGrow;
+            break;
+        }
+        // three slots: threads may still read level L-1's slot while level L
+        // starts; level L-2's slot (= level L+1's) is free
+        const uint32_t par = levels % 3;
+        if (gtid == 0) st->fail[(levels + 1) % 3] = kNone;
+        // expand
+        const uint64_t trips = (items + stride - 1) / stride;
+        for (uint64_t it = 0; it < trips; ++it) {
+            const uint64_t t = gtid + it * stride;
+            const bool valid = t < items;
+            unsigned long long key = 0, disc = 0;
+            if (valid) {
+                const uint64_t i = wb + t / A.k;
+                const uint32_t la = (uint32_t)(t % A.k);
+                const unsigned long long pk = __ldcg(A.rec.key + i);
+                const uint32_t pa = A.da[(uint64_t)la * A.na + (uint32_t)(pk >> 32)];
+                const uint32_t pb = A.db[(uint64_t)A.to_b[la] * A.nb + (uint32_t)pk];
+                key = ((unsigned long long)pa << 32) | pb;
+                disc = ((unsigned long long)(i + 1) << 32) | la;
+            }
+            const uint32_t sl = tile_find_or_insert(tile, valid, key, A.table, mask);
+            if (valid) {
+                const unsigned long long old = atomicMin(&A.table[sl].disc, disc);
+                A.item_slot[t] = (old >= ((unsigned long long)(wb + 1) << 32)) ? sl : kNone;
+            }
+        }
+        grid.sync();
+        // winner counts per contiguous chunk
+        const uint64_t chunk = (items + gridDim.x - 1) / gridDim.x;
+        const uint64_t c0 = min(items, blockIdx.x * chunk), c1 = min(items, c0 + chunk);
+        uint32_t c = 0;
+        for (uint64_t t = c0 + threadIdx.x; t < c1; t += blockDim.x) c += item_wins(A.table, A.item_slot, wb, t, A.k);
+        c = __reduce_add_sync(0xffffffffu, c);
+        if ((threadIdx.x & 31u) == 0) red[threadIdx.x >> 5] = c;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t tot = 0;
+            for (int w = 0; w < kThreads / 32; ++w) tot += red[w];
+            A.cta_cnt[blockIdx.x] = tot;
+        }
+        grid.sync();
+        // prefix of this CTA, total of the level
+        uint32_t pre = 0, total = 0;
+        for (uint32_t j = threadIdx.x; j < gridDim.x; j += blockDim.x) {
+            const uint32_t v = __ldcg(A.cta_cnt + j);
+            total += v;
+            if (j < blockIdx.x) pre += v;
+        }
+        pre = __reduce_add_sync(0xffffffffu, pre);
+        total = __reduce_add_sync(0xffffffffu, total);
+        __syncthreads();
+        if ((threadIdx.x & 31u) == 0) {
+            red[threadIdx.x >> 5] = pre;
+            ws[threadIdx.x >> 5] = total;
+        }
+        __syncthreads();
+        pre = 0;
+        total = 0;
+        for (int w = 0; w < kThreads / 32; ++w) {
+            pre += red[w];
+            total += ws[w];
+        }
+        __syncthreads();
+        // emit in item order
+        uint32_t run = pre;
+        for (uint64_t base = c0; base < c1; base += blockDim.x) {
+            const uint64_t t = base + threadIdx.x;
+            const bool win = t < c1 && item_wins(A.table, A.item_slot, wb, t, A.k);
+            uint32_t tot;
+            const uint32_t e = block_exclusive_scan<kThreads>(win ? 1u : 0u, &tot, ws);
+            if (win) {
+                const uint32_t posn = run + e;
+                const uint64_t r = we + posn;
+                const unsigned long long key = __ldcg(&A.table[A.item_slot[t]].key);
+                A.rec.key[r] = key;
+                A.rec.parent[r] = (uint32_t)(wb + t / A.k);
+                A.rec.letter[r] = (uint32_t)(t % A.k);
+                const bool fa = A.acc_a[key >> 32], fb = A.acc_b[(uint32_t)key];
+                const bool fails = A.mode == DFAKIT_MODE_INCLUSION ? (fa && !fb) : (fa != fb);
+                if (fails) atomicMin(&st->fail[par], posn);
+            }
+            run += tot;
+        }
+        grid.sync();
+        const uint32_t ff = *(volatile uint32_t*)&st->fail[par];
+        if (ff != kNone && A.mode != DFAKIT_MODE_FULL) {
+            if (we + ff >= A.max_visited) {
+                status = kBfsBudget;
+            } else {
+                status = kBfsFail;
+                if (gtid == 0) st->fail_rec = (uint32_t)(we + ff);
+            }
+            we = we + ff + 1;  // explored count reported on failure
+            break;
+        }
+        if (we + total > A.max_visited) {
+            status = kBfsBudget;
+            break;
+        }
+        if (ff != kNone && first_fail_all == ~0ull) first_fail_all = we + ff;
+        ++levels;
+        wb = we;
+        we += total;
+    }
+    if (gtid == 0) {
+        st->wb = wb;
+        st->we = we;
+        st->levels = levels;
+        st->status = status;
+        st->first_fail_all = first_fail_all;
+    }
+}
+
+// union-find Hopcroft-Karp: one barrier per level
+struct UfArgs {
+    Rec rec;
+    uint64_t cap;
+    const uint32_t *da, *db;
+    uint32_t na, nb, k;
+    const uint8_t *acc_a, *acc_b;
+    uint32_t* P;
+    uint32_t* count;
+    uint32_t* fail_rec;
+    uint32_t* out;  // {levels, explored}
+};
+
+__global__ void __launch_bounds__(kThreads) uf_persistent_kernel(UfArgs A) {
+    cg::grid_group grid = cg::this_grid();
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t gtid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    uint64_t wb = 0, we = 1;
+    uint32_t levels = 0;
+    while (wb < we) {
+        const uint64_t items = (we - wb) * A.k;
+        for (uint64_t t = gtid; t < items; t += stride) {
+            const uint64_t i = wb + t / A.k;
+            const uint32_t la = (uint32_t)(t % A.k);
+            const unsigned long long pk = __ldcg(A.rec.key + i);
+            const uint32_t pa = A.da[(uint64_t)la * A.na + (uint32_t)(pk >> 32)];
+            const uint32_t pb = A.db[(uint64_t)la * A.nb + (uint32_t)pk];
+            if (!uf_union(A.P, pa, A.na + pb)) continue;
+            const uint32_t r = atomicAdd(A.count, 1u);
+            if (r >= A.cap) continue;  // cannot happen: at most na+nb-1 unions
+            A.rec.key[r] = ((unsigned long long)pa << 32) | pb;
+            A.rec.parent[r] = (uint32_t)i;
+            A.rec.letter[r] = la;
+            if (A.acc_a[pa] != A.acc_b[pb]) atomicMin(A.fail_rec, r);
+        }
+        grid.sync();
+        ++levels;
+        if (*(volatile uint32_t*)A.fail_rec != kNone) break;
+        wb = we;
+        we = *(volatile uint32_t*)A.count;
+        grid.sync();  // every thread has read count before the next level appends
+    }
+    if (gtid == 0) {
+        A.out[0] = levels;
+        A.out[1] = *(volatile uint32_t*)A.count;
+    }
+}
+
 struct RecStore {
     DBuf<unsigned long long> key;
     DBuf<uint32_t> parent, letter;
@@ -326,56 +551,59 @@ ProductOut explore_product_device(Ctx* ctx, const DevDfa& a, const DevDfa& b, in
 
     DBuf<Slot> table;
     uint64_t cap = 0;
-    DBuf<uint32_t> item_slot, flag, pos, ff(1, s), total(1, s);
+    DBuf<uint32_t> item_slot;
+    DBuf<BfsState> dst(1, s);
+    int per_sm = 0;
+    DK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bfs_persistent_kernel, kThreads, 0));
+    if (per_sm < 1) throw Error(DFAKIT_E_RESOURCE, "bfs kernel does not fit an SM");
+    const unsigned grid_n = (unsigned)(per_sm * ctx->num_sms);
+    DBuf<uint32_t> cta_cnt(grid_n, s);
+    BfsState hs{};
+    hs.wb = 0;
+    hs.we = 1;
+    hs.first_fail_all = first_fail_all;
+    hs.status = kBfsRunning;
+    hs.fail[0] = hs.fail[1] = hs.fail[2] = kNone;
+    DK_CUDA(cudaMemcpyAsync(dst.get(), &hs, sizeof(hs), cudaMemcpyHostToDevice, s));
     uint64_t wb = 0, we = 1;
-    while (wb < we) {
-        const uint64_t wave = we - wb;
-        const uint64_t items = wave * k;
-        // capacity for everything seen so far plus every possible new pair, at load <= 1/2
+    for (;;) {
+        // room for the next level: table at load <= 1/2, records, items; grown
+        // geometrically so the kernel returns here O(log) times
+        const uint64_t items = (we - wb) * k;
         const uint64_t need = next_pow2(2 * (we + items) + 64);
         if (need > cap) {
-            table.alloc(need, s);
-            cap = need;
-            DK_CUDA(cudaMemsetAsync(table.get(), 0xff, need * sizeof(Slot), s));
+            const uint64_t nc = std::max<uint64_t>(need, cap * 4);
+            table.alloc(nc, s);
+            cap = nc;
+            DK_CUDA(cudaMemsetAsync(table.get(), 0xff, cap * sizeof(Slot), s));
             DK_LAUNCH(ctx, reinsert_kernel, grid_for(we), kThreads, 0, s, rs.key.get(), we, table.get(), cap - 1);
         }
-        rs.ensure(we + items, we, s);
-        if (items > item_slot.n) {
-            item_slot.alloc(items, s);
-            flag.alloc(items, s);
-            pos.alloc(items, s);
-        }
-        if (items) {
-            DK_LAUNCH_B(ctx, 44.0 * items, expand_kernel, grid_for(items), kThreads, 0, s, rs.view(), wb, items, k, a.delta, a.n,
-                      b.delta, b.n, to_b.get(), table.get(), cap - 1, item_slot.get());
-            DK_LAUNCH(ctx, winner_flags_kernel, grid_for(items), kThreads, 0, s, wb, items, k, table.get(),
-                      item_slot.get(), flag.get());
-            exclusive_scan_u32(ctx, flag.get(), pos.get(), items, total.get(), s);
-            DK_CUDA(cudaMemsetAsync(ff.get(), 0xff, 4, s));
-            DK_LAUNCH(ctx, emit_kernel, grid_for(items), kThreads, 0, s, rs.view(), wb, we, items, k, table.get(),
-                      item_slot.get(), flag.get(), pos.get(), a.acc, b.acc, mode, ff.get());
-        }
-        uint32_t fresh = 0, first = kNone;
-        if (items) {
-            read_words(ctx, total.get(), 4, &fresh, s);
-            read_words(ctx, ff.get(), 4, &first, s);
-        }
-        if (first != kNone && mode != DFAKIT_MODE_FULL) {
-            if (we + first >= max_visited)
-                throw Error(DFAKIT_E_RESOURCE, "product exploration exceeded the visited-set budget of " +
-                                                   std::to_string(max_visited) + " pairs");
+        rs.ensure(std::max<uint64_t>(we + items, (we + items) * 2), we, s);
+        if (std::max<uint64_t>(items, 1) > item_slot.n) item_slot.alloc(std::max<uint64_t>(items, 1) * 4, s);
+        BfsArgs A{rs.view(), rs.cap, table.get(), cap, item_slot.get(), item_slot.n, cta_cnt.get(), a.delta, b.delta,
+                  to_b.get(), a.n, b.n, k, a.acc, b.acc, mode, max_visited, dst.get()};
+        void* args[] = {(void*)&A};
+        prof_begin_launch(ctx, s);
+        DK_CUDA(cudaLaunchCooperativeKernel((const void*)bfs_persistent_kernel, grid_n, kThreads, args, 0, s));
+        note_launch(ctx);
+        prof_end_launch(ctx, s, "bfs_persistent_kernel", 0, 0);
+        read_words(ctx, dst.get(), sizeof(hs), &hs, s);
+        wb = hs.wb;
+        we = hs.we;
+        out.levels = hs.levels;
+        first_fail_all = hs.first_fail_all;
+        if (hs.status == kBfsFail) {
             out.verdict = DFAKIT_COUNTEREXAMPLE;
-            out.explored = we + first + 1;
-            out.word = walk_word(ctx, rs, (uint32_t)(we + first), s);
+            out.explored = we;
+            out.word = walk_word(ctx, rs, hs.fail_rec, s);
             return out;
         }
-        if (we + fresh > max_visited)
+        if (hs.status == kBfsBudget)
             throw Error(DFAKIT_E_RESOURCE, "product exploration exceeded the visited-set budget of " +
                                                std::to_string(max_visited) + " pairs");
-        if (first != kNone && first_fail_all == ~0ull) first_fail_all = we + first;
-        ++out.levels;
-        wb = we;
-        we += fresh;
+        if (hs.status == kBfsDone) break;
+        // kBfsGrow: loop to grow and relaunch
+        hs.status = kBfsRunning;
     }
     out.explored = we;
     if (mode == DFAKIT_MODE_FULL && first_fail_all != ~0ull) {
@@ -416,24 +644,28 @@ ProductOut check_equiv_uf_device(Ctx* ctx, const DevDfa& a, const DevDfa& b, cud
     DK_CUDA(cudaMemcpyAsync(rs.letter.get(), &zero, 4, cudaMemcpyHostToDevice, s));
     DK_CUDA(cudaMemcpyAsync(cnt.get(), &one, 4, cudaMemcpyHostToDevice, s));
     DK_CUDA(cudaMemsetAsync(fail.get(), 0xff, 4, s));
-    uint64_t wb = 0, we = 1;
-    while (wb < we) {
-        const uint64_t items = (we - wb) * k;
-        if (items)
-            DK_LAUNCH(ctx, uf_expand_kernel, grid_for(items), kThreads, 0, s, rs.view(), wb, items, k, a.delta, a.n,
-                      b.delta, b.n, a.acc, b.acc, P.get(), cnt.get(), rs.cap, fail.get());
-        uint32_t words[2] = {0, 0};
-        read_words(ctx, cnt.get(), 4, &words[0], s);
-        read_words(ctx, fail.get(), 4, &words[1], s);
-        ++out.levels;
-        if (words[1] != kNone) {
-            out.verdict = DFAKIT_COUNTEREXAMPLE;
-            out.explored = words[0];
-            out.word = walk_word(ctx, rs, words[1], s);
-            return out;
-        }
-        wb = we;
-        we = words[0];
+    DBuf<uint32_t> res(2, s);
+    int per_sm = 0;
+    DK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, uf_persistent_kernel, kThreads, 0));
+    if (per_sm < 1) throw Error(DFAKIT_E_RESOURCE, "union-find kernel does not fit an SM");
+    UfArgs A{rs.view(), rs.cap, a.delta, b.delta, a.n, b.n, k, a.acc, b.acc, P.get(), cnt.get(), fail.get(),
+             res.get()};
+    void* args[] = {(void*)&A};
+    prof_begin_launch(ctx, s);
+    DK_CUDA(cudaLaunchCooperativeKernel((const void*)uf_persistent_kernel, (unsigned)(per_sm * ctx->num_sms), kThreads,
+                                        args, 0, s));
+    note_launch(ctx);
+    prof_end_launch(ctx, s, "uf_persistent_kernel", 0, 0);
+    uint32_t words[3] = {0, 0, 0};
+    read_words(ctx, res.get(), 8, words, s);
+    read_words(ctx, fail.get(), 4, &words[2], s);
+    out.levels = words[0];
+    const uint64_t we = words[1];
+    if (words[2] != kNone) {
+        out.verdict = DFAKIT_COUNTEREXAMPLE;
+        out.explored = we;
+        out.word = walk_word(ctx, rs, words[2], s);
+        return out;
     }
     out.verdict = DFAKIT_EQUIVALENT;
     out.explored = we;
