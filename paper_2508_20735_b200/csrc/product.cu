@@ -572,7 +572,9 @@ ProductOut explore_product_device(Ctx* ctx, const DevDfa& a, const DevDfa& b, in
         const uint64_t items = (we - wb) * k;
         const uint64_t need = next_pow2(2 * (we + items) + 64);
         if (need > cap) {
-            const uint64_t nc = std::max<uint64_t>(need, cap * 4);
+            // start at 2^20 slots (16 MB) and grow 8x: the early, tiny levels
+            // cost no relaunch, large explorations only a few
+            const uint64_t nc = std::max<uint64_t>(need, std::max<uint64_t>(1ull << 20, cap * 8));
             table.alloc(nc, s);
             cap = nc;
             DK_CUDA(cudaMemsetAsync(table.get(), 0xff, cap * sizeof(Slot), s));
