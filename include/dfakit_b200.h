@@ -107,9 +107,11 @@ typedef struct {
     uint64_t max_pair_nodes;    /* trans budget, minimize.hpp:38 (0 = default 2^16)    */
     uint32_t fingerprint_bits;  /* sort_pr: 0 = 64; smaller values force collisions    */
     uint32_t grouping;          /* sort_pr: 0 = auto (counting table / radix-bucketed
-                                   shared-memory hashing), 1 = full LSD radix sort of
-                                   the keys + adjacent difference + scan (literal
-                                   paper Alg. 4)                                      */
+                                   shared-memory hashing; the persistent device loop
+                                   once <= 2^17 states are active), 1 = full LSD radix
+                                   sort of the keys + adjacent difference + scan
+                                   (literal paper Alg. 4), 2 = auto without the
+                                   persistent loop (every pass host-staged)          */
 } dfakit_options;
 
 typedef struct dfakit_ctx dfakit_ctx;

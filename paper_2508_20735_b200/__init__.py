@@ -167,13 +167,15 @@ def minimize(dfa: Dfa, algo: Algorithm, policy: ElectionPolicy = ElectionPolicy.
     sort_pr knobs (testing / comparison): force_exact never uses fingerprint
     keys, fingerprint_bits < 64 forces collisions, grouping="radix_sort"
     groups keys with the full LSD radix sort of the literal Alg. 4 instead of
-    the counting-table / radix-bucket hashing default."""
+    the counting-table / radix-bucket hashing default, grouping="staged"
+    keeps every pass host-staged (no persistent small-m device loop)."""
     view = dfa.c_view()
     blocks = np.zeros(max(dfa.num_states, 1), np.uint32)
-    if grouping not in ("auto", "radix_sort"):
-        raise ValueError(f"grouping must be 'auto' or 'radix_sort', not {grouping!r}")
+    codes = {"auto": 0, "radix_sort": 1, "staged": 2}
+    if grouping not in codes:
+        raise ValueError(f"grouping must be one of {sorted(codes)}, not {grouping!r}")
     opts = COptions(policy.kind, int(force_exact), policy.seed, max_transitions, max_pair_nodes, fingerprint_bits,
-                    int(grouping == "radix_sort"))
+                    codes[grouping])
     rep = CReport()
     check(lib.dfakit_minimize(_ctx(ctx).handle, C.byref(view), int(algo), C.byref(opts), blocks.ctypes.data,
                               C.byref(rep)))

@@ -25,7 +25,7 @@ struct RefineResult {
 struct SortOptions {
     bool force_exact = false;
     uint32_t fingerprint_bits = 64;
-    uint32_t grouping = 0;  // 0 = auto (table / bucket hashing), 1 = LSD radix sort (literal Alg. 4)
+    uint32_t grouping = 0;  // 0 = auto, 1 = LSD radix sort (literal Alg. 4), 2 = host-staged passes only
 };
 
 // Key plan of one sortPR pass (see plan_pass in refine_sort.cu).

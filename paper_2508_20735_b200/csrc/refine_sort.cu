@@ -40,6 +40,8 @@
 //
 // The fixed-point test of l.19 is the block count: B' = B - A + R where A is
 // the number of active blocks and R the number of runs found.
+#include <cooperative_groups.h>
+
 #include <algorithm>
 
 #include "prims.cuh"
@@ -682,6 +684,173 @@ void with_lab_type(const KeyLab& kl, F&& f) {
     else f(static_cast<const uint32_t*>(kl.p));
 }
 
+// ---- persistent small-m engine ---------------------------------------------------
+//
+// Once few states are active (and on small automata with many passes --
+// Fibonacci: one pass per state), a pass is a few microseconds of work and
+// the host round trips dominate.  This cooperative kernel runs the remaining
+// passes on the device: per pass, insert every active key into a global
+// open-addressing table (L2 resident; atomicMin elects the run minimum,
+// atomicAdd sizes the run), count heads / active blocks / survivors and
+// verify fingerprint runs, then relabel, append survivors and clear the
+// other of two tables for the next pass -- three grid barriers.  A verified collision re-runs the pass with a new salt; after
+// three in one pass the kernel hands the pass back to the host engine (which
+// falls back to exact letter chunks).  Counters are triple-buffered so a
+// slot is reset only after every thread has read it.
+
+namespace cg = cooperative_groups;
+
+struct PersistCtr {
+    uint32_t runs, ablk, surv, collision, listed, pad[3];
+};
+
+struct SmallState {
+    uint32_t B, A;
+    uint64_t m;
+    uint64_t passes, iters, collisions;
+    uint32_t list_sel;  // which list buffer holds the active states on exit
+    uint32_t status;    // 0 fixed point / drained, 1 hand back (collisions)
+    uint64_t salt;
+    uint32_t strikes, pad;
+};
+
+struct SmallArgs {
+    const uint32_t* delta;
+    uint32_t n, k;
+    uint32_t* lab;
+    uint32_t* list[2];
+    uint32_t* slot;  // per active entry
+    unsigned long long* tkey;  // two tables of tcap + 1 slots
+    uint32_t* trep;
+    uint32_t* tcnt;
+    uint32_t tcap;  // power of two
+    PersistCtr* ctr;  // [3]
+    SmallState* st;
+    uint32_t field_bits;  // packed keys when nonzero
+    uint64_t fp_mask;     // fingerprint mask (testing hook)
+};
+
+__global__ void __launch_bounds__(kThreads) small_persistent_kernel(SmallArgs A) {
+    cg::grid_group grid = cg::this_grid();
+    const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
+    SmallState s = *A.st;
+    uint32_t sel = s.list_sel;
+    uint64_t pass_no = 0;  // counter / table slot index
+    const uint32_t T = A.tcap;
+    s.status = 0;
+    // tables alternate by pass: pass p inserts into table p & 1 while the
+    // relabel phase of pass p clears table (p + 1) & 1 for the next pass
+    for (uint32_t e = tid; e <= T; e += stride) {
+        A.tkey[e] = kEmptyKey;
+        A.trep[e] = kNone;
+        A.tcnt[e] = 0;
+    }
+    grid.sync();
+    while (s.m > 0) {
+        PersistCtr* c = A.ctr + (pass_no % 3);
+        if (tid == 0) A.ctr[(pass_no + 1) % 3] = PersistCtr{};
+        const uint32_t m = (uint32_t)s.m;
+        const uint32_t* list = A.list[sel];
+        uint32_t* next = A.list[sel ^ 1];
+        const uint32_t tb = (uint32_t)(pass_no & 1) * (T + 1);  // this pass's table
+        const uint32_t ob = (T + 1) - tb;                       // the other one
+        SigParams p{};
+        p.kind = A.field_bits ? kKeyPacked : kKeyFingerprint;
+        p.a0 = 0;
+        p.a1 = A.k;
+        p.field_bits = A.field_bits;
+        p.salt = s.salt;
+        p.fp_mask = A.fp_mask;
+        // keys, insert, elect the run minimum, count the run (slot T: a ~0 key)
+        for (uint32_t i = tid; i < m; i += stride) {
+            const uint32_t q = list[i];
+            const uint64_t key = tuple_key<uint32_t, 8>(q, A.lab[q], A.delta, A.n, A.lab, p);
+            const unsigned long long hk = p.kind == kKeyPacked ? mix64(key) : key;
+            uint32_t sl;
+            if (hk == kEmptyKey) {
+                sl = T;
+            } else {
+                sl = (uint32_t)mix64(hk) & (T - 1);
+                for (;;) {
+                    const unsigned long long old = atomicCAS(&A.tkey[tb + sl], kEmptyKey, hk);
+                    if (old == kEmptyKey || old == hk) break;
+                    sl = (sl + 1) & (T - 1);
+                }
+            }
+            A.slot[i] = tb + sl;
+            atomicMin(&A.trep[tb + sl], q);
+            atomicAdd(&A.tcnt[tb + sl], 1u);
+        }
+        grid.sync();
+        // counters + fingerprint verification
+        uint32_t heads = 0, ablk = 0, surv = 0;
+        bool clash = false;
+        for (uint32_t i = tid; i < m; i += stride) {
+            const uint32_t q = list[i], sl = A.slot[i];
+            const uint32_t r = __ldcg(&A.trep[sl]);
+            const bool multi = __ldcg(&A.tcnt[sl]) >= 2, head = r == q;
+            heads += head;
+            ablk += head && multi;
+            surv += multi;
+            if (!A.field_bits && !head && !same_tuple(q, r, A.delta, A.n, A.k, A.lab)) clash = true;
+        }
+        if (__syncthreads_or(clash) && threadIdx.x == 0) atomicOr(&c->collision, 1u);
+        flush_counters<kThreads>(heads, ablk, surv, &c->runs, &c->ablk, &c->surv);
+        grid.sync();
+        PersistCtr cv;
+        cv.runs = __ldcg(&c->runs);
+        cv.ablk = __ldcg(&c->ablk);
+        cv.surv = __ldcg(&c->surv);
+        cv.collision = __ldcg(&c->collision);
+        ++s.passes;
+        ++pass_no;
+        const uint32_t newB = s.B - s.A + cv.runs;
+        const bool retry = cv.collision != 0;
+        if (!retry && newB == s.B) break;  // fixed point (reference l.411)
+        if (retry && s.strikes + 1 >= 3) {
+            ++s.collisions;
+            --s.passes;
+            s.status = 1;  // three collisions: hand the pass back to the host engine
+            break;
+        }
+        // relabel + append survivors (order is free: keys carry the labels);
+        // clear the other table for the next pass
+        if (!retry) {
+            uint32_t* listed = &c->listed;
+            for (uint32_t i = tid; i < m; i += stride) {
+                const uint32_t q = list[i], sl = A.slot[i];
+                A.lab[q] = __ldcg(&A.trep[sl]);
+                const bool multi = __ldcg(&A.tcnt[sl]) >= 2;
+                const uint32_t at = warp_append(listed, multi);
+                if (multi) next[at] = q;
+            }
+        }
+        for (uint32_t e = tid; e <= T; e += stride) {
+            A.tkey[ob + e] = kEmptyKey;
+            A.trep[ob + e] = kNone;
+            A.tcnt[ob + e] = 0;
+        }
+        grid.sync();
+        if (retry) {
+            ++s.collisions;
+            ++s.strikes;
+            --s.passes;
+            s.salt = mix64(s.salt + 0x1234567ull);
+            continue;
+        }
+        s.strikes = 0;
+        ++s.iters;
+        s.B = newB;
+        s.A = cv.ablk;
+        s.m = cv.surv;
+        sel ^= 1;
+    }
+    if (tid == 0) {
+        s.list_sel = sel;
+        *A.st = s;
+    }
+}
+
 }  // namespace
 
 LeaderInfo leader_info(Ctx* ctx, const DevDfa& d, cudaStream_t s) {
@@ -737,6 +906,54 @@ PassPlan plan_pass(uint32_t n, uint32_t k, uint32_t B, uint64_t m, uint32_t coll
     p.key_bits = p.strategy == kPlanFingerprint ? 64u : (uint32_t)(k1 * p.field_bits);
     return p;
 }
+
+namespace {
+
+constexpr uint64_t kSmallPersistMax = 1u << 17;
+
+struct SmallRun {
+    SmallState st;
+    const uint32_t* list_out;
+};
+
+SmallRun run_small_persistent(Ctx* ctx, const DevDfa& d, uint32_t* lab, uint32_t* list_in, uint32_t* list_other,
+                              uint64_t m, uint32_t B, uint32_t A, uint64_t salt, uint64_t fp_mask, cudaStream_t s) {
+    const uint32_t n = d.n, k = d.k;
+    const uint32_t label_bits = bits_for(n ? n - 1 : 0);
+    const uint32_t field_bits = (uint64_t)(k + 1) * label_bits <= 64 ? label_bits : 0;
+    uint32_t T = 64;
+    while (T < 2 * m) T <<= 1;
+    DBuf<uint32_t> slot(m, s), trep(2 * (T + 1), s), tcnt(2 * (T + 1), s);
+    DBuf<unsigned long long> tkey(2 * (T + 1), s);
+    DBuf<PersistCtr> ctr(3, s);
+    DBuf<SmallState> st(1, s);
+    DK_CUDA(cudaMemsetAsync(ctr.get(), 0, 3 * sizeof(PersistCtr), s));
+    SmallState hs{};
+    hs.B = B;
+    hs.A = A;
+    hs.m = m;
+    hs.salt = salt;
+    hs.list_sel = 0;
+    DK_CUDA(cudaMemcpyAsync(st.get(), &hs, sizeof(hs), cudaMemcpyHostToDevice, s));
+    SmallArgs args{d.delta, n, k, lab, {list_in, list_other}, slot.get(), tkey.get(), trep.get(), tcnt.get(), T,
+                   ctr.get(), st.get(), field_bits, fp_mask};
+    int per_sm = 0;
+    DK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, small_persistent_kernel, kThreads, 0));
+    if (per_sm < 1) throw Error(DFAKIT_E_RESOURCE, "persistent sort_pr kernel does not fit an SM");
+    const uint64_t want = (m + kThreads - 1) / kThreads;
+    const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)ctx->num_sms));
+    void* kargs[] = {(void*)&args};
+    prof_begin_launch(ctx, s);
+    DK_CUDA(cudaLaunchCooperativeKernel((const void*)small_persistent_kernel, grid, kThreads, kargs, 0, s));
+    note_launch(ctx);
+    prof_end_launch(ctx, s, "small_persistent_kernel", 0, 0);
+    SmallRun r;
+    read_words(ctx, st.get(), sizeof(SmallState), &r.st, s);
+    r.list_out = r.st.list_sel ? list_other : list_in;
+    return r;
+}
+
+}  // namespace
 
 RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uint32_t* block_out, cudaStream_t s) {
     RefineResult res;
@@ -797,6 +1014,30 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
     };
 
     while (m > 0) {
+        // few active states: the remaining passes on the device (no host
+        // round trip per pass); a pass with three collisions comes back here
+        if (m <= kSmallPersistMax && o.grouping == 0 && !o.force_exact && collisions_this_pass == 0) {
+            const bool identity = list == nullptr;
+            if (identity) {  // materialise the identity list
+                iota_u32(ctx, list_buf, m, s);
+                list = list_buf;
+            }
+            SmallRun sr = run_small_persistent(ctx, d, w.lab.get(), list == list_buf ? list_buf : list_alt,
+                                               list == list_buf ? list_alt : list_buf, m, B, A, salt, fp_mask, s);
+            res.passes += sr.st.passes;
+            res.iters += sr.st.iters;
+            res.collisions += sr.st.collisions;
+            res.sorted += 0;
+            B = sr.st.B;
+            A = sr.st.A;
+            m = sr.st.m;
+            salt = sr.st.salt;
+            if (sr.st.status == 0) break;  // fixed point reached on the device
+            // three collisions: the host engine takes the pass
+            list = sr.list_out;
+            if (list == list_alt) std::swap(list_buf, list_alt);
+            collisions_this_pass = 3;
+        }
         ++res.passes;
         const PassPlan plan = plan_pass(n, k, B, m, collisions_this_pass, o.force_exact);
         const bool fingerprint = plan.strategy == kPlanFingerprint, chunked = plan.strategy == kPlanChunked;

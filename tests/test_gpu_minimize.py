@@ -42,6 +42,8 @@ def test_random_sweep_all_minimisers(dk, oracle):
             want = oracle.minimize(algo, t[0], t[1])
             got = run(dk, algo, dfa)
             assert same(got, want), (i, algo, n, k, frac, s, got.refining_iterations, want.refine_iters)
+        staged = dk.sort_pr(dfa, grouping="staged")
+        assert same(staged, oracle.minimize("sort", t[0], t[1])), (i, "staged")
         moore = oracle.minimize("moore", t[0], t[1])
         for seed in (1, 2, 3):
             got = dk.naive_pr(dfa, dk.ElectionPolicy.arbitrary(seed))
@@ -153,7 +155,8 @@ def test_sort_exact_paths_and_collision_recovery(dk, oracle):
         want = oracle.minimize("moore", t[0], t[1])
         dfa = mkdfa(dk, t)
         for kw in ({}, {"force_exact": True}, {"fingerprint_bits": 6}, {"grouping": "radix_sort"},
-                   {"grouping": "radix_sort", "fingerprint_bits": 6}):
+                   {"grouping": "radix_sort", "fingerprint_bits": 6}, {"grouping": "staged"},
+                   {"grouping": "staged", "fingerprint_bits": 6}):
             rep = dk.sort_pr(dfa, **kw)
             assert same(rep, want), kw
             collisions += rep.hash_collisions
@@ -180,7 +183,8 @@ def test_grouping_strategies(dk, oracle):
         t = copies(base, c)
         want = oracle.minimize("moore", t[0], t[1])
         dfa = mkdfa(dk, t)
-        for kw in ({}, {"fingerprint_bits": 6}, {"force_exact": True}, {"grouping": "radix_sort"}):
+        for kw in ({}, {"fingerprint_bits": 6}, {"force_exact": True}, {"grouping": "radix_sort"},
+                   {"grouping": "staged"}, {"grouping": "staged", "fingerprint_bits": 6}):
             assert same(dk.sort_pr(dfa, **kw), want), (n0, c, k, kw)
         for algo in ("naive", "naive-fused"):
             assert same(run(dk, algo, dfa), oracle.minimize(algo, t[0], t[1])), (n0, c, algo)
