@@ -221,7 +221,10 @@ typedef struct {
     uint32_t strategy;      /* dfakit_plan_strategy                                   */
     uint32_t field_bits;    /* packed keys: bits per field                            */
     uint32_t key_bits;      /* packed key width; 64 for fingerprints                  */
-    uint32_t keylab_bytes;  /* 0: gather min-state labels; 1/2/4: dense block ids     */
+    uint32_t keylab_bytes;  /* 0: gather min-state labels; 1/2/4: dense block ids;
+                               255: one bit per state (callers may set it when the
+                               partition has <= 2 blocks; dfakit_shard_keylab then
+                               writes a bitmap of (n + 31) / 32 words)            */
 } dfakit_pass_plan;
 
 /* Key plan of one sort_pr pass (host only; no device needed). */

@@ -37,6 +37,11 @@ struct PassPlan {
     uint32_t keylab_bytes = 0;  // 0: gather min-state labels; 1/2/4: dense block ids of that width
 };
 PassPlan plan_pass(uint32_t n, uint32_t k, uint32_t B, uint64_t m, uint32_t collisions, bool force_exact);
+// PassPlan::keylab_bytes tag for one-bit key labels (two-block partitions);
+// used from kBitLabelsMinStates states on, where a byte per state would
+// crowd the L2 (below it the byte array is resident and cheaper to gather)
+constexpr uint32_t kKeylabBits = 255;
+constexpr uint32_t kBitLabelsMinStates = 1u << 25;
 
 // Sharded sortPR primitives (refine_sort.cu; driven by sharded.py).
 // counters: device uint32[4] = {runs, active blocks, active states, collision}.

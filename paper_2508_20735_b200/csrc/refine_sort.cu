@@ -132,6 +132,20 @@ __device__ __forceinline__ uint64_t fp_step(uint64_t h, uint32_t x) {
     return mix64(h ^ ((uint64_t)x * 0xD6E8FEB86659FD93ull));
 }
 
+// Key-label readers: a dense / min-state label array of T, or one bit per
+// state (a two-block partition: the initial {F, Q \ F} of every run -- a
+// 10M-state automaton's bitmap is 1.25 MB and stays L2-resident where a byte
+// array of a 100M-state one does not).
+template <typename T>
+struct ArrLab {
+    const T* p;
+    __device__ __forceinline__ uint32_t operator[](uint32_t i) const { return (uint32_t)__ldg(p + i); }
+};
+struct BitLab {
+    const uint32_t* w;
+    __device__ __forceinline__ uint32_t operator[](uint32_t i) const { return (__ldg(w + (i >> 5)) >> (i & 31u)) & 1u; }
+};
+
 // Key of q's (block, signature) tuple.  Letters are processed in chunks of
 // 16: all delta loads of a chunk are issued before the first label gather,
 // and all gathers before the first use, so a thread keeps up to 16
@@ -139,9 +153,9 @@ __device__ __forceinline__ uint64_t fp_step(uint64_t h, uint32_t x) {
 // memory latencies per letter).
 constexpr int kLetterChunk = 16;  // default; the counting-table kernel runs best with 8
 
-template <typename LT, int CH = kLetterChunk>
+template <typename LR, int CH = kLetterChunk>
 __device__ __forceinline__ uint64_t tuple_key(uint32_t q, uint32_t lead, const uint32_t* __restrict__ delta,
-                                              uint32_t n, const LT* __restrict__ lab, const SigParams& p) {
+                                              uint32_t n, LR lab, const SigParams& p) {
     const bool packed = p.kind == kKeyPacked;
     uint64_t key = packed ? (uint64_t)lead : fp_step(p.salt, lead);
     for (uint32_t a = p.a0; a < p.a1; a += CH) {
@@ -151,7 +165,7 @@ __device__ __forceinline__ uint64_t tuple_key(uint32_t q, uint32_t lead, const u
             if (a + j < p.a1) t[j] = ld_stream(delta + (uint64_t)(a + j) * n + q);
 #pragma unroll
         for (int j = 0; j < CH; ++j)
-            if (a + j < p.a1) t[j] = (uint32_t)lab[t[j]];
+            if (a + j < p.a1) t[j] = lab[t[j]];
 #pragma unroll
         for (int j = 0; j < CH; ++j)
             if (a + j < p.a1) key = packed ? (key << p.field_bits) | t[j] : fp_step(key + a + j, t[j]);
@@ -161,15 +175,15 @@ __device__ __forceinline__ uint64_t tuple_key(uint32_t q, uint32_t lead, const u
 
 // Plain signature kernel (radix-sort grouping and the exact chunked path):
 // one thread per active state, (key, state) written in list order.
-template <typename LT>
+template <typename LR>
 __global__ void __launch_bounds__(kThreads) signature_kernel(const uint32_t* __restrict__ list, uint64_t m,
                                                              const uint32_t* __restrict__ delta, uint32_t n,
-                                                             const LT* __restrict__ lab,
+                                                             LR lab,
                                                              const uint32_t* __restrict__ head, SigParams p,
                                                              uint64_t* __restrict__ keys, uint32_t* __restrict__ vals) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t q = list ? list[i] : p.q0 + (uint32_t)i;
-        keys[i] = tuple_key<LT>(q, head ? head[i] : (uint32_t)lab[q], delta, n, lab, p);
+        keys[i] = tuple_key<LR>(q, head ? head[i] : lab[q], delta, n, lab, p);
         vals[i] = q;
     }
 }
@@ -178,10 +192,10 @@ __global__ void __launch_bounds__(kThreads) signature_kernel(const uint32_t* __r
 
 // step 1: signature + table of (run minimum, run size), in shared memory
 // when <= 13 bits; equal keys of a warp are combined first (match_any)
-template <typename LT>
+template <typename LR>
 __global__ void __launch_bounds__(512, 3) sig_table_kernel(const uint32_t* __restrict__ list, uint64_t m,
                                                         const uint32_t* __restrict__ delta, uint32_t n,
-                                                        const LT* __restrict__ lab, SigParams p, uint32_t nbits,
+                                                        LR lab, SigParams p, uint32_t nbits,
                                                         uint32_t* __restrict__ keys32, uint32_t* __restrict__ tmin,
                                                         uint32_t* __restrict__ tcnt) {
     extern __shared__ uint32_t st[];  // [tsize] minima, then [tsize] counts (shared mode only)
@@ -198,7 +212,7 @@ __global__ void __launch_bounds__(512, 3) sig_table_kernel(const uint32_t* __res
     }
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t q = list ? list[i] : p.q0 + (uint32_t)i;
-        const uint32_t key = (uint32_t)tuple_key<LT, 8>(q, (uint32_t)lab[q], delta, n, lab, p);
+        const uint32_t key = (uint32_t)tuple_key<LR, 8>(q, lab[q], delta, n, lab, p);
         keys32[i] = key;
         const unsigned peers = __match_any_sync(__activemask(), key);
         const uint32_t mq = __reduce_min_sync(peers, q);
@@ -288,6 +302,17 @@ __global__ void dense2_kernel(const uint32_t* __restrict__ lab, uint32_t n, uint
         out[q] = lab[q] != l0;
 }
 
+// bitmap of a two-block partition: bit q = (lab[q] != lab[0]); one warp per word
+__global__ void dense2_bits_kernel(const uint32_t* __restrict__ lab, uint32_t n, uint32_t* __restrict__ out) {
+    const uint32_t l0 = lab[0];
+    const uint32_t words = (n + 31) / 32;
+    for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < words; w += (gridDim.x * blockDim.x) >> 5) {
+        const uint32_t q = w * 32 + (threadIdx.x & 31u);
+        const unsigned b = __ballot_sync(0xffffffffu, q < n && lab[q] != l0);
+        if ((threadIdx.x & 31u) == 0) out[w] = b;
+    }
+}
+
 // ---- bucket strategy -----------------------------------------------------------------
 
 constexpr int kGrpThreads = 256;
@@ -351,16 +376,16 @@ __device__ __forceinline__ void bucket_append(unsigned long long hk, uint32_t q,
 // Signature + fused radix partition: (hkey, state) appended to bucket
 // hkey >> shift.  Slots b*cap .. b*cap+cap-1; the excess goes to the
 // overflow region at nb*cap (counted in ctr->overflow).
-template <typename LT>
+template <typename LR>
 __global__ void __launch_bounds__(kThreads, 5) sig_bucket_kernel(const uint32_t* __restrict__ list, uint64_t m,
                                                               const uint32_t* __restrict__ delta, uint32_t n,
-                                                              const LT* __restrict__ lab, SigParams p,
+                                                              LR lab, SigParams p,
                                                               uint32_t nb, uint32_t* __restrict__ bcnt,
                                                               uint4* __restrict__ bent,
                                                               IterCounters* __restrict__ ctr) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t q = list ? list[i] : p.q0 + (uint32_t)i;
-        const uint64_t key = tuple_key<LT>(q, (uint32_t)lab[q], delta, n, lab, p);
+        const uint64_t key = tuple_key<LR>(q, lab[q], delta, n, lab, p);
         const unsigned long long hk = p.kind == kKeyPacked ? mix64(key) : key;
         bucket_append(hk, q, 0u, nb, bcnt, bent, ctr);
     }
@@ -657,7 +682,7 @@ __global__ void gather_dense_kernel(const uint32_t* __restrict__ list, uint64_t 
 struct Workspace {
     DBuf<uint32_t> lab, lab2, list0, list1, vals0, vals1, heads, pos, run_start, scratch, cur, tmin, tcnt, trank, next32;
     DBuf<uint16_t> next16;
-    DBuf<uint32_t> dense32;
+    DBuf<uint32_t> dense32, bits;
     DBuf<uint8_t> dense8;
     DBuf<uint16_t> dense16;
     DBuf<uint64_t> keys0, keys1;
@@ -677,12 +702,17 @@ struct KeyLab {
     int bytes;
 };
 
+constexpr int kBitLabels = (int)kKeylabBits;  // KeyLab::bytes tag: one bit per state
+
 template <typename F>
 void with_lab_type(const KeyLab& kl, F&& f) {
-    if (kl.bytes == 1) f(static_cast<const uint8_t*>(kl.p));
-    else if (kl.bytes == 2) f(static_cast<const uint16_t*>(kl.p));
-    else f(static_cast<const uint32_t*>(kl.p));
+    if (kl.bytes == kBitLabels) f(BitLab{static_cast<const uint32_t*>(kl.p)});
+    else if (kl.bytes == 1) f(ArrLab<uint8_t>{static_cast<const uint8_t*>(kl.p)});
+    else if (kl.bytes == 2) f(ArrLab<uint16_t>{static_cast<const uint16_t*>(kl.p)});
+    else f(ArrLab<uint32_t>{static_cast<const uint32_t*>(kl.p)});
 }
+
+double keylab_bytes_per_state(const KeyLab& kl) { return kl.bytes == kBitLabels ? 0.125 : (double)kl.bytes; }
 
 // ---- persistent small-m engine ---------------------------------------------------
 //
@@ -764,7 +794,7 @@ __global__ void __launch_bounds__(kThreads) small_persistent_kernel(SmallArgs A)
         // keys, insert, elect the run minimum, count the run (slot T: a ~0 key)
         for (uint32_t i = tid; i < m; i += stride) {
             const uint32_t q = list[i];
-            const uint64_t key = tuple_key<uint32_t, 8>(q, A.lab[q], A.delta, A.n, A.lab, p);
+            const uint64_t key = tuple_key<ArrLab<uint32_t>, 8>(q, A.lab[q], A.delta, A.n, ArrLab<uint32_t>{A.lab}, p);
             const unsigned long long hk = p.kind == kKeyPacked ? mix64(key) : key;
             uint32_t sl;
             if (hk == kEmptyKey) {
@@ -969,9 +999,13 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
     DK_CUDA(cudaFuncSetAttribute(bucket_group_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)sizeof(GroupSmem)));
     const int smem_table = (int)(2u << kSmemTableBits) * 4;
-    DK_CUDA(cudaFuncSetAttribute(sig_table_kernel<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_table));
-    DK_CUDA(cudaFuncSetAttribute(sig_table_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_table));
-    DK_CUDA(cudaFuncSetAttribute(sig_table_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_table));
+    DK_CUDA(cudaFuncSetAttribute(sig_table_kernel<BitLab>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_table));
+    DK_CUDA(cudaFuncSetAttribute(sig_table_kernel<ArrLab<uint8_t>>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 smem_table));
+    DK_CUDA(cudaFuncSetAttribute(sig_table_kernel<ArrLab<uint16_t>>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 smem_table));
+    DK_CUDA(cudaFuncSetAttribute(sig_table_kernel<ArrLab<uint32_t>>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 smem_table));
     IterCounters* dctr = w.ctr.get();
 
     // initial partition {F, Q\F} with min-state labels
@@ -1046,6 +1080,11 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
         if (plan.keylab_bytes) {
             if (next_valid && plan.strategy != kPlanChunked) {
                 kl = w.next16.get() && prev_nbits <= 16 ? KeyLab{w.next16.get(), 2} : KeyLab{w.next32.get(), 4};
+            } else if (B <= 2 && plan.strategy != kPlanChunked && n >= kBitLabelsMinStates) {
+                if (!w.bits.get()) w.bits.alloc((n + 31) / 32, s);
+                DK_LAUNCH(ctx, dense2_bits_kernel, grid_for((uint64_t)n), kThreads, 0, s, w.lab.get(), n,
+                          w.bits.get());
+                kl = KeyLab{w.bits.get(), kBitLabels};
             } else if (B <= 2 && plan.strategy != kPlanChunked) {
                 if (!w.dense8.get()) w.dense8.alloc(n, s);
                 DK_LAUNCH(ctx, dense2_kernel, grid_for(n), kThreads, 0, s, w.lab.get(), n, w.dense8.get());
@@ -1085,7 +1124,7 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
             const unsigned tg = (unsigned)std::min<uint64_t>((m + 511) / 512, (uint64_t)ctx->num_sms * 3);
             with_lab_type(kl, [&](auto lab) {
                 // algorithmic HBM bytes: delta rows + key out (+ list), the key-label array once
-                DK_LAUNCH_BU(ctx, (double)m * (4.0 + 4.0 * k + list_b) + (double)kl.bytes * n, (double)m * k,
+                DK_LAUNCH_BU(ctx, (double)m * (4.0 + 4.0 * k + list_b) + keylab_bytes_per_state(kl) * n, (double)m * k,
                              sig_table_kernel, tg,
                             512, smem, s, list, m, d.delta, n, lab, p, nbits, w.heads.get(), w.tmin.get(),
                             w.tcnt.get());
@@ -1143,7 +1182,7 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
             if (!state_order) DK_CUDA(cudaMemsetAsync(w.keep_slot.get(), 0, espace, s));
             with_lab_type(kl, [&](auto lab) {
                 // algorithmic HBM bytes: delta rows (+ list), (hkey, state) out, the key-label array once
-                DK_LAUNCH_BU(ctx, (double)m * (4.0 * k + 16.0 + list_b) + (double)kl.bytes * n, (double)m * k,
+                DK_LAUNCH_BU(ctx, (double)m * (4.0 * k + 16.0 + list_b) + keylab_bytes_per_state(kl) * n, (double)m * k,
                              sig_bucket_kernel,
                             grid_for(m, kThreads, (unsigned)ctx->num_sms * 8u), kThreads, 0, s, list, m, d.delta, n,
                             lab, p, nb, w.bcnt.get(), w.bent.get(), dctr);
@@ -1222,7 +1261,7 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
             uint32_t* svals = w.vals0.get();
             if (!chunked) {
                 with_lab_type(kl, [&](auto lab) {
-                    DK_LAUNCH_BU(ctx, (double)m * (12.0 + 4.0 * k + list_b) + (double)kl.bytes * n, (double)m * k,
+                    DK_LAUNCH_BU(ctx, (double)m * (12.0 + 4.0 * k + list_b) + keylab_bytes_per_state(kl) * n, (double)m * k,
                                  signature_kernel, g, kThreads, 0, s, list, m, d.delta, n, lab, nullptr, p,
                                 w.keys0.get(), w.vals0.get());
                 });
@@ -1261,8 +1300,8 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
                     pc.a0 = a;
                     pc.a1 = a + c_letters;
                     pc.field_bits = field_bits;
-                    DK_LAUNCH_B(ctx, (double)m * (24.0 + 8.0 * c_letters), signature_kernel<uint32_t>, g, kThreads, 0,
-                                s, elist, m, d.delta, n, static_cast<const uint32_t*>(kl.p), w.cur.get(), pc,
+                    DK_LAUNCH_B(ctx, (double)m * (24.0 + 8.0 * c_letters), signature_kernel<ArrLab<uint32_t>>, g, kThreads, 0,
+                                s, elist, m, d.delta, n, ArrLab<uint32_t>{static_cast<const uint32_t*>(kl.p)}, w.cur.get(), pc,
                                 w.keys0.get(), w.vals0.get());
                     const bool flip = radix_sort_pairs(ctx, rb, m, cur_bits + c_letters * field_bits, s);
                     res.sorted += m;
@@ -1339,10 +1378,10 @@ __device__ __forceinline__ uint32_t owner_of(unsigned long long hk, uint32_t wor
 }
 
 // entries {hk, state, dest} in list order + per-destination counts
-template <typename LT>
+template <typename LR>
 __global__ void __launch_bounds__(kThreads) sig_entries_kernel(const uint32_t* __restrict__ list, uint64_t m,
                                                                const uint32_t* __restrict__ delta, uint32_t n,
-                                                               const LT* __restrict__ lab, SigParams p,
+                                                               LR lab, SigParams p,
                                                                uint32_t world, uint4* __restrict__ tmp,
                                                                uint32_t* __restrict__ counts) {
     __shared__ uint32_t cnt[kMaxWorld];
@@ -1350,7 +1389,7 @@ __global__ void __launch_bounds__(kThreads) sig_entries_kernel(const uint32_t* _
     __syncthreads();
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t q = list ? list[i] : p.q0 + (uint32_t)i;
-        const uint64_t key = tuple_key<LT>(q, (uint32_t)lab[q], delta, n, lab, p);
+        const uint64_t key = tuple_key<LR>(q, lab[q], delta, n, lab, p);
         const unsigned long long hk = p.kind == kKeyPacked ? mix64(key) : key;
         const uint32_t d = owner_of(hk, world);
         tmp[i] = make_uint4((uint32_t)hk, (uint32_t)(hk >> 32), q, d);
@@ -1471,7 +1510,9 @@ ShardInit shard_init(Ctx* ctx, const DevDfa& d, uint32_t lo, uint32_t hi, uint32
 void shard_keylab(Ctx* ctx, const uint32_t* lab, uint32_t n, uint32_t num_blocks, const PassPlan& plan, void* out,
                   uint32_t* scratch, cudaStream_t s) {
     if (!plan.keylab_bytes) return;
-    if (num_blocks <= 2 && plan.keylab_bytes == 1)  // two blocks: no scan
+    if (plan.keylab_bytes == kBitLabels)  // two blocks: a bitmap, no scan
+        DK_LAUNCH(ctx, dense2_bits_kernel, grid_for((uint64_t)n), kThreads, 0, s, lab, n, static_cast<uint32_t*>(out));
+    else if (num_blocks <= 2 && plan.keylab_bytes == 1)  // two blocks: no scan
         DK_LAUNCH(ctx, dense2_kernel, grid_for(n), kThreads, 0, s, lab, n, static_cast<uint8_t*>(out));
     else
         dense_labels(ctx, lab, n, out, (int)plan.keylab_bytes, scratch, s);
@@ -1492,9 +1533,9 @@ void shard_table_signature(Ctx* ctx, const DevDfa& d, const void* keylab, const 
     SigParams p = sig_params(plan, d.k, 0);
     p.q0 = list_base;
     with_lab_type(KeyLab{keylab, plan.keylab_bytes ? (int)plan.keylab_bytes : 4}, [&](auto lab) {
-        using LT = std::remove_const_t<std::remove_pointer_t<decltype(lab)>>;
-        DK_CUDA(cudaFuncSetAttribute(sig_table_kernel<LT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_table));
-        DK_LAUNCH_BU(ctx, (double)m * (8.0 + 4.0 * d.k), (double)m * d.k, sig_table_kernel<LT>, tg, 512, smem, s, list, m, d.delta,
+        using LR = decltype(lab);
+        DK_CUDA(cudaFuncSetAttribute(sig_table_kernel<LR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_table));
+        DK_LAUNCH_BU(ctx, (double)m * (8.0 + 4.0 * d.k), (double)m * d.k, sig_table_kernel<LR>, tg, 512, smem, s, list, m, d.delta,
                     d.n, lab, p, nbits, keys32, tmin, tcnt);
     });
 }

@@ -154,7 +154,7 @@ RefineResult sort_pr_sharded_device(Ctx* ctx, NcclComm* cm, const DevDfa& d, uin
     DBuf<uint32_t> dctr(8, s), counts(world, s), keys32;
     DBuf<uint8_t> kl8;
     DBuf<uint16_t> kl16, next16;
-    DBuf<uint32_t> kl32, next32, tmin, tcnt, results, back;
+    DBuf<uint32_t> kl32, next32, tmin, tcnt, results, back, bits;
     DBuf<uint4> send, recv;
     uint32_t* hmail = reinterpret_cast<uint32_t*>(ctx->mailbox);
     auto read_u32 = [&](const uint32_t* p, size_t count, uint32_t* out) {
@@ -193,7 +193,11 @@ RefineResult sort_pr_sharded_device(Ctx* ctx, NcclComm* cm, const DevDfa& d, uin
                 plan.keylab_bytes = carried_bytes;
             } else {
                 void* out;
-                if (plan.keylab_bytes == 1) {
+                if (plan.keylab_bytes == 1 && B <= 2 && n >= kBitLabelsMinStates) {  // two blocks, large n: a bitmap
+                    if (!bits.get()) bits.alloc(((uint64_t)n + 31) / 32, s);
+                    plan.keylab_bytes = kKeylabBits;
+                    out = bits.get();
+                } else if (plan.keylab_bytes == 1) {
                     if (!kl8.get()) kl8.alloc(n, s);
                     out = kl8.get();
                 } else if (plan.keylab_bytes == 2) {

@@ -41,6 +41,8 @@ import numpy as np
 from ._native import CDfa as _CDfa, Context, CPassPlan, check, lib
 
 PLAN_TABLE, PLAN_PACKED, PLAN_FINGERPRINT, PLAN_CHUNKED = 0, 1, 2, 3
+KEYLAB_BITS = 255  # PassPlan.keylab_bytes tag: one bit per state
+BIT_LABELS_MIN_STATES = 1 << 25  # refine.cuh kBitLabelsMinStates
 _SALT0 = 0x5EED5EED5EED
 
 
@@ -178,8 +180,13 @@ class CudaShardOps:
     def keylab(self, lab, plan, num_blocks):
         if not plan.keylab_bytes:
             return lab
-        dt = {1: self.torch.uint8, 2: self.torch.int16, 4: self.torch.int32}[plan.keylab_bytes]
-        out = self._buf(f"keylab{plan.keylab_bytes}", self.n, dt)
+        if plan.keylab_bytes == 1 and num_blocks <= 2 and self.n >= BIT_LABELS_MIN_STATES:
+            plan.keylab_bytes = KEYLAB_BITS  # two blocks, large n: one bit per state
+        if plan.keylab_bytes == KEYLAB_BITS:
+            out = self._buf("keylab_bits", (self.n + 31) // 32, self.torch.int32)
+        else:
+            dt = {1: self.torch.uint8, 2: self.torch.int16, 4: self.torch.int32}[plan.keylab_bytes]
+            out = self._buf(f"keylab{plan.keylab_bytes}", self.n, dt)
         check(lib.dfakit_shard_keylab(self.ctx.handle, lab.data_ptr(), self.n, num_blocks, C.byref(plan),
                                       out.data_ptr(), self.stream))
         return out

@@ -260,3 +260,22 @@ def test_config4_size_1B_transitions_single_gpu(dk):
     dd = d.view(k, n).long()
     for x in range(k):
         assert torch.equal(blk[dd[x]], blk[dd[x][rep_of]])
+    del dd, rep_of, first
+    # the native sharded engine (world size 1, NCCL) gives the same partition
+    import os
+    import socket
+    import torch.distributed as dist
+    from paper_2508_20735_b200 import sharded
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = str(sk.getsockname()[1])
+    sk.close()
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        comm = sharded.NativeComm(ctx)
+        b2, r2 = sharded.sort_pr_sharded_native(ctx, comm, d, a, n, k)
+        assert torch.equal(b2, b) and r2.refining_iterations == rep.refining_iterations
+        comm.close()
+    finally:
+        dist.destroy_process_group()
