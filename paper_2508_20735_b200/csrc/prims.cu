@@ -122,28 +122,6 @@ void iota_u32(Ctx* ctx, uint32_t* p, uint64_t n, cudaStream_t s) {
     if (n) DK_LAUNCH(ctx, iota_kernel, grid_for(n), kThreads, 0, s, p, n);
 }
 
-__global__ void flag_to_u32_kernel(const uint8_t* __restrict__ f, uint64_t n, uint32_t* __restrict__ o) {
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-        o[i] = f[i] ? 1u : 0u;
-}
-
-__global__ void compact_scatter_kernel(const uint32_t* __restrict__ in, const uint8_t* __restrict__ f, uint64_t n,
-                                       const uint32_t* __restrict__ pos, uint32_t* __restrict__ out) {
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-        if (f[i]) out[pos[i]] = in ? in[i] : (uint32_t)i;
-}
-
-uint32_t compact_u32(Ctx* ctx, const uint32_t* in, const uint8_t* flag, uint64_t n, uint32_t* out,
-                     uint32_t* scratch, cudaStream_t s) {
-    if (n == 0) return 0;
-    DK_LAUNCH(ctx, flag_to_u32_kernel, grid_for(n), kThreads, 0, s, flag, n, scratch);
-    exclusive_scan_u32(ctx, scratch, scratch, n, scratch + n, s);
-    DK_LAUNCH(ctx, compact_scatter_kernel, grid_for(n), kThreads, 0, s, in, flag, n, scratch, out);
-    uint32_t total = 0;
-    read_words(ctx, scratch + n, sizeof(uint32_t), &total, s);
-    return total;
-}
-
 // ---------------------------------------------------------------------------
 // tiled compaction / head scan: per-tile counts, one-CTA scan of the tile
 // counts, then an apply pass that re-reads its tile (coalesced), scans it in
@@ -294,11 +272,6 @@ void head_scan(Ctx* ctx, const uint32_t* lab, uint64_t n, uint32_t* pos, uint32_
 // ---------------------------------------------------------------------------
 // canonical renumbering
 // ---------------------------------------------------------------------------
-
-__global__ void head_flags_kernel(const uint32_t* __restrict__ lab, uint64_t n, uint32_t* __restrict__ f) {
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-        f[i] = lab[i] == (uint32_t)i ? 1u : 0u;
-}
 
 __global__ void relabel_kernel(const uint32_t* __restrict__ lab, uint64_t n, const uint32_t* __restrict__ dense,
                                uint32_t* __restrict__ out) {

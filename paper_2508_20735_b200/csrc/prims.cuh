@@ -43,11 +43,6 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* t
 void exclusive_scan_u32(Ctx* ctx, const uint32_t* in, uint32_t* out, uint64_t n, uint32_t* total_dev,
                         cudaStream_t s);
 
-// Compacts in[i] where flag[i] != 0, preserving order (in == nullptr means
-// in[i] = i).  Returns the count (synchronises).  scratch holds n+1 uint32.
-uint32_t compact_u32(Ctx* ctx, const uint32_t* in, const uint8_t* flag, uint64_t n, uint32_t* out,
-                     uint32_t* scratch, cudaStream_t s);
-
 // LSD radix sort on bits [0, nbits) of 64-bit keys with 32-bit values.
 // Stable.  Ping-pongs between (k0,v0) and (k1,v1); returns true when the
 // sorted data ended in (k1,v1).
