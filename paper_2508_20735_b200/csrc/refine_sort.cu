@@ -1061,7 +1061,6 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
             res.passes += sr.st.passes;
             res.iters += sr.st.iters;
             res.collisions += sr.st.collisions;
-            res.sorted += 0;
             B = sr.st.B;
             A = sr.st.A;
             m = sr.st.m;
@@ -1107,7 +1106,6 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
         const double list_b = list ? 4.0 : 0.0;
         IterCounters c{};
         uint32_t* dst = (list == list_buf) ? list_alt : list_buf;
-        bool listed = false;  // survivors already compacted into dst
 
         if (plan.strategy == kPlanTable && o.grouping != 1) {
             // ---- table strategy
@@ -1148,7 +1146,6 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
             next_valid = full;
             prev_nbits = nbits;
             compact_flags(ctx, list, w.keep.get(), m, dst, &dctr->listed, s);
-            listed = true;
             read_words(ctx, dctr, sizeof(c), &c, s);
         } else if (!chunked && o.grouping != 1) {
             // ---- bucket strategy
@@ -1244,7 +1241,6 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
                     compact_flags(ctx, w.eval.get(), w.keep_slot.get(), bspace + c.overflow, dst, &dctr->listed, s);
                 }
             }
-            listed = true;
         } else {
             // ---- radix-sort grouping: (key, state) pairs, LSD radix sort, runs
             if (!w.keys0.get()) {
@@ -1334,7 +1330,6 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
                         state_order ? w.act.get() : nullptr, dctr);
             if (state_order) compact_flags(ctx, nullptr, w.act.get(), n, dst, &dctr->listed, s);
             else compact_flags(ctx, svals, w.keep.get(), m, dst, &dctr->listed, s);
-            listed = true;
             read_words(ctx, dctr, sizeof(c), &c, s);
         }
 
@@ -1345,7 +1340,7 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
         B = newB;
         A = c.active_blocks;
         m = c.active_states;
-        if (listed && m) {
+        if (m) {  // every strategy compacted the survivors into dst
             list = dst;
             if (dst == list_alt) std::swap(list_buf, list_alt);
         }

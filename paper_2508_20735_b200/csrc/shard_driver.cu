@@ -156,11 +156,9 @@ RefineResult sort_pr_sharded_device(Ctx* ctx, NcclComm* cm, const DevDfa& d, uin
     DBuf<uint16_t> kl16, next16;
     DBuf<uint32_t> kl32, next32, tmin, tcnt, results, back, bits;
     DBuf<uint4> send, recv;
-    uint32_t* hmail = reinterpret_cast<uint32_t*>(ctx->mailbox);
     auto read_u32 = [&](const uint32_t* p, size_t count, uint32_t* out) {
         read_words(ctx, p, count * sizeof(uint32_t), out, s);
     };
-    (void)hmail;
 
     const ShardInit si = shard_init(ctx, d, lo, hi, lab.get(), act.get(), s);
     uint32_t B = si.num_blocks, A = si.active_blocks;
