@@ -108,6 +108,20 @@ void fill_report(dfakit_report* r, const dk::RefineResult& rr, uint32_t algo, ui
     r->device_ms = ms;
 }
 
+constexpr uint32_t kStreamMinStates = 1u << 20;  // below this the copy is too short to split
+constexpr uint32_t kStreamChunks = 8;
+
+dk::RefineResult run_sort_streamed(dk::Ctx* c, const dk::DevDfa& v, const dfakit_options* o, uint32_t* block_out,
+                                   cudaStream_t s, const dk::DeltaStream* ds) {
+    dfakit_options def{};
+    if (!o) o = &def;
+    dk::SortOptions so;
+    so.force_exact = o->force_exact != 0;
+    so.fingerprint_bits = o->fingerprint_bits ? o->fingerprint_bits : 64;
+    so.grouping = o->grouping;
+    return dk::sort_pr_device(c, v, so, block_out, s, ds);
+}
+
 dk::RefineResult run_algo(dk::Ctx* c, const dk::DevDfa& v, dfakit_algorithm algo, const dfakit_options* o,
                           uint32_t* block_out, uint8_t* apart_dev, cudaStream_t s) {
     dfakit_options def{};
@@ -142,14 +156,58 @@ void minimize_host(dfakit_ctx* ctx, const dfakit_dfa* dfa, dfakit_algorithm algo
     dk::Ctx* c = ctx->c;
     DK_CUDA(cudaSetDevice(c->device));
     cudaStream_t s = c->stream;
+    const uint32_t n = dfa->num_states, k = dfa->alphabet_size;
+    const bool sortish = algo == DFAKIT_ALGO_SORT_PR || algo == DFAKIT_ALGO_MOORE;
+    const bool stream_in = sortish && (!opts || opts->grouping != 1) && n >= kStreamMinStates && k > 0;
     Staged st;
-    stage(c, dfa, st, s);
-    const uint32_t n = dfa->num_states;
+    dk::DeltaStream ds;
+    std::vector<uint32_t> bounds;
+    std::vector<cudaEvent_t> ready;
+    if (stream_in) {
+        // delta in state-range chunks on the copy stream; pass 1 consumes
+        // them as they land (validation included), hiding under the copy
+        const uint64_t total = (uint64_t)n * k;
+        st.delta.alloc(total, s);
+        st.acc.alloc(n, s);
+        DK_CUDA(cudaMemcpyAsync(st.acc.get(), dfa->accepting, n, cudaMemcpyHostToDevice, s));
+        if (!c->copy_stream) DK_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+        cudaEvent_t allocated;
+        DK_CUDA(cudaEventCreateWithFlags(&allocated, cudaEventDisableTiming));
+        DK_CUDA(cudaEventRecord(allocated, s));
+        DK_CUDA(cudaStreamWaitEvent(c->copy_stream, allocated, 0));
+        cudaEventDestroy(allocated);
+        const uint32_t chunks = kStreamChunks;
+        for (uint32_t i = 0; i <= chunks; ++i) bounds.push_back((uint32_t)((uint64_t)n * i / chunks));
+        ready.resize(chunks);
+        for (uint32_t i = 0; i < chunks; ++i) {
+            const uint32_t q0 = bounds[i], q1 = bounds[i + 1];
+            DK_CUDA(cudaEventCreateWithFlags(&ready[i], cudaEventDisableTiming));
+            if (q1 > q0)
+                DK_CUDA(cudaMemcpy2DAsync(st.delta.get() + q0, (size_t)n * 4, dfa->delta + q0, (size_t)n * 4,
+                                          (size_t)(q1 - q0) * 4, k, cudaMemcpyHostToDevice, c->copy_stream));
+            DK_CUDA(cudaEventRecord(ready[i], c->copy_stream));
+        }
+        st.view = dk::DevDfa{n, k, st.delta.get(), st.acc.get(), dfa->initial};
+        ds.chunks = chunks;
+        ds.bounds = bounds.data();
+        ds.ready = ready.data();
+    } else {
+        stage(c, dfa, st, s);
+    }
+    struct EventsGuard {  // every exit (errors included) drains the copy stream first
+        std::vector<cudaEvent_t>& e;
+        cudaStream_t cs;
+        ~EventsGuard() {
+            if (cs && !e.empty()) cudaStreamSynchronize(cs);
+            for (auto x : e) cudaEventDestroy(x);
+        }
+    } guard_events{ready, c->copy_stream};
     dk::DBuf<uint32_t> blocks(n ? n : 1, s);
     dk::DBuf<uint8_t> ap;
     if (apart && algo == DFAKIT_ALGO_TRANS) ap.alloc((uint64_t)n * n ? (uint64_t)n * n : 1, s);
     DK_CUDA(cudaEventRecord(c->ev0, s));
-    dk::RefineResult rr = run_algo(c, st.view, algo, opts, blocks.get(), ap.get(), s);
+    dk::RefineResult rr = stream_in ? run_sort_streamed(c, st.view, opts, blocks.get(), s, &ds)
+                                    : run_algo(c, st.view, algo, opts, blocks.get(), ap.get(), s);
     DK_CUDA(cudaEventRecord(c->ev1, s));
     if (n && block_of) DK_CUDA(cudaMemcpyAsync(block_of, blocks.get(), (size_t)n * 4, cudaMemcpyDeviceToHost, s));
     if (ap.get() && n) DK_CUDA(cudaMemcpyAsync(apart, ap.get(), (size_t)n * n, cudaMemcpyDeviceToHost, s));

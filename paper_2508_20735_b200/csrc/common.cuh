@@ -70,6 +70,7 @@ struct Ctx {
     int device = 0;
     int num_sms = 148;
     cudaStream_t stream = nullptr;
+    cudaStream_t copy_stream = nullptr;  // host->device input streaming (lazily created)
     bool own_stream = true;
     uint64_t* mailbox = nullptr;  // pinned host, 64 words
     uint64_t* dmailbox = nullptr; // device, 64 words

@@ -101,6 +101,7 @@ void ctx_destroy(Ctx* c) {
     if (c->dmailbox) cudaFree(c->dmailbox);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
+    if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     if (c->stream && c->own_stream) cudaStreamDestroy(c->stream);
     delete c;
 }

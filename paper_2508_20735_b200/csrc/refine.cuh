@@ -79,7 +79,16 @@ RefineResult sort_pr_sharded_device(Ctx* ctx, NcclComm* comm, const DevDfa& d, u
                                     uint64_t* exchanged);
 
 // All block_out arrays are device arrays of n entries, canonical numbering.
-RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uint32_t* block_out, cudaStream_t s);
+// Host-buffer calls stream delta to the device in state-range chunks on a
+// copy stream; pass 1 of sort_pr then consumes chunk c once ready[c] fired
+// (range check + counting-table signatures), hiding under the PCIe copy.
+struct DeltaStream {
+    uint32_t chunks = 0;
+    const uint32_t* bounds = nullptr;  // host, chunks + 1 state indices
+    const cudaEvent_t* ready = nullptr;
+};
+RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uint32_t* block_out, cudaStream_t s,
+                            const DeltaStream* ds = nullptr);
 RefineResult naive_pr_device(Ctx* ctx, const DevDfa& d, int policy, uint64_t seed, uint32_t* block_out,
                              cudaStream_t s);
 RefineResult naive_pr_fused_device(Ctx* ctx, const DevDfa& d, uint32_t* block_out, cudaStream_t s);

@@ -146,14 +146,17 @@ struct BitLab {
     __device__ __forceinline__ uint32_t operator[](uint32_t i) const { return (__ldg(w + (i >> 5)) >> (i & 31u)) & 1u; }
 };
 
-// Key of q's (block, signature) tuple.  Letters are processed in chunks of
+// Key of q's (block, signature) tuple.  CLAMP: successor ids are clamped to
+// n - 1 -- streamed host-buffer calls validate delta while pass 1 already
+// consumes it (the range-check flag is read after the pass and the call
+// fails), so an out-of-range target must not fault meanwhile.  Letters are processed in chunks of
 // 16: all delta loads of a chunk are issued before the first label gather,
 // and all gathers before the first use, so a thread keeps up to 16
 // independent loads in flight (the loop-carried version serialised two
 // memory latencies per letter).
 constexpr int kLetterChunk = 16;  // default; the counting-table kernel runs best with 8
 
-template <typename LR, int CH = kLetterChunk>
+template <typename LR, int CH = kLetterChunk, bool CLAMP = false>
 __device__ __forceinline__ uint64_t tuple_key(uint32_t q, uint32_t lead, const uint32_t* __restrict__ delta,
                                               uint32_t n, LR lab, const SigParams& p) {
     const bool packed = p.kind == kKeyPacked;
@@ -162,7 +165,10 @@ __device__ __forceinline__ uint64_t tuple_key(uint32_t q, uint32_t lead, const u
         uint32_t t[CH];
 #pragma unroll
         for (int j = 0; j < CH; ++j)
-            if (a + j < p.a1) t[j] = ld_stream(delta + (uint64_t)(a + j) * n + q);
+            if (a + j < p.a1) {
+                t[j] = ld_stream(delta + (uint64_t)(a + j) * n + q);
+                if (CLAMP) t[j] = min(t[j], n - 1);
+            }
 #pragma unroll
         for (int j = 0; j < CH; ++j)
             if (a + j < p.a1) t[j] = lab[t[j]];
@@ -192,7 +198,7 @@ __global__ void __launch_bounds__(kThreads) signature_kernel(const uint32_t* __r
 
 // step 1: signature + table of (run minimum, run size), in shared memory
 // when <= 13 bits; equal keys of a warp are combined first (match_any)
-template <typename LR>
+template <typename LR, bool CLAMP = false>
 __global__ void __launch_bounds__(512, 3) sig_table_kernel(const uint32_t* __restrict__ list, uint64_t m,
                                                         const uint32_t* __restrict__ delta, uint32_t n,
                                                         LR lab, SigParams p, uint32_t nbits,
@@ -212,7 +218,7 @@ __global__ void __launch_bounds__(512, 3) sig_table_kernel(const uint32_t* __res
     }
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t q = list ? list[i] : p.q0 + (uint32_t)i;
-        const uint32_t key = (uint32_t)tuple_key<LR, 8>(q, lab[q], delta, n, lab, p);
+        const uint32_t key = (uint32_t)tuple_key<LR, 8, CLAMP>(q, lab[q], delta, n, lab, p);
         keys32[i] = key;
         const unsigned peers = __match_any_sync(__activemask(), key);
         const uint32_t mq = __reduce_min_sync(peers, q);
@@ -300,6 +306,16 @@ __global__ void dense2_kernel(const uint32_t* __restrict__ lab, uint32_t n, uint
     const uint32_t l0 = lab[0];
     for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x)
         out[q] = lab[q] != l0;
+}
+
+// delta targets of states [q0, q1) must be < n (reference dfa.cpp validation)
+__global__ void range_check_rows_kernel(const uint32_t* __restrict__ delta, uint32_t n, uint32_t k, uint32_t q0,
+                                        uint32_t q1, uint32_t* __restrict__ bad) {
+    const uint64_t w = q1 - q0, total = w * k;
+    bool b = false;
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total; t += (uint64_t)gridDim.x * blockDim.x)
+        b |= __ldcs(delta + (t / w) * n + q0 + t % w) >= n;
+    if (__syncthreads_or(b) && threadIdx.x == 0) atomicOr(bad, 1u);
 }
 
 // bitmap of a two-block partition: bit q = (lab[q] != lab[0]); one warp per word
@@ -985,7 +1001,8 @@ SmallRun run_small_persistent(Ctx* ctx, const DevDfa& d, uint32_t* lab, uint32_t
 
 }  // namespace
 
-RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uint32_t* block_out, cudaStream_t s) {
+RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uint32_t* block_out, cudaStream_t s,
+                            const DeltaStream* ds) {
     RefineResult res;
     const uint32_t n = d.n, k = d.k;
     if (n == 0) return res;
@@ -1047,10 +1064,31 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
         return KeyLab{p, bytes};
     };
 
+    // streamed input: which chunks the compute stream has waited for
+    uint32_t* bad = reinterpret_cast<uint32_t*>(ctx->dmailbox) + 40;
+    bool streamed = ds && ds->chunks;
+    auto check_streamed = [&] {
+        if (!streamed) return;
+        uint32_t b = 0;
+        read_words(ctx, bad, 4, &b, s);
+        if (b) throw Error(DFAKIT_E_INVALID, "delta: transition target out of range");
+        streamed = false;
+    };
+    // paths other than the chunked pass 1 take the whole input, validated
+    // before any kernel reads it
+    auto wait_all_chunks = [&] {
+        if (!streamed) return;
+        for (uint32_t c = 0; c < ds->chunks; ++c) DK_CUDA(cudaStreamWaitEvent(s, ds->ready[c], 0));
+        DK_CUDA(cudaMemsetAsync(bad, 0, 4, s));
+        DK_LAUNCH(ctx, range_check_rows_kernel, grid_for((uint64_t)n * k), kThreads, 0, s, d.delta, n, k, 0u, n, bad);
+        check_streamed();
+    };
     while (m > 0) {
         // few active states: the remaining passes on the device (no host
         // round trip per pass); a pass with three collisions comes back here
         if (m <= kSmallPersistMax && o.grouping == 0 && !o.force_exact && collisions_this_pass == 0) {
+            wait_all_chunks();
+            check_streamed();
             const bool identity = list == nullptr;
             if (identity) {  // materialise the identity list
                 iota_u32(ctx, list_buf, m, s);
@@ -1119,14 +1157,42 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
             DK_CUDA(cudaMemsetAsync(w.tcnt.get(), 0, tsize * sizeof(uint32_t), s));
             const bool local = nbits <= kSmemTableBits;
             const size_t smem = local ? (size_t)(2u << nbits) * 4 : 0;
-            const unsigned tg = (unsigned)std::min<uint64_t>((m + 511) / 512, (uint64_t)ctx->num_sms * 3);
-            with_lab_type(kl, [&](auto lab) {
-                // algorithmic HBM bytes: delta rows + key out (+ list), the key-label array once
-                DK_LAUNCH_BU(ctx, (double)m * (4.0 + 4.0 * k + list_b) + keylab_bytes_per_state(kl) * n, (double)m * k,
-                             sig_table_kernel, tg,
-                            512, smem, s, list, m, d.delta, n, lab, p, nbits, w.heads.get(), w.tmin.get(),
-                            w.tcnt.get());
-            });
+            auto sig_table = [&](uint32_t q0, uint64_t mm, bool clamp) {
+                const unsigned tg = (unsigned)std::min<uint64_t>((mm + 511) / 512, (uint64_t)ctx->num_sms * 3);
+                SigParams pc = p;
+                pc.q0 = q0;
+                with_lab_type(kl, [&](auto lab) {
+                    using LR = decltype(lab);
+                    // algorithmic HBM bytes: delta rows + key out (+ list), the key-label array once
+                    const double bytes = (double)mm * (4.0 + 4.0 * k + list_b) + keylab_bytes_per_state(kl) * n;
+                    if (clamp) {
+                        auto sig_table_clamped_kernel = sig_table_kernel<LR, true>;
+                        DK_CUDA(cudaFuncSetAttribute(sig_table_clamped_kernel,
+                                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                     (int)(2u << kSmemTableBits) * 4));
+                        DK_LAUNCH_BU(ctx, bytes, (double)mm * k, sig_table_clamped_kernel, tg, 512, smem, s, list,
+                                     mm, d.delta, n, lab, pc, nbits, w.heads.get() + q0, w.tmin.get(), w.tcnt.get());
+                    } else {
+                        DK_LAUNCH_BU(ctx, bytes, (double)mm * k, sig_table_kernel<LR>, tg, 512, smem, s, list, mm,
+                                     d.delta, n, lab, pc, nbits, w.heads.get() + q0, w.tmin.get(), w.tcnt.get());
+                    }
+                });
+            };
+            if (streamed && list == nullptr) {
+                // pass 1 chunk by chunk as delta arrives
+                DK_CUDA(cudaMemsetAsync(bad, 0, 4, s));
+                for (uint32_t c = 0; c < ds->chunks; ++c) {
+                    const uint32_t q0 = ds->bounds[c], q1 = ds->bounds[c + 1];
+                    DK_CUDA(cudaStreamWaitEvent(s, ds->ready[c], 0));
+                    if (q1 == q0) continue;
+                    DK_LAUNCH(ctx, range_check_rows_kernel, grid_for((uint64_t)(q1 - q0) * k), kThreads, 0, s,
+                              d.delta, n, k, q0, q1, bad);
+                    sig_table(q0, q1 - q0, true);
+                }
+            } else {
+                wait_all_chunks();
+                sig_table(0, m, false);
+            }
             // a table pass over every state sees every block of the next
             // partition as one table key: the ranks of the occupied entries
             // are compact block ids, the next pass's key labels (no O(n) scan)
@@ -1148,6 +1214,7 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
             compact_flags(ctx, list, w.keep.get(), m, dst, &dctr->listed, s);
             read_words(ctx, dctr, sizeof(c), &c, s);
         } else if (!chunked && o.grouping != 1) {
+            wait_all_chunks();
             // ---- bucket strategy
             // 2^D buckets of 768..1536 expected keys (Poisson tail well inside
             // the 2048 slots unless keys repeat)
@@ -1216,6 +1283,7 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
                 read_words(ctx, dctr, sizeof(c), &c, s);
             }
             res.sorted += m;
+            check_streamed();
             if (fingerprint && c.collision) {
                 // verified collision: nothing was written to the labels
                 ++res.collisions;
@@ -1242,6 +1310,7 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
                 }
             }
         } else {
+            wait_all_chunks();
             // ---- radix-sort grouping: (key, state) pairs, LSD radix sort, runs
             if (!w.keys0.get()) {
                 w.keys0.alloc(n, s);
@@ -1333,6 +1402,7 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
             read_words(ctx, dctr, sizeof(c), &c, s);
         }
 
+        check_streamed();
         collisions_this_pass = 0;
         const uint32_t newB = B - A + c.runs;
         if (newB == B) break;  // fixed point: no block split (reference l.411)
@@ -1345,6 +1415,8 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
             if (dst == list_alt) std::swap(list_buf, list_alt);
         }
     }
+    wait_all_chunks();  // inputs that needed no pass are still validated
+    check_streamed();
     res.num_blocks = canonical_from_min_labels(ctx, w.lab.get(), n, block_out, w.scratch.get(), s);
     return res;
 }

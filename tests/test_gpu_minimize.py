@@ -279,3 +279,17 @@ def test_config4_size_1B_transitions_single_gpu(dk):
         comm.close()
     finally:
         dist.destroy_process_group()
+
+
+def test_streamed_host_input(dk, oracle):
+    """Host-buffer calls from 2^20 states stream delta in chunks and run pass 1
+    as they land: same partition and pass count, and an out-of-range target in
+    the last chunk is still rejected."""
+    t = oracle.gen_random(1_500_000, 3, 0.5, 21)
+    want = oracle.minimize("moore", t[0], t[1])
+    for f in (dk.sort_pr, dk.moore_minimize):
+        assert same(f(mkdfa(dk, t)), want), f
+    bad = t[0].copy()
+    bad[2][-1] = 1_500_000
+    with pytest.raises(ValueError, match="out of range"):
+        dk.sort_pr(dk.Dfa(bad, t[1], 0))
