@@ -288,6 +288,14 @@ dfakit_status dfakit_comm_init(dfakit_ctx* ctx, const uint8_t* id128, int world,
 void dfakit_comm_destroy(dfakit_comm* comm);
 dfakit_status dfakit_sort_pr_sharded(dfakit_ctx* ctx, dfakit_comm* comm, const dfakit_dfa* dfa, uint32_t* block_of,
                                      dfakit_report* report, uint64_t* exchanged, void* stream);
+/* In-process communicator: `world` ranks as threads of one process, each
+ * with its own context (on any devices, e.g. all on one GPU), collectives
+ * staged through host memory.  Runs the native driver's multi-rank path
+ * where NCCL cannot (it refuses two ranks on one device); for testing. */
+typedef struct dfakit_local_hub dfakit_local_hub;
+dfakit_status dfakit_local_hub_create(int world, dfakit_local_hub** out);
+void dfakit_local_hub_destroy(dfakit_local_hub* hub);
+dfakit_status dfakit_comm_init_local(dfakit_local_hub* hub, int rank, dfakit_comm** out);
 
 /* ---- calibration ---------------------------------------------------------------
  * Measured ceiling of the signature kernels' random block-label gathers:

@@ -24,6 +24,10 @@ struct dfakit_comm {
     dk::NcclComm* c;
 };
 
+struct dfakit_local_hub {
+    dk::LocalHub* h;
+};
+
 namespace {
 
 thread_local std::string g_last_error;
@@ -534,6 +538,26 @@ void dfakit_comm_destroy(dfakit_comm* comm) {
     if (!comm) return;
     dk::nccl_comm_destroy(comm->c);
     delete comm;
+}
+
+dfakit_status dfakit_local_hub_create(int world, dfakit_local_hub** out) {
+    return guard([&] {
+        if (!out) throw dk::Error(DFAKIT_E_INVALID, "null out");
+        *out = new dfakit_local_hub{dk::local_hub_create(world)};
+    });
+}
+
+void dfakit_local_hub_destroy(dfakit_local_hub* hub) {
+    if (!hub) return;
+    dk::local_hub_destroy(hub->h);
+    delete hub;
+}
+
+dfakit_status dfakit_comm_init_local(dfakit_local_hub* hub, int rank, dfakit_comm** out) {
+    return guard([&] {
+        if (!hub || !out) throw dk::Error(DFAKIT_E_INVALID, "null argument");
+        *out = new dfakit_comm{dk::local_comm_init(hub->h, rank)};
+    });
 }
 
 dfakit_status dfakit_sort_pr_sharded(dfakit_ctx* ctx, dfakit_comm* comm, const dfakit_dfa* dfa, uint32_t* block_of,

@@ -75,6 +75,12 @@ struct NcclComm;
 void nccl_unique_id(uint8_t out[128]);
 NcclComm* nccl_comm_init(Ctx* ctx, const uint8_t id[128], int world, int rank);
 void nccl_comm_destroy(NcclComm* c);
+// in-process hub: `world` ranks as threads sharing one device (testing the
+// driver's multi-rank path on a single GPU)
+struct LocalHub;
+LocalHub* local_hub_create(int world);
+void local_hub_destroy(LocalHub* h);
+NcclComm* local_comm_init(LocalHub* hub, int rank);
 RefineResult sort_pr_sharded_device(Ctx* ctx, NcclComm* comm, const DevDfa& d, uint32_t* block_out, cudaStream_t s,
                                     uint64_t* exchanged);
 

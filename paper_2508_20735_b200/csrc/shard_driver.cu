@@ -21,7 +21,9 @@
 
 #include <algorithm>
 #include <cstring>
+#include <condition_variable>
 #include <mutex>
+#include <vector>
 
 #include "prims.cuh"
 #include "refine.cuh"
@@ -82,7 +84,7 @@ void nccl_check(ncclResult_t r, const char* what) {
 uint64_t mix64_host(uint64_t z) { return mix64(z); }
 
 // one grouped send/recv round: element_bytes-sized elements, counts per peer
-void all_to_all_v(const NcclApi& api, ncclComm_t comm, int world, const void* send,
+void grouped_all_to_all_v(const NcclApi& api, ncclComm_t comm, int world, const void* send,
                   const std::vector<uint64_t>& scount, void* recv, const std::vector<uint64_t>& rcount,
                   size_t element_bytes, cudaStream_t s) {
     nccl_check(api.GroupStart(), "ncclGroupStart");
@@ -104,10 +106,122 @@ void all_to_all_v(const NcclApi& api, ncclComm_t comm, int world, const void* se
 
 }  // namespace
 
+// Collectives of the pass loop on stream s.  NCCL in production; the local
+// hub runs several ranks as threads of one process sharing a device (each
+// with its own context), staging through host memory -- the way the
+// driver's multi-rank path is tested on a single GPU.
 struct NcclComm {
-    ncclComm_t comm = nullptr;
+    virtual ~NcclComm() = default;
     int world = 1, rank = 0;
+    virtual void allreduce_u32(uint32_t* buf, size_t count, bool use_min, cudaStream_t s) = 0;
+    // full holds world slices of `bytes`; this rank's slice is at rank * bytes
+    virtual void allgather(void* full, size_t bytes, cudaStream_t s) = 0;
+    virtual void all_to_all_v(const void* send, const std::vector<uint64_t>& scount, void* recv,
+                              const std::vector<uint64_t>& rcount, size_t element_bytes, cudaStream_t s) = 0;
 };
+
+namespace {
+
+struct NcclImpl : NcclComm {
+    ncclComm_t comm = nullptr;
+    ~NcclImpl() override {
+        if (comm) nccl().CommDestroy(comm);
+    }
+    void allreduce_u32(uint32_t* buf, size_t count, bool use_min, cudaStream_t s) override {
+        nccl_check(nccl().AllReduce(buf, buf, count, ncclUint32, use_min ? ncclMin : ncclSum, comm, s), "allreduce");
+    }
+    void allgather(void* full, size_t bytes, cudaStream_t s) override {
+        nccl_check(nccl().AllGather(static_cast<char*>(full) + (uint64_t)rank * bytes, full, bytes, ncclUint8, comm, s),
+                   "allgather");
+    }
+    void all_to_all_v(const void* send, const std::vector<uint64_t>& scount, void* recv,
+                      const std::vector<uint64_t>& rcount, size_t element_bytes, cudaStream_t s) override {
+        grouped_all_to_all_v(nccl(), comm, world, send, scount, recv, rcount, element_bytes, s);
+    }
+};
+
+}  // namespace
+
+struct LocalHub {
+    explicit LocalHub(int w) : world(w), host(w), counts(w) {}
+    int world;
+    std::mutex mu;
+    std::condition_variable cv;
+    int arrived = 0;
+    uint64_t generation = 0;
+    std::vector<std::vector<uint8_t>> host;
+    std::vector<std::vector<uint64_t>> counts;
+    void barrier() {
+        std::unique_lock<std::mutex> lk(mu);
+        const uint64_t gen = generation;
+        if (++arrived == world) {
+            arrived = 0;
+            ++generation;
+            cv.notify_all();
+        } else {
+            cv.wait(lk, [&] { return generation != gen; });
+        }
+    }
+};
+
+namespace {
+
+struct LocalImpl : NcclComm {
+    LocalHub* hub = nullptr;
+    void publish(const void* dev, size_t bytes, cudaStream_t s) {
+        auto& h = hub->host[rank];
+        h.resize(bytes);
+        if (bytes) DK_CUDA(cudaMemcpyAsync(h.data(), dev, bytes, cudaMemcpyDeviceToHost, s));
+        DK_CUDA(cudaStreamSynchronize(s));
+    }
+    void allreduce_u32(uint32_t* buf, size_t count, bool use_min, cudaStream_t s) override {
+        publish(buf, count * 4, s);
+        hub->barrier();
+        std::vector<uint32_t> acc(count);
+        for (int r = 0; r < world; ++r) {
+            const uint32_t* v = reinterpret_cast<const uint32_t*>(hub->host[r].data());
+            for (size_t i = 0; i < count; ++i)
+                acc[i] = r == 0 ? v[i] : (use_min ? std::min(acc[i], v[i]) : acc[i] + v[i]);
+        }
+        if (count) DK_CUDA(cudaMemcpyAsync(buf, acc.data(), count * 4, cudaMemcpyHostToDevice, s));
+        DK_CUDA(cudaStreamSynchronize(s));
+        hub->barrier();
+    }
+    void allgather(void* full, size_t bytes, cudaStream_t s) override {
+        publish(static_cast<char*>(full) + (uint64_t)rank * bytes, bytes, s);
+        hub->barrier();
+        for (int r = 0; r < world; ++r)
+            if (bytes)
+                DK_CUDA(cudaMemcpyAsync(static_cast<char*>(full) + (uint64_t)r * bytes, hub->host[r].data(), bytes,
+                                        cudaMemcpyHostToDevice, s));
+        DK_CUDA(cudaStreamSynchronize(s));
+        hub->barrier();
+    }
+    void all_to_all_v(const void* send, const std::vector<uint64_t>& scount, void* recv,
+                      const std::vector<uint64_t>& rcount, size_t element_bytes, cudaStream_t s) override {
+        uint64_t total = 0;
+        for (uint64_t c : scount) total += c;
+        publish(send, total * element_bytes, s);
+        hub->counts[rank] = scount;
+        hub->barrier();
+        uint64_t ro = 0;
+        for (int r = 0; r < world; ++r) {
+            uint64_t off = 0;
+            for (int j = 0; j < rank; ++j) off += hub->counts[r][j];
+            const uint64_t c = hub->counts[r][rank];
+            if (c != rcount[r]) throw Error(DFAKIT_E_INVALID, "local hub: receive count mismatch");
+            if (c)
+                DK_CUDA(cudaMemcpyAsync(static_cast<char*>(recv) + ro * element_bytes,
+                                        hub->host[r].data() + off * element_bytes, c * element_bytes,
+                                        cudaMemcpyHostToDevice, s));
+            ro += c;
+        }
+        DK_CUDA(cudaStreamSynchronize(s));
+        hub->barrier();
+    }
+};
+
+}  // namespace
 
 void nccl_unique_id(uint8_t out[128]) {
     ncclUniqueId id;
@@ -121,26 +235,38 @@ NcclComm* nccl_comm_init(Ctx* ctx, const uint8_t id[128], int world, int rank) {
     DK_CUDA(cudaSetDevice(ctx->device));
     ncclUniqueId uid;
     std::memcpy(&uid, id, sizeof(uid));
-    NcclComm* c = new NcclComm();
+    NcclImpl* c = new NcclImpl();
     c->world = world;
     c->rank = rank;
     const ncclResult_t r = nccl().CommInitRank(&c->comm, world, uid, rank);
     if (r != ncclSuccess) {
+        c->comm = nullptr;
         delete c;
         nccl_check(r, "ncclCommInitRank");
     }
     return c;
 }
 
-void nccl_comm_destroy(NcclComm* c) {
-    if (!c) return;
-    if (c->comm) nccl().CommDestroy(c->comm);
-    delete c;
+LocalHub* local_hub_create(int world) {
+    if (world < 1 || world > 64) throw Error(DFAKIT_E_INVALID, "local hub: world size out of range");
+    return new LocalHub(world);
 }
+
+void local_hub_destroy(LocalHub* h) { delete h; }
+
+NcclComm* local_comm_init(LocalHub* hub, int rank) {
+    if (!hub || rank < 0 || rank >= hub->world) throw Error(DFAKIT_E_INVALID, "local comm: bad rank");
+    LocalImpl* c = new LocalImpl();
+    c->hub = hub;
+    c->world = hub->world;
+    c->rank = rank;
+    return c;
+}
+
+void nccl_comm_destroy(NcclComm* c) { delete c; }
 
 RefineResult sort_pr_sharded_device(Ctx* ctx, NcclComm* cm, const DevDfa& d, uint32_t* block_out, cudaStream_t s,
                                     uint64_t* exchanged) {
-    const NcclApi& api = nccl();
     RefineResult res;
     const uint32_t n = d.n, k = d.k;
     const int world = cm->world, rank = cm->rank;
@@ -220,8 +346,8 @@ RefineResult sort_pr_sharded_device(Ctx* ctx, NcclComm* cm, const DevDfa& d, uin
             }
             if (keys32.n < std::max(1u, m)) keys32.alloc(std::max(1u, hi - lo), s);
             shard_table_signature(ctx, d, keylab, plan, lst, lo, m, keys32.get(), tmin.get(), tcnt.get(), s);
-            nccl_check(api.AllReduce(tmin.get(), tmin.get(), tsize, ncclUint32, ncclMin, cm->comm, s), "allreduce");
-            nccl_check(api.AllReduce(tcnt.get(), tcnt.get(), tsize, ncclUint32, ncclSum, cm->comm, s), "allreduce");
+            cm->allreduce_u32(tmin.get(), tsize, true, s);
+            cm->allreduce_u32(tcnt.get(), tsize, false, s);
             if (hi > lo) DK_CUDA(cudaMemsetAsync(act.get() + lo, 0, hi - lo, s));
             if (m_total == n) {
                 // every block of the next partition is one table key
@@ -235,7 +361,7 @@ RefineResult sort_pr_sharded_device(Ctx* ctx, NcclComm* cm, const DevDfa& d, uin
             }
             shard_table_apply(ctx, plan, lst, lo, keys32.get(), m, tmin.get(), tcnt.get(), lab.get(), act.get(),
                               next_kl, dctr.get(), s);
-            nccl_check(api.AllReduce(dctr.get(), dctr.get(), 4, ncclUint32, ncclSum, cm->comm, s), "allreduce");
+            cm->allreduce_u32(dctr.get(), 4, false, s);
             read_u32(dctr.get(), 4, ctr);
         } else {
             if (send.n < std::max(1u, m)) send.alloc(std::max(1u, hi - lo), s);
@@ -246,16 +372,16 @@ RefineResult sort_pr_sharded_device(Ctx* ctx, NcclComm* cm, const DevDfa& d, uin
             for (int r = 0; r < world; ++r) scount[r] = sc32[r];
             // counts: one word to every peer
             DBuf<uint32_t> rc(world, s);
-            all_to_all_v(api, cm->comm, world, counts.get(), ones, rc.get(), ones, sizeof(uint32_t), s);
+            cm->all_to_all_v(counts.get(), ones, rc.get(), ones, sizeof(uint32_t), s);
             read_u32(rc.get(), world, rc32.data());
             uint64_t rtotal = 0;
             for (int r = 0; r < world; ++r) rtotal += (rcount[r] = rc32[r]);
             if (recv.n < std::max<uint64_t>(1, rtotal)) recv.alloc(std::max<uint64_t>(1, rtotal) * 5 / 4, s);
-            all_to_all_v(api, cm->comm, world, send.get(), scount, recv.get(), rcount, sizeof(uint4), s);
+            cm->all_to_all_v(send.get(), scount, recv.get(), rcount, sizeof(uint4), s);
             sent += m;
             if (results.n < std::max<uint64_t>(1, rtotal)) results.alloc(std::max<uint64_t>(1, rtotal) * 5 / 4, s);
             shard_group(ctx, d, lab.get(), plan, recv.get(), rtotal, results.get(), dctr.get(), s);
-            nccl_check(api.AllReduce(dctr.get(), dctr.get(), 4, ncclUint32, ncclSum, cm->comm, s), "allreduce");
+            cm->allreduce_u32(dctr.get(), 4, false, s);
             read_u32(dctr.get(), 4, ctr);
             if (ctr[3]) {
                 // verified fingerprint collision on some owner: nothing applied
@@ -267,7 +393,7 @@ RefineResult sort_pr_sharded_device(Ctx* ctx, NcclComm* cm, const DevDfa& d, uin
             }
             if (B - A + ctr[0] == B) break;  // fixed point (reference l.411)
             if (back.n < std::max(1u, m)) back.alloc(std::max(1u, hi - lo), s);
-            all_to_all_v(api, cm->comm, world, results.get(), rcount, back.get(), scount, sizeof(uint32_t), s);
+            cm->all_to_all_v(results.get(), rcount, back.get(), scount, sizeof(uint32_t), s);
             if (hi > lo) DK_CUDA(cudaMemsetAsync(act.get() + lo, 0, hi - lo, s));
             shard_apply(ctx, send.get(), back.get(), m, lab.get(), act.get(), s);
         }
@@ -278,14 +404,10 @@ RefineResult sort_pr_sharded_device(Ctx* ctx, NcclComm* cm, const DevDfa& d, uin
         B = newB;
         A = ctr[1];
         m_total = ctr[2];
-        nccl_check(api.AllGather(lab.get() + (uint64_t)rank * shard, lab.get(), shard * sizeof(uint32_t), ncclUint8,
-                                 cm->comm, s),
-                   "allgather");
+        cm->allgather(lab.get(), (size_t)shard * sizeof(uint32_t), s);
         if (next_kl) {
             const size_t es = plan.key_bits <= 16 ? 2 : 4;
-            nccl_check(api.AllGather(static_cast<char*>(next_kl) + (uint64_t)rank * shard * es, next_kl, shard * es,
-                                     ncclUint8, cm->comm, s),
-                       "allgather");
+            cm->allgather(next_kl, (size_t)shard * es, s);
             carried = next_kl;
             carried_bytes = (uint32_t)es;
         }
