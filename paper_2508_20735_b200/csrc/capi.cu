@@ -665,7 +665,7 @@ dfakit_status dfakit_shard_group(dfakit_ctx* ctx, const dfakit_dfa* dfa, const u
     return on_device(ctx, stream, [&](dk::Ctx* c, cudaStream_t s) {
         check_view(dfa, "shard_group");
         if (dfa->num_states > 0x7fffffffu) throw dk::Error(DFAKIT_E_INVALID, "shard_group: more than 2^31 states");
-        dk::shard_group(c, device_view(dfa), lab, plan_in(plan), static_cast<const uint4*>(recv_entries), count,
+        dk::shard_group(c, device_view(dfa), lab, 4, plan_in(plan), static_cast<const uint4*>(recv_entries), count,
                         results, counters, s);
     });
 }

@@ -63,8 +63,10 @@ void shard_table_apply(Ctx* ctx, const PassPlan& plan, const uint32_t* list, uin
 void shard_sig_partition(Ctx* ctx, const DevDfa& d, const void* keylab, const PassPlan& plan, uint64_t salt,
                          const uint32_t* list, uint32_t list_base, uint64_t m, uint32_t world, uint4* send,
                          uint32_t* send_counts, cudaStream_t s);
-void shard_group(Ctx* ctx, const DevDfa& d, const uint32_t* lab, const PassPlan& plan, const uint4* recv,
-                 uint64_t count, uint32_t* results, uint32_t* counters, cudaStream_t s);
+// verify_lab: any injective labelling of the current blocks (verify_bytes
+// 4 / 2 / 1 / kKeylabBits) -- the min-state labels, or the pass's key labels
+void shard_group(Ctx* ctx, const DevDfa& d, const void* verify_lab, uint32_t verify_bytes, const PassPlan& plan,
+                 const uint4* recv, uint64_t count, uint32_t* results, uint32_t* counters, cudaStream_t s);
 void shard_apply(Ctx* ctx, const uint4* send, const uint32_t* results, uint64_t count, uint32_t* lab, uint8_t* act,
                  cudaStream_t s);
 void shard_compact(Ctx* ctx, const uint8_t* act, uint32_t lo, uint32_t hi, uint32_t* list, uint32_t* count_dev,

@@ -339,8 +339,11 @@ constexpr unsigned long long kEmptyKey = ~0ull;         // a real ~0 key takes t
 constexpr uint32_t kBucketShift = 20;                   // bucket = hkey bits [20, 20 + D): slots use the low
                                                         // bits, the sharded engine's owner rank the top 32
 
+// q and r have the same (block, signature) tuple under any injective block
+// labelling `lab` (min-state labels, or the pass's key labels)
+template <typename LR>
 __device__ __forceinline__ bool same_tuple(uint32_t q, uint32_t r, const uint32_t* __restrict__ delta, uint32_t n,
-                                           uint32_t k, const uint32_t* __restrict__ lab) {
+                                           uint32_t k, LR lab) {
     if (lab[q] != lab[r]) return false;
     for (uint32_t a = 0; a < k; ++a) {
         const uint32_t* row = delta + (uint64_t)a * n;
@@ -445,9 +448,10 @@ __device__ __forceinline__ void emit(const GroupOut& o, uint64_t slot, uint32_t 
 
 // One CTA per bucket (persistent over buckets).  Buckets whose count
 // exceeds the capacity are left to the ghash fallback.
+template <typename LR>
 __global__ void __launch_bounds__(kGrpThreads) bucket_group_kernel(
     const uint32_t* __restrict__ bcnt, uint32_t nb, const uint4* __restrict__ bent, int fingerprint,
-    const uint32_t* __restrict__ delta, uint32_t n, uint32_t k, const uint32_t* __restrict__ lab_in, GroupOut o,
+    const uint32_t* __restrict__ delta, uint32_t n, uint32_t k, LR lab_in, GroupOut o,
     IterCounters* __restrict__ ctr) {
     extern __shared__ __align__(16) unsigned char grp_raw[];
     GroupSmem& sm = *reinterpret_cast<GroupSmem*>(grp_raw);
@@ -573,10 +577,11 @@ __global__ void ghash_multi_kernel(const uint32_t* __restrict__ bcnt, uint32_t n
     }
 }
 
+template <typename LR>
 __global__ void __launch_bounds__(kThreads) ghash_out_kernel(
     const uint32_t* __restrict__ bcnt, uint32_t nb, uint32_t ovf, const uint4* __restrict__ bent,
     const uint32_t* __restrict__ grep, const uint32_t* __restrict__ gslot, const uint8_t* __restrict__ gmul,
-    int fingerprint, const uint32_t* __restrict__ delta, uint32_t n, uint32_t k, const uint32_t* __restrict__ lab_in,
+    int fingerprint, const uint32_t* __restrict__ delta, uint32_t n, uint32_t k, LR lab_in,
     GroupOut o, IterCounters* __restrict__ ctr) {
     const uint64_t total = (uint64_t)nb * kGrpCap + ovf;
     uint32_t heads = 0, ablk = 0, surv = 0;
@@ -635,7 +640,7 @@ __global__ void verify_runs_kernel(const uint64_t* __restrict__ keys, const uint
     for (uint64_t i = 1 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
          i += (uint64_t)gridDim.x * blockDim.x) {
         if (keys[i] != keys[i - 1]) continue;
-        if (!same_tuple(vals[i], vals[i - 1], delta, n, k, lab)) atomicOr(&ctr->collision, 1u);
+        if (!same_tuple(vals[i], vals[i - 1], delta, n, k, ArrLab<uint32_t>{lab})) atomicOr(&ctr->collision, 1u);
     }
 }
 
@@ -838,7 +843,7 @@ __global__ void __launch_bounds__(kThreads) small_persistent_kernel(SmallArgs A)
             heads += head;
             ablk += head && multi;
             surv += multi;
-            if (!A.field_bits && !head && !same_tuple(q, r, A.delta, A.n, A.k, A.lab)) clash = true;
+            if (!A.field_bits && !head && !same_tuple(q, r, A.delta, A.n, A.k, ArrLab<uint32_t>{A.lab})) clash = true;
         }
         if (__syncthreads_or(clash) && threadIdx.x == 0) atomicOr(&c->collision, 1u);
         flush_counters<kThreads>(heads, ablk, surv, &c->runs, &c->ablk, &c->surv);
@@ -1013,7 +1018,7 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
     w.scratch.alloc((uint64_t)n + 1, s);
     w.keep.alloc(n, s);
     w.ctr.alloc(1, s);
-    DK_CUDA(cudaFuncSetAttribute(bucket_group_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    DK_CUDA(cudaFuncSetAttribute(bucket_group_kernel<ArrLab<uint32_t>>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)sizeof(GroupSmem)));
     const int smem_table = (int)(2u << kSmemTableBits) * 4;
     DK_CUDA(cudaFuncSetAttribute(sig_table_kernel<BitLab>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_table));
@@ -1257,7 +1262,7 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
             // algorithmic HBM bytes: (hkey, state) in, label + survivor flag out
             DK_LAUNCH_B(ctx, (double)m * (16.0 + 4.0 + 1.0 + (direct ? 0.0 : 4.0)), bucket_group_kernel, gg,
                         kGrpThreads, sizeof(GroupSmem), s, w.bcnt.get(), nb, w.bent.get(), fingerprint ? 1 : 0,
-                        d.delta, n, k, w.lab.get(), go, dctr);
+                        d.delta, n, k, ArrLab<uint32_t>{w.lab.get()}, go, dctr);
             read_words(ctx, dctr, sizeof(c), &c, s);
             if (c.overflow) {
                 // heavy duplication: overflowed buckets through a global table
@@ -1278,8 +1283,8 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
                 DK_LAUNCH(ctx, ghash_multi_kernel, eg, kThreads, 0, s, w.bcnt.get(), nb, c.overflow, w.bent.get(),
                           w.grep.get(), w.gslot.get(), w.gmul.get());
                 DK_LAUNCH(ctx, ghash_out_kernel, eg, kThreads, 0, s, w.bcnt.get(), nb, c.overflow, w.bent.get(),
-                          w.grep.get(), w.gslot.get(), w.gmul.get(), fingerprint ? 1 : 0, d.delta, n, k, w.lab.get(),
-                          go, dctr);
+                          w.grep.get(), w.gslot.get(), w.gmul.get(), fingerprint ? 1 : 0, d.delta, n, k,
+                          ArrLab<uint32_t>{w.lab.get()}, go, dctr);
                 read_words(ctx, dctr, sizeof(c), &c, s);
             }
             res.sorted += m;
@@ -1649,8 +1654,8 @@ void shard_sig_partition(Ctx* ctx, const DevDfa& d, const void* keylab, const Pa
                 send);
 }
 
-void shard_group(Ctx* ctx, const DevDfa& d, const uint32_t* lab, const PassPlan& plan, const uint4* recv,
-                 uint64_t count, uint32_t* results, uint32_t* counters, cudaStream_t s) {
+void shard_group(Ctx* ctx, const DevDfa& d, const void* verify_lab, uint32_t verify_bytes, const PassPlan& plan,
+                 const uint4* recv, uint64_t count, uint32_t* results, uint32_t* counters, cudaStream_t s) {
     IterCounters* dctr = reinterpret_cast<IterCounters*>(ctx->dmailbox) + 4;
     DK_CUDA(cudaMemsetAsync(dctr, 0, sizeof(IterCounters), s));
     if (count) {
@@ -1665,11 +1670,15 @@ void shard_group(Ctx* ctx, const DevDfa& d, const uint32_t* lab, const PassPlan&
                     bcnt.get(), bent.get(), dctr);
         const int fp = plan.strategy == kPlanFingerprint ? 1 : 0;
         GroupOut go{0, 0, nullptr, nullptr, nullptr, nullptr, results};
-        DK_CUDA(cudaFuncSetAttribute(bucket_group_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)sizeof(GroupSmem)));
         const unsigned gg = (unsigned)std::min<uint64_t>(nb, (uint64_t)ctx->num_sms * 4);
-        DK_LAUNCH_B(ctx, 20.0 * count, bucket_group_kernel, gg, kGrpThreads, sizeof(GroupSmem), s, bcnt.get(), nb,
-                    bent.get(), fp, d.delta, d.n, d.k, lab, go, dctr);
+        const KeyLab vl{verify_lab, (int)verify_bytes};
+        with_lab_type(vl, [&](auto lab) {
+            using LR = decltype(lab);
+            DK_CUDA(cudaFuncSetAttribute(bucket_group_kernel<LR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)sizeof(GroupSmem)));
+            DK_LAUNCH_B(ctx, 20.0 * count, bucket_group_kernel, gg, kGrpThreads, sizeof(GroupSmem), s, bcnt.get(),
+                        nb, bent.get(), fp, d.delta, d.n, d.k, lab, go, dctr);
+        });
         IterCounters c{};
         read_words(ctx, dctr, sizeof(c), &c, s);
         if (c.overflow) {
@@ -1686,8 +1695,10 @@ void shard_group(Ctx* ctx, const DevDfa& d, const uint32_t* lab, const PassPlan&
                       gkey.get(), grep.get(), gslot.get());
             DK_LAUNCH(ctx, ghash_multi_kernel, eg, kThreads, 0, s, bcnt.get(), nb, c.overflow, bent.get(), grep.get(),
                       gslot.get(), gmul.get());
-            DK_LAUNCH(ctx, ghash_out_kernel, eg, kThreads, 0, s, bcnt.get(), nb, c.overflow, bent.get(), grep.get(),
-                      gslot.get(), gmul.get(), fp, d.delta, d.n, d.k, lab, go, dctr);
+            with_lab_type(vl, [&](auto lab) {
+                DK_LAUNCH(ctx, ghash_out_kernel, eg, kThreads, 0, s, bcnt.get(), nb, c.overflow, bent.get(),
+                          grep.get(), gslot.get(), gmul.get(), fp, d.delta, d.n, d.k, lab, go, dctr);
+            });
         }
     }
     DK_CUDA(cudaMemcpyAsync(counters, dctr, 4 * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));

@@ -298,6 +298,7 @@ RefineResult sort_pr_sharded_device(Ctx* ctx, NcclComm* cm, const DevDfa& d, uin
     uint64_t salt = 0x5EED5EED5EEDull;
     uint32_t strikes = 0;
     const void* carried = nullptr;  // key labels of the current partition (ranks of a full table pass)
+    bool lab_stale = false;         // other ranks' slices of `lab` not yet exchanged
     uint32_t carried_bytes = 0;
     uint64_t sent = 0;
     while (m_total > 0) {
@@ -310,6 +311,12 @@ RefineResult sort_pr_sharded_device(Ctx* ctx, NcclComm* cm, const DevDfa& d, uin
             plan.keylab_bytes = 0;
         }
         const uint32_t* lst = m == hi - lo ? nullptr : list.get();
+        // the other ranks' min-state labels are needed unless the pass
+        // gathers carried key labels
+        if (lab_stale && !(plan.keylab_bytes && carried)) {
+            cm->allgather(lab.get(), (size_t)shard * sizeof(uint32_t), s);
+            lab_stale = false;
+        }
         const void* keylab = lab.get();
         if (plan.keylab_bytes) {
             if (carried) {
@@ -380,7 +387,13 @@ RefineResult sort_pr_sharded_device(Ctx* ctx, NcclComm* cm, const DevDfa& d, uin
             cm->all_to_all_v(send.get(), scount, recv.get(), rcount, sizeof(uint4), s);
             sent += m;
             if (results.n < std::max<uint64_t>(1, rtotal)) results.alloc(std::max<uint64_t>(1, rtotal) * 5 / 4, s);
-            shard_group(ctx, d, lab.get(), plan, recv.get(), rtotal, results.get(), dctr.get(), s);
+            // verification compares any injective labelling: the key labels when
+            // the min-state labels of other ranks are stale
+            if (lab_stale)
+                shard_group(ctx, d, keylab, plan.keylab_bytes ? plan.keylab_bytes : 4, plan, recv.get(), rtotal,
+                            results.get(), dctr.get(), s);
+            else
+                shard_group(ctx, d, lab.get(), 4, plan, recv.get(), rtotal, results.get(), dctr.get(), s);
             cm->allreduce_u32(dctr.get(), 4, false, s);
             read_u32(dctr.get(), 4, ctr);
             if (ctr[3]) {
@@ -404,15 +417,22 @@ RefineResult sort_pr_sharded_device(Ctx* ctx, NcclComm* cm, const DevDfa& d, uin
         B = newB;
         A = ctr[1];
         m_total = ctr[2];
-        cm->allgather(lab.get(), (size_t)shard * sizeof(uint32_t), s);
+        // label exchange: the carried key labels when the next pass gathers
+        // them (the min-state labels follow only when a pass or the final
+        // numbering needs them), else the min-state labels
         if (next_kl) {
             const size_t es = plan.key_bits <= 16 ? 2 : 4;
             cm->allgather(next_kl, (size_t)shard * es, s);
             carried = next_kl;
             carried_bytes = (uint32_t)es;
+            lab_stale = true;
+        } else {
+            cm->allgather(lab.get(), (size_t)shard * sizeof(uint32_t), s);
+            lab_stale = false;
         }
         compact();
     }
+    if (lab_stale) cm->allgather(lab.get(), (size_t)shard * sizeof(uint32_t), s);
     res.num_blocks = canonical_from_min_labels(ctx, lab.get(), n, block_out, scratch.get(), s);
     if (exchanged) *exchanged = sent;
     return res;
