@@ -264,6 +264,8 @@ struct BfsArgs {
     Slot* table;
     uint64_t cap;  // slots (power of two)
     uint32_t* item_slot;
+    uint8_t* item_win;  // winner flags of the counting phase, reused by the emit phase
+    unsigned long long* item_key;  // each item's pair key (coalesced; spares a random table read)
     uint64_t item_cap;
     uint32_t* cta_cnt;
     const uint32_t *da, *db, *to_b;
@@ -324,6 +326,7 @@ __global__ void __launch_bounds__(kThreads) bfs_persistent_kernel(BfsArgs A) {
             if (valid) {
                 const unsigned long long old = atomicMin(&A.table[sl].disc, disc);
                 A.item_slot[t] = (old >= ((unsigned long long)(wb + 1) << 32)) ? sl : kNone;
+                A.item_key[t] = key;
             }
         }
         grid.sync();
@@ -331,7 +334,11 @@ __global__ void __launch_bounds__(kThreads) bfs_persistent_kernel(BfsArgs A) {
         const uint64_t chunk = (items + gridDim.x - 1) / gridDim.x;
         const uint64_t c0 = min(items, blockIdx.x * chunk), c1 = min(items, c0 + chunk);
         uint32_t c = 0;
-        for (uint64_t t = c0 + threadIdx.x; t < c1; t += blockDim.x) c += item_wins(A.table, A.item_slot, wb, t, A.k);
+        for (uint64_t t = c0 + threadIdx.x; t < c1; t += blockDim.x) {
+            const bool w = item_wins(A.table, A.item_slot, wb, t, A.k);
+            A.item_win[t] = w;
+            c += w;
+        }
         c = __reduce_add_sync(0xffffffffu, c);
         if ((threadIdx.x & 31u) == 0) red[threadIdx.x >> 5] = c;
         __syncthreads();
@@ -367,13 +374,13 @@ __global__ void __launch_bounds__(kThreads) bfs_persistent_kernel(BfsArgs A) {
         uint32_t run = pre;
         for (uint64_t base = c0; base < c1; base += blockDim.x) {
             const uint64_t t = base + threadIdx.x;
-            const bool win = t < c1 && item_wins(A.table, A.item_slot, wb, t, A.k);
+            const bool win = t < c1 && A.item_win[t];
             uint32_t tot;
             const uint32_t e = block_exclusive_scan<kThreads>(win ? 1u : 0u, &tot, ws);
             if (win) {
                 const uint32_t posn = run + e;
                 const uint64_t r = we + posn;
-                const unsigned long long key = __ldcg(&A.table[A.item_slot[t]].key);
+                const unsigned long long key = A.item_key[t];
                 A.rec.key[r] = key;
                 A.rec.parent[r] = (uint32_t)(wb + t / A.k);
                 A.rec.letter[r] = (uint32_t)(t % A.k);
@@ -566,23 +573,35 @@ ProductOut explore_product_device(Ctx* ctx, const DevDfa& a, const DevDfa& b, in
     hs.fail[0] = hs.fail[1] = hs.fail[2] = kNone;
     DK_CUDA(cudaMemcpyAsync(dst.get(), &hs, sizeof(hs), cudaMemcpyHostToDevice, s));
     uint64_t wb = 0, we = 1;
+    DBuf<uint8_t> item_win;
+    DBuf<unsigned long long> item_key;
     for (;;) {
-        // room for the next level: table at load <= 1/2, records, items; grown
-        // geometrically so the kernel returns here O(log) times
+        // room for the next level: table at load <= 1/2; the record store and
+        // the item buffers are sized with the table (cap / 2 each), so the
+        // kernel comes back only when the table must grow (4x from 2^20)
         const uint64_t items = (we - wb) * k;
         const uint64_t need = next_pow2(2 * (we + items) + 64);
         if (need > cap) {
-            // start at 2^20 slots (16 MB) and grow 8x: the early, tiny levels
-            // cost no relaunch, large explorations only a few
-            const uint64_t nc = std::max<uint64_t>(need, std::max<uint64_t>(1ull << 20, cap * 8));
+            // first allocation sized for 2 max(nA, nB) pairs (the usual size of
+            // an equivalence product; bounded by the visited budget), so most
+            // explorations run in one launch without re-insertion
+            const uint64_t guess = next_pow2(2 * std::min<uint64_t>(max_visited, 2ull * std::max(a.n, b.n)) + 64);
+            const uint64_t nc = cap ? std::max<uint64_t>(need, cap * 4)
+                                    : std::max<uint64_t>(need, std::max<uint64_t>(1ull << 20, guess));
             table.alloc(nc, s);
             cap = nc;
             DK_CUDA(cudaMemsetAsync(table.get(), 0xff, cap * sizeof(Slot), s));
             DK_LAUNCH(ctx, reinsert_kernel, grid_for(we), kThreads, 0, s, rs.key.get(), we, table.get(), cap - 1);
         }
-        rs.ensure(std::max<uint64_t>(we + items, (we + items) * 2), we, s);
-        if (std::max<uint64_t>(items, 1) > item_slot.n) item_slot.alloc(std::max<uint64_t>(items, 1) * 4, s);
-        BfsArgs A{rs.view(), rs.cap, table.get(), cap, item_slot.get(), item_slot.n, cta_cnt.get(), a.delta, b.delta,
+        rs.ensure(std::max<uint64_t>(cap / 2, we + items), we, s);
+        const uint64_t icap = std::max<uint64_t>(cap / 2, items);
+        if (icap > item_slot.n) {
+            item_slot.alloc(icap, s);
+            item_win.alloc(icap, s);
+            item_key.alloc(icap, s);
+        }
+        BfsArgs A{rs.view(), rs.cap, table.get(), cap, item_slot.get(), item_win.get(), item_key.get(), item_slot.n,
+                  cta_cnt.get(), a.delta, b.delta,
                   to_b.get(), a.n, b.n, k, a.acc, b.acc, mode, max_visited, dst.get()};
         void* args[] = {(void*)&A};
         prof_begin_launch(ctx, s);
