@@ -137,10 +137,14 @@ def ncu_traffic(kernel: str):
     try:
         with open(path) as f:
             j = json.load(f)
-        k = j["kernels"][kernel]
-        return {"dram_bytes_per_launch": k["dram_bytes_per_launch"], "source": f"profiles/ncu_summary.json ({j['tag']})"}
+        def norm(s):
+            s = s.split("(")[0].split("<")[0].strip()
+            return s[5:] if s.startswith("void ") else s
+        ks = {norm(name): v for name, v in j["kernels"].items()}
+        k = ks[norm(kernel)]
+        return k["dram_bytes_per_launch"], f"profiles/ncu_summary.json ({j['tag']}, {k['workload']} workload)"
     except Exception:
-        return None
+        return None, None
 
 
 # --------------------------------------------------------------------------
@@ -262,8 +266,9 @@ def roofline_of(kernels, steps, gather_peak, n):
                                  "every SM busy, measured in this run",
                   "all_gather_kernels": [{"name": x["name"], "gathers_per_s": x["units"] / (x["ms"] / 1000.0),
                                           "frac": x["units"] / (x["ms"] / 1000.0) / gather_peak} for x in g]}
+    traffic, traffic_src = ncu_traffic(top["name"])
     return {"bound": "hbm", "kernel": top["name"], "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak, "traffic": ncu_traffic(top["name"]),
+            "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
             "algorithmic_bytes_per_launch": top["bytes"] / max(top["launches"], 1),
             "avg_launch_ms": top["ms"] / max(top["launches"], 1), "share_of_step": top["ms"] / prof_ms,
             "peak_source": peak_src,

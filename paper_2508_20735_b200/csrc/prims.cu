@@ -110,8 +110,13 @@ __global__ void fill_kernel(uint32_t* p, uint64_t n, uint32_t v) {
 }
 
 __global__ void iota_kernel(uint32_t* p, uint64_t n) {
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-        p[i] = (uint32_t)i;
+    const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t nv = ((uintptr_t)p & 15u) == 0 ? n / 4 : 0;  // four per 16-byte store
+    for (uint64_t v = tid; v < nv; v += stride) {
+        const uint32_t i = (uint32_t)(4 * v);
+        __stcs(reinterpret_cast<uint4*>(p) + v, make_uint4(i, i + 1, i + 2, i + 3));
+    }
+    for (uint64_t i = 4 * nv + tid; i < n; i += stride) p[i] = (uint32_t)i;
 }
 
 void fill_u32(Ctx* ctx, uint32_t* p, uint64_t n, uint32_t value, cudaStream_t s) {
@@ -142,7 +147,9 @@ __device__ __forceinline__ uint32_t elem_flag(const uint32_t* __restrict__ lab, 
 template <bool HEADS>
 __global__ void __launch_bounds__(kCpThreads) tile_count_kernel(const uint32_t* __restrict__ lab,
                                                                 const uint8_t* __restrict__ flag, uint64_t n,
-                                                                uint32_t* __restrict__ sums) {
+                                                                uint32_t* __restrict__ sums,
+                                                                const uint32_t* __restrict__ skip) {
+    if (skip && *skip == n) return;
     __shared__ uint32_t ws[kCpThreads / 32];
     const uint64_t base = (uint64_t)blockIdx.x * kCpTile;
     uint32_t c = 0;
@@ -164,7 +171,9 @@ __global__ void __launch_bounds__(kCpThreads) tile_count_kernel(const uint32_t* 
 
 // exclusive scan of `tiles` counts in place by one CTA; total -> *total
 __global__ void __launch_bounds__(1024) scan_counts_kernel(uint32_t* __restrict__ sums, uint32_t tiles,
-                                                           uint32_t* __restrict__ total) {
+                                                           uint32_t* __restrict__ total,
+                                                           const uint32_t* __restrict__ skip, uint64_t n) {
+    if (skip && *skip == n) return;
     __shared__ uint32_t ws[32];
     uint32_t carry = 0;
     for (uint32_t b = 0; b < tiles; b += 1024) {
@@ -195,7 +204,9 @@ __global__ void __launch_bounds__(kCpThreads) tile_apply_kernel(const uint32_t* 
                                                                 const uint8_t* __restrict__ flag,
                                                                 const uint32_t* __restrict__ in, uint64_t n,
                                                                 const uint32_t* __restrict__ offs,
-                                                                uint32_t* __restrict__ out, uint32_t id_base) {
+                                                                uint32_t* __restrict__ out, uint32_t id_base,
+                                                                const uint32_t* __restrict__ skip) {
+    if (skip && *skip == n) return;
     __shared__ CompactSmem sm;
     const unsigned tid = threadIdx.x;
     const uint64_t base = (uint64_t)blockIdx.x * kCpTile;
@@ -245,7 +256,7 @@ __global__ void __launch_bounds__(kCpThreads) tile_apply_kernel(const uint32_t* 
 
 template <bool HEADS>
 void tiled_scan(Ctx* ctx, const uint32_t* lab, const uint8_t* flag, const uint32_t* in, uint64_t n, uint32_t* out,
-                uint32_t* total_dev, cudaStream_t s, uint32_t id_base = 0) {
+                uint32_t* total_dev, cudaStream_t s, uint32_t id_base = 0, const uint32_t* skip = nullptr) {
     if (n == 0) {
         DK_CUDA(cudaMemsetAsync(total_dev, 0, sizeof(uint32_t), s));
         return;
@@ -254,15 +265,16 @@ void tiled_scan(Ctx* ctx, const uint32_t* lab, const uint8_t* flag, const uint32
     if (tiles > 0xffffffffull) throw Error(DFAKIT_E_RESOURCE, "scan: too many tiles");
     DBuf<uint32_t> sums(tiles, s);
     const double eb = HEADS ? 4.0 : 1.0;
-    DK_LAUNCH_B(ctx, eb * n, tile_count_kernel<HEADS>, (unsigned)tiles, kCpThreads, 0, s, lab, flag, n, sums.get());
-    DK_LAUNCH(ctx, scan_counts_kernel, 1, 1024, 0, s, sums.get(), (uint32_t)tiles, total_dev);
+    DK_LAUNCH_B(ctx, eb * n, tile_count_kernel<HEADS>, (unsigned)tiles, kCpThreads, 0, s, lab, flag, n, sums.get(),
+                skip);
+    DK_LAUNCH(ctx, scan_counts_kernel, 1, 1024, 0, s, sums.get(), (uint32_t)tiles, total_dev, skip, n);
     DK_LAUNCH_B(ctx, HEADS ? 8.0 * n : (double)n * (1.0 + (in ? 4.0 : 0.0)), tile_apply_kernel<HEADS>,
-                (unsigned)tiles, kCpThreads, 0, s, lab, flag, in, n, sums.get(), out, id_base);
+                (unsigned)tiles, kCpThreads, 0, s, lab, flag, in, n, sums.get(), out, id_base, skip);
 }
 
 void compact_flags(Ctx* ctx, const uint32_t* in, const uint8_t* flag, uint64_t n, uint32_t* out,
-                   uint32_t* count_dev, cudaStream_t s, uint32_t id_base) {
-    tiled_scan<false>(ctx, nullptr, flag, in, n, out, count_dev, s, id_base);
+                   uint32_t* count_dev, cudaStream_t s, uint32_t id_base, const uint32_t* skip_if_all) {
+    tiled_scan<false>(ctx, nullptr, flag, in, n, out, count_dev, s, id_base, skip_if_all);
 }
 
 void head_scan(Ctx* ctx, const uint32_t* lab, uint64_t n, uint32_t* pos, uint32_t* total_dev, cudaStream_t s) {
@@ -321,8 +333,12 @@ uint32_t dense_labels(Ctx* ctx, const uint32_t* lab, uint64_t n, void* out, int 
 }
 
 uint32_t canonical_from_min_labels(Ctx* ctx, const uint32_t* lab, uint64_t n, uint32_t* out, uint32_t* scratch,
-                                   cudaStream_t s) {
+                                   cudaStream_t s, uint64_t known_blocks) {
     if (n == 0) return 0;
+    if (known_blocks == n) {  // every block a singleton: block q is number q
+        iota_u32(ctx, out, n, s);
+        return (uint32_t)n;
+    }
     head_scan(ctx, lab, n, scratch, scratch + n, s);
     DK_LAUNCH(ctx, relabel_kernel, grid_for(n), kThreads, 0, s, lab, n, scratch, out);
     uint32_t total = 0;

@@ -57,12 +57,15 @@ bool radix_sort_pairs(Ctx* ctx, RadixBuffers b, uint64_t m, uint32_t nbits, cuda
 bool radix_sort_pairs_range(Ctx* ctx, RadixBuffers b, uint64_t m, uint32_t bit_lo, uint32_t bit_hi,
                             cudaStream_t s);
 
-// Single-pass stream compaction (decoupled look-back, one launch):
+// Stream compaction (tile counts, one-CTA scan, apply):
 // out[j] = in ? in[i] : id_base + i for the j-th i with flag[i] != 0, order
 // preserved.
-// *count_dev receives the count.  Returns nothing (no host sync).
+// *count_dev receives the count.  Returns nothing (no host sync).  When
+// skip_if_all is given and *skip_if_all == n on the device, every launch
+// exits at once (all flags set: the caller keeps the identity list) and
+// neither out nor *count_dev is written.
 void compact_flags(Ctx* ctx, const uint32_t* in, const uint8_t* flag, uint64_t n, uint32_t* out,
-                   uint32_t* count_dev, cudaStream_t s, uint32_t id_base = 0);
+                   uint32_t* count_dev, cudaStream_t s, uint32_t id_base = 0, const uint32_t* skip_if_all = nullptr);
 
 // Dense first-occurrence block ids of min-state labels written in the
 // narrowest type that holds them: bytes = 1, 2 or 4 (uint8/uint16/uint32).
@@ -78,8 +81,10 @@ void iota_u32(Ctx* ctx, uint32_t* p, uint64_t n, cudaStream_t s);
 // label is its minimum member, so heads are states with lab[q] == q and the
 // dense id of a block is the number of heads before its label.
 // out may alias nothing; scratch holds n+1 uint32.  Returns the block count.
+// known_blocks == n (the caller's block count says every block is a
+// singleton): the numbering is the identity, no scan.
 uint32_t canonical_from_min_labels(Ctx* ctx, const uint32_t* lab, uint64_t n, uint32_t* out, uint32_t* scratch,
-                                   cudaStream_t s);
+                                   cudaStream_t s, uint64_t known_blocks = 0);
 
 // Rewrites arbitrary block labels (label values < n) in place so every
 // block is labelled by its minimum member.  scratch holds n uint32.

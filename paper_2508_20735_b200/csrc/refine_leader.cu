@@ -111,13 +111,58 @@ __device__ __forceinline__ bool differs_from_leader(uint32_t q, uint32_t L, cons
     return false;
 }
 
-// Alg. 2 (naive_pr): elect, barrier, follow, barrier.
+// Election write of one warp: split lanes with the same leader L combine
+// their priorities (match_any + reduce_min) and one of them issues the
+// atomicMin -- and only if the slot does not already hold a smaller value
+// (slots only decrease within a pass, so a stale read errs towards issuing).
+// On a chain every state of a warp shares its leader, and without this the
+// whole block's split states hammered one slot (same-address atomics
+// serialise at L2).  All 32 lanes must call it.
+__device__ __forceinline__ void elect(unsigned long long* __restrict__ slot, uint32_t L, uint32_t epoch, uint32_t prio,
+                                      bool split) {
+    const unsigned sm = __ballot_sync(0xffffffffu, split);
+    if (!split) return;
+    const unsigned peers = __match_any_sync(sm, L);
+    const uint32_t best = __reduce_min_sync(peers, prio);
+    if (lane_id() == (unsigned)(__ffs(peers) - 1)) {
+        const unsigned long long v = ((unsigned long long)epoch << 32) | best;
+        if (*(volatile unsigned long long*)&slot[L] > v) atomicMin(&slot[L], v);
+    }
+}
+
+// CTA-wide append of the lanes with pred set: one counter atomic per CTA
+// (a per-warp atomic on the single split counter serialised 10^5 -- 10^6
+// times per pass on large automata).  All threads of the CTA must call it;
+// sh holds kThreads / 32 + 1 words.
+__device__ __forceinline__ uint32_t cta_append(uint32_t* counter, bool pred, uint32_t* sh) {
+    constexpr unsigned W = kThreads / 32;
+    const unsigned lane = lane_id(), wid = threadIdx.x >> 5;
+    const unsigned m = __ballot_sync(0xffffffffu, pred);
+    __syncthreads();  // sh of the previous call is consumed
+    if (lane == 0) sh[wid] = __popc(m);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t run = 0;
+        for (unsigned w = 0; w < W; ++w) {
+            const uint32_t c = sh[w];
+            sh[w] = run;
+            run += c;
+        }
+        sh[W] = run ? atomicAdd(counter, run) : 0u;
+    }
+    __syncthreads();
+    return sh[W] + sh[wid] + __popc(m & ((1u << lane) - 1u));
+}
+
+// Alg. 2 (naive_pr): elect, barrier, follow, barrier.  The state loop is
+// uniform across a CTA (cta_append synchronises it).
 __global__ void __launch_bounds__(kThreads) naive_persistent_kernel(const uint32_t* __restrict__ delta, uint32_t n,
                                                                     uint32_t k, uint32_t* __restrict__ lab,
                                                                     unsigned long long* __restrict__ slot,
                                                                     uint32_t* __restrict__ split_list,
                                                                     uint32_t* __restrict__ cnt, int policy,
                                                                     uint64_t seed, PersistOut* __restrict__ out) {
+    __shared__ uint32_t sh[kThreads / 32 + 1];
     cg::grid_group grid = cg::this_grid();
     const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
     uint64_t pass = 0;
@@ -125,11 +170,12 @@ __global__ void __launch_bounds__(kThreads) naive_persistent_kernel(const uint32
         const Prio pr = make_prio(policy, seed, pass);
         const uint32_t epoch = 0xffffffffu - (uint32_t)pass;
         uint32_t* c = cnt + (pass & 1);
-        for (uint32_t q = tid; q < n; q += stride) {
-            const uint32_t L = lab[q];
+        for (uint32_t q0 = blockIdx.x * blockDim.x; q0 < n; q0 += stride) {
+            const uint32_t q = q0 + threadIdx.x;
+            const uint32_t L = q < n ? lab[q] : q;
             const bool split = L != q && differs_from_leader(q, L, delta, n, k, lab, [](uint32_t v) { return v; });
-            if (split) atomicMin(&slot[L], ((unsigned long long)epoch << 32) | pr.enc(q));
-            const uint32_t at = warp_append(c, split);
+            elect(slot, L, epoch, split ? pr.enc(q) : 0u, split);
+            const uint32_t at = cta_append(c, split, sh);
             if (split) split_list[at] = q;
         }
         grid.sync();
@@ -153,6 +199,7 @@ __global__ void __launch_bounds__(kThreads) fused_persistent_kernel(const uint32
                                                                     unsigned long long* __restrict__ slot1,
                                                                     uint32_t* __restrict__ cnt,
                                                                     PersistOut* __restrict__ out) {
+    __shared__ uint32_t red[kThreads / 32];
     cg::grid_group grid = cg::this_grid();
     const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
     uint64_t pass = 0;
@@ -166,18 +213,24 @@ __global__ void __launch_bounds__(kThreads) fused_persistent_kernel(const uint32
         // leaving barrier p - 1; the one of pass p - 2 is free
         uint32_t* c = cnt + (pass % 3);
         if (tid == 0) cnt[(pass + 1) % 3] = 0;
-        for (uint32_t q = tid; q < n; q += stride) {
-            const uint32_t L = resolve(cur[q], prev_slot);
+        uint32_t splits = 0;
+        for (uint32_t q0 = blockIdx.x * blockDim.x; q0 < n; q0 += stride) {
+            const uint32_t q = q0 + threadIdx.x;
+            const uint32_t L = q < n ? resolve(cur[q], prev_slot) : q;
             const bool split = L != q && differs_from_leader(q, L, delta, n, k, cur,
                                                              [&](uint32_t v) { return resolve(v, prev_slot); });
-            if (split) {
-                atomicMin(&slot[L], ((unsigned long long)epoch << 32) | q);
-                next[q] = kPending | L;
-            } else {
-                next[q] = L;
-            }
-            const unsigned sm = __ballot_sync(__activemask(), split);
-            if (sm && (threadIdx.x & 31u) == (unsigned)(__ffs(sm) - 1)) atomicAdd(c, (uint32_t)__popc(sm));
+            elect(slot, L, epoch, q, split);
+            if (q < n) next[q] = split ? (kPending | L) : L;
+            splits += split;
+        }
+        // one counter atomic per CTA
+        splits = __reduce_add_sync(0xffffffffu, splits);
+        if (lane_id() == 0) red[threadIdx.x >> 5] = splits;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t t = 0;
+            for (int w = 0; w < kThreads / 32; ++w) t += red[w];
+            if (t) atomicAdd(c, t);
         }
         grid.sync();
         if (*(volatile uint32_t*)c == 0) break;

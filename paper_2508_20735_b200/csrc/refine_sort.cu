@@ -64,11 +64,32 @@ struct IterCounters {
     uint32_t pad[2];
 };
 
+// Minimum accepting / rejecting state and class sizes.  Byte loads left the
+// kernel latency-bound (one 32-byte sector per warp request); 16-byte aligned
+// inputs are read 16 flags per load.
 __global__ void __launch_bounds__(kThreads) leader_info_kernel(const uint8_t* __restrict__ acc, uint32_t n,
                                                                uint32_t* __restrict__ info) {
     __shared__ uint32_t red[4][kThreads / 32];
     uint32_t mina = kNone, minr = kNone, ca = 0, cr = 0;
-    for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
+    const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
+    const bool vec = ((uintptr_t)acc & 15u) == 0;
+    const uint32_t nv = vec ? n / 16 : 0;
+    for (uint32_t v = tid; v < nv; v += stride) {
+        const uint4 w = __ldcs(reinterpret_cast<const uint4*>(acc) + v);
+        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const uint32_t q = v * 16 + j;
+            if ((ws[j >> 2] >> (8 * (j & 3))) & 0xffu) {
+                mina = min(mina, q);
+                ++ca;
+            } else {
+                minr = min(minr, q);
+                ++cr;
+            }
+        }
+    }
+    for (uint32_t q = nv * 16 + tid; q < n; q += stride) {
         if (acc[q]) {
             mina = min(mina, q);
             ++ca;
@@ -104,10 +125,48 @@ __global__ void __launch_bounds__(kThreads) leader_info_kernel(const uint8_t* __
     }
 }
 
+// lab[q] = la / lr by class; four flags per load when acc is 4-byte aligned
 __global__ void init_labels_kernel(const uint8_t* __restrict__ acc, uint32_t n, uint32_t la, uint32_t lr,
                                    uint32_t* __restrict__ lab) {
-    for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x)
-        lab[q] = acc[q] ? la : lr;
+    const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
+    const bool vec = ((uintptr_t)acc & 3u) == 0 && ((uintptr_t)lab & 15u) == 0;
+    const uint32_t nv = vec ? n / 4 : 0;
+    for (uint32_t v = tid; v < nv; v += stride) {
+        const uint32_t w = __ldcs(reinterpret_cast<const uint32_t*>(acc) + v);
+        __stcs(reinterpret_cast<uint4*>(lab) + v, make_uint4(w & 0xffu ? la : lr, (w >> 8) & 0xffu ? la : lr,
+                                                            (w >> 16) & 0xffu ? la : lr, w >> 24 ? la : lr));
+    }
+    for (uint32_t q = nv * 4 + tid; q < n; q += stride) lab[q] = acc[q] ? la : lr;
+}
+
+// Key labels of the initial partition straight from the flags: dense ids
+// (block of state 0 = 0) as bytes, or one bit per state
+__global__ void acc_dense2_kernel(const uint8_t* __restrict__ acc, uint32_t n, uint8_t* __restrict__ out) {
+    const uint32_t a0 = acc[0] != 0;
+    const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
+    const bool vec = ((uintptr_t)acc & 15u) == 0 && ((uintptr_t)out & 15u) == 0;
+    const uint32_t nv = vec ? n / 16 : 0;
+    auto flags4 = [a0](uint32_t w) {  // byte j -> (byte j != 0) ^ a0
+        uint32_t o = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) o |= ((((w >> (8 * j)) & 0xffu) != 0) ^ a0) << (8 * j);
+        return o;
+    };
+    for (uint32_t v = tid; v < nv; v += stride) {
+        const uint4 w = __ldcs(reinterpret_cast<const uint4*>(acc) + v);
+        reinterpret_cast<uint4*>(out)[v] = make_uint4(flags4(w.x), flags4(w.y), flags4(w.z), flags4(w.w));
+    }
+    for (uint32_t q = nv * 16 + tid; q < n; q += stride) out[q] = (acc[q] != 0) ^ a0;
+}
+
+__global__ void acc_dense2_bits_kernel(const uint8_t* __restrict__ acc, uint32_t n, uint32_t* __restrict__ out) {
+    const uint32_t a0 = acc[0] != 0;
+    const uint32_t words = (n + 31) / 32;
+    for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < words; w += (gridDim.x * blockDim.x) >> 5) {
+        const uint32_t q = w * 32 + (threadIdx.x & 31u);
+        const unsigned b = __ballot_sync(0xffffffffu, q < n && ((acc[q] != 0) ^ a0));
+        if ((threadIdx.x & 31u) == 0) out[w] = b;
+    }
 }
 
 // active = states whose initial block has >= 2 members
@@ -292,6 +351,61 @@ __global__ void __launch_bounds__(kThreads) table_apply_kernel(const uint32_t* _
         heads += rep == q;
         ablk += (rep == q) && multi;
         surv += multi;
+    }
+    flush_counters<kThreads>(heads, ablk, surv, &ctr->runs, &ctr->active_blocks, &ctr->active_states);
+}
+
+// Same over the identity list (states 0 .. m-1), four states per thread
+// with 16-byte key / label loads and stores (the scalar kernel sat at
+// ~2.4 TB/s: one 4-byte access per thread in flight).  Requires 16-byte
+// aligned keys32 / lab, 8-byte next16, 4-byte keep / next32.
+__global__ void __launch_bounds__(kThreads) table_apply_vec_kernel(const uint32_t* __restrict__ keys32, uint64_t m,
+                                                                   const uint32_t* __restrict__ tmin,
+                                                                   const uint32_t* __restrict__ tcnt,
+                                                                   uint32_t* __restrict__ lab,
+                                                                   uint8_t* __restrict__ keep,
+                                                                   const uint32_t* __restrict__ rank,
+                                                                   uint16_t* __restrict__ next16,
+                                                                   uint32_t* __restrict__ next32,
+                                                                   IterCounters* __restrict__ ctr) {
+    uint32_t heads = 0, ablk = 0, surv = 0;
+    const uint64_t nv = m / 4;
+    const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t v = tid; v < nv + (m & 3); v += stride) {
+        if (v < nv) {
+            const uint4 kv = __ldcs(reinterpret_cast<const uint4*>(keys32) + v);
+            const uint32_t key[4] = {kv.x, kv.y, kv.z, kv.w};
+            uint32_t rep[4], rk[4], kp = 0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint32_t q = (uint32_t)(4 * v + j);
+                rep[j] = tmin[key[j]];
+                const bool multi = tcnt[key[j]] >= 2;
+                if (rank) rk[j] = rank[key[j]];
+                kp |= (uint32_t)multi << (8 * j);
+                heads += rep[j] == q;
+                ablk += (rep[j] == q) && multi;
+                surv += multi;
+            }
+            __stcs(reinterpret_cast<uint4*>(lab) + v, make_uint4(rep[0], rep[1], rep[2], rep[3]));
+            if (keep) reinterpret_cast<uint32_t*>(keep)[v] = kp;
+            if (next16)
+                reinterpret_cast<uint2*>(next16)[v] = make_uint2((rk[0] & 0xffffu) | (rk[1] << 16),
+                                                                 (rk[2] & 0xffffu) | (rk[3] << 16));
+            if (next32) reinterpret_cast<uint4*>(next32)[v] = make_uint4(rk[0], rk[1], rk[2], rk[3]);
+        } else {  // tail: m % 4 states, one per thread
+            const uint64_t i = 4 * nv + (v - nv);
+            const uint32_t key = keys32[i], q = (uint32_t)i;
+            const uint32_t rep = tmin[key];
+            const bool multi = tcnt[key] >= 2;
+            lab[q] = rep;
+            if (next16) next16[q] = (uint16_t)rank[key];
+            if (next32) next32[q] = rank[key];
+            if (keep) keep[i] = multi;
+            heads += rep == q;
+            ablk += (rep == q) && multi;
+            surv += multi;
+        }
     }
     flush_counters<kThreads>(heads, ablk, surv, &ctr->runs, &ctr->active_blocks, &ctr->active_states);
 }
@@ -1032,10 +1146,19 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
 
     // initial partition {F, Q\F} with min-state labels
     LeaderInfo li = leader_info(ctx, d, s);
-    init_leader_labels(ctx, d, li, w.lab.get(), s);
     uint32_t B = (li.min_acc != kNone) + (li.min_rej != kNone);
     uint32_t A = (li.cnt_acc >= 2) + (li.cnt_rej >= 2);
     uint64_t m = (li.cnt_acc >= 2 ? li.cnt_acc : 0) + (li.cnt_rej >= 2 ? li.cnt_rej : 0);
+    // A first pass over every state with the counting table and dense key
+    // labels (taken from the flags) overwrites every label: the initial
+    // min-state labels are never read then.
+    {
+        const PassPlan p0 = plan_pass(n, k, B, m, 0, o.force_exact);
+        const bool small_first = m <= kSmallPersistMax && o.grouping == 0 && !o.force_exact;
+        const bool skip_init = m == n && !small_first && o.grouping != 1 && p0.strategy == kPlanTable &&
+                               p0.keylab_bytes != 0;
+        if (!skip_init) init_leader_labels(ctx, d, li, w.lab.get(), s);
+    }
     const uint32_t* list = nullptr;  // nullptr = identity (all states active)
     uint32_t* list_buf = w.list0.get();
     uint32_t* list_alt = w.list1.get();
@@ -1052,6 +1175,7 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
     uint32_t prev_nbits = 0;
     const uint64_t fp_mask = o.fingerprint_bits >= 64 ? ~0ull : ((1ull << o.fingerprint_bits) - 1ull);
     uint32_t collisions_this_pass = 0;
+    bool all_survive = false;
 
     auto dense_keylab = [&](int bytes) -> KeyLab {
         void* p;
@@ -1124,12 +1248,19 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
                 kl = w.next16.get() && prev_nbits <= 16 ? KeyLab{w.next16.get(), 2} : KeyLab{w.next32.get(), 4};
             } else if (B <= 2 && plan.strategy != kPlanChunked && n >= kBitLabelsMinStates) {
                 if (!w.bits.get()) w.bits.alloc((n + 31) / 32, s);
-                DK_LAUNCH(ctx, dense2_bits_kernel, grid_for((uint64_t)n), kThreads, 0, s, w.lab.get(), n,
-                          w.bits.get());
+                if (res.iters == 0)  // still the initial partition: from the flags
+                    DK_LAUNCH(ctx, acc_dense2_bits_kernel, grid_for((uint64_t)n), kThreads, 0, s, d.acc, n,
+                              w.bits.get());
+                else
+                    DK_LAUNCH(ctx, dense2_bits_kernel, grid_for((uint64_t)n), kThreads, 0, s, w.lab.get(), n,
+                              w.bits.get());
                 kl = KeyLab{w.bits.get(), kBitLabels};
             } else if (B <= 2 && plan.strategy != kPlanChunked) {
                 if (!w.dense8.get()) w.dense8.alloc(n, s);
-                DK_LAUNCH(ctx, dense2_kernel, grid_for(n), kThreads, 0, s, w.lab.get(), n, w.dense8.get());
+                if (res.iters == 0)
+                    DK_LAUNCH(ctx, acc_dense2_kernel, grid_for(n), kThreads, 0, s, d.acc, n, w.dense8.get());
+                else
+                    DK_LAUNCH(ctx, dense2_kernel, grid_for(n), kThreads, 0, s, w.lab.get(), n, w.dense8.get());
                 kl = KeyLab{w.dense8.get(), 1};
             } else {
                 kl = dense_keylab(plan.keylab_bytes);
@@ -1210,14 +1341,26 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
                 if (nbits <= 16 && !w.next16.get()) w.next16.alloc(n, s);
                 if (nbits > 16 && !w.next32.get()) w.next32.alloc(n, s);
             }
-            DK_LAUNCH_B(ctx, (double)m * (9.0 + 2 * list_b), table_apply_kernel, g, kThreads, 0, s, list,
-                        w.heads.get(), m, w.tmin.get(), w.tcnt.get(), w.lab.get(), w.keep.get(), nullptr,
-                        full ? w.trank.get() : nullptr, full && nbits <= 16 ? w.next16.get() : nullptr,
-                        full && nbits > 16 ? w.next32.get() : nullptr, 0u, dctr);
+            auto a16 = [](const void* x) { return ((uintptr_t)x & 15u) == 0; };
+            const bool vec = full && a16(w.heads.get()) && a16(w.lab.get()) && a16(w.keep.get()) &&
+                             a16(nbits <= 16 ? (void*)w.next16.get() : (void*)w.next32.get());
+            if (vec)  // identity list, four states per thread
+                DK_LAUNCH_B(ctx, (double)m * (9.0 + (nbits <= 16 ? 2.0 : 4.0)), table_apply_vec_kernel,
+                            grid_for((m + 3) / 4), kThreads, 0, s, w.heads.get(), m, w.tmin.get(), w.tcnt.get(),
+                            w.lab.get(), w.keep.get(), w.trank.get(), nbits <= 16 ? w.next16.get() : nullptr,
+                            nbits > 16 ? w.next32.get() : nullptr, dctr);
+            else
+                DK_LAUNCH_B(ctx, (double)m * (9.0 + 2 * list_b), table_apply_kernel, g, kThreads, 0, s, list,
+                            w.heads.get(), m, w.tmin.get(), w.tcnt.get(), w.lab.get(), w.keep.get(), nullptr,
+                            full ? w.trank.get() : nullptr, full && nbits <= 16 ? w.next16.get() : nullptr,
+                            full && nbits > 16 ? w.next32.get() : nullptr, 0u, dctr);
             next_valid = full;
             prev_nbits = nbits;
-            compact_flags(ctx, list, w.keep.get(), m, dst, &dctr->listed, s);
+            // every state survives (the first pass of a random automaton):
+            // the compaction exits at once and the identity list stays
+            compact_flags(ctx, list, w.keep.get(), m, dst, &dctr->listed, s, 0u, list ? nullptr : &dctr->active_states);
             read_words(ctx, dctr, sizeof(c), &c, s);
+            if (!list && c.active_states == m) all_survive = true;
         } else if (!chunked && o.grouping != 1) {
             wait_all_chunks();
             // ---- bucket strategy
@@ -1243,7 +1386,8 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
             if (state_order && !w.act.get()) w.act.alloc(n, s);
             if (fingerprint && direct) {
                 if (!w.lab2.get()) w.lab2.alloc(n, s);
-                DK_CUDA(cudaMemcpyAsync(w.lab2.get(), w.lab.get(), (size_t)n * 4, cudaMemcpyDeviceToDevice, s));
+                // a pass over every state writes every label of the copy
+                if (list) DK_CUDA(cudaMemcpyAsync(w.lab2.get(), w.lab.get(), (size_t)n * 4, cudaMemcpyDeviceToDevice, s));
             }
             uint32_t* out_lab = fingerprint && direct ? w.lab2.get() : w.lab.get();
             DK_CUDA(cudaMemsetAsync(w.bcnt.get(), 0, (size_t)nb * 4, s));
@@ -1415,14 +1559,16 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
         B = newB;
         A = c.active_blocks;
         m = c.active_states;
-        if (m) {  // every strategy compacted the survivors into dst
+        if (all_survive) {  // identity list kept (nothing was compacted)
+            all_survive = false;
+        } else if (m) {  // every strategy compacted the survivors into dst
             list = dst;
             if (dst == list_alt) std::swap(list_buf, list_alt);
         }
     }
     wait_all_chunks();  // inputs that needed no pass are still validated
     check_streamed();
-    res.num_blocks = canonical_from_min_labels(ctx, w.lab.get(), n, block_out, w.scratch.get(), s);
+    res.num_blocks = canonical_from_min_labels(ctx, w.lab.get(), n, block_out, w.scratch.get(), s, B);
     return res;
 }
 
