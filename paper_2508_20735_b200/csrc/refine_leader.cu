@@ -83,7 +83,10 @@ struct PersistOut {
 // letters are issued together (delta rows of q and L, then the labels), so
 // a thread waits on two memory latencies per chunk, not per letter; the
 // early exit is per chunk.  lab_of maps a stored label to the current one.
-template <typename F>
+// STREAM: delta rows are read once per pass with evict-first loads (large
+// automata); the single-CTA kernels re-read them every pass from L1 / shared
+// memory instead.
+template <typename F, bool STREAM = true>
 __device__ __forceinline__ bool differs_from_leader(uint32_t q, uint32_t L, const uint32_t* __restrict__ delta,
                                                     uint32_t n, uint32_t k, const uint32_t* lab, F lab_of) {
     constexpr int C = 8;
@@ -93,7 +96,7 @@ __device__ __forceinline__ bool differs_from_leader(uint32_t q, uint32_t L, cons
         for (int j = 0; j < C; ++j)
             if (a + j < k) {
                 const uint32_t* row = delta + (uint64_t)(a + j) * n;
-                tq[j] = ld_stream(row + q);
+                tq[j] = STREAM ? ld_stream(row + q) : row[q];
                 tl[j] = row[L];
             }
 #pragma unroll
@@ -130,60 +133,48 @@ __device__ __forceinline__ void elect(unsigned long long* __restrict__ slot, uin
     }
 }
 
-// CTA-wide append of the lanes with pred set: one counter atomic per CTA
-// (a per-warp atomic on the single split counter serialised 10^5 -- 10^6
-// times per pass on large automata).  All threads of the CTA must call it;
-// sh holds kThreads / 32 + 1 words.
-__device__ __forceinline__ uint32_t cta_append(uint32_t* counter, bool pred, uint32_t* sh) {
-    constexpr unsigned W = kThreads / 32;
-    const unsigned lane = lane_id(), wid = threadIdx.x >> 5;
-    const unsigned m = __ballot_sync(0xffffffffu, pred);
-    __syncthreads();  // sh of the previous call is consumed
-    if (lane == 0) sh[wid] = __popc(m);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        uint32_t run = 0;
-        for (unsigned w = 0; w < W; ++w) {
-            const uint32_t c = sh[w];
-            sh[w] = run;
-            run += c;
-        }
-        sh[W] = run ? atomicAdd(counter, run) : 0u;
-    }
-    __syncthreads();
-    return sh[W] + sh[wid] + __popc(m & ((1u << lane) - 1u));
-}
-
-// Alg. 2 (naive_pr): elect, barrier, follow, barrier.  The state loop is
-// uniform across a CTA (cta_append synchronises it).
+// Alg. 2 (naive_pr): elect, barrier, follow, barrier.  Every CTA appends its
+// split states to its own segment of split_list (seg entries, shared-memory
+// cursor: a global cursor serialised 10^5 -- 10^6 warp atomics per pass on
+// large automata) and adds its count to the pass counter once; in the follow
+// phase each CTA relabels its own segment.
 __global__ void __launch_bounds__(kThreads) naive_persistent_kernel(const uint32_t* __restrict__ delta, uint32_t n,
                                                                     uint32_t k, uint32_t* __restrict__ lab,
                                                                     unsigned long long* __restrict__ slot,
                                                                     uint32_t* __restrict__ split_list,
                                                                     uint32_t* __restrict__ cnt, int policy,
                                                                     uint64_t seed, PersistOut* __restrict__ out) {
-    __shared__ uint32_t sh[kThreads / 32 + 1];
+    __shared__ uint32_t cta_cnt[2];
     cg::grid_group grid = cg::this_grid();
     const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
+    const uint32_t seg = (n + stride - 1) / stride * blockDim.x;
+    uint32_t* my_list = split_list + (uint64_t)blockIdx.x * seg;
+    if (threadIdx.x == 0) cta_cnt[0] = 0;
+    __syncthreads();
     uint64_t pass = 0;
     for (;; ++pass) {
         const Prio pr = make_prio(policy, seed, pass);
         const uint32_t epoch = 0xffffffffu - (uint32_t)pass;
         uint32_t* c = cnt + (pass & 1);
+        uint32_t* cc = cta_cnt + (pass & 1);
+        if (threadIdx.x == 0) cta_cnt[(pass + 1) & 1] = 0;
         for (uint32_t q0 = blockIdx.x * blockDim.x; q0 < n; q0 += stride) {
             const uint32_t q = q0 + threadIdx.x;
             const uint32_t L = q < n ? lab[q] : q;
             const bool split = L != q && differs_from_leader(q, L, delta, n, k, lab, [](uint32_t v) { return v; });
             elect(slot, L, epoch, split ? pr.enc(q) : 0u, split);
-            const uint32_t at = cta_append(c, split, sh);
-            if (split) split_list[at] = q;
+            const uint32_t at = warp_append(cc, split);
+            if (split) my_list[at] = q;
         }
+        __syncthreads();
+        const uint32_t mine = *(volatile uint32_t*)cc;
+        if (threadIdx.x == 0 && mine) atomicAdd(c, mine);
         grid.sync();
         const uint32_t total = *(volatile uint32_t*)c;
         if (total == 0) break;
         if (tid == 0) cnt[(pass + 1) & 1] = 0;
-        for (uint32_t i = tid; i < total; i += stride) {
-            const uint32_t q = split_list[i];
+        for (uint32_t i = threadIdx.x; i < mine; i += blockDim.x) {
+            const uint32_t q = my_list[i];
             lab[q] = pr.dec((uint32_t)slot[lab[q]]);
         }
         grid.sync();
@@ -238,6 +229,196 @@ __global__ void __launch_bounds__(kThreads) fused_persistent_kernel(const uint32
     if (tid == 0) *out = PersistOut{(uint32_t)(pass + 1), (uint32_t)pass};
 }
 
+// ---- single-CTA variants ---------------------------------------------------------
+//
+// Small automata with many passes (the Fibonacci family: one split per pass)
+// spend a persistent kernel's time in grid barriers (~2 us each).  When the
+// pass state fits one SM's shared memory and a pass is little work
+// (n * k <= kOneWork), one CTA of 1024 threads runs every pass with
+// __syncthreads between phases: labels, election slots and the split list
+// live in shared memory, delta too when it fits (else L1-cached loads).
+
+constexpr int kOneThreads = 1024;
+constexpr uint64_t kOneWork = 1u << 16;     // n * k per pass
+constexpr size_t kOneSmem = 227 * 1024;     // opt-in shared memory per CTA
+constexpr size_t kOneMisc = 64 * sizeof(uint32_t);
+
+__device__ __forceinline__ const uint32_t* stage_delta(const uint32_t* delta_g, uint32_t n, uint32_t k,
+                                                       uint32_t* smem_delta) {
+    if (!smem_delta) return delta_g;
+    const uint64_t total = (uint64_t)n * k;
+    for (uint64_t i = threadIdx.x; i < total; i += blockDim.x) smem_delta[i] = __ldg(delta_g + i);
+    return smem_delta;
+}
+
+// Split test of R states per thread at once (the single-CTA kernels: few
+// states per thread, every load a dependent shared-memory / L1 round trip,
+// so the R chains are interleaved instead of run one after another; all k
+// letters are compared, n * k is small there).  Bit r of the result: state
+// qs[r] (< n) differs from its leader Ls[r] on some letter.
+template <int R, typename F>
+__device__ __forceinline__ uint32_t batch_differs(const uint32_t (&qs)[R], const uint32_t (&Ls)[R],
+                                                  const uint32_t* delta, uint32_t n, uint32_t k, const uint32_t* lab,
+                                                  F lab_of) {
+    uint32_t dif = 0;
+    for (uint32_t a = 0; a < k; ++a) {
+        const uint32_t* row = delta + (uint64_t)a * n;
+        uint32_t tq[R], tl[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const uint32_t q = min(qs[r], n - 1), L = min(Ls[r], n - 1);
+            tq[r] = row[q];
+            tl[r] = row[L];
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            tq[r] = lab[tq[r]];
+            tl[r] = lab[tl[r]];
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+            if (lab_of(tq[r]) != lab_of(tl[r])) dif |= 1u << r;
+    }
+    return dif;
+}
+
+constexpr int kOneBatch = 8;  // states per thread per batch
+
+// Alg. 2 in one CTA.  Shared layout: slot[n] (u64), lab[n], split_list[n],
+// misc[64] (counters, append scratch), then delta[k * n] when SMEM_DELTA.
+template <bool SMEM_DELTA>
+__global__ void __launch_bounds__(kOneThreads, 1) naive_one_kernel(const uint32_t* __restrict__ delta_g, uint32_t n,
+                                                                   uint32_t k, uint32_t* __restrict__ lab_g,
+                                                                   int policy, uint64_t seed,
+                                                                   PersistOut* __restrict__ out) {
+    extern __shared__ __align__(16) unsigned char one_raw[];
+    unsigned long long* slot = reinterpret_cast<unsigned long long*>(one_raw);
+    uint32_t* lab = reinterpret_cast<uint32_t*>(slot + n);
+    uint32_t* split_list = lab + n;
+    uint32_t* misc = split_list + n;  // [0, 1] split counters
+    const uint32_t* delta = stage_delta(delta_g, n, k, SMEM_DELTA ? misc + 64 : nullptr);
+    for (uint32_t q = threadIdx.x; q < n; q += blockDim.x) {
+        slot[q] = ~0ull;
+        lab[q] = lab_g[q];
+    }
+    if (threadIdx.x < 2) misc[threadIdx.x] = 0;
+    __syncthreads();
+    uint64_t pass = 0;
+    for (;; ++pass) {
+        const Prio pr = make_prio(policy, seed, pass);
+        const uint32_t epoch = 0xffffffffu - (uint32_t)pass;
+        uint32_t* c = misc + (pass & 1);
+        for (uint32_t q0 = 0; q0 < n; q0 += blockDim.x * kOneBatch) {
+            uint32_t qs[kOneBatch], Ls[kOneBatch];
+#pragma unroll
+            for (int r = 0; r < kOneBatch; ++r) {
+                qs[r] = q0 + r * blockDim.x + threadIdx.x;
+                Ls[r] = qs[r] < n ? lab[qs[r]] : qs[r];
+            }
+            const uint32_t dif = batch_differs(qs, Ls, delta, n, k, lab, [](uint32_t v) { return v; });
+#pragma unroll
+            for (int r = 0; r < kOneBatch; ++r) {
+                const bool split = Ls[r] != qs[r] && ((dif >> r) & 1u);
+                if (!__any_sync(0xffffffffu, split)) continue;
+                elect(slot, Ls[r], epoch, split ? pr.enc(qs[r]) : 0u, split);
+                const uint32_t at = warp_append(c, split);
+                if (split) split_list[at] = qs[r];
+            }
+        }
+        __syncthreads();
+        const uint32_t total = *(volatile uint32_t*)c;
+        if (total == 0) break;
+        if (threadIdx.x == 0) misc[(pass + 1) & 1] = 0;
+        for (uint32_t i = threadIdx.x; i < total; i += blockDim.x) {
+            const uint32_t q = split_list[i];
+            lab[q] = pr.dec((uint32_t)slot[lab[q]]);
+        }
+        __syncthreads();
+    }
+    for (uint32_t q = threadIdx.x; q < n; q += blockDim.x) lab_g[q] = lab[q];
+    if (threadIdx.x == 0) *out = PersistOut{(uint32_t)(pass + 1), (uint32_t)pass};
+}
+
+// Alg. 3 in one CTA.  Shared layout: slot0[n], slot1[n] (u64), lab0[n],
+// lab1[n], misc[64], then delta when SMEM_DELTA.  The final labels are
+// resolved in shared memory and written to lab_g.
+template <bool SMEM_DELTA>
+__global__ void __launch_bounds__(kOneThreads, 1) fused_one_kernel(const uint32_t* __restrict__ delta_g, uint32_t n,
+                                                                   uint32_t k, uint32_t* __restrict__ lab_g,
+                                                                   PersistOut* __restrict__ out) {
+    extern __shared__ __align__(16) unsigned char one_raw[];
+    unsigned long long* slot0 = reinterpret_cast<unsigned long long*>(one_raw);
+    unsigned long long* slot1 = slot0 + n;
+    uint32_t* lab0 = reinterpret_cast<uint32_t*>(slot1 + n);
+    uint32_t* lab1 = lab0 + n;
+    uint32_t* misc = lab1 + n;
+    const uint32_t* delta = stage_delta(delta_g, n, k, SMEM_DELTA ? misc + 64 : nullptr);
+    for (uint32_t q = threadIdx.x; q < n; q += blockDim.x) {
+        slot0[q] = ~0ull;
+        slot1[q] = ~0ull;
+        lab0[q] = lab_g[q];
+    }
+    if (threadIdx.x < 3) misc[threadIdx.x] = 0;
+    __syncthreads();
+    uint64_t pass = 0;
+    for (;; ++pass) {
+        const uint32_t* cur = (pass & 1) ? lab1 : lab0;
+        uint32_t* next = (pass & 1) ? lab0 : lab1;
+        const unsigned long long* prev_slot = (pass & 1) ? slot0 : slot1;
+        unsigned long long* slot = (pass & 1) ? slot1 : slot0;
+        const uint32_t epoch = 0xffffffffu - (uint32_t)pass;
+        uint32_t* c = misc + (pass % 3);
+        if (threadIdx.x == 0) misc[(pass + 1) % 3] = 0;
+        uint32_t splits = 0;
+        auto lab_of = [&](uint32_t v) { return resolve(v, prev_slot); };
+        for (uint32_t q0 = 0; q0 < n; q0 += blockDim.x * kOneBatch) {
+            uint32_t qs[kOneBatch], Ls[kOneBatch];
+#pragma unroll
+            for (int r = 0; r < kOneBatch; ++r) {
+                qs[r] = q0 + r * blockDim.x + threadIdx.x;
+                Ls[r] = qs[r] < n ? resolve(cur[qs[r]], prev_slot) : qs[r];
+            }
+            const uint32_t dif = batch_differs(qs, Ls, delta, n, k, cur, lab_of);
+#pragma unroll
+            for (int r = 0; r < kOneBatch; ++r) {
+                const bool split = Ls[r] != qs[r] && ((dif >> r) & 1u);
+                if (__any_sync(0xffffffffu, split)) elect(slot, Ls[r], epoch, qs[r], split);
+                if (qs[r] < n) next[qs[r]] = split ? (kPending | Ls[r]) : Ls[r];
+                splits += split;
+            }
+        }
+        splits = __reduce_add_sync(0xffffffffu, splits);
+        if (lane_id() == 0 && splits) atomicAdd(c, splits);
+        __syncthreads();
+        if (*(volatile uint32_t*)c == 0) break;
+    }
+    // pass p wrote labels (p & 1) ? lab0 : lab1 resolved through slots of pass p
+    const uint32_t* fin = (pass & 1) ? lab0 : lab1;
+    const unsigned long long* fslot = (pass & 1) ? slot1 : slot0;
+    for (uint32_t q = threadIdx.x; q < n; q += blockDim.x) lab_g[q] = resolve(fin[q], fslot);
+    if (threadIdx.x == 0) *out = PersistOut{(uint32_t)(pass + 1), (uint32_t)pass};
+}
+
+// Single-CTA plan: mode 0 = not applicable, 1 = delta from global (L1),
+// 2 = delta in shared memory.  bytes_per_state: the kernel's shared arrays
+// per state.  threads: kOneBatch states per thread (fewer threads for small
+// n -- idle batch slots still cost shared-memory wavefronts every pass).
+struct OnePlan {
+    int mode;
+    size_t smem;
+    unsigned threads;
+};
+OnePlan one_plan(uint32_t n, uint32_t k, size_t bytes_per_state) {
+    if ((uint64_t)n * k > kOneWork) return {0, 0, 0};
+    const size_t base = bytes_per_state * n + kOneMisc;
+    if (base > kOneSmem) return {0, 0, 0};
+    const unsigned threads =
+        (unsigned)std::min<uint64_t>(kOneThreads, std::max<uint64_t>(32, ((uint64_t)n + 8 * 32 - 1) / (8 * 32) * 32));
+    const size_t with_delta = base + (size_t)4 * n * k;
+    if (with_delta <= kOneSmem) return {2, with_delta, threads};
+    return {1, base, threads};
+}
+
 unsigned coop_grid(Ctx* ctx, const void* kernel, uint32_t n) {
     int per_sm = 0;
     DK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, 0));
@@ -283,15 +464,29 @@ RefineResult naive_pr_device(Ctx* ctx, const DevDfa& d, int policy, uint64_t see
     LeaderInfo li = leader_info(ctx, d, s);
     if (li.min_acc == kNone || li.min_rej == kNone) return single_block(ctx, n, block_out, s);
     RefineResult res;
-    DBuf<uint32_t> lab(n, s), split(n, s), scratch((uint64_t)n + 1, s);
+    DBuf<uint32_t> lab(n, s), split, scratch((uint64_t)n + 1, s);
     DBuf<unsigned long long> slot(n, s);
     DBuf<uint32_t> cnt(2, s);
     DBuf<PersistOut> out(1, s);
     DK_CUDA(cudaMemsetAsync(slot.get(), 0xff, (size_t)n * sizeof(unsigned long long), s));
     DK_CUDA(cudaMemsetAsync(cnt.get(), 0, 2 * sizeof(uint32_t), s));
     init_leader_labels(ctx, d, li, lab.get(), s);
-    {
+    if (const OnePlan op = one_plan(n, d.k, 16); op.mode) {
+        DK_CUDA(cudaFuncSetAttribute(op.mode == 2 ? naive_one_kernel<true> : naive_one_kernel<false>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)op.smem));
+        if (op.mode == 2)
+            DK_LAUNCH(ctx, naive_one_kernel<true>, 1, op.threads, op.smem, s, d.delta, n, d.k, lab.get(), policy,
+                      seed, out.get());
+        else
+            DK_LAUNCH(ctx, naive_one_kernel<false>, 1, op.threads, op.smem, s, d.delta, n, d.k, lab.get(), policy,
+                      seed, out.get());
+        PersistOut o{};
+        read_words(ctx, out.get(), sizeof(o), &o, s);
+        res.passes = o.passes;
+        res.iters = o.iters;
+    } else {
         const unsigned g = coop_grid(ctx, (const void*)naive_persistent_kernel, n);
+        split.alloc((uint64_t)n + (uint64_t)g * kThreads, s);  // one segment per CTA
         const uint32_t* delta = d.delta;
         uint32_t k = d.k;
         uint32_t* labp = lab.get();
@@ -333,6 +528,20 @@ RefineResult naive_pr_fused_device(Ctx* ctx, const DevDfa& d, uint32_t* block_ou
     DK_CUDA(cudaMemsetAsync(cnt.get(), 0, 3 * sizeof(uint32_t), s));
     init_leader_labels(ctx, d, li, lab0.get(), s);
     PersistOut o{};
+    if (const OnePlan op = one_plan(n, d.k, 24); op.mode) {
+        DK_CUDA(cudaFuncSetAttribute(op.mode == 2 ? fused_one_kernel<true> : fused_one_kernel<false>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)op.smem));
+        if (op.mode == 2)
+            DK_LAUNCH(ctx, fused_one_kernel<true>, 1, op.threads, op.smem, s, d.delta, n, d.k, lab0.get(), out.get());
+        else
+            DK_LAUNCH(ctx, fused_one_kernel<false>, 1, op.threads, op.smem, s, d.delta, n, d.k, lab0.get(),
+                      out.get());
+        read_words(ctx, out.get(), sizeof(o), &o, s);
+        res.passes = o.passes;
+        res.iters = o.iters;
+        res.num_blocks = canonical_from_min_labels(ctx, lab0.get(), n, block_out, scratch.get(), s);
+        return res;
+    }
     {
         const unsigned g = coop_grid(ctx, (const void*)fused_persistent_kernel, n);
         const uint32_t* delta = d.delta;

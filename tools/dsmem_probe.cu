@@ -72,6 +72,51 @@ __global__ void global_kernel(const uint32_t* __restrict__ tab, uint32_t words, 
     if (acc == 0x12345u) sink[0] = acc;
 }
 
+// load-variant probe: does any PTX load flavour beat one line per SM per clock?
+template <int V>
+__device__ __forceinline__ uint32_t ldv(const uint32_t* p) {
+    uint32_t r;
+    if (V == 0) r = __ldg(p);
+    else if (V == 1) asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(r) : "l"(p));
+    else if (V == 2) asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));
+    else if (V == 3) asm volatile("ld.global.nc.L2::64B.u32 %0, [%1];" : "=r"(r) : "l"(p));
+    else r = *(volatile const uint32_t*)p;
+    return r;
+}
+
+template <int V>
+__global__ void variant_kernel(const uint32_t* __restrict__ tab, uint32_t words, uint32_t rounds, uint32_t* sink) {
+    uint64_t x = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) * 0x9E3779B97F4A7C15ull + 1;
+    uint32_t acc = 0;
+    for (uint32_t r = 0; r < rounds; ++r) {
+        uint32_t v[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = ldv<V>(tab + __umulhi((uint32_t)lcg(x), words));
+#pragma unroll
+        for (int j = 0; j < 16; ++j) acc += v[j];
+    }
+    if (acc == 0x12345u) sink[0] = acc;
+}
+
+// cp.async 4-byte gathers into shared memory (LDGSTS), 16 per round
+__global__ void cpasync_kernel(const uint32_t* __restrict__ tab, uint32_t words, uint32_t rounds, uint32_t* sink) {
+    __shared__ uint32_t buf[256 * 16];
+    uint64_t x = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) * 0x9E3779B97F4A7C15ull + 1;
+    uint32_t acc = 0;
+    for (uint32_t r = 0; r < rounds; ++r) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const uint32_t* src = tab + __umulhi((uint32_t)lcg(x), words);
+            const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&buf[j * 256 + threadIdx.x]);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src));
+        }
+        asm volatile("cp.async.wait_all;" ::: "memory");
+#pragma unroll
+        for (int j = 0; j < 16; ++j) acc += buf[j * 256 + threadIdx.x];
+    }
+    if (acc == 0x12345u) sink[0] = acc;
+}
+
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("%s: %s\n", #x, cudaGetErrorString(e)); return 1; } } while (0)
 
 int main() {
@@ -97,6 +142,33 @@ int main() {
         float ms;
         cudaEventElapsedTime(&ms, a, b);
         printf("global  table %8.2f MB: %.3e gathers/s\n", words * 4e-6, (double)grid * threads * rounds * 16 / (ms * 1e-3));
+        cudaFree(t);
+    }
+    {
+        const uint32_t words = 5000000u;
+        uint32_t* t;
+        CK(cudaMalloc(&t, words * 4ull));
+        CK(cudaMemset(t, 1, words * 4ull));
+        const unsigned grid = sms * 8, threads = 256;
+        const char* names[] = {"ld.global.nc", "ld.global.cg", "ld.nc.L1::no_allocate", "ld.nc.L2::64B", "ld.volatile", "cp.async.ca 4B"};
+        for (int v = 0; v < 6; ++v) {
+            for (int rep = 0; rep < 2; ++rep) {
+                if (rep) cudaEventRecord(a);
+                switch (v) {
+                    case 0: variant_kernel<0><<<grid, threads>>>(t, words, rounds, sink); break;
+                    case 1: variant_kernel<1><<<grid, threads>>>(t, words, rounds, sink); break;
+                    case 2: variant_kernel<2><<<grid, threads>>>(t, words, rounds, sink); break;
+                    case 3: variant_kernel<3><<<grid, threads>>>(t, words, rounds, sink); break;
+                    case 4: variant_kernel<4><<<grid, threads>>>(t, words, rounds, sink); break;
+                    case 5: cpasync_kernel<<<grid, threads>>>(t, words, rounds, sink); break;
+                }
+                if (rep) cudaEventRecord(b);
+            }
+            CK(cudaEventSynchronize(b));
+            float ms;
+            cudaEventElapsedTime(&ms, a, b);
+            printf("variant %-24s 20 MB: %.3e gathers/s\n", names[v], (double)grid * threads * rounds * 16 / (ms * 1e-3));
+        }
         cudaFree(t);
     }
     for (uint32_t kb : {16u, 64u, 160u, 200u}) {
