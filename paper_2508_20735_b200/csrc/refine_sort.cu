@@ -453,6 +453,14 @@ constexpr unsigned long long kEmptyKey = ~0ull;         // a real ~0 key takes t
 constexpr uint32_t kBucketShift = 20;                   // bucket = hkey bits [20, 20 + D): slots use the low
                                                         // bits, the sharded engine's owner rank the top 32
 
+// Bucket cursors are kCntStride words apart (one per 32-byte sector): the
+// cursor atomics of a pass are spread over nb sectors instead of nb / 8 --
+// L2 serialises atomics per sector, and packed cursors made the appends wait.
+#ifndef DFAKIT_CNT_STRIDE
+#define DFAKIT_CNT_STRIDE 8
+#endif
+constexpr uint32_t kCntStride = DFAKIT_CNT_STRIDE;
+
 // q and r have the same (block, signature) tuple under any injective block
 // labelling `lab` (min-state labels, or the pass's key labels)
 template <typename LR>
@@ -488,7 +496,7 @@ __device__ __forceinline__ void bucket_append(unsigned long long hk, uint32_t q,
     const unsigned peers = __match_any_sync(act, b);
     const unsigned leader = __ffs(peers) - 1;
     uint32_t base = 0;
-    if (lane == leader) base = atomicAdd(&bcnt[b], (uint32_t)__popc(peers));
+    if (lane == leader) base = atomicAdd(&bcnt[b * kCntStride], (uint32_t)__popc(peers));
     base = __shfl_sync(act, base, leader);
     const uint32_t pos = base + (uint32_t)__popc(peers & lt);
     uint64_t slot;
@@ -573,7 +581,7 @@ __global__ void __launch_bounds__(kGrpThreads) bucket_group_kernel(
     uint32_t heads = 0, ablk = 0, surv = 0;
     bool clash = false;
     for (uint32_t b = blockIdx.x; b < nb; b += gridDim.x) {
-        const uint32_t len = bcnt[b];
+        const uint32_t len = bcnt[b * kCntStride];
         if (len == 0 || len > kGrpCap) continue;  // uniform across the CTA
         const uint32_t T = max(64u, pow2_at_least(2 * len));
         for (uint32_t e = tid; e <= T; e += kGrpThreads) {
@@ -647,7 +655,7 @@ __device__ __forceinline__ bool fallback_elem(uint64_t e, const uint32_t* __rest
                                               uint32_t ovf) {
     const uint64_t bspace = (uint64_t)nb * kGrpCap;
     if (e >= bspace) return e - bspace < ovf;
-    return bcnt[e / kGrpCap] > kGrpCap;
+    return bcnt[(e / kGrpCap) * kCntStride] > kGrpCap;
 }
 
 __global__ void ghash_insert_kernel(const uint32_t* __restrict__ bcnt, uint32_t nb, uint32_t ovf,
@@ -725,7 +733,7 @@ __global__ void slot_apply_kernel(const uint32_t* __restrict__ bcnt, uint32_t nb
     const uint64_t bspace = (uint64_t)nb * kGrpCap, total = bspace + ovf;
     for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
          e += (uint64_t)gridDim.x * blockDim.x) {
-        if (e < bspace && (uint32_t)(e % kGrpCap) >= min(bcnt[e / kGrpCap], kGrpCap)) continue;
+        if (e < bspace && (uint32_t)(e % kGrpCap) >= min(bcnt[(e / kGrpCap) * kCntStride], kGrpCap)) continue;
         const uint32_t q = bent[e].z;
         lab[q] = rep_slot[e];
         if (act) act[q] = keep_slot[e];
@@ -1370,7 +1378,7 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
             while (D < 24 && ((uint64_t)1 << D) * (kGrpCap * 3 / 4) < m) ++D;
             const uint32_t nb = 1u << D;
             const uint64_t bspace = (uint64_t)nb * kGrpCap, espace = bspace + m;
-            if (w.bcnt.n < nb) w.bcnt.alloc(nb, s);
+            if (w.bcnt.n < (uint64_t)nb * kCntStride) w.bcnt.alloc((uint64_t)nb * kCntStride, s);
             if (w.bent.n < espace) {
                 w.bent.alloc(espace, s);
                 w.keep_slot.alloc(espace, s);
@@ -1390,7 +1398,7 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
                 if (list) DK_CUDA(cudaMemcpyAsync(w.lab2.get(), w.lab.get(), (size_t)n * 4, cudaMemcpyDeviceToDevice, s));
             }
             uint32_t* out_lab = fingerprint && direct ? w.lab2.get() : w.lab.get();
-            DK_CUDA(cudaMemsetAsync(w.bcnt.get(), 0, (size_t)nb * 4, s));
+            DK_CUDA(cudaMemsetAsync(w.bcnt.get(), 0, (size_t)nb * kCntStride * 4, s));
             if (state_order) DK_CUDA(cudaMemsetAsync(w.act.get(), 0, n, s));
             if (!state_order) DK_CUDA(cudaMemsetAsync(w.keep_slot.get(), 0, espace, s));
             with_lab_type(kl, [&](auto lab) {
@@ -1809,9 +1817,9 @@ void shard_group(Ctx* ctx, const DevDfa& d, const void* verify_lab, uint32_t ver
         while (D < 24 && ((uint64_t)1 << D) * (kGrpCap * 3 / 4) < count) ++D;
         const uint32_t nb = 1u << D;
         const uint64_t bspace = (uint64_t)nb * kGrpCap, espace = bspace + count;
-        DBuf<uint32_t> bcnt(nb, s);
+        DBuf<uint32_t> bcnt((uint64_t)nb * kCntStride, s);
         DBuf<uint4> bent(espace, s);
-        DK_CUDA(cudaMemsetAsync(bcnt.get(), 0, (size_t)nb * 4, s));
+        DK_CUDA(cudaMemsetAsync(bcnt.get(), 0, (size_t)nb * kCntStride * 4, s));
         DK_LAUNCH_B(ctx, 32.0 * count, entry_bucket_kernel, grid_for(count), kThreads, 0, s, recv, count, nb,
                     bcnt.get(), bent.get(), dctr);
         const int fp = plan.strategy == kPlanFingerprint ? 1 : 0;
