@@ -580,8 +580,19 @@ __global__ void __launch_bounds__(kGrpThreads) bucket_group_kernel(
     const unsigned tid = threadIdx.x;
     uint32_t heads = 0, ablk = 0, surv = 0;
     bool clash = false;
+    uint32_t len_next = blockIdx.x < nb ? bcnt[blockIdx.x * kCntStride] : 0u;
     for (uint32_t b = blockIdx.x; b < nb; b += gridDim.x) {
-        const uint32_t len = bcnt[b * kCntStride];
+        const uint32_t len = len_next;
+        // the next bucket's length now, its entries into L2 while this one
+        // is grouped (one prefetch per 128-byte line)
+        const uint32_t bn = b + gridDim.x;
+        if (bn < nb) {
+            len_next = bcnt[bn * kCntStride];
+            const uint32_t lines = (min(len_next, kGrpCap) * 16u + 127u) / 128u;
+            const char* base = reinterpret_cast<const char*>(bent + (uint64_t)bn * kGrpCap);
+            for (uint32_t l = tid; l < lines; l += kGrpThreads)
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(base + 128ull * l));
+        }
         if (len == 0 || len > kGrpCap) continue;  // uniform across the CTA
         const uint32_t T = max(64u, pow2_at_least(2 * len));
         for (uint32_t e = tid; e <= T; e += kGrpThreads) {
@@ -619,14 +630,10 @@ __global__ void __launch_bounds__(kGrpThreads) bucket_group_kernel(
                     }
                 }
                 slot[j] = s;
-                atomicMin(&sm.rep[s], q[j]);
+                // a member that finds the slot already claimed makes the run
+                // multi-member (whoever came first): no separate marking sweep
+                if (atomicMin(&sm.rep[s], q[j]) != kNone) sm.multi[s] = 1;
             }
-        }
-        __syncthreads();
-#pragma unroll
-        for (int j = 0; j < kGrpItems; ++j) {
-            const uint32_t idx = j * kGrpThreads + tid;
-            if (idx < len && sm.rep[slot[j]] != q[j]) sm.multi[slot[j]] = 1;
         }
         __syncthreads();
 #pragma unroll

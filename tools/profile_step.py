@@ -11,6 +11,7 @@ workloads:
   equiv     equivalence + inclusion (hash-set product BFS) and union-find HK, 10M x 2
   sharded   the sharded engine at world size 1 (NCCL), 10M x 10
   trans     trans_minimize (CH92) on Fibonacci 12
+  fib       naive_pr / naive_pr_fused (single-CTA kernels) and sort_pr (persistent small-m engine) on Fibonacci 19
   calib     the random-gather calibration probe
 
 Numbers printed under ncu are never bench values.
@@ -27,7 +28,7 @@ sys.path.insert(0, ROOT)
 def main():
     p = argparse.ArgumentParser()
     p.add_argument("--workload", default="synth",
-                   choices=["synth", "radix", "naive", "chain", "equiv", "sharded", "trans", "calib"])
+                   choices=["synth", "radix", "naive", "chain", "equiv", "sharded", "trans", "calib", "fib"])
     p.add_argument("--states", type=int, default=None)
     p.add_argument("--alphabet", type=int, default=10)
     p.add_argument("--reps", type=int, default=2)
@@ -53,6 +54,15 @@ def main():
         for _ in range(a.reps):
             nat.check(nat.lib.dfakit_calibrate_gather(ctx.handle, n, 4, 100_000_000, C.byref(r)))
         print("gathers/s", r.value)
+        return
+    if w == "fib":
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import pyoracle
+        d, acc, _ = pyoracle.COracle().gen_family("fib", 19)
+        dfa = dk.Dfa(d, acc, 0)
+        for fn in (dk.naive_pr, dk.naive_pr_fused, dk.sort_pr):
+            res = fn(dfa, ctx=ctx)
+        print("passes", res.refining_iterations)
         return
     if w == "trans":
         sys.path.insert(0, os.path.join(ROOT, "oracle"))
