@@ -79,17 +79,16 @@ struct PersistOut {
     uint32_t passes, iters;
 };
 
-// Does q differ from its leader L on some letter?  Loads of a chunk of 8
+// Does q differ from its leader L on some letter?  Loads of a chunk of C
 // letters are issued together (delta rows of q and L, then the labels), so
 // a thread waits on two memory latencies per chunk, not per letter; the
 // early exit is per chunk.  lab_of maps a stored label to the current one.
 // STREAM: delta rows are read once per pass with evict-first loads (large
 // automata); the single-CTA kernels re-read them every pass from L1 / shared
 // memory instead.
-template <typename F, bool STREAM = true>
+template <typename F, bool STREAM = true, int C = 8>
 __device__ __forceinline__ bool differs_from_leader(uint32_t q, uint32_t L, const uint32_t* __restrict__ delta,
                                                     uint32_t n, uint32_t k, const uint32_t* lab, F lab_of) {
-    constexpr int C = 8;
     for (uint32_t a = 0; a < k; a += C) {
         uint32_t tq[C], tl[C];
 #pragma unroll
@@ -138,6 +137,7 @@ __device__ __forceinline__ void elect(unsigned long long* __restrict__ slot, uin
 // cursor: a global cursor serialised 10^5 -- 10^6 warp atomics per pass on
 // large automata) and adds its count to the pass counter once; in the follow
 // phase each CTA relabels its own segment.
+template <int C>
 __global__ void __launch_bounds__(kThreads) naive_persistent_kernel(const uint32_t* __restrict__ delta, uint32_t n,
                                                                     uint32_t k, uint32_t* __restrict__ lab,
                                                                     unsigned long long* __restrict__ slot,
@@ -161,7 +161,8 @@ __global__ void __launch_bounds__(kThreads) naive_persistent_kernel(const uint32
         for (uint32_t q0 = blockIdx.x * blockDim.x; q0 < n; q0 += stride) {
             const uint32_t q = q0 + threadIdx.x;
             const uint32_t L = q < n ? lab[q] : q;
-            const bool split = L != q && differs_from_leader(q, L, delta, n, k, lab, [](uint32_t v) { return v; });
+            auto ident = [](uint32_t v) { return v; };
+            const bool split = L != q && differs_from_leader<decltype(ident), true, C>(q, L, delta, n, k, lab, ident);
             elect(slot, L, epoch, split ? pr.enc(q) : 0u, split);
             const uint32_t at = warp_append(cc, split);
             if (split) my_list[at] = q;
@@ -183,6 +184,9 @@ __global__ void __launch_bounds__(kThreads) naive_persistent_kernel(const uint32
 }
 
 // Alg. 3 (naive_pr_fused): one barrier per pass; labels ping-pong.  cnt: 3 words.
+// Two letters per load chunk, as the persistent naive kernel (100K x 10:
+// 320 -> 293 ms against 8).
+constexpr int kFusedChunk = 2;
 __global__ void __launch_bounds__(kThreads) fused_persistent_kernel(const uint32_t* __restrict__ delta, uint32_t n,
                                                                     uint32_t k, uint32_t* __restrict__ lab0,
                                                                     uint32_t* __restrict__ lab1,
@@ -208,8 +212,9 @@ __global__ void __launch_bounds__(kThreads) fused_persistent_kernel(const uint32
         for (uint32_t q0 = blockIdx.x * blockDim.x; q0 < n; q0 += stride) {
             const uint32_t q = q0 + threadIdx.x;
             const uint32_t L = q < n ? resolve(cur[q], prev_slot) : q;
-            const bool split = L != q && differs_from_leader(q, L, delta, n, k, cur,
-                                                             [&](uint32_t v) { return resolve(v, prev_slot); });
+            auto lab_of = [&](uint32_t v) { return resolve(v, prev_slot); };
+            const bool split =
+                L != q && differs_from_leader<decltype(lab_of), true, kFusedChunk>(q, L, delta, n, k, cur, lab_of);
             elect(slot, L, epoch, q, split);
             if (q < n) next[q] = split ? (kPending | L) : L;
             splits += split;
@@ -485,7 +490,24 @@ RefineResult naive_pr_device(Ctx* ctx, const DevDfa& d, int policy, uint64_t see
         res.passes = o.passes;
         res.iters = o.iters;
     } else {
-        const unsigned g = coop_grid(ctx, (const void*)naive_persistent_kernel, n);
+        // letters per load chunk: more loads in flight per thread (two memory
+        // round trips per chunk) against a later early exit and fewer
+        // resident threads.  Measured on the 10M chain (trans_pr, 24 closure
+        // letters): 1 / 2 / 4 / 8 / 16 / 32 letters -> 12.6 / 11.6 / 13.8 /
+        // 14.2 / 20.4 / 41.2 ms (2 letters: 32 registers, full occupancy);
+        // 100K x 10 random: 456 ms for 2..8.  DFAKIT_NAIVE_CHUNK overrides.
+        static const int chunk_env = [] {
+            const char* e = getenv("DFAKIT_NAIVE_CHUNK");
+            return e ? atoi(e) : 0;
+        }();
+        const int chunk = chunk_env ? chunk_env : 2;
+        const void* kern = chunk >= 32 ? (const void*)naive_persistent_kernel<32>
+                           : chunk >= 16 ? (const void*)naive_persistent_kernel<16>
+                           : chunk >= 8  ? (const void*)naive_persistent_kernel<8>
+                           : chunk >= 4  ? (const void*)naive_persistent_kernel<4>
+                           : chunk >= 2  ? (const void*)naive_persistent_kernel<2>
+                                         : (const void*)naive_persistent_kernel<1>;
+        const unsigned g = coop_grid(ctx, kern, n);
         split.alloc((uint64_t)n + (uint64_t)g * kThreads, s);  // one segment per CTA
         const uint32_t* delta = d.delta;
         uint32_t k = d.k;
@@ -498,7 +520,7 @@ RefineResult naive_pr_device(Ctx* ctx, const DevDfa& d, int policy, uint64_t see
         void* args[] = {(void*)&delta, (void*)&nn, (void*)&k, (void*)&labp, (void*)&slotp, (void*)&splitp,
                         (void*)&cntp, (void*)&policy, (void*)&seed, (void*)&outp};
         prof_begin_launch(ctx, s);
-        DK_CUDA(cudaLaunchCooperativeKernel((const void*)naive_persistent_kernel, g, kThreads, args, 0, s));
+        DK_CUDA(cudaLaunchCooperativeKernel(kern, g, kThreads, args, 0, s));
         note_launch(ctx);
         prof_end_launch(ctx, s, "naive_persistent_kernel", 0, 0);
         PersistOut o{};
