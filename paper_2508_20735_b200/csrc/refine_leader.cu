@@ -115,11 +115,11 @@ __device__ __forceinline__ bool differs_from_leader(uint32_t q, uint32_t L, cons
 
 // Election write of one warp: split lanes with the same leader L combine
 // their priorities (match_any + reduce_min) and one of them issues the
-// atomicMin -- and only if the slot does not already hold a smaller value
-// (slots only decrease within a pass, so a stale read errs towards issuing).
-// On a chain every state of a warp shares its leader, and without this the
-// whole block's split states hammered one slot (same-address atomics
-// serialise at L2).  All 32 lanes must call it.
+// atomicMin.  On a chain every state of a warp shares its leader, and
+// without the combine the whole block's split states hammered one slot
+// (same-address atomics serialise at L2).  A plain reduction measured better
+// than reading the slot first to skip it (chain 12.6 -> 12.5 ms, 100K x 10
+// naive 456 -> 429 ms, fused 294 -> 274 ms).  All 32 lanes must call it.
 __device__ __forceinline__ void elect(unsigned long long* __restrict__ slot, uint32_t L, uint32_t epoch, uint32_t prio,
                                       bool split) {
     const unsigned sm = __ballot_sync(0xffffffffu, split);
@@ -128,7 +128,7 @@ __device__ __forceinline__ void elect(unsigned long long* __restrict__ slot, uin
     const uint32_t best = __reduce_min_sync(peers, prio);
     if (lane_id() == (unsigned)(__ffs(peers) - 1)) {
         const unsigned long long v = ((unsigned long long)epoch << 32) | best;
-        if (*(volatile unsigned long long*)&slot[L] > v) atomicMin(&slot[L], v);
+        atomicMin(&slot[L], v);  // result unused: a fire-and-forget reduction
     }
 }
 
