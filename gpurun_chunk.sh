@@ -2,10 +2,8 @@
 cd "$GRAFT_REPO_ROOT"
 mkdir -p gpurun_out
 : > gpurun_out/chunk.log
-for v in with without; do
-  cp exp/$v.so paper_2508_20735_b200/lib/libdfakit_b200.so
-  echo "$v" >> gpurun_out/chunk.log
-  timeout -s KILL 120 python tools/kprof.py chain --reps 2 2>&1 | grep -E "wall" >> gpurun_out/chunk.log
-  timeout -s KILL 120 python tools/kprof.py naive --reps 1 2>&1 | grep -E "wall" >> gpurun_out/chunk.log
-  timeout -s KILL 120 python tools/kprof.py naive --algo naive_pr_fused --reps 1 2>&1 | grep -E "wall" >> gpurun_out/chunk.log
-done
+timeout -s KILL 120 python tools/kprof.py naive --reps 1 2>&1 | grep -E "wall" >> gpurun_out/chunk.log
+timeout -s KILL 120 python tools/kprof.py naive --algo naive_pr_fused --reps 1 2>&1 | grep -E "wall" >> gpurun_out/chunk.log
+timeout -s KILL 120 python tools/kprof.py chain --reps 2 2>&1 | grep -E "wall" >> gpurun_out/chunk.log
+timeout -s KILL 900 python -m pytest tests -q -m gpu -p no:cacheprovider --timeout 400 -rf -x > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout -s KILL 600 python tools/family_timing.py > gpurun_out/families.jsonl 2> gpurun_out/families.err

@@ -138,14 +138,12 @@ __device__ __forceinline__ void elect(unsigned long long* __restrict__ slot, uin
 // large automata) and adds its count to the pass counter once; in the follow
 // phase each CTA relabels its own segment.
 template <int C>
-__global__ void __launch_bounds__(kThreads) naive_persistent_kernel(const uint32_t* __restrict__ delta, uint32_t n,
-                                                                    uint32_t k, uint32_t* __restrict__ lab,
-                                                                    unsigned long long* __restrict__ slot,
-                                                                    uint32_t* __restrict__ split_list,
-                                                                    uint32_t* __restrict__ cnt, int policy,
-                                                                    uint64_t seed, PersistOut* __restrict__ out) {
+__global__ void __launch_bounds__(kThreads)
+    naive_persistent_kernel(const uint32_t* __restrict__ delta, uint32_t n, uint32_t k, uint32_t* __restrict__ lab,
+                            unsigned long long* __restrict__ slot, uint32_t* __restrict__ split_list,
+                            uint32_t* __restrict__ cnt, int policy, uint64_t seed, PersistOut* __restrict__ out) {
     __shared__ uint32_t cta_cnt[2];
-    cg::grid_group grid = cg::this_grid();
+    auto sync_all = [] { cg::this_grid().sync(); };
     const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
     const uint32_t seg = (n + stride - 1) / stride * blockDim.x;
     uint32_t* my_list = split_list + (uint64_t)blockIdx.x * seg;
@@ -162,7 +160,8 @@ __global__ void __launch_bounds__(kThreads) naive_persistent_kernel(const uint32
             const uint32_t q = q0 + threadIdx.x;
             const uint32_t L = q < n ? lab[q] : q;
             auto ident = [](uint32_t v) { return v; };
-            const bool split = L != q && differs_from_leader<decltype(ident), true, C>(q, L, delta, n, k, lab, ident);
+            const bool split =
+                L != q && differs_from_leader<decltype(ident), true, C>(q, L, delta, n, k, lab, ident);
             elect(slot, L, epoch, split ? pr.enc(q) : 0u, split);
             const uint32_t at = warp_append(cc, split);
             if (split) my_list[at] = q;
@@ -170,7 +169,7 @@ __global__ void __launch_bounds__(kThreads) naive_persistent_kernel(const uint32
         __syncthreads();
         const uint32_t mine = *(volatile uint32_t*)cc;
         if (threadIdx.x == 0 && mine) atomicAdd(c, mine);
-        grid.sync();
+        sync_all();
         const uint32_t total = *(volatile uint32_t*)c;
         if (total == 0) break;
         if (tid == 0) cnt[(pass + 1) & 1] = 0;
@@ -178,7 +177,7 @@ __global__ void __launch_bounds__(kThreads) naive_persistent_kernel(const uint32
             const uint32_t q = my_list[i];
             lab[q] = pr.dec((uint32_t)slot[lab[q]]);
         }
-        grid.sync();
+        sync_all();
     }
     if (tid == 0) *out = PersistOut{(uint32_t)(pass + 1), (uint32_t)pass};
 }
@@ -428,10 +427,12 @@ unsigned coop_grid(Ctx* ctx, const void* kernel, uint32_t n) {
     int per_sm = 0;
     DK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, 0));
     if (per_sm < 1) throw Error(DFAKIT_E_RESOURCE, "cooperative kernel does not fit an SM");
-    // a grid barrier costs more with more CTAs: small automata (many cheap
-    // passes) run one CTA per SM, large ones fill every SM
+    // every resident CTA up to one state per thread: a pass is latency-bound
+    // (dependent label / delta loads per state), so resident threads beat
+    // the cheaper barrier of a smaller grid (100K x 10 naive: 427 ms with one
+    // CTA per SM, 336 ms with every SM full)
     const uint64_t need = ((uint64_t)n + kThreads - 1) / kThreads;
-    const uint64_t cap = n <= (1u << 22) ? (uint64_t)ctx->num_sms : (uint64_t)per_sm * ctx->num_sms;
+    const uint64_t cap = (uint64_t)per_sm * ctx->num_sms;
     return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(need, cap));
 }
 
@@ -490,23 +491,12 @@ RefineResult naive_pr_device(Ctx* ctx, const DevDfa& d, int policy, uint64_t see
         res.passes = o.passes;
         res.iters = o.iters;
     } else {
-        // letters per load chunk: more loads in flight per thread (two memory
-        // round trips per chunk) against a later early exit and fewer
-        // resident threads.  Measured on the 10M chain (trans_pr, 24 closure
-        // letters): 1 / 2 / 4 / 8 / 16 / 32 letters -> 12.6 / 11.6 / 13.8 /
-        // 14.2 / 20.4 / 41.2 ms (2 letters: 32 registers, full occupancy);
-        // 100K x 10 random: 456 ms for 2..8.  DFAKIT_NAIVE_CHUNK overrides.
-        static const int chunk_env = [] {
-            const char* e = getenv("DFAKIT_NAIVE_CHUNK");
-            return e ? atoi(e) : 0;
-        }();
-        const int chunk = chunk_env ? chunk_env : 2;
-        const void* kern = chunk >= 32 ? (const void*)naive_persistent_kernel<32>
-                           : chunk >= 16 ? (const void*)naive_persistent_kernel<16>
-                           : chunk >= 8  ? (const void*)naive_persistent_kernel<8>
-                           : chunk >= 4  ? (const void*)naive_persistent_kernel<4>
-                           : chunk >= 2  ? (const void*)naive_persistent_kernel<2>
-                                         : (const void*)naive_persistent_kernel<1>;
+        // The persistent kernels test two letters per load chunk (more loads
+        // in flight per thread against a later early exit and fewer resident
+        // threads; measured on the 10M chain, trans_pr with 24 closure
+        // letters: 1 / 2 / 4 / 8 / 16 / 32 letters -> 12.6 / 11.6 / 13.8 /
+        // 14.2 / 20.4 / 41.2 ms; 2 letters: 32 registers, full occupancy).
+        const void* kern = (const void*)naive_persistent_kernel<2>;
         const unsigned g = coop_grid(ctx, kern, n);
         split.alloc((uint64_t)n + (uint64_t)g * kThreads, s);  // one segment per CTA
         const uint32_t* delta = d.delta;

@@ -293,3 +293,24 @@ def test_streamed_host_input(dk, oracle):
     bad[2][-1] = 1_500_000
     with pytest.raises(ValueError, match="out of range"):
         dk.sort_pr(dk.Dfa(bad, t[1], 0))
+
+
+def test_naive_kernel_paths(dk, oracle):
+    """Leader election through each of its kernels: single CTA with delta in
+    shared memory (n * k small), single CTA with delta from L1 (shared arrays
+    fit, delta does not), and the persistent grid kernels (n * k > 2^16) --
+    pass counts exact for min_index, partitions for arbitrary(seed)."""
+    cases = [(900, 3, 0.5, 11),     # one CTA, delta in shared memory
+             (4000, 12, 0.3, 12),   # one CTA, delta from global / L1
+             (3000, 30, 0.5, 13),   # persistent grid kernels
+             (2500, 40, 0.2, 14)]
+    for n, k, frac, seed in cases:
+        t = oracle.gen_random(n, k, frac, seed)
+        dfa = mkdfa(dk, t)
+        for algo in ("naive", "naive-fused"):
+            want = oracle.minimize(algo, t[0], t[1])
+            got = run(dk, algo, dfa)
+            assert same(got, want), (n, k, algo, got.refining_iterations, want.refine_iters)
+        moore = oracle.minimize("moore", t[0], t[1])
+        got = dk.naive_pr(dfa, dk.ElectionPolicy.arbitrary(7))
+        assert np.array_equal(got.partition.block_of, moore.blocks), (n, k)
