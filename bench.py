@@ -24,6 +24,7 @@ from __future__ import annotations
 import argparse
 import ctypes as C
 import json
+import re
 import os
 import socket
 import sys
@@ -138,8 +139,10 @@ def ncu_traffic(kernel: str):
         with open(path) as f:
             j = json.load(f)
         def norm(s):
-            s = s.split("(")[0].split("<")[0].strip()
-            return s[5:] if s.startswith("void ") else s
+            for tok in re.findall(r"[A-Za-z_]\w*", s):
+                if tok.endswith("_kernel"):
+                    return tok
+            return s
         ks = {norm(name): v for name, v in j["kernels"].items()}
         k = ks[norm(kernel)]
         return k["dram_bytes_per_launch"], f"profiles/ncu_summary.json ({j['tag']}, {k['workload']} workload)"

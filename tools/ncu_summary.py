@@ -45,10 +45,13 @@ SCALE = {"dur_us": TIME, "dram_rd": BYTES, "dram_wr": BYTES}
 
 
 def short(name):
-    name = name.split("(")[0]
-    for p in ("dk::<unnamed>::", "dk::", "<unnamed>::", "unnamed>::", "(anonymous namespace)::"):
-        name = name.replace(p, "")
-    return name.split("<")[0] if "<" in name and name.index("<") > 0 else name
+    """Kernel name without namespaces, template arguments and parameters
+    (the first identifier ending in `_kernel`)."""
+    import re
+    for tok in re.findall(r"[A-Za-z_]\w*", name.split("(")[0] if "_kernel(" in name else name):
+        if tok.endswith("_kernel"):
+            return tok
+    return name.split("(")[0]
 
 
 def read_raw(rep):
