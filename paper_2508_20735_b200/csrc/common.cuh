@@ -72,8 +72,9 @@ struct Ctx {
     cudaStream_t stream = nullptr;
     cudaStream_t copy_stream = nullptr;  // host->device input streaming (lazily created)
     bool own_stream = true;
-    uint64_t* mailbox = nullptr;  // pinned host, 64 words
+    uint64_t* mailbox = nullptr;  // pinned host, 64 words: [0, 56) read_words, [56, 64) deferred reads
     uint64_t* dmailbox = nullptr; // device, 64 words
+    cudaEvent_t info_ev = nullptr;  // marks a deferred mailbox read (no timing)
     uint64_t launches = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     bool profiling = false;

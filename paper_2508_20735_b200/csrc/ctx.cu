@@ -63,7 +63,7 @@ std::string prof_collect(Ctx* ctx) {
 }
 
 void read_words(Ctx* ctx, const void* dsrc, size_t bytes, void* hdst, cudaStream_t s) {
-    if (bytes > 64 * sizeof(uint64_t)) throw Error(DFAKIT_E_INVALID, "read_words: too large");
+    if (bytes > 56 * sizeof(uint64_t)) throw Error(DFAKIT_E_INVALID, "read_words: too large");
     DK_CUDA(cudaMemcpyAsync(ctx->mailbox, dsrc, bytes, cudaMemcpyDeviceToHost, s));
     DK_CUDA(cudaStreamSynchronize(s));
     std::memcpy(hdst, ctx->mailbox, bytes);
@@ -85,6 +85,7 @@ Ctx* ctx_create(int device) {
     DK_CUDA(cudaMalloc(reinterpret_cast<void**>(&c->dmailbox), 64 * sizeof(uint64_t)));
     DK_CUDA(cudaEventCreate(&c->ev0));
     DK_CUDA(cudaEventCreate(&c->ev1));
+    DK_CUDA(cudaEventCreateWithFlags(&c->info_ev, cudaEventDisableTiming));
     // keep freed pool memory around: repeated calls reuse it without cudaMalloc
     cudaMemPool_t pool;
     DK_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
@@ -101,6 +102,7 @@ void ctx_destroy(Ctx* c) {
     if (c->dmailbox) cudaFree(c->dmailbox);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
+    if (c->info_ev) cudaEventDestroy(c->info_ev);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     if (c->stream && c->own_stream) cudaStreamDestroy(c->stream);
     delete c;

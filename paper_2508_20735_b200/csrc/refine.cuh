@@ -114,6 +114,11 @@ struct LeaderInfo {
     uint32_t min_acc, min_rej, cnt_acc, cnt_rej;
 };
 LeaderInfo leader_info(Ctx* ctx, const DevDfa& d, cudaStream_t s);
+// Same, read back later: the kernel and a copy into the pinned mailbox are
+// queued now; leader_info_wait() waits for that copy only (kernels queued
+// after it keep the device busy meanwhile).
+void leader_info_async(Ctx* ctx, const DevDfa& d, cudaStream_t s);
+LeaderInfo leader_info_wait(Ctx* ctx);
 void init_leader_labels(Ctx* ctx, const DevDfa& d, const LeaderInfo& li, uint32_t* lab, cudaStream_t s);
 
 // product exploration

@@ -1044,6 +1044,23 @@ LeaderInfo leader_info(Ctx* ctx, const DevDfa& d, cudaStream_t s) {
     return li;
 }
 
+void leader_info_async(Ctx* ctx, const DevDfa& d, cudaStream_t s) {
+    uint32_t* info = reinterpret_cast<uint32_t*>(ctx->dmailbox);
+    DK_CUDA(cudaMemsetAsync(info, 0xff, 2 * sizeof(uint32_t), s));
+    DK_CUDA(cudaMemsetAsync(info + 2, 0, 2 * sizeof(uint32_t), s));
+    DK_LAUNCH(ctx, leader_info_kernel, grid_for(d.n, kThreads, (unsigned)ctx->num_sms * 8u), kThreads, 0, s, d.acc,
+              d.n, info);
+    DK_CUDA(cudaMemcpyAsync(ctx->mailbox + 56, info, sizeof(LeaderInfo), cudaMemcpyDeviceToHost, s));
+    DK_CUDA(cudaEventRecord(ctx->info_ev, s));
+}
+
+LeaderInfo leader_info_wait(Ctx* ctx) {
+    DK_CUDA(cudaEventSynchronize(ctx->info_ev));
+    LeaderInfo li;
+    std::memcpy(&li, ctx->mailbox + 56, sizeof(li));
+    return li;
+}
+
 void init_leader_labels(Ctx* ctx, const DevDfa& d, const LeaderInfo& li, uint32_t* lab, cudaStream_t s) {
     DK_LAUNCH(ctx, init_labels_kernel, grid_for(d.n), kThreads, 0, s, d.acc, d.n, li.min_acc, li.min_rej, lab);
 }
@@ -1159,15 +1176,34 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
                                  smem_table));
     IterCounters* dctr = w.ctr.get();
 
-    // initial partition {F, Q\F} with min-state labels
-    LeaderInfo li = leader_info(ctx, d, s);
-    uint32_t B = (li.min_acc != kNone) + (li.min_rej != kNone);
-    uint32_t A = (li.cnt_acc >= 2) + (li.cnt_rej >= 2);
-    uint64_t m = (li.cnt_acc >= 2 ? li.cnt_acc : 0) + (li.cnt_rej >= 2 ? li.cnt_rej : 0);
-    // A first pass over every state with the counting table and dense key
-    // labels (taken from the flags) overwrites every label: the initial
-    // min-state labels are never read then.
-    {
+    // initial partition {F, Q\F} with min-state labels.
+    // Large automata whose first pass is a counting-table pass with dense key
+    // labels (taken from the flags) run that pass over every state without
+    // waiting for the class sizes: the pass overwrites every label (the
+    // initial min-state labels are never read), and a singleton or empty
+    // class only adds its own single-member run, so with A = B (every
+    // nonempty class counted active) B - A + runs, the survivors and the pass
+    // count are those of the reference's pass over the non-singleton
+    // classes.  The class sizes are read after the pass is queued.
+    const bool streamed_in = ds && ds->chunks;
+    const PassPlan p_full = plan_pass(n, k, 2, n, 0, o.force_exact);
+    const bool deferred_info = !streamed_in && (uint64_t)n > kSmallPersistMax && o.grouping != 1 && !o.force_exact &&
+                               p_full.strategy == kPlanTable && p_full.keylab_bytes != 0;
+    LeaderInfo li{};
+    uint32_t B, A;
+    uint64_t m;
+    if (deferred_info) {
+        leader_info_async(ctx, d, s);
+        B = 2;  // the plan's assumption; corrected from the counts after the pass
+        A = 2;
+        m = n;
+    } else {
+        li = leader_info(ctx, d, s);
+        B = (li.min_acc != kNone) + (li.min_rej != kNone);
+        A = (li.cnt_acc >= 2) + (li.cnt_rej >= 2);
+        m = (li.cnt_acc >= 2 ? li.cnt_acc : 0) + (li.cnt_rej >= 2 ? li.cnt_rej : 0);
+        // a first pass over every state with the counting table and dense key
+        // labels overwrites every label: no initial labels then
         const PassPlan p0 = plan_pass(n, k, B, m, 0, o.force_exact);
         const bool small_first = m <= kSmallPersistMax && o.grouping == 0 && !o.force_exact;
         const bool skip_init = m == n && !small_first && o.grouping != 1 && p0.strategy == kPlanTable &&
@@ -1374,6 +1410,11 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
             // every state survives (the first pass of a random automaton):
             // the compaction exits at once and the identity list stays
             compact_flags(ctx, list, w.keep.get(), m, dst, &dctr->listed, s, 0u, list ? nullptr : &dctr->active_states);
+            if (deferred_info && res.passes == 1) {  // the class sizes, read while the pass ran
+                li = leader_info_wait(ctx);
+                B = (li.min_acc != kNone) + (li.min_rej != kNone);
+                A = B;
+            }
             read_words(ctx, dctr, sizeof(c), &c, s);
             if (!list && c.active_states == m) all_survive = true;
         } else if (!chunked && o.grouping != 1) {

@@ -314,3 +314,29 @@ def test_naive_kernel_paths(dk, oracle):
         moore = oracle.minimize("moore", t[0], t[1])
         got = dk.naive_pr(dfa, dk.ElectionPolicy.arbitrary(7))
         assert np.array_equal(got.partition.block_of, moore.blocks), (n, k)
+
+
+def test_first_pass_class_edge_cases_large(dk, oracle):
+    """Large automata (past the small-m engine) whose first pass runs over
+    every state before the class sizes are read: a singleton accepting class,
+    a singleton rejecting class, all accepting, none accepting -- partition
+    and pass counts exact against the oracle."""
+    n, k = 300_000, 3
+    delta, acc, _ = oracle.gen_random(n, k, 0.5, 77)
+    for name in ("one_acc", "one_rej", "all_acc", "no_acc"):
+        a = np.zeros(n, dtype=np.uint8)
+        if name == "one_acc":
+            a[12345] = 1
+        elif name == "one_rej":
+            a[:] = 1
+            a[0] = 0
+        elif name == "all_acc":
+            a[:] = 1
+        want = oracle.minimize("sort", delta, a)
+        got = dk.sort_pr(dk.Dfa(delta, a, 0))
+        assert same(got, want), (name, got.refining_iterations, want.refine_iters, got.partition.num_blocks,
+                                 want.num_blocks)
+    a = acc.copy()  # a nonzero flag other than 1 still means accepting
+    a[a != 0] = 7
+    want = oracle.minimize("sort", delta, acc)
+    assert same(dk.sort_pr(dk.Dfa(delta, a, 0)), want)
