@@ -52,7 +52,8 @@ struct ShardInit {
 ShardInit shard_init(Ctx* ctx, const DevDfa& d, uint32_t lo, uint32_t hi, uint32_t* lab, uint8_t* act,
                      cudaStream_t s);
 void shard_keylab(Ctx* ctx, const uint32_t* lab, uint32_t n, uint32_t num_blocks, const PassPlan& plan, void* out,
-                  uint32_t* scratch, cudaStream_t s);
+                  uint32_t* scratch, cudaStream_t s,
+                  const uint8_t* initial_acc = nullptr);
 // list == nullptr: the active states are list_base .. list_base + m - 1
 void shard_table_signature(Ctx* ctx, const DevDfa& d, const void* keylab, const PassPlan& plan, const uint32_t* list,
                            uint32_t list_base, uint64_t m, uint32_t* keys32, uint32_t* tmin, uint32_t* tcnt,

@@ -1781,15 +1781,26 @@ ShardInit shard_init(Ctx* ctx, const DevDfa& d, uint32_t lo, uint32_t hi, uint32
     return r;
 }
 
+// initial_acc: the partition is still {F, Q \ F}: two-block key labels come
+// straight from the flags (10 MB read instead of 40).
 void shard_keylab(Ctx* ctx, const uint32_t* lab, uint32_t n, uint32_t num_blocks, const PassPlan& plan, void* out,
-                  uint32_t* scratch, cudaStream_t s) {
+                  uint32_t* scratch, cudaStream_t s, const uint8_t* initial_acc) {
     if (!plan.keylab_bytes) return;
-    if (plan.keylab_bytes == kBitLabels)  // two blocks: a bitmap, no scan
-        DK_LAUNCH(ctx, dense2_bits_kernel, grid_for((uint64_t)n), kThreads, 0, s, lab, n, static_cast<uint32_t*>(out));
-    else if (num_blocks <= 2 && plan.keylab_bytes == 1)  // two blocks: no scan
-        DK_LAUNCH(ctx, dense2_kernel, grid_for(n), kThreads, 0, s, lab, n, static_cast<uint8_t*>(out));
-    else
+    if (plan.keylab_bytes == kBitLabels) {  // two blocks: a bitmap, no scan
+        if (initial_acc)
+            DK_LAUNCH(ctx, acc_dense2_bits_kernel, grid_for((uint64_t)n), kThreads, 0, s, initial_acc, n,
+                      static_cast<uint32_t*>(out));
+        else
+            DK_LAUNCH(ctx, dense2_bits_kernel, grid_for((uint64_t)n), kThreads, 0, s, lab, n,
+                      static_cast<uint32_t*>(out));
+    } else if (num_blocks <= 2 && plan.keylab_bytes == 1) {  // two blocks: no scan
+        if (initial_acc)
+            DK_LAUNCH(ctx, acc_dense2_kernel, grid_for(n), kThreads, 0, s, initial_acc, n, static_cast<uint8_t*>(out));
+        else
+            DK_LAUNCH(ctx, dense2_kernel, grid_for(n), kThreads, 0, s, lab, n, static_cast<uint8_t*>(out));
+    } else {
         dense_labels(ctx, lab, n, out, (int)plan.keylab_bytes, scratch, s);
+    }
 }
 
 void shard_table_signature(Ctx* ctx, const DevDfa& d, const void* keylab, const PassPlan& plan, const uint32_t* list,

@@ -294,7 +294,8 @@ RefineResult sort_pr_sharded_device(Ctx* ctx, NcclComm* cm, const DevDfa& d, uin
         shard_compact(ctx, act.get(), lo, hi, list.get(), dctr.get() + 4, s);
         read_u32(dctr.get() + 4, 1, &m);
     };
-    compact();
+    if (m_total == n) m = hi - lo;  // every state active: the identity range
+    else compact();
     uint64_t salt = 0x5EED5EED5EEDull;
     uint32_t strikes = 0;
     const void* carried = nullptr;  // key labels of the current partition (ranks of a full table pass)
@@ -338,7 +339,7 @@ RefineResult sort_pr_sharded_device(Ctx* ctx, NcclComm* cm, const DevDfa& d, uin
                     if (!kl32.get()) kl32.alloc(n, s);
                     out = kl32.get();
                 }
-                shard_keylab(ctx, lab.get(), n, B, plan, out, scratch.get(), s);
+                shard_keylab(ctx, lab.get(), n, B, plan, out, scratch.get(), s, res.iters == 0 ? d.acc : nullptr);
                 keylab = out;
             }
         }
@@ -426,14 +427,18 @@ RefineResult sort_pr_sharded_device(Ctx* ctx, NcclComm* cm, const DevDfa& d, uin
             carried = next_kl;
             carried_bytes = (uint32_t)es;
             lab_stale = true;
-        } else {
+        } else if (B < n) {
             cm->allgather(lab.get(), (size_t)shard * sizeof(uint32_t), s);
             lab_stale = false;
+        } else {
+            lab_stale = true;  // all singletons: the numbering needs no labels
         }
-        compact();
+        if (m_total == n) m = hi - lo;  // every state survives: the identity range, no compaction
+        else compact();
     }
-    if (lab_stale) cm->allgather(lab.get(), (size_t)shard * sizeof(uint32_t), s);
-    res.num_blocks = canonical_from_min_labels(ctx, lab.get(), n, block_out, scratch.get(), s);
+    // an all-singleton partition is numbered by identity (no label exchange)
+    if (lab_stale && B < n) cm->allgather(lab.get(), (size_t)shard * sizeof(uint32_t), s);
+    res.num_blocks = canonical_from_min_labels(ctx, lab.get(), n, block_out, scratch.get(), s, B);
     if (exchanged) *exchanged = sent;
     return res;
 }
