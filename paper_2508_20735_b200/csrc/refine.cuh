@@ -118,7 +118,7 @@ LeaderInfo leader_info(Ctx* ctx, const DevDfa& d, cudaStream_t s);
 // Same, read back later: the kernel and a copy into the pinned mailbox are
 // queued now; leader_info_wait() waits for that copy only (kernels queued
 // after it keep the device busy meanwhile).
-void leader_info_async(Ctx* ctx, const DevDfa& d, cudaStream_t s);
+void leader_info_async(Ctx* ctx, const DevDfa& d, cudaStream_t s, uint8_t* dense2 = nullptr);
 LeaderInfo leader_info_wait(Ctx* ctx);
 void init_leader_labels(Ctx* ctx, const DevDfa& d, const LeaderInfo& li, uint32_t* lab, cudaStream_t s);
 

@@ -67,15 +67,29 @@ struct IterCounters {
 // Minimum accepting / rejecting state and class sizes.  Byte loads left the
 // kernel latency-bound (one 32-byte sector per warp request); 16-byte aligned
 // inputs are read 16 flags per load.
+// dense2 (optional): also writes the initial partition's dense block ids,
+// dense2[q] = (acc[q] != 0) ^ (acc[0] != 0), from the same loads.
+__device__ __forceinline__ uint32_t flags4(uint32_t w, uint32_t a0) {  // byte j -> (byte j != 0) ^ a0
+    uint32_t o = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) o |= ((((w >> (8 * j)) & 0xffu) != 0) ^ a0) << (8 * j);
+    return o;
+}
+
 __global__ void __launch_bounds__(kThreads) leader_info_kernel(const uint8_t* __restrict__ acc, uint32_t n,
-                                                               uint32_t* __restrict__ info) {
+                                                               uint32_t* __restrict__ info,
+                                                               uint8_t* __restrict__ dense2) {
     __shared__ uint32_t red[4][kThreads / 32];
     uint32_t mina = kNone, minr = kNone, ca = 0, cr = 0;
     const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
-    const bool vec = ((uintptr_t)acc & 15u) == 0;
+    const bool vec = ((uintptr_t)acc & 15u) == 0 && ((uintptr_t)dense2 & 15u) == 0;
     const uint32_t nv = vec ? n / 16 : 0;
+    const uint32_t a0 = n ? acc[0] != 0 : 0u;
     for (uint32_t v = tid; v < nv; v += stride) {
         const uint4 w = __ldcs(reinterpret_cast<const uint4*>(acc) + v);
+        if (dense2)
+            reinterpret_cast<uint4*>(dense2)[v] =
+                make_uint4(flags4(w.x, a0), flags4(w.y, a0), flags4(w.z, a0), flags4(w.w, a0));
         const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
@@ -90,6 +104,7 @@ __global__ void __launch_bounds__(kThreads) leader_info_kernel(const uint8_t* __
         }
     }
     for (uint32_t q = nv * 16 + tid; q < n; q += stride) {
+        if (dense2) dense2[q] = (acc[q] != 0) ^ a0;
         if (acc[q]) {
             mina = min(mina, q);
             ++ca;
@@ -146,15 +161,9 @@ __global__ void acc_dense2_kernel(const uint8_t* __restrict__ acc, uint32_t n, u
     const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
     const bool vec = ((uintptr_t)acc & 15u) == 0 && ((uintptr_t)out & 15u) == 0;
     const uint32_t nv = vec ? n / 16 : 0;
-    auto flags4 = [a0](uint32_t w) {  // byte j -> (byte j != 0) ^ a0
-        uint32_t o = 0;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) o |= ((((w >> (8 * j)) & 0xffu) != 0) ^ a0) << (8 * j);
-        return o;
-    };
     for (uint32_t v = tid; v < nv; v += stride) {
         const uint4 w = __ldcs(reinterpret_cast<const uint4*>(acc) + v);
-        reinterpret_cast<uint4*>(out)[v] = make_uint4(flags4(w.x), flags4(w.y), flags4(w.z), flags4(w.w));
+        reinterpret_cast<uint4*>(out)[v] = make_uint4(flags4(w.x, a0), flags4(w.y, a0), flags4(w.z, a0), flags4(w.w, a0));
     }
     for (uint32_t q = nv * 16 + tid; q < n; q += stride) out[q] = (acc[q] != 0) ^ a0;
 }
@@ -408,6 +417,33 @@ __global__ void __launch_bounds__(kThreads) table_apply_vec_kernel(const uint32_
         }
     }
     flush_counters<kThreads>(heads, ablk, surv, &ctr->runs, &ctr->active_blocks, &ctr->active_states);
+}
+
+// ranks of the occupied table entries in one CTA (tables of <= 2^14
+// entries: the counting tables of two-block-derived keys): rank[e] = number
+// of occupied entries before e
+__global__ void __launch_bounds__(1024) table_rank_one_kernel(const uint32_t* __restrict__ tcnt, uint32_t tsize,
+                                                              uint32_t* __restrict__ rank) {
+    __shared__ uint32_t ws[32];
+    uint32_t carry = 0;
+    for (uint32_t b = 0; b < tsize; b += 1024 * 4) {
+        const uint32_t e0 = b + threadIdx.x * 4;
+        uint32_t f[4], c = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            f[j] = e0 + j < tsize && tcnt[e0 + j] ? 1u : 0u;
+            c += f[j];
+        }
+        uint32_t tot;
+        uint32_t o = carry + block_exclusive_scan<1024>(c, &tot, ws);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (e0 + j < tsize) {
+                rank[e0 + j] = o;
+                o += f[j];
+            }
+        carry += tot;
+    }
 }
 
 __global__ void table_occupied_kernel(const uint32_t* __restrict__ tcnt, uint32_t tsize, uint32_t* __restrict__ occ) {
@@ -1038,18 +1074,18 @@ LeaderInfo leader_info(Ctx* ctx, const DevDfa& d, cudaStream_t s) {
     const uint32_t init[4] = {kNone, kNone, 0, 0};
     DK_CUDA(cudaMemcpyAsync(info, init, sizeof(init), cudaMemcpyHostToDevice, s));
     DK_LAUNCH(ctx, leader_info_kernel, grid_for(d.n, kThreads, (unsigned)ctx->num_sms * 8u), kThreads, 0, s, d.acc,
-              d.n, info);
+              d.n, info, (uint8_t*)nullptr);
     LeaderInfo li;
     read_words(ctx, info, sizeof(li), &li, s);
     return li;
 }
 
-void leader_info_async(Ctx* ctx, const DevDfa& d, cudaStream_t s) {
+void leader_info_async(Ctx* ctx, const DevDfa& d, cudaStream_t s, uint8_t* dense2) {
     uint32_t* info = reinterpret_cast<uint32_t*>(ctx->dmailbox);
     DK_CUDA(cudaMemsetAsync(info, 0xff, 2 * sizeof(uint32_t), s));
     DK_CUDA(cudaMemsetAsync(info + 2, 0, 2 * sizeof(uint32_t), s));
     DK_LAUNCH(ctx, leader_info_kernel, grid_for(d.n, kThreads, (unsigned)ctx->num_sms * 8u), kThreads, 0, s, d.acc,
-              d.n, info);
+              d.n, info, dense2);
     DK_CUDA(cudaMemcpyAsync(ctx->mailbox + 56, info, sizeof(LeaderInfo), cudaMemcpyDeviceToHost, s));
     DK_CUDA(cudaEventRecord(ctx->info_ev, s));
 }
@@ -1192,8 +1228,13 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
     LeaderInfo li{};
     uint32_t B, A;
     uint64_t m;
+    bool dense8_ready = false;  // the first pass's byte key labels, written by the class-size kernel
     if (deferred_info) {
-        leader_info_async(ctx, d, s);
+        if (n < kBitLabelsMinStates) {
+            w.dense8.alloc(n, s);
+            dense8_ready = true;
+        }
+        leader_info_async(ctx, d, s, dense8_ready ? w.dense8.get() : nullptr);
         B = 2;  // the plan's assumption; corrected from the counts after the pass
         A = 2;
         m = n;
@@ -1308,10 +1349,10 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
                 kl = KeyLab{w.bits.get(), kBitLabels};
             } else if (B <= 2 && plan.strategy != kPlanChunked) {
                 if (!w.dense8.get()) w.dense8.alloc(n, s);
-                if (res.iters == 0)
-                    DK_LAUNCH(ctx, acc_dense2_kernel, grid_for(n), kThreads, 0, s, d.acc, n, w.dense8.get());
-                else
+                if (res.iters != 0)
                     DK_LAUNCH(ctx, dense2_kernel, grid_for(n), kThreads, 0, s, w.lab.get(), n, w.dense8.get());
+                else if (!dense8_ready)  // else written with the class sizes
+                    DK_LAUNCH(ctx, acc_dense2_kernel, grid_for(n), kThreads, 0, s, d.acc, n, w.dense8.get());
                 kl = KeyLab{w.dense8.get(), 1};
             } else {
                 kl = dense_keylab(plan.keylab_bytes);
@@ -1386,9 +1427,13 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
             const bool full = list == nullptr;
             if (full) {
                 if (w.trank.n < tsize) w.trank.alloc(tsize, s);
-                DK_LAUNCH(ctx, table_occupied_kernel, grid_for(tsize), kThreads, 0, s, w.tcnt.get(), (uint32_t)tsize,
-                          w.trank.get());
-                exclusive_scan_u32(ctx, w.trank.get(), w.trank.get(), tsize, nullptr, s);
+                if (tsize <= (1u << 14)) {
+                    DK_LAUNCH(ctx, table_rank_one_kernel, 1, 1024, 0, s, w.tcnt.get(), (uint32_t)tsize, w.trank.get());
+                } else {
+                    DK_LAUNCH(ctx, table_occupied_kernel, grid_for(tsize), kThreads, 0, s, w.tcnt.get(),
+                              (uint32_t)tsize, w.trank.get());
+                    exclusive_scan_u32(ctx, w.trank.get(), w.trank.get(), tsize, nullptr, s);
+                }
                 if (nbits <= 16 && !w.next16.get()) w.next16.alloc(n, s);
                 if (nbits > 16 && !w.next32.get()) w.next32.alloc(n, s);
             }
