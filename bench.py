@@ -582,6 +582,30 @@ def extras(dk, nat, ctx, torch, sharded, args):
     s, r = timed(u, 1)
     out["equiv_union_find_10M_equal"] = {"ms": s * 1000, "verdict": int(r.verdict), "unions": int(r.explored_states),
                                          "levels": int(r.levels), "pairs_per_s": int(r.explored_states) / s}
+    # ... and differing: B's flag flipped at the state 30 letters-0 from its
+    # initial state (so a counterexample of length <= 30 exists)
+    qb = int(init2.value)
+    for _ in range(30):
+        qb = int(d2[qb].item())
+    a2[qb] ^= 1
+    torch.cuda.synchronize()
+    for mode, name in ((0, "equivalence"), (1, "inclusion")):
+        res = nat.CProduct()
+
+        def h():
+            nat.check(nat.lib.dfakit_explore_product_device(ctx.handle, C.byref(va), C.byref(vb), mode, None, 1 << 32,
+                                                            cex.ctypes.data, len(cex), C.byref(res), ctx.stream))
+            return res
+
+        s, r = timed(h, 1)
+        out[f"{name}_naive_hk_10M_differing"] = {"ms": s * 1000, "verdict": int(r.verdict),
+                                                 "explored_pairs": int(r.explored_states), "levels": int(r.levels),
+                                                 "counterexample_len": int(r.counterexample_len),
+                                                 "pairs_per_s": int(r.explored_states) / s}
+    s, r = timed(u, 1)
+    out["equiv_union_find_10M_differing"] = {"ms": s * 1000, "verdict": int(r.verdict),
+                                             "unions": int(r.explored_states), "levels": int(r.levels),
+                                             "pairs_per_s": int(r.explored_states) / s}
     return out
 
 
