@@ -998,7 +998,12 @@ __global__ void __launch_bounds__(kThreads) small_persistent_kernel(SmallArgs A)
             atomicAdd(&A.tcnt[tb + sl], 1u);
         }
         grid.sync();
-        // counters + fingerprint verification
+        // counters + fingerprint verification.  Packed keys need no
+        // verification, so their relabel, survivor append and clearing of the
+        // other table happen in this sweep too (two barriers per pass instead
+        // of three): a fixed-point pass rewrites every label with itself and
+        // its appended list is never used.
+        const bool fused = A.field_bits != 0;
         uint32_t heads = 0, ablk = 0, surv = 0;
         bool clash = false;
         for (uint32_t i = tid; i < m; i += stride) {
@@ -1008,8 +1013,20 @@ __global__ void __launch_bounds__(kThreads) small_persistent_kernel(SmallArgs A)
             heads += head;
             ablk += head && multi;
             surv += multi;
-            if (!A.field_bits && !head && !same_tuple(q, r, A.delta, A.n, A.k, ArrLab<uint32_t>{A.lab})) clash = true;
+            if (fused) {
+                A.lab[q] = r;
+                const uint32_t at = warp_append(&c->listed, multi);
+                if (multi) next[at] = q;
+            } else if (!head && !same_tuple(q, r, A.delta, A.n, A.k, ArrLab<uint32_t>{A.lab})) {
+                clash = true;
+            }
         }
+        if (fused)
+            for (uint32_t e = tid; e <= T; e += stride) {
+                A.tkey[ob + e] = kEmptyKey;
+                A.trep[ob + e] = kNone;
+                A.tcnt[ob + e] = 0;
+            }
         if (__syncthreads_or(clash) && threadIdx.x == 0) atomicOr(&c->collision, 1u);
         flush_counters<kThreads>(heads, ablk, surv, &c->runs, &c->ablk, &c->surv);
         grid.sync();
@@ -1031,22 +1048,24 @@ __global__ void __launch_bounds__(kThreads) small_persistent_kernel(SmallArgs A)
         }
         // relabel + append survivors (order is free: keys carry the labels);
         // clear the other table for the next pass
-        if (!retry) {
-            uint32_t* listed = &c->listed;
-            for (uint32_t i = tid; i < m; i += stride) {
-                const uint32_t q = list[i], sl = A.slot[i];
-                A.lab[q] = __ldcg(&A.trep[sl]);
-                const bool multi = __ldcg(&A.tcnt[sl]) >= 2;
-                const uint32_t at = warp_append(listed, multi);
-                if (multi) next[at] = q;
+        if (!fused) {
+            if (!retry) {
+                uint32_t* listed = &c->listed;
+                for (uint32_t i = tid; i < m; i += stride) {
+                    const uint32_t q = list[i], sl = A.slot[i];
+                    A.lab[q] = __ldcg(&A.trep[sl]);
+                    const bool multi = __ldcg(&A.tcnt[sl]) >= 2;
+                    const uint32_t at = warp_append(listed, multi);
+                    if (multi) next[at] = q;
+                }
             }
+            for (uint32_t e = tid; e <= T; e += stride) {
+                A.tkey[ob + e] = kEmptyKey;
+                A.trep[ob + e] = kNone;
+                A.tcnt[ob + e] = 0;
+            }
+            grid.sync();
         }
-        for (uint32_t e = tid; e <= T; e += stride) {
-            A.tkey[ob + e] = kEmptyKey;
-            A.trep[ob + e] = kNone;
-            A.tcnt[ob + e] = 0;
-        }
-        grid.sync();
         if (retry) {
             ++s.collisions;
             ++s.strikes;
