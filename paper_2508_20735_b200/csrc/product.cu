@@ -4,9 +4,10 @@
 // explore_product: level-synchronous BFS over the synchronous product with
 // a lock-free open-addressing hash set of packed (qA, qB) pairs.  Each
 // 16-byte slot holds the key and a "discoverer" word (parent record << 32 |
-// letter); probing is tile-cooperative: 4 lanes inspect a 4-slot (64 B)
-// window per step with ballots for match / empty, and the leader claims an
-// empty slot with a 64-bit CAS.  Within a wave every (frontier record,
+// letter); every lane first tries its key's home slot alone, and keys that
+// collide continue with tile-cooperative probing: 4 lanes inspect a 4-slot
+// (64 B) window per step with ballots for match / empty, and the leader
+// claims an empty slot with a 64-bit CAS.  Within a wave every (frontier record,
 // letter) item atomicMin's its discoverer into the slot it reached, so the
 // minimum (parent, letter) -- the pair's position in the reference's
 // sequential insertion order -- wins.  A flag + exclusive scan then emits the
@@ -47,33 +48,53 @@ struct Rec {
 
 __device__ __forceinline__ uint64_t slot_hash(uint64_t key) { return mix64(key ^ 0x243F6A8885A308D3ull); }
 
-// Tile-cooperative find-or-insert of every lane's key.  Returns the slot of
-// this lane's key (kNone when !valid).
+// Find-or-insert of every lane's key.  Probe order is linear from the home
+// slot.  Each lane first inspects its home slot on its own (at the table's
+// load <= 1/2 that settles almost every key in one round trip, and the lanes'
+// round trips overlap); keys whose home slot holds another key continue
+// tile-cooperatively: 4 lanes inspect a 4-slot window (home + 1 ...) per step
+// with ballots for match / empty, and the leader claims an empty slot with a
+// 64-bit CAS.  Slots only go empty -> full, so scanning in one fixed order and
+// claiming the first empty slot never inserts a key twice.  Returns the slot
+// of this lane's key (kNone when !valid).
 __device__ uint32_t tile_find_or_insert(cg::thread_block_tile<kTile> tile, bool valid, unsigned long long key,
                                         Slot* __restrict__ table, uint64_t mask) {
     uint32_t mine = kNone;
+    bool open = false;
+    if (valid) {
+        const uint64_t home = slot_hash(key) & mask;
+        unsigned long long e = __ldcg(&table[home].key);
+        if (e == kEmpty) e = atomicCAS(&table[home].key, kEmpty, key);
+        if (e == kEmpty || e == key)
+            mine = (uint32_t)home;
+        else
+            open = true;
+    }
+    if (!tile.any(open)) return mine;
     const unsigned lane = tile.thread_rank();
     for (int j = 0; j < kTile; ++j) {
+        if (!tile.shfl(open, j)) continue;
         const unsigned long long kj = tile.shfl(key, j);
-        const bool vj = tile.shfl(valid, j);
-        if (!vj) continue;
-        uint64_t base = slot_hash(kj) & mask & ~(uint64_t)(kTile - 1);
+        uint64_t base = (slot_hash(kj) + 1) & mask;
         uint32_t found = kNone;
         for (;;) {
-            const unsigned long long e = __ldcg(&table[base + lane].key);
+            const uint64_t sl = (base + lane) & mask;
+            const unsigned long long e = __ldcg(&table[sl].key);
             const unsigned match = tile.ballot(e == kj);
-            if (match) {
-                found = (uint32_t)(base + __ffs(match) - 1);
-                break;
-            }
             const unsigned empty = tile.ballot(e == kEmpty);
-            if (empty) {
-                const unsigned leader = __ffs(empty) - 1;
+            // the first slot in probe order that holds kj or is empty
+            const unsigned hit = match | empty;
+            if (hit) {
+                const unsigned first = __ffs(hit) - 1;
+                if (match & (1u << first)) {
+                    found = (uint32_t)((base + first) & mask);
+                    break;
+                }
                 unsigned long long old = 0;
-                if (lane == leader) old = atomicCAS(&table[base + leader].key, kEmpty, kj);
-                old = tile.shfl(old, leader);
+                if (lane == first) old = atomicCAS(&table[(base + first) & mask].key, kEmpty, kj);
+                old = tile.shfl(old, first);
                 if (old == kEmpty || old == kj) {
-                    found = (uint32_t)(base + leader);
+                    found = (uint32_t)((base + first) & mask);
                     break;
                 }
                 continue;  // lost the slot to another key: re-read the window
@@ -582,10 +603,11 @@ ProductOut explore_product_device(Ctx* ctx, const DevDfa& a, const DevDfa& b, in
         const uint64_t items = (we - wb) * k;
         const uint64_t need = next_pow2(2 * (we + items) + 64);
         if (need > cap) {
-            // first allocation sized for 2 max(nA, nB) pairs (the usual size of
-            // an equivalence product; bounded by the visited budget), so most
-            // explorations run in one launch without re-insertion
-            const uint64_t guess = next_pow2(2 * std::min<uint64_t>(max_visited, 2ull * std::max(a.n, b.n)) + 64);
+            // first allocation sized for max(nA, nB) pairs at load 1/2 (the
+            // usual size of an equivalence product; bounded by the visited
+            // budget), so most explorations run in one launch without
+            // re-insertion, and the table initialisation stays small
+            const uint64_t guess = next_pow2(2 * std::min<uint64_t>(max_visited, std::max(a.n, b.n)) + 64);
             const uint64_t nc = cap ? std::max<uint64_t>(need, cap * 4)
                                     : std::max<uint64_t>(need, std::max<uint64_t>(1ull << 20, guess));
             table.alloc(nc, s);

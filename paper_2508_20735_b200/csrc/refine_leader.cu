@@ -437,14 +437,13 @@ unsigned coop_grid(Ctx* ctx, const void* kernel, uint32_t n) {
 }
 
 // Alg. 5 l.7: delta^T(q, a^(2^i)) = delta^T(delta^T(q, a^(2^(i-1))), a^(2^(i-1)))
-__global__ void double_kernel(uint32_t* __restrict__ out, uint32_t n, uint32_t k, uint32_t levels, uint32_t level) {
-    const uint64_t total = (uint64_t)k * n;
-    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total;
-         t += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t a = (uint32_t)(t / n), q = (uint32_t)(t % n);
-        const uint32_t* prev = out + ((uint64_t)a * levels + level - 1) * n;
-        out[((uint64_t)a * levels + level) * n + q] = prev[prev[q]];
-    }
+// (blockIdx.y = letter; no per-element division)
+__global__ void double_kernel(uint32_t* __restrict__ out, uint32_t n, uint32_t levels, uint32_t level, uint32_t a0) {
+    const uint32_t a = a0 + blockIdx.y;
+    const uint32_t* __restrict__ prev = out + ((uint64_t)a * levels + level - 1) * n;
+    uint32_t* __restrict__ dst = out + ((uint64_t)a * levels + level) * n;
+    for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x)
+        __stcs(dst + q, __ldg(prev + __ldcs(prev + q)));
 }
 
 RefineResult single_block(Ctx* ctx, uint32_t n, uint32_t* block_out, cudaStream_t s) {
@@ -587,7 +586,11 @@ void transitive_alphabet_device(Ctx* ctx, const DevDfa& d, uint32_t* out, cudaSt
         DK_CUDA(cudaMemcpyAsync(out + (uint64_t)a * levels * n, d.delta + (uint64_t)a * n, (size_t)n * sizeof(uint32_t),
                                 cudaMemcpyDeviceToDevice, s));
     for (uint32_t lv = 1; lv < levels; ++lv)
-        DK_LAUNCH_B(ctx, 12.0 * k * n, double_kernel, grid_for((uint64_t)k * n), kThreads, 0, s, out, n, k, levels, lv);
+        for (uint32_t a0 = 0; a0 < k; a0 += 65535u) {
+            const uint32_t ka = std::min(k - a0, 65535u);
+            DK_LAUNCH_B(ctx, 12.0 * ka * n, double_kernel, dim3(grid_for(n, kThreads, 148u * 16u), ka), kThreads, 0, s,
+                        out, n, levels, lv, a0);
+        }
 }
 
 RefineResult trans_pr_device(Ctx* ctx, const DevDfa& d, int policy, uint64_t seed, uint64_t max_transitions,
