@@ -195,8 +195,11 @@ def test_config0_random_1M_k2(dk, oracle):
     """BASELINE configs[0]: random complete DFA, 1M states, |Sigma|=2."""
     t = oracle.gen_random(1_000_000, 2, 0.5, 7)
     want = oracle.minimize("moore", t[0], t[1])
-    rep = dk.sort_pr(mkdfa(dk, t))
+    dfa = mkdfa(dk, t)
+    rep = dk.sort_pr(dfa)
     assert same(rep, want)
+    # the literal radix-sort grouping over ~330 sort tiles per digit (look-back chains)
+    assert same(dk.sort_pr(dfa, grouping="radix_sort"), want)
 
 
 @pytest.mark.slow

@@ -12,7 +12,7 @@ run() {  # name regex count skip workload-args...
 }
 run sort 'sig_table_kernel|sig_bucket_kernel|bucket_group_kernel|table_apply_vec_kernel|tile_apply_kernel|tile_count_kernel|acc_dense2_kernel|iota_kernel|leader_info_kernel|table_occupied_kernel' 12 0 --workload synth --reps 1
 cp /tmp/prof/sort.ncu-rep gpurun_out/prof_sort.ncu-rep
-run radix 'signature_kernel|radix_hist_kernel|radix_scatter_kernel|run_heads_kernel|run_apply_kernel|run_min_kernel|verify_runs_kernel' 14 0 --workload radix --reps 1
+run radix 'signature_kernel|radix_hist_all_kernel|radix_onesweep_kernel|radix_bins_kernel|run_heads_kernel|run_apply_kernel|run_min_kernel|verify_runs_kernel' 14 0 --workload radix --reps 1
 run naive 'naive_persistent_kernel|fused_persistent_kernel' 2 0 --workload naive
 run chain 'double_kernel|naive_persistent_kernel' 6 0 --workload chain --reps 1
 cp /tmp/prof/chain.ncu-rep gpurun_out/prof_chain.ncu-rep

@@ -25,6 +25,7 @@ def main():
     p.add_argument("--param", type=int, default=19)
     p.add_argument("--algo", default=None)
     p.add_argument("--reps", type=int, default=3)
+    p.add_argument("--grouping", type=int, default=0, help="dfakit_options.grouping (1 = radix_sort)")
     a = p.parse_args()
     import torch
     import paper_2508_20735_b200 as dk
@@ -55,7 +56,7 @@ def main():
 
     def run():
         rep = nat.CReport()
-        opts = nat.COptions(0, 0, 0, 1 << 40, 1 << 24, 64, 0)
+        opts = nat.COptions(0, 0, 0, 1 << 40, 1 << 24, 64, a.grouping)
         nat.check(nat.lib.dfakit_minimize_device(ctx.handle, C.byref(view), int(dk.Algorithm[algo]), C.byref(opts),
                                                  out.data_ptr(), C.byref(rep), ctx.stream))
         return rep
