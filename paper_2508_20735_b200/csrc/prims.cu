@@ -351,7 +351,8 @@ uint32_t canonical_from_min_labels(Ctx* ctx, const uint32_t* lab, uint64_t n, ui
 //      digit's output run.  Keys and values are read once and written once
 //      per digit: no separate histogram or scan pass.
 // Look-back words are 64-bit {tag:24 | flag:8 | count:32}; the tag is the
-// digit pass (+1), so one memset per sort clears every pass's words.
+// digit pass (+1), so the passes share one array, zeroed once per sort: a
+// word left by the previous pass reads as "not yet published".
 // ---------------------------------------------------------------------------
 
 constexpr int kRadixBits = 8;
@@ -535,7 +536,7 @@ bool radix_sort_pairs_range(Ctx* ctx, RadixBuffers b, uint64_t m, uint32_t bit_l
     // [hist: passes x 256][tile counters: passes] then the look-back words
     const size_t small = (size_t)passes * kRadix + passes;
     const size_t small_words = (small + 1) / 2 * 2;  // 8-byte alignment of the look-back words
-    const size_t bytes = small_words * 4 + (size_t)passes * tiles * kRadix * 8;
+    const size_t bytes = small_words * 4 + (size_t)tiles * kRadix * 8;  // look-back words shared by the passes
     DBuf<unsigned char> scratch(bytes, s);
     DK_CUDA(cudaMemsetAsync(scratch.get(), 0, bytes, s));
     uint32_t* hist = reinterpret_cast<uint32_t*>(scratch.get());
@@ -552,7 +553,7 @@ bool radix_sort_pairs_range(Ctx* ctx, RadixBuffers b, uint64_t m, uint32_t bit_l
         uint64_t* kout = flipped ? b.k0 : b.k1;
         uint32_t* vout = flipped ? b.v0 : b.v1;
         DK_LAUNCH_B(ctx, 24.0 * m, radix_onesweep_kernel<kLookWin>, tiles, kSortThreads, sizeof(OnesweepSmem), s, kin, vin, m,
-                    shift, hist + (size_t)p * kRadix, look + (size_t)p * tiles * kRadix, ctr + p, p + 1, kout, vout);
+                    shift, hist + (size_t)p * kRadix, look, ctr + p, p + 1, kout, vout);
         flipped = !flipped;
     }
     return flipped;
