@@ -453,16 +453,15 @@ __global__ void __launch_bounds__(kSortThreads, 3) radix_onesweep_kernel(
         const bool valid = i < m;
         const unsigned vmask = __ballot_sync(0xffffffffu, valid);
         const uint32_t d = digit_of(key[j], shift);
-        uint32_t r = 0;
-        unsigned peers = 0;
-        if (valid) {
-            peers = __match_any_sync(vmask, d);
-            r = sm.warp_hist[wid][d] + (uint32_t)__popc(peers & lt_mask);
-        }
-        __syncwarp();
-        if (valid && lane == (unsigned)(__ffs(peers) - 1)) sm.warp_hist[wid][d] += (uint32_t)__popc(peers);
-        __syncwarp();
-        rank[j] = valid ? r : kNone;
+        // the lowest lane of each digit group bumps the warp's counter of
+        // the digit (one shared atomic round trip); its peers read the old
+        // count from it
+        const unsigned peers = valid ? __match_any_sync(vmask, d) : 0u;
+        const unsigned leader = valid ? (unsigned)(__ffs(peers) - 1) : lane;
+        uint32_t base = 0;
+        if (valid && lane == leader) base = atomicAdd(&sm.warp_hist[wid][d], (uint32_t)__popc(peers));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        rank[j] = valid ? base + (uint32_t)__popc(peers & lt_mask) : kNone;
     }
     __syncthreads();
     uint32_t tile_count = 0;

@@ -21,6 +21,7 @@
 // when its union succeeds.
 #include <cooperative_groups.h>
 
+#include <cstdlib>
 #include <vector>
 
 #include "prims.cuh"
@@ -596,6 +597,16 @@ ProductOut explore_product_device(Ctx* ctx, const DevDfa& a, const DevDfa& b, in
     uint64_t wb = 0, we = 1;
     DBuf<uint8_t> item_win;
     DBuf<unsigned long long> item_key;
+    // first table: 2^20 slots at least.  DFAKIT_TEST_TABLE_LOG2=<b> (tests
+    // only) starts at 2^b slots sized for nothing, so small explorations run
+    // at load up to 1/2 -- home-slot collisions, the tile-cooperative
+    // windows, growth and re-insertion all happen
+    uint64_t min_slots = 1ull << 20;
+    bool tiny = false;
+    if (const char* t = getenv("DFAKIT_TEST_TABLE_LOG2")) {
+        min_slots = 1ull << std::min(30, std::max(4, atoi(t)));
+        tiny = true;
+    }
     for (;;) {
         // room for the next level: table at load <= 1/2; the record store and
         // the item buffers are sized with the table (cap / 2 each), so the
@@ -607,9 +618,10 @@ ProductOut explore_product_device(Ctx* ctx, const DevDfa& a, const DevDfa& b, in
             // usual size of an equivalence product; bounded by the visited
             // budget), so most explorations run in one launch without
             // re-insertion, and the table initialisation stays small
-            const uint64_t guess = next_pow2(2 * std::min<uint64_t>(max_visited, std::max(a.n, b.n)) + 64);
+            const uint64_t guess =
+                tiny ? 0 : next_pow2(2 * std::min<uint64_t>(max_visited, std::max(a.n, b.n)) + 64);
             const uint64_t nc = cap ? std::max<uint64_t>(need, cap * 4)
-                                    : std::max<uint64_t>(need, std::max<uint64_t>(1ull << 20, guess));
+                                    : std::max<uint64_t>(need, std::max<uint64_t>(min_slots, guess));
             table.alloc(nc, s);
             cap = nc;
             DK_CUDA(cudaMemsetAsync(table.get(), 0xff, cap * sizeof(Slot), s));

@@ -55,6 +55,33 @@ def test_random_products_vs_oracle(dk, oracle):
             assert accepts(A, u.counterexample) != accepts(B, u.counterexample)
 
 
+def test_products_through_table_collisions(dk, oracle, monkeypatch):
+    """A 64-slot first table (test hook): explorations run at load up to 1/2,
+    so keys collide on their home slots and go through the tile-cooperative
+    windows, and the table grows and re-inserts the records; results must
+    not change."""
+    ctx = dk.default_context()
+    A = oracle.gen_random(3000, 2, 0.5, 1)
+    da = mkdfa(dk, A)
+    l0 = ctx.kernel_launches
+    dk.explore_product(da, da, dk.ExploreMode["full"])
+    plain = ctx.kernel_launches - l0
+    monkeypatch.setenv("DFAKIT_TEST_TABLE_LOG2", "6")
+    l0 = ctx.kernel_launches
+    r = dk.explore_product(da, da, dk.ExploreMode["full"])
+    assert same(r, oracle.explore("full", A, A))
+    assert ctx.kernel_launches - l0 > plain + 2  # the 64-slot table grew: re-insertions, relaunches
+    g = random.Random(77)
+    for i in range(40):
+        na, nb, k = g.randint(20, 800), g.randint(20, 800), g.randint(1, 4)
+        frac = g.randint(1, 9) / 10
+        A = oracle.gen_random(na, k, frac, g.getrandbits(64))
+        B = A if i % 3 == 0 else oracle.gen_random(nb, k, frac, g.getrandbits(64))
+        da, db = mkdfa(dk, A), mkdfa(dk, B)
+        for mode in ("equivalence", "inclusion", "full"):
+            assert same(dk.explore_product(da, db, dk.ExploreMode[mode]), oracle.explore(mode, A, B)), (i, mode)
+
+
 def test_acceptance_product_sizes(dk, oracle, golden):
     """Acceptance criteria 5 and 6 (Table 4 / Table 5 state counts)."""
     acc = golden["acceptance"]
