@@ -420,6 +420,8 @@ def run_b200(args, rank, world, local):
     e2e_transitions = transitions * (1 if sharded_engine else world)
     e2e = {"value": e2e_transitions / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
            "ms_per_step": e2e_s * 1000.0, "api": api}
+    if rank == 0:
+        e2e["pcie"] = pcie_bound(torch, h_delta, delta, h_blocks, blocks, h2d, d2h, e2e_s)
 
     cfg = {"workload": workload_name(n, k, world if sharded_engine else 1), "states": n, "alphabet": k,
            "transitions": n * k, "algorithm": "sort_pr", "engine": engine, "passes": passes,
@@ -450,6 +452,31 @@ def run_b200(args, rank, world, local):
         print(json.dumps(line), flush=True)
     if use_dist:
         dist.destroy_process_group()
+
+
+def pcie_bound(torch, h_in, d_in, h_out, d_out, h2d, d2h, e2e_s):
+    """The e2e step's transfer floor, measured in the same run: plain pinned
+    copies of the step's input (H2D) and result (D2H) buffers, CUDA events on
+    a side stream.  ms_floor = the step's bytes at those rates; frac = floor /
+    e2e step time (how much of the e2e step is the PCIe link itself)."""
+    s = torch.cuda.Stream()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    best_in = best_out = float("inf")
+    with torch.cuda.stream(s):
+        for _ in range(3):
+            ev[0].record(s)
+            d_in.copy_(h_in, non_blocking=True)
+            ev[1].record(s)
+            h_out.copy_(d_out, non_blocking=True)
+            ev[2].record(s)
+            ev[2].synchronize()
+            best_in = min(best_in, ev[0].elapsed_time(ev[1]))
+            best_out = min(best_out, ev[1].elapsed_time(ev[2]))
+    h2d_gbps = h_in.numel() * h_in.element_size() / (best_in / 1000.0) / 1e9
+    d2h_gbps = h_out.numel() * h_out.element_size() / (best_out / 1000.0) / 1e9
+    floor_ms = (h2d / h2d_gbps + d2h / d2h_gbps) / 1e6
+    return {"h2d_GBps": h2d_gbps, "d2h_GBps": d2h_gbps, "transfer_floor_ms": floor_ms,
+            "frac_of_e2e_step": floor_ms / (e2e_s * 1000.0)}
 
 
 def extras(dk, nat, ctx, torch, sharded, args):
