@@ -851,6 +851,133 @@ __global__ void __launch_bounds__(kThreads) run_apply_kernel(const uint32_t* __r
     flush_counters<kThreads>(0u, ablk, surv, &ctr->runs, &ctr->active_blocks, &ctr->active_states);
 }
 
+// Run labels in one pass, for a stably sorted (key, state) sequence whose
+// states were increasing before the sort (the pass's list was): inside a run
+// of equal keys the states are still increasing, so the run minimum -- the
+// new min-state label of the run's block -- is the state at the run head.
+// Every element takes the state of the nearest head at or before it; the
+// elements of a tile that continue a run from earlier tiles get its head
+// state by decoupled look-back (a tile with a head publishes the state of its
+// last head at once; a tile without one publishes "transparent" and, once
+// resolved, the state it carried).  Replaces heads + scan + run starts + run
+// minima + apply (8 launches, 5 full passes) of the general path.
+constexpr int kRunItems = 8;
+constexpr int kRunTile = kThreads * kRunItems;
+constexpr unsigned long long kRunAgg = 1ull, kRunPre = 2ull;
+
+__global__ void __launch_bounds__(kThreads) run_label_kernel(const uint64_t* __restrict__ keys,
+                                                             const uint32_t* __restrict__ vals, uint64_t m,
+                                                             unsigned long long* __restrict__ look,
+                                                             uint32_t* __restrict__ tile_ctr,
+                                                             uint32_t* __restrict__ lab, uint8_t* __restrict__ keep,
+                                                             uint8_t* __restrict__ act,
+                                                             IterCounters* __restrict__ ctr) {
+    __shared__ uint32_t s_tile, s_carry;
+    __shared__ uint32_t s_has[kThreads / 32], s_val[kThreads / 32];
+    const unsigned lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+    if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    const uint64_t i0 = (uint64_t)tile * kRunTile + (uint64_t)threadIdx.x * kRunItems;
+    uint64_t key[kRunItems + 2];  // [0] = element i0 - 1, [kRunItems + 1] = element i0 + kRunItems
+    uint32_t val[kRunItems];
+#pragma unroll
+    for (int j = 0; j < kRunItems + 2; ++j) {
+        const uint64_t i = i0 + j - 1;
+        key[j] = (j == 0 && i0 == 0) || i >= m ? ~0ull : __ldcs(keys + i);
+    }
+#pragma unroll
+    for (int j = 0; j < kRunItems; ++j) val[j] = i0 + j < m ? __ldcs(vals + i0 + j) : 0u;
+    uint32_t head_mask = 0, multi_mask = 0, has = 0, last = 0;
+#pragma unroll
+    for (int j = 0; j < kRunItems; ++j) {
+        const uint64_t i = i0 + j;
+        if (i >= m) break;
+        const bool head = i == 0 || key[j + 1] != key[j];
+        const bool multi = (i > 0 && key[j] == key[j + 1]) || (i + 1 < m && key[j + 2] == key[j + 1]);
+        if (head) {
+            head_mask |= 1u << j;
+            has = 1;
+            last = val[j];
+        }
+        if (multi) multi_mask |= 1u << j;
+    }
+    // exclusive "last head before me" over the lanes, then over the warps
+    uint32_t c_has = 0, c_val = 0;
+    {
+        uint32_t h = has, v = last;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t hh = __shfl_up_sync(0xffffffffu, h, o), vv = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= (unsigned)o && !h) {
+                h = hh;
+                v = vv;
+            }
+        }
+        c_has = __shfl_up_sync(0xffffffffu, h, 1);
+        c_val = __shfl_up_sync(0xffffffffu, v, 1);
+        if (lane == 0) c_has = 0;
+        if (lane == 31) {
+            s_has[wid] = h;
+            s_val[wid] = v;
+        }
+    }
+    __syncthreads();
+    if (!c_has) {
+        for (int w = (int)wid - 1; w >= 0; --w)
+            if (s_has[w]) {
+                c_has = 1;
+                c_val = s_val[w];
+                break;
+            }
+    }
+    if (threadIdx.x == 0) {
+        uint32_t t_has = 0, t_val = 0;
+        for (int w = kThreads / 32 - 1; w >= 0; --w)
+            if (s_has[w]) {
+                t_has = 1;
+                t_val = s_val[w];
+                break;
+            }
+        volatile unsigned long long* lk = look;
+        if (t_has) lk[tile] = (kRunPre << 32) | t_val;
+        else lk[tile] = kRunAgg << 32;
+        // the carry into this tile (needed unless the tile starts with a head)
+        uint32_t carry = 0;
+        if (tile > 0 && (head_mask & 1u) == 0) {
+            for (int64_t t = (int64_t)tile - 1; t >= 0;) {
+                const unsigned long long v = lk[t];
+                const unsigned long long f = v >> 32;
+                if (f == 0) continue;  // not published yet
+                if (f == kRunPre) {
+                    carry = (uint32_t)v;
+                    break;
+                }
+                --t;  // transparent: no head there
+            }
+            if (!t_has) lk[tile] = (kRunPre << 32) | carry;  // resolved: later tiles stop here
+        }
+        s_carry = carry;
+    }
+    __syncthreads();
+    uint32_t hv = c_has ? c_val : s_carry;
+    uint32_t nh = 0, ab = 0, sv = 0;
+#pragma unroll
+    for (int j = 0; j < kRunItems; ++j) {
+        const uint64_t i = i0 + j;
+        if (i >= m) break;
+        const bool head = (head_mask >> j) & 1u, multi = (multi_mask >> j) & 1u;
+        if (head) hv = val[j];
+        lab[val[j]] = hv;
+        if (keep) keep[i] = multi;
+        if (act && multi) act[val[j]] = 1;  // act was zeroed
+        nh += head;
+        ab += head && multi;
+        sv += multi;
+    }
+    flush_counters<kThreads>(nh, ab, sv, &ctr->runs, &ctr->active_blocks, &ctr->active_states);
+}
+
 // chunked exact refinement: run index of every sorted element becomes the
 // leading field of the next chunk's key
 __global__ void run_index_kernel(const uint32_t* __restrict__ heads, const uint32_t* __restrict__ pos, uint64_t m,
@@ -1287,6 +1414,10 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
     const uint64_t fp_mask = o.fingerprint_bits >= 64 ? ~0ull : ((1ull << o.fingerprint_bits) - 1ull);
     uint32_t collisions_this_pass = 0;
     bool all_survive = false;
+    // the active list is in increasing state order (identity, flag
+    // compactions in state order, and order-preserving table compactions);
+    // lists in bucket-slot or sorted order clear it
+    bool list_inc = true;
 
     auto dense_keylab = [&](int bytes) -> KeyLab {
         void* p;
@@ -1347,6 +1478,7 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
             // three collisions: the host engine takes the pass
             list = sr.list_out;
             if (list == list_alt) std::swap(list_buf, list_alt);
+            list_inc = false;
             collisions_this_pass = 3;
         }
         ++res.passes;
@@ -1568,6 +1700,7 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
                 DK_LAUNCH_B(ctx, (double)m * 13.0, slot_apply_kernel, grid_for(bspace + c.overflow), kThreads, 0, s,
                             w.bcnt.get(), nb, c.overflow, w.bent.get(), w.rep_slot.get(), w.keep_slot.get(),
                             w.lab.get(), state_order ? w.act.get() : nullptr);
+            list_inc = state_order;
             if (c.active_states) {
                 if (state_order) compact_flags(ctx, nullptr, w.act.get(), n, dst, &dctr->listed, s);
                 else {
@@ -1651,11 +1784,6 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
                     cur_bits = bits_for(m - 1);
                 }
             }
-            DK_LAUNCH(ctx, run_heads_kernel, g, kThreads, 0, s, skeys, m, w.heads.get());
-            exclusive_scan_u32(ctx, w.heads.get(), w.pos.get(), m, &dctr->runs, s);
-            DK_LAUNCH(ctx, run_starts_kernel, g, kThreads, 0, s, w.heads.get(), w.pos.get(), m, w.run_start.get());
-            DK_CUDA(cudaMemsetAsync(w.scratch.get(), 0xff, m * sizeof(uint32_t), s));
-            DK_LAUNCH(ctx, run_min_kernel, g, kThreads, 0, s, w.heads.get(), w.pos.get(), svals, m, w.scratch.get());
             // big passes flag survivors per state so the next list is increasing
             // (coalesced delta rows); small ones keep the sorted order
             const bool state_order = m >= (uint64_t)n / 16;
@@ -1663,9 +1791,27 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
                 if (!w.act.get()) w.act.alloc(n, s);
                 DK_CUDA(cudaMemsetAsync(w.act.get(), 0, n, s));
             }
-            DK_LAUNCH_B(ctx, 25.0 * m, run_apply_kernel, g, kThreads, 0, s, w.heads.get(), w.pos.get(), svals, m,
-                        w.run_start.get(), w.scratch.get(), w.lab.get(), w.keep.get(),
-                        state_order ? w.act.get() : nullptr, dctr);
+            if (!chunked && list_inc) {
+                // states entered the sort increasing: each run's minimum is its head
+                const uint64_t tiles = (m + kRunTile - 1) / kRunTile;
+                DBuf<unsigned long long> look(tiles + 1, s);  // look-back words + the tile counter
+                DK_CUDA(cudaMemsetAsync(look.get(), 0, (tiles + 1) * 8, s));
+                DK_LAUNCH_B(ctx, 17.0 * m, run_label_kernel, (unsigned)tiles, kThreads, 0, s, skeys, svals, m,
+                            look.get(), reinterpret_cast<uint32_t*>(look.get() + tiles), w.lab.get(),
+                            state_order ? nullptr : w.keep.get(), state_order ? w.act.get() : nullptr, dctr);
+            } else {
+                DK_LAUNCH(ctx, run_heads_kernel, g, kThreads, 0, s, skeys, m, w.heads.get());
+                exclusive_scan_u32(ctx, w.heads.get(), w.pos.get(), m, &dctr->runs, s);
+                DK_LAUNCH(ctx, run_starts_kernel, g, kThreads, 0, s, w.heads.get(), w.pos.get(), m,
+                          w.run_start.get());
+                DK_CUDA(cudaMemsetAsync(w.scratch.get(), 0xff, m * sizeof(uint32_t), s));
+                DK_LAUNCH(ctx, run_min_kernel, g, kThreads, 0, s, w.heads.get(), w.pos.get(), svals, m,
+                          w.scratch.get());
+                DK_LAUNCH_B(ctx, 25.0 * m, run_apply_kernel, g, kThreads, 0, s, w.heads.get(), w.pos.get(), svals, m,
+                            w.run_start.get(), w.scratch.get(), w.lab.get(), w.keep.get(),
+                            state_order ? w.act.get() : nullptr, dctr);
+            }
+            list_inc = state_order;
             if (state_order) compact_flags(ctx, nullptr, w.act.get(), n, dst, &dctr->listed, s);
             else compact_flags(ctx, svals, w.keep.get(), m, dst, &dctr->listed, s);
             read_words(ctx, dctr, sizeof(c), &c, s);
