@@ -170,3 +170,38 @@ def test_large_equal_and_differing_pairs(dk, oracle):
     assert same(r, o) and r.verdict == dk.Verdict.counterexample
     r = dk.check_inclusion(mkdfa(dk, A), mkdfa(dk, C))
     assert same(r, oracle.explore("inclusion", A, C))
+
+
+@pytest.mark.slow
+def test_config3_full_size_10M(dk, oracle):
+    """BASELINE configs[3] at full size, the bench's shape: a 10M-state DFA
+    over two letters against a relabelled copy (equal: ~8M product pairs, 42
+    levels) and against the copy with the accepting bit flipped at the state
+    30 letters-0 from the initial state (differing).  Verdict, explored pairs,
+    levels and counterexample word identical to the oracle's."""
+    n, k = 10_000_000, 2
+    d, a, _ = oracle.gen_synth(n, k, 11)
+    perm = np.random.default_rng(5).permutation(n).astype(np.uint32)
+    d2 = np.empty_like(d)
+    for l in range(k):
+        d2[l][perm] = perm[d[l]]
+    a2 = np.empty_like(a)
+    a2[perm] = a
+    A, B = (d, a, 0), (d2, a2, int(perm[0]))
+    da, db = mkdfa(dk, A), mkdfa(dk, B)
+    for mode in ("equivalence", "inclusion"):
+        r = dk.explore_product(da, db, dk.ExploreMode[mode])
+        assert same(r, oracle.explore(mode, A, B)), mode
+    assert dk.check_equiv_uf(da, db).verdict == dk.Verdict.equivalent
+    q = int(perm[0])
+    for _ in range(30):
+        q = int(d2[0][q])
+    a3 = a2.copy()
+    a3[q] ^= 1
+    C = (d2, a3, int(perm[0]))
+    dc = mkdfa(dk, C)
+    for mode in ("equivalence", "inclusion"):
+        r = dk.explore_product(da, dc, dk.ExploreMode[mode])
+        assert same(r, oracle.explore(mode, A, C)), mode
+    u = dk.check_equiv_uf(da, dc)
+    assert u.verdict == dk.Verdict.counterexample and accepts(A, u.counterexample) != accepts(C, u.counterexample)
