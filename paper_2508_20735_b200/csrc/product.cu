@@ -413,7 +413,9 @@ __global__ void __launch_bounds__(kThreads) bfs_persistent_kernel(BfsArgs A) {
             run += tot;
         }
         grid.sync();
-        const uint32_t ff = *(volatile uint32_t*)&st->fail[par];
+        if (threadIdx.x == 0) red[0] = *(volatile uint32_t*)&st->fail[par];  // one read per CTA
+        __syncthreads();
+        const uint32_t ff = red[0];
         if (ff != kNone && A.mode != DFAKIT_MODE_FULL) {
             if (we + ff >= A.max_visited) {
                 status = kBfsBudget;
@@ -456,6 +458,7 @@ struct UfArgs {
 };
 
 __global__ void __launch_bounds__(kThreads) uf_persistent_kernel(UfArgs A) {
+    __shared__ uint32_t s_bc[2];
     cg::grid_group grid = cg::this_grid();
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     const uint64_t gtid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
@@ -479,10 +482,15 @@ __global__ void __launch_bounds__(kThreads) uf_persistent_kernel(UfArgs A) {
         }
         grid.sync();
         ++levels;
-        if (*(volatile uint32_t*)A.fail_rec != kNone) break;
+        if (threadIdx.x == 0) {  // one read per CTA
+            s_bc[0] = *(volatile uint32_t*)A.fail_rec;
+            s_bc[1] = *(volatile uint32_t*)A.count;
+        }
+        __syncthreads();
+        if (s_bc[0] != kNone) break;
         wb = we;
-        we = *(volatile uint32_t*)A.count;
-        grid.sync();  // every thread has read count before the next level appends
+        we = s_bc[1];
+        grid.sync();  // every CTA has read count before the next level appends
     }
     if (gtid == 0) {
         A.out[0] = levels;

@@ -143,6 +143,7 @@ __global__ void __launch_bounds__(kThreads)
                             unsigned long long* __restrict__ slot, uint32_t* __restrict__ split_list,
                             uint32_t* __restrict__ cnt, int policy, uint64_t seed, PersistOut* __restrict__ out) {
     __shared__ uint32_t cta_cnt[2];
+    __shared__ uint32_t s_total;
     auto sync_all = [] { cg::this_grid().sync(); };
     const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
     const uint32_t seg = (n + stride - 1) / stride * blockDim.x;
@@ -170,7 +171,11 @@ __global__ void __launch_bounds__(kThreads)
         const uint32_t mine = *(volatile uint32_t*)cc;
         if (threadIdx.x == 0 && mine) atomicAdd(c, mine);
         sync_all();
-        const uint32_t total = *(volatile uint32_t*)c;
+        // one read per CTA, shared through shared memory: every thread
+        // reading the counter put thousands of warp requests on one L2 slice
+        if (threadIdx.x == 0) s_total = *(volatile uint32_t*)c;
+        __syncthreads();
+        const uint32_t total = s_total;
         if (total == 0) break;
         if (tid == 0) cnt[(pass + 1) & 1] = 0;
         for (uint32_t i = threadIdx.x; i < mine; i += blockDim.x) {
@@ -194,6 +199,7 @@ __global__ void __launch_bounds__(kThreads) fused_persistent_kernel(const uint32
                                                                     uint32_t* __restrict__ cnt,
                                                                     PersistOut* __restrict__ out) {
     __shared__ uint32_t red[kThreads / 32];
+    __shared__ uint32_t s_total;
     cg::grid_group grid = cg::this_grid();
     const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
     uint64_t pass = 0;
@@ -228,7 +234,9 @@ __global__ void __launch_bounds__(kThreads) fused_persistent_kernel(const uint32
             if (t) atomicAdd(c, t);
         }
         grid.sync();
-        if (*(volatile uint32_t*)c == 0) break;
+        if (threadIdx.x == 0) s_total = *(volatile uint32_t*)c;  // one read per CTA
+        __syncthreads();
+        if (s_total == 0) break;
     }
     if (tid == 0) *out = PersistOut{(uint32_t)(pass + 1), (uint32_t)pass};
 }

@@ -1157,11 +1157,17 @@ __global__ void __launch_bounds__(kThreads) small_persistent_kernel(SmallArgs A)
         if (__syncthreads_or(clash) && threadIdx.x == 0) atomicOr(&c->collision, 1u);
         flush_counters<kThreads>(heads, ablk, surv, &c->runs, &c->ablk, &c->surv);
         grid.sync();
-        PersistCtr cv;
-        cv.runs = __ldcg(&c->runs);
-        cv.ablk = __ldcg(&c->ablk);
-        cv.surv = __ldcg(&c->surv);
-        cv.collision = __ldcg(&c->collision);
+        // one read per CTA, shared through shared memory (every thread reading
+        // the same counters queued thousands of requests on one L2 slice)
+        __shared__ PersistCtr s_cv;
+        if (threadIdx.x == 0) {
+            s_cv.runs = __ldcg(&c->runs);
+            s_cv.ablk = __ldcg(&c->ablk);
+            s_cv.surv = __ldcg(&c->surv);
+            s_cv.collision = __ldcg(&c->collision);
+        }
+        __syncthreads();
+        const PersistCtr cv = s_cv;
         ++s.passes;
         ++pass_no;
         const uint32_t newB = s.B - s.A + cv.runs;
