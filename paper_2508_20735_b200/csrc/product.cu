@@ -372,10 +372,14 @@ __global__ void __launch_bounds__(kThreads) bfs_persistent_kernel(BfsArgs A) {
         grid.sync();
         // prefix of this CTA, total of the level
         uint32_t pre = 0, total = 0;
-        for (uint32_t j = threadIdx.x; j < gridDim.x; j += blockDim.x) {
-            const uint32_t v = __ldcg(A.cta_cnt + j);
-            total += v;
-            if (j < blockIdx.x) pre += v;
+        // four counts per 16-byte load (the count array is padded with zeros):
+        // every CTA reads all of them, so this is gridDim^2 / 4 requests
+        for (uint32_t j4 = threadIdx.x; j4 < (gridDim.x + 3) / 4; j4 += blockDim.x) {
+            const uint4 v = __ldcg(reinterpret_cast<const uint4*>(A.cta_cnt) + j4);
+            const uint32_t j = 4 * j4;
+            total += v.x + v.y + v.z + v.w;
+            pre += (j < blockIdx.x ? v.x : 0u) + (j + 1 < blockIdx.x ? v.y : 0u) + (j + 2 < blockIdx.x ? v.z : 0u) +
+                   (j + 3 < blockIdx.x ? v.w : 0u);
         }
         pre = __reduce_add_sync(0xffffffffu, pre);
         total = __reduce_add_sync(0xffffffffu, total);
@@ -594,7 +598,8 @@ ProductOut explore_product_device(Ctx* ctx, const DevDfa& a, const DevDfa& b, in
     DK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bfs_persistent_kernel, kThreads, 0));
     if (per_sm < 1) throw Error(DFAKIT_E_RESOURCE, "bfs kernel does not fit an SM");
     const unsigned grid_n = (unsigned)(per_sm * ctx->num_sms);
-    DBuf<uint32_t> cta_cnt(grid_n, s);
+    DBuf<uint32_t> cta_cnt((grid_n + 3) / 4 * 4, s);  // padded for 16-byte reads
+    DK_CUDA(cudaMemsetAsync(cta_cnt.get(), 0, cta_cnt.n * sizeof(uint32_t), s));
     BfsState hs{};
     hs.wb = 0;
     hs.we = 1;
