@@ -74,6 +74,8 @@ struct Ctx {
     bool own_stream = true;
     uint64_t* mailbox = nullptr;  // pinned host, 64 words: [0, 56) read_words, [56, 64) deferred reads
     uint64_t* dmailbox = nullptr; // device, 64 words
+    uint32_t* fastbox = nullptr;  // pinned host, device-written: [0] sequence number, [2, 2 + 112) payload
+    uint32_t fast_seq = 0;
     cudaEvent_t info_ev = nullptr;  // marks a deferred mailbox read (no timing)
     uint64_t launches = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
