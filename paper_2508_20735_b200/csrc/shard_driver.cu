@@ -277,13 +277,14 @@ RefineResult sort_pr_sharded_device(Ctx* ctx, NcclComm* cm, const DevDfa& d, uin
     const uint32_t hi = std::min<uint64_t>(n, (uint64_t)(rank + 1) * shard);
     DBuf<uint32_t> lab((uint64_t)world * shard, s), list(std::max(1u, hi - lo), s), scratch((uint64_t)n + 1, s);
     DBuf<uint8_t> act(n, s);
-    DBuf<uint32_t> dctr(8, s), counts(world, s), keys32;
+    DBuf<uint32_t> dctr(8, s), counts(2 * (uint64_t)world, s), keys32;  // [send counts | receive counts]
     DBuf<uint8_t> kl8;
     DBuf<uint16_t> kl16, next16;
     DBuf<uint32_t> kl32, next32, tmin, tcnt, results, back, bits;
     DBuf<uint4> send, recv;
     auto read_u32 = [&](const uint32_t* p, size_t count, uint32_t* out) {
-        read_words(ctx, p, count * sizeof(uint32_t), out, s);
+        for (size_t i = 0; i < count; i += 112)  // read_words moves at most 112 words
+            read_words(ctx, p + i, std::min<size_t>(112, count - i) * sizeof(uint32_t), out + i, s);
     };
 
     const ShardInit si = shard_init(ctx, d, lo, hi, lab.get(), act.get(), s);
@@ -374,14 +375,14 @@ RefineResult sort_pr_sharded_device(Ctx* ctx, NcclComm* cm, const DevDfa& d, uin
         } else {
             if (send.n < std::max(1u, m)) send.alloc(std::max(1u, hi - lo), s);
             shard_sig_partition(ctx, d, keylab, plan, salt, lst, lo, m, (uint32_t)world, send.get(), counts.get(), s);
-            std::vector<uint32_t> sc32(world), rc32(world);
-            read_u32(counts.get(), world, sc32.data());
+            // counts: one word to every peer, then both vectors in one readback
+            std::vector<uint32_t> c32(2 * (size_t)world);
             std::vector<uint64_t> scount(world), rcount(world), ones(world, 1);
+            cm->all_to_all_v(counts.get(), ones, counts.get() + world, ones, sizeof(uint32_t), s);
+            read_u32(counts.get(), 2 * (size_t)world, c32.data());
+            const uint32_t* sc32 = c32.data();
+            const uint32_t* rc32 = c32.data() + world;
             for (int r = 0; r < world; ++r) scount[r] = sc32[r];
-            // counts: one word to every peer
-            DBuf<uint32_t> rc(world, s);
-            cm->all_to_all_v(counts.get(), ones, rc.get(), ones, sizeof(uint32_t), s);
-            read_u32(rc.get(), world, rc32.data());
             uint64_t rtotal = 0;
             for (int r = 0; r < world; ++r) rtotal += (rcount[r] = rc32[r]);
             if (recv.n < std::max<uint64_t>(1, rtotal)) recv.alloc(std::max<uint64_t>(1, rtotal) * 5 / 4, s);
