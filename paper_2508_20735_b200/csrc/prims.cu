@@ -112,7 +112,9 @@ void fill_u32(Ctx* ctx, uint32_t* p, uint64_t n, uint32_t value, cudaStream_t s)
 }
 
 void iota_u32(Ctx* ctx, uint32_t* p, uint64_t n, cudaStream_t s) {
-    if (n) DK_LAUNCH(ctx, iota_kernel, grid_for(n), kThreads, 0, s, p, n);
+    // ~8 16-byte stores per thread: one store per thread made the launch of
+    // ~10^4 CTAs the cost of a 40 MB write
+    if (n) DK_LAUNCH(ctx, iota_kernel, grid_for(n / 4 + 1, kThreads, (unsigned)ctx->num_sms * 8u), kThreads, 0, s, p, n);
 }
 
 // ---------------------------------------------------------------------------

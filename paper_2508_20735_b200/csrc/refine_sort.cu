@@ -70,10 +70,7 @@ struct IterCounters {
 // dense2 (optional): also writes the initial partition's dense block ids,
 // dense2[q] = (acc[q] != 0) ^ (acc[0] != 0), from the same loads.
 __device__ __forceinline__ uint32_t flags4(uint32_t w, uint32_t a0) {  // byte j -> (byte j != 0) ^ a0
-    uint32_t o = 0;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) o |= ((((w >> (8 * j)) & 0xffu) != 0) ^ a0) << (8 * j);
-    return o;
+    return (__vcmpne4(w, 0u) & 0x01010101u) ^ (a0 * 0x01010101u);
 }
 
 __global__ void __launch_bounds__(kThreads) leader_info_kernel(const uint8_t* __restrict__ acc, uint32_t n,
@@ -92,15 +89,13 @@ __global__ void __launch_bounds__(kThreads) leader_info_kernel(const uint8_t* __
                 make_uint4(flags4(w.x, a0), flags4(w.y, a0), flags4(w.z, a0), flags4(w.w, a0));
         const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            const uint32_t q = v * 16 + j;
-            if ((ws[j >> 2] >> (8 * (j & 3))) & 0xffu) {
-                mina = min(mina, q);
-                ++ca;
-            } else {
-                minr = min(minr, q);
-                ++cr;
-            }
+        for (int j = 0; j < 4; ++j) {  // four flags per byte-SIMD compare
+            const uint32_t nz = __vcmpne4(ws[j], 0u), q0 = v * 16 + 4 * j;
+            const uint32_t c = __popc(nz) >> 3;
+            ca += c;
+            cr += 4 - c;
+            if (nz) mina = min(mina, q0 + ((__ffs(nz) - 1) >> 3));
+            if (~nz) minr = min(minr, q0 + ((__ffs(~nz) - 1) >> 3));
         }
     }
     for (uint32_t q = nv * 16 + tid; q < n; q += stride) {
