@@ -107,73 +107,6 @@ __device__ uint32_t tile_find_or_insert(cg::thread_block_tile<kTile> tile, bool 
     return mine;
 }
 
-// one item per (frontier record, letter)
-__global__ void __launch_bounds__(kThreads) expand_kernel(Rec rec, uint64_t wb, uint64_t items, uint32_t k,
-                                                          const uint32_t* __restrict__ da, uint32_t na,
-                                                          const uint32_t* __restrict__ db, uint32_t nb,
-                                                          const uint32_t* __restrict__ to_b, Slot* __restrict__ table,
-                                                          uint64_t mask, uint32_t* __restrict__ item_slot) {
-    auto tile = cg::tiled_partition<kTile>(cg::this_thread_block());
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    const uint64_t first = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    // uniform trip count so tiles stay converged
-    const uint64_t trips = (items + stride - 1) / stride;
-    for (uint64_t it = 0; it < trips; ++it) {
-        const uint64_t t = first + it * stride;
-        const bool valid = t < items;
-        unsigned long long key = 0, disc = 0;
-        if (valid) {
-            const uint64_t i = wb + t / k;
-            const uint32_t la = (uint32_t)(t % k);
-            const unsigned long long pk = rec.key[i];
-            const uint32_t qa = (uint32_t)(pk >> 32), qb = (uint32_t)pk;
-            const uint32_t pa = da[(uint64_t)la * na + qa];
-            const uint32_t pb = db[(uint64_t)to_b[la] * nb + qb];
-            key = ((unsigned long long)pa << 32) | pb;
-            disc = ((unsigned long long)(i + 1) << 32) | la;  // +1: reinserted slots hold 0
-        }
-        const uint32_t s = tile_find_or_insert(tile, valid, key, table, mask);
-        if (valid) {
-            const unsigned long long old = atomicMin(&table[s].disc, disc);
-            // slots discovered in earlier waves carry a parent below wb (stored +1)
-            item_slot[t] = (old >= ((unsigned long long)(wb + 1) << 32)) ? s : kNone;
-        }
-    }
-}
-
-__global__ void winner_flags_kernel(uint64_t wb, uint64_t items, uint32_t k, const Slot* __restrict__ table,
-                                    const uint32_t* __restrict__ item_slot, uint32_t* __restrict__ flag) {
-    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < items;
-         t += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t s = item_slot[t];
-        uint32_t f = 0;
-        if (s != kNone) {
-            const unsigned long long disc = ((unsigned long long)(wb + t / k + 1) << 32) | (uint32_t)(t % k);
-            f = __ldcg(&table[s].disc) == disc;
-        }
-        flag[t] = f;
-    }
-}
-
-__global__ void emit_kernel(Rec rec, uint64_t wb, uint64_t we, uint64_t items, uint32_t k,
-                            const Slot* __restrict__ table, const uint32_t* __restrict__ item_slot,
-                            const uint32_t* __restrict__ flag, const uint32_t* __restrict__ pos,
-                            const uint8_t* __restrict__ acc_a, const uint8_t* __restrict__ acc_b, int mode,
-                            uint32_t* __restrict__ first_fail) {
-    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < items;
-         t += (uint64_t)gridDim.x * blockDim.x) {
-        if (!flag[t]) continue;
-        const unsigned long long key = table[item_slot[t]].key;
-        const uint64_t r = we + pos[t];
-        rec.key[r] = key;
-        rec.parent[r] = (uint32_t)(wb + t / k);
-        rec.letter[r] = (uint32_t)(t % k);
-        const bool fa = acc_a[key >> 32], fb = acc_b[(uint32_t)key];
-        const bool fails = mode == DFAKIT_MODE_INCLUSION ? (fa && !fb) : (fa != fb);
-        if (fails) atomicMin(first_fail, pos[t]);
-    }
-}
-
 __global__ void reinsert_kernel(const unsigned long long* __restrict__ keys, uint64_t count, Slot* __restrict__ table,
                                 uint64_t mask) {
     auto tile = cg::tiled_partition<kTile>(cg::this_thread_block());
@@ -233,30 +166,6 @@ __global__ void uf_init_kernel(uint32_t* P, uint64_t total) {
 }
 
 __global__ void uf_seed_kernel(uint32_t* P, uint32_t a, uint32_t b) { uf_union(P, a, b); }
-
-__global__ void __launch_bounds__(kThreads) uf_expand_kernel(Rec rec, uint64_t wb, uint64_t items, uint32_t k,
-                                                             const uint32_t* __restrict__ da, uint32_t na,
-                                                             const uint32_t* __restrict__ db, uint32_t nb,
-                                                             const uint8_t* __restrict__ acc_a,
-                                                             const uint8_t* __restrict__ acc_b, uint32_t* __restrict__ P,
-                                                             uint32_t* __restrict__ count, uint64_t cap,
-                                                             uint32_t* __restrict__ fail_rec) {
-    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < items;
-         t += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t i = wb + t / k;
-        const uint32_t la = (uint32_t)(t % k);
-        const unsigned long long pk = rec.key[i];
-        const uint32_t pa = da[(uint64_t)la * na + (uint32_t)(pk >> 32)];
-        const uint32_t pb = db[(uint64_t)la * nb + (uint32_t)pk];
-        if (!uf_union(P, pa, na + pb)) continue;
-        const uint32_t r = atomicAdd(count, 1u);
-        if (r >= cap) continue;  // cannot happen: at most na+nb-1 unions
-        rec.key[r] = ((unsigned long long)pa << 32) | pb;
-        rec.parent[r] = (uint32_t)i;
-        rec.letter[r] = la;
-        if (acc_a[pa] != acc_b[pb]) atomicMin(fail_rec, r);
-    }
-}
 
 // ---- persistent BFS ------------------------------------------------------------
 //
