@@ -343,3 +343,17 @@ def test_first_pass_class_edge_cases_large(dk, oracle):
     a[a != 0] = 7
     want = oracle.minimize("sort", delta, acc)
     assert same(dk.sort_pr(dk.Dfa(delta, a, 0)), want)
+
+
+def test_naive_persistent_grid_stride(dk, oracle):
+    """More states than resident threads (every CTA loops over several
+    states per pass): 2000 relabelled copies of a 200-state DFA, 400K states,
+    through the persistent naive / fused kernels -- pass counts and
+    partitions exact."""
+    base = oracle.gen_random(200, 4, 0.5, 4242)
+    t = copies(base, 2000)
+    dfa = mkdfa(dk, t)
+    for algo in ("naive", "naive-fused"):
+        want = oracle.minimize(algo, t[0], t[1])
+        got = run(dk, algo, dfa)
+        assert same(got, want), (algo, got.refining_iterations, want.refine_iters)
