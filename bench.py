@@ -502,6 +502,36 @@ def extras(dk, nat, ctx, torch, sharded, args):
             return rep
         return f
 
+    # configs[0]: random complete DFA, 1M states, |Sigma| = 2, from the
+    # reference's own generator (gen_random, libstdc++ mt19937_64), minimised
+    # on the GPU and by the reference (oracle/_ref, one thread) -- same input,
+    # same partition
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle
+    gen = pyoracle.COracle()
+    hd, ha, _ = gen.gen_random(1_000_000, 2, 0.5, 7)
+    n, k = hd.shape[1], hd.shape[0]
+    d = torch.from_numpy(np.ascontiguousarray(hd).view(np.int32).reshape(-1)).cuda()
+    a = torch.from_numpy(np.ascontiguousarray(ha)).cuda()
+    b = torch.empty(n, dtype=torch.int32, device="cuda")
+    view = nat.CDfa(n, k, d.data_ptr(), a.data_ptr(), -1)
+    s, r = timed(minimize(view, "sort_pr", b), 5)
+    c0 = {"ms": s * 1000, "passes": int(r.passes), "refining_iterations": int(r.refining_iterations),
+          "blocks": int(r.num_blocks), "transitions_per_s": n * k * int(r.passes) / s}
+    try:
+        ref = pyoracle.RefLib()
+        t0 = time.perf_counter()
+        rr = ref.minimize("sort", hd, ha)
+        c0["reference_ms"] = (time.perf_counter() - t0) * 1000
+        c0["reference_kind"] = "reference (oracle/_ref, one thread)"
+        c0["same_partition"] = bool(np.array_equal(b.cpu().numpy().view(np.uint32), rr.blocks)
+                                    and rr.refine_iters == int(r.refining_iterations))
+        c0["speedup_vs_reference"] = c0["reference_ms"] / c0["ms"]
+    except Exception as e:  # the compiled reference is optional on the box
+        c0["reference_ms"] = None
+        c0["reference_note"] = f"oracle/_ref unavailable: {e}"
+    out["sort_pr_config0_1M_k2"] = c0
+    del d, a, b
     # configs[1] at full size: the literal Alg. 4 grouping (full LSD radix sort
     # of the keys + adjacent difference + scan) beside the default
     n, k = args.states, args.alphabet
