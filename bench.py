@@ -629,6 +629,23 @@ def extras(dk, nat, ctx, torch, sharded, args):
         out[f"{name}_naive_hk_10M_equal"] = {"ms": s * 1000, "verdict": int(r.verdict),
                                              "explored_pairs": int(r.explored_states), "levels": int(r.levels),
                                              "pairs_per_s": int(r.explored_states) / s}
+    # the same pair through the reference's explore_product (oracle/_ref, one
+    # thread): pairs / s on identical inputs, verdict and counts compared
+    try:
+        ref = pyoracle.RefLib()
+        hA = (d.cpu().numpy().view(np.uint32).reshape(k, n), a.cpu().numpy(), 0)
+        hB = (d2.cpu().numpy().view(np.uint32).reshape(k, n), a2.cpu().numpy(), int(init2.value))
+        t0 = time.perf_counter()
+        ro = ref.explore("equivalence", hA, hB)
+        dt = time.perf_counter() - t0
+        g = out["equivalence_naive_hk_10M_equal"]
+        out["equivalence_reference_10M_equal"] = {
+            "ms": dt * 1000, "verdict": ro.verdict, "explored_pairs": ro.explored, "levels": ro.levels,
+            "pairs_per_s": ro.explored / dt, "kind": "reference (oracle/_ref, one thread)",
+            "same_result": ro.explored == g["explored_pairs"] and ro.levels == g["levels"] and g["verdict"] == 0,
+            "gpu_speedup": dt * 1000 / g["ms"]}
+    except Exception as e:  # the compiled reference is optional on the box
+        out["equivalence_reference_10M_equal"] = {"note": f"oracle/_ref unavailable: {e}"}
     res = nat.CProduct()
 
     def u():
