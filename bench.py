@@ -603,6 +603,29 @@ def extras(dk, nat, ctx, torch, sharded, args):
     s, r = timed(minimize(view, "trans_pr", b), 2)
     out["trans_pr_chain_10M"] = {"ms": s * 1000, "passes": int(r.passes),
                                  "closure_iterations": int(r.closure_iterations), "blocks": int(r.num_blocks)}
+    # configs[2] shape at 1M states on both sides: trans_pr on the GPU and the
+    # reference's trans_pr (oracle/_ref, one thread) on the same chain
+    hd, ha, _ = gen.gen_chain(1_000_000)
+    n1 = hd.shape[1]
+    d = torch.from_numpy(np.ascontiguousarray(hd).view(np.int32).reshape(-1)).cuda()
+    a = torch.from_numpy(np.ascontiguousarray(ha)).cuda()
+    b = torch.empty(n1, dtype=torch.int32, device="cuda")
+    view = nat.CDfa(n1, 1, d.data_ptr(), a.data_ptr(), 0)
+    s, r = timed(minimize(view, "trans_pr", b), 3)
+    c2 = {"ms": s * 1000, "passes": int(r.passes), "closure_iterations": int(r.closure_iterations),
+          "blocks": int(r.num_blocks)}
+    try:
+        t0 = time.perf_counter()
+        rr = pyoracle.RefLib().minimize("transpr", hd, ha)
+        c2["reference_ms"] = (time.perf_counter() - t0) * 1000
+        c2["reference_kind"] = "reference (oracle/_ref, one thread)"
+        c2["same_partition"] = bool(np.array_equal(b.cpu().numpy().view(np.uint32), rr.blocks)
+                                    and rr.refine_iters == int(r.refining_iterations))
+        c2["speedup_vs_reference"] = c2["reference_ms"] / c2["ms"]
+    except Exception as e:
+        c2["reference_note"] = f"oracle/_ref unavailable: {e}"
+    out["trans_pr_chain_1M_vs_reference"] = c2
+    del d, a, b
     # configs[3]: equivalence / inclusion of two 10M-state DFAs
     n, k = 10_000_000, 2
     d = torch.empty(k * n, dtype=torch.int32, device="cuda")
