@@ -593,6 +593,29 @@ def extras(dk, nat, ctx, torch, sharded, args):
         s, r = timed(minimize(view, algo, b), 2)
         out[f"{algo}_100K_k10"] = {"ms": s * 1000, "passes": int(r.passes), "blocks": int(r.num_blocks),
                                    "transitions_per_s": n * k * int(r.passes) / s}
+    # ... and at 20K states through the compiled reference too (one thread),
+    # sort vs naive on identical input (the reference's naive_pr at 100K
+    # states would take minutes)
+    n, k = 20_000, 10
+    hd, ha, _ = gen.gen_synth(n, k, 7)
+    d = torch.from_numpy(np.ascontiguousarray(hd).view(np.int32).reshape(-1)).cuda()
+    a = torch.from_numpy(np.ascontiguousarray(ha)).cuda()
+    b = torch.empty(n, dtype=torch.int32, device="cuda")
+    view = nat.CDfa(n, k, d.data_ptr(), a.data_ptr(), -1)
+    for algo, ralgo in (("sort_pr", "sort"), ("naive_pr", "naive"), ("naive_pr_fused", "naive-fused")):
+        s, r = timed(minimize(view, algo, b), 2)
+        e = {"ms": s * 1000, "passes": int(r.passes)}
+        try:
+            t0 = time.perf_counter()
+            rr = pyoracle.RefLib().minimize(ralgo, hd, ha)
+            e["reference_ms"] = (time.perf_counter() - t0) * 1000
+            e["same_partition"] = bool(np.array_equal(b.cpu().numpy().view(np.uint32), rr.blocks)
+                                       and rr.refine_iters == int(r.refining_iterations))
+            e["speedup_vs_reference"] = e["reference_ms"] / e["ms"]
+        except Exception as ex:
+            e["reference_note"] = f"oracle/_ref unavailable: {ex}"
+        out[f"{algo}_20K_k10_vs_reference"] = e
+    del d, a, b
     # configs[2]: chain DFA (n-pass worst case) with partial transitive closure
     n = 10_000_000
     d = torch.empty(n, dtype=torch.int32, device="cuda")
