@@ -1,5 +1,6 @@
 // ctx.cu -- device context, error state and small readbacks.
 #include <atomic>
+#include <chrono>
 #include <cstring>
 
 #include "common.cuh"
@@ -81,16 +82,22 @@ void read_words(Ctx* ctx, const void* dsrc, size_t bytes, void* hdst, cudaStream
     const uint32_t seq = ++ctx->fast_seq;
     mailbox_kernel<<<1, 128, 0, s>>>(static_cast<const uint8_t*>(dsrc), (uint32_t)bytes, ctx->fastbox, seq);
     DK_CUDA(cudaGetLastError());
+    // spin for short waits (the pass loop's readbacks follow sub-millisecond
+    // kernels); past ~200 us block in cudaStreamSynchronize instead of
+    // burning a core behind a long kernel
     volatile uint32_t* flag = ctx->fastbox;
+    const auto t0 = std::chrono::steady_clock::now();
     for (uint32_t spin = 1;; ++spin) {
         if (*flag == seq) break;
-        if ((spin & 4095u) == 0) {  // a failed launch never writes the flag
-            const cudaError_t e = cudaStreamQuery(s);
-            if (e == cudaSuccess) {
-                if (*flag == seq) break;
-                throw Error(DFAKIT_E_CUDA, "read_words: stream completed without the mailbox write");
+        if ((spin & 1023u) == 0) {
+            const cudaError_t e = cudaStreamQuery(s);  // a failed launch never writes the flag
+            if (e != cudaSuccess && e != cudaErrorNotReady)
+                throw Error(DFAKIT_E_CUDA, std::string("read_words: ") + cudaGetErrorString(e));
+            if (e == cudaSuccess || std::chrono::steady_clock::now() - t0 > std::chrono::microseconds(200)) {
+                DK_CUDA(cudaStreamSynchronize(s));
+                if (*flag != seq) throw Error(DFAKIT_E_CUDA, "read_words: stream completed without the mailbox write");
+                break;
             }
-            if (e != cudaErrorNotReady) throw Error(DFAKIT_E_CUDA, std::string("read_words: ") + cudaGetErrorString(e));
         }
     }
     std::atomic_thread_fence(std::memory_order_acquire);
