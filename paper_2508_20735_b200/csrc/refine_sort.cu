@@ -363,15 +363,37 @@ __global__ void __launch_bounds__(kThreads) table_apply_kernel(const uint32_t* _
 // with 16-byte key / label loads and stores (the scalar kernel sat at
 // ~2.4 TB/s: one 4-byte access per thread in flight).  Requires 16-byte
 // aligned keys32 / lab, 8-byte next16, 4-byte keep / next32.
+// STAGE: tables of <= kApplyStageMax entries are copied into shared memory
+// first (the three table lookups per state were L1 gathers over 128-byte
+// lines); tsize is the table size then.
+constexpr uint32_t kApplyStageMax = 2048;
+
+template <bool STAGE>
 __global__ void __launch_bounds__(kThreads) table_apply_vec_kernel(const uint32_t* __restrict__ keys32, uint64_t m,
-                                                                   const uint32_t* __restrict__ tmin,
-                                                                   const uint32_t* __restrict__ tcnt,
+                                                                   const uint32_t* __restrict__ tmin_g,
+                                                                   const uint32_t* __restrict__ tcnt_g,
                                                                    uint32_t* __restrict__ lab,
                                                                    uint8_t* __restrict__ keep,
-                                                                   const uint32_t* __restrict__ rank,
+                                                                   const uint32_t* __restrict__ rank_g,
                                                                    uint16_t* __restrict__ next16,
                                                                    uint32_t* __restrict__ next32,
-                                                                   IterCounters* __restrict__ ctr) {
+                                                                   IterCounters* __restrict__ ctr, uint32_t tsize) {
+    __shared__ uint32_t s_min[STAGE ? kApplyStageMax : 1], s_cnt[STAGE ? kApplyStageMax : 1],
+        s_rank[STAGE ? kApplyStageMax : 1];
+    const uint32_t* tmin = tmin_g;
+    const uint32_t* tcnt = tcnt_g;
+    const uint32_t* rank = rank_g;
+    if (STAGE) {
+        for (uint32_t i = threadIdx.x; i < tsize; i += blockDim.x) {
+            s_min[i] = tmin_g[i];
+            s_cnt[i] = tcnt_g[i];
+            if (rank_g) s_rank[i] = rank_g[i];
+        }
+        __syncthreads();
+        tmin = s_min;
+        tcnt = s_cnt;
+        rank = rank_g ? s_rank : nullptr;
+    }
     uint32_t heads = 0, ablk = 0, surv = 0;
     const uint64_t nv = m / 4;
     const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, stride = (uint64_t)gridDim.x * blockDim.x;
@@ -1592,11 +1614,17 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
             auto a16 = [](const void* x) { return ((uintptr_t)x & 15u) == 0; };
             const bool vec = full && a16(w.heads.get()) && a16(w.lab.get()) && a16(w.keep.get()) &&
                              a16(nbits <= 16 ? (void*)w.next16.get() : (void*)w.next32.get());
-            if (vec)  // identity list, four states per thread
-                DK_LAUNCH_B(ctx, (double)m * (9.0 + (nbits <= 16 ? 2.0 : 4.0)), table_apply_vec_kernel,
+            if (vec && tsize <= kApplyStageMax)  // identity list, four states per thread, tables in smem
+                DK_LAUNCH_B(ctx, (double)m * (9.0 + (nbits <= 16 ? 2.0 : 4.0)), table_apply_vec_kernel<true>,
+                            grid_for((m + 3) / 4, kThreads, (unsigned)ctx->num_sms * 4u), kThreads, 0, s,
+                            w.heads.get(), m, w.tmin.get(), w.tcnt.get(), w.lab.get(), w.keep.get(), w.trank.get(),
+                            nbits <= 16 ? w.next16.get() : nullptr, nbits > 16 ? w.next32.get() : nullptr, dctr,
+                            (uint32_t)tsize);
+            else if (vec)  // identity list, four states per thread
+                DK_LAUNCH_B(ctx, (double)m * (9.0 + (nbits <= 16 ? 2.0 : 4.0)), table_apply_vec_kernel<false>,
                             grid_for((m + 3) / 4), kThreads, 0, s, w.heads.get(), m, w.tmin.get(), w.tcnt.get(),
                             w.lab.get(), w.keep.get(), w.trank.get(), nbits <= 16 ? w.next16.get() : nullptr,
-                            nbits > 16 ? w.next32.get() : nullptr, dctr);
+                            nbits > 16 ? w.next32.get() : nullptr, dctr, (uint32_t)tsize);
             else
                 DK_LAUNCH_B(ctx, (double)m * (9.0 + 2 * list_b), table_apply_kernel, g, kThreads, 0, s, list,
                             w.heads.get(), m, w.tmin.get(), w.tcnt.get(), w.lab.get(), w.keep.get(), nullptr,
