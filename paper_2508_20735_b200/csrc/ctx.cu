@@ -1,6 +1,8 @@
 // ctx.cu -- device context, error state and small readbacks.
 #include <atomic>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
@@ -34,6 +36,17 @@ std::string prof_collect(Ctx* ctx) {
         double ms = 0, bytes = 0, units = 0;
     };
     std::vector<Agg> aggs;
+    // DFAKIT_PROF_TIMELINE=1: every recorded launch with its start offset and
+    // duration on stderr (development aid: gaps between launches)
+    const bool timeline = getenv("DFAKIT_PROF_TIMELINE") != nullptr;
+    for (size_t i = 0; timeline && i < ctx->prof.size(); ++i) {
+        auto& r = ctx->prof[i];
+        DK_CUDA(cudaEventSynchronize(r.b));
+        float t0 = 0, ms = 0;
+        DK_CUDA(cudaEventElapsedTime(&t0, ctx->prof[0].a, r.a));
+        DK_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+        fprintf(stderr, "timeline %4zu %10.4f ms  %9.4f ms  %s\n", i, t0, ms, r.name);
+    }
     for (auto& r : ctx->prof) {
         DK_CUDA(cudaEventSynchronize(r.b));
         float ms = 0;

@@ -1,6 +1,8 @@
 // prims.cu -- scan, compaction and the LSD radix sort.
 //
 // Radix sort design: see "radix sort (one sweep per digit)" below.
+#include <algorithm>
+
 #include "prims.cuh"
 
 namespace dk {
@@ -105,6 +107,52 @@ __global__ void iota_kernel(uint32_t* p, uint64_t n) {
         __stcs(reinterpret_cast<uint4*>(p) + v, make_uint4(i, i + 1, i + 2, i + 3));
     }
     for (uint64_t i = 4 * nv + tid; i < n; i += stride) p[i] = (uint32_t)i;
+}
+
+struct FillArgs {
+    uint8_t* p[4];
+    uint64_t bytes[4];
+    uint32_t value[4];
+};
+
+// blockIdx.y = region; 16-byte stores between a byte head and tail
+__global__ void fill_regions_kernel(FillArgs a) {
+    uint8_t* p = a.p[blockIdx.y];
+    const uint64_t nb = a.bytes[blockIdx.y];
+    if (!p || !nb) return;
+    const uint32_t v8 = a.value[blockIdx.y] & 0xffu, w = v8 * 0x01010101u;
+    const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, stride = (uint64_t)gridDim.x * blockDim.x;
+    uint64_t head = (16u - ((uintptr_t)p & 15u)) & 15u;
+    if (head > nb) head = nb;
+    for (uint64_t i = tid; i < head; i += stride) p[i] = (uint8_t)v8;
+    const uint64_t nv = (nb - head) / 16;
+    uint4* q = reinterpret_cast<uint4*>(p + head);
+    for (uint64_t i = tid; i < nv; i += stride) q[i] = make_uint4(w, w, w, w);
+    for (uint64_t i = head + 16 * nv + tid; i < nb; i += stride) p[i] = (uint8_t)v8;
+}
+
+void Fills::add(void* ptr, uint64_t nbytes, uint8_t v) {
+    if (!ptr || !nbytes) return;
+    if (count == 4) throw Error(DFAKIT_E_INVALID, "Fills: more than four regions");
+    p[count] = ptr;
+    bytes[count] = nbytes;
+    value[count] = v;
+    ++count;
+}
+
+void Fills::flush(Ctx* ctx, cudaStream_t s) {
+    if (!count) return;
+    FillArgs a{};
+    uint64_t most = 0;
+    for (int i = 0; i < 4; ++i) {
+        a.p[i] = static_cast<uint8_t*>(p[i]);
+        a.bytes[i] = i < count ? bytes[i] : 0;
+        a.value[i] = value[i];
+        most = std::max<uint64_t>(most, bytes[i]);
+    }
+    const unsigned gx = grid_for(most / 16 + 1, kThreads, (unsigned)ctx->num_sms * 4u);
+    DK_LAUNCH(ctx, fill_regions_kernel, dim3(gx, (unsigned)count), kThreads, 0, s, a);
+    count = 0;
 }
 
 void fill_u32(Ctx* ctx, uint32_t* p, uint64_t n, uint32_t value, cudaStream_t s) {

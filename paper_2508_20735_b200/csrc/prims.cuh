@@ -73,6 +73,18 @@ void compact_flags(Ctx* ctx, const uint32_t* in, const uint8_t* flag, uint64_t n
 uint32_t dense_labels(Ctx* ctx, const uint32_t* lab, uint64_t n, void* out, int bytes, uint32_t* scratch,
                       cudaStream_t s);
 
+// Up to four byte-fills (cudaMemsetAsync semantics) in one launch: each
+// separate memset is its own operation on the stream (~2-3 us of the pass
+// prologue each).
+struct Fills {
+    void* p[4] = {nullptr, nullptr, nullptr, nullptr};
+    uint64_t bytes[4] = {0, 0, 0, 0};
+    uint32_t value[4] = {0, 0, 0, 0};
+    int count = 0;
+    void add(void* ptr, uint64_t nbytes, uint8_t v);
+    void flush(Ctx* ctx, cudaStream_t s);
+};
+
 // Fills [0, n) with value.
 void fill_u32(Ctx* ctx, uint32_t* p, uint64_t n, uint32_t value, cudaStream_t s);
 void iota_u32(Ctx* ctx, uint32_t* p, uint64_t n, cudaStream_t s);

@@ -1533,7 +1533,8 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
             }
         }
         next_valid = false;
-        DK_CUDA(cudaMemsetAsync(dctr, 0, sizeof(IterCounters), s));
+        Fills fills;  // the pass prologue's fills, one launch before its first kernel
+        fills.add(dctr, sizeof(IterCounters), 0);
         const unsigned g = grid_for(m);
         const uint32_t nbits = plan.key_bits;
         SigParams p{};
@@ -1555,8 +1556,9 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
                 w.tcnt.alloc(tsize, s);
             }
             if (!w.heads.get()) w.heads.alloc((uint64_t)n + 1, s);
-            DK_CUDA(cudaMemsetAsync(w.tmin.get(), 0xff, tsize * sizeof(uint32_t), s));
-            DK_CUDA(cudaMemsetAsync(w.tcnt.get(), 0, tsize * sizeof(uint32_t), s));
+            fills.add(w.tmin.get(), tsize * sizeof(uint32_t), 0xff);
+            fills.add(w.tcnt.get(), tsize * sizeof(uint32_t), 0);
+            fills.flush(ctx, s);
             const bool local = nbits <= kSmemTableBits;
             const size_t smem = local ? (size_t)(2u << nbits) * 4 : 0;
             auto sig_table = [&](uint32_t q0, uint64_t mm, bool clamp) {
@@ -1633,15 +1635,17 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
             next_valid = full;
             prev_nbits = nbits;
             // every state survives (the first pass of a random automaton):
-            // the compaction exits at once and the identity list stays
-            compact_flags(ctx, list, w.keep.get(), m, dst, &dctr->listed, s, 0u, list ? nullptr : &dctr->active_states);
             if (deferred_info && res.passes == 1) {  // the class sizes, read while the pass ran
                 li = leader_info_wait(ctx);
                 B = (li.min_acc != kNone) + (li.min_rej != kNone);
                 A = B;
             }
             read_words(ctx, dctr, sizeof(c), &c, s);
+            // compaction after the readback: when every state survives the
+            // identity list stays and nothing is launched (three launches of
+            // ~2.4K CTAs that would only exit cost ~25 us)
             if (!list && c.active_states == m) all_survive = true;
+            else if (c.active_states && B - A + c.runs != B) compact_flags(ctx, list, w.keep.get(), m, dst, &dctr->listed, s);
         } else if (!chunked && o.grouping != 1) {
             wait_all_chunks();
             // ---- bucket strategy
@@ -1671,9 +1675,10 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
                 if (list) DK_CUDA(cudaMemcpyAsync(w.lab2.get(), w.lab.get(), (size_t)n * 4, cudaMemcpyDeviceToDevice, s));
             }
             uint32_t* out_lab = fingerprint && direct ? w.lab2.get() : w.lab.get();
-            DK_CUDA(cudaMemsetAsync(w.bcnt.get(), 0, (size_t)nb * kCntStride * 4, s));
-            if (state_order) DK_CUDA(cudaMemsetAsync(w.act.get(), 0, n, s));
-            if (!state_order) DK_CUDA(cudaMemsetAsync(w.keep_slot.get(), 0, espace, s));
+            fills.add(w.bcnt.get(), (size_t)nb * kCntStride * 4, 0);
+            if (state_order) fills.add(w.act.get(), n, 0);
+            if (!state_order) fills.add(w.keep_slot.get(), espace, 0);
+            fills.flush(ctx, s);
             with_lab_type(kl, [&](auto lab) {
                 // algorithmic HBM bytes: delta rows (+ list), (hkey, state) out, the key-label array once
                 DK_LAUNCH_BU(ctx, (double)m * (4.0 * k + 16.0 + list_b) + keylab_bytes_per_state(kl) * n, (double)m * k,
@@ -1742,6 +1747,7 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
             }
         } else {
             wait_all_chunks();
+            fills.flush(ctx, s);
             // ---- radix-sort grouping: (key, state) pairs, LSD radix sort, runs
             if (!w.keys0.get()) {
                 w.keys0.alloc(n, s);
