@@ -133,6 +133,11 @@ Ctx* ctx_create(int device) {
     DK_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&c->fastbox), 128 * sizeof(uint32_t), cudaHostAllocMapped));
     std::memset(c->fastbox, 0, 128 * sizeof(uint32_t));
     DK_CUDA(cudaMalloc(reinterpret_cast<void**>(&c->dmailbox), 64 * sizeof(uint64_t)));
+    {  // leader_info_kernel's accumulators (words 0-3) and CTA counter (word 12), re-armed by the kernel
+        uint32_t init[128] = {};
+        init[0] = init[1] = 0xffffffffu;
+        DK_CUDA(cudaMemcpy(c->dmailbox, init, sizeof(init), cudaMemcpyHostToDevice));
+    }
     DK_CUDA(cudaEventCreate(&c->ev0));
     DK_CUDA(cudaEventCreate(&c->ev1));
     DK_CUDA(cudaEventCreateWithFlags(&c->info_ev, cudaEventDisableTiming));

@@ -73,9 +73,13 @@ __device__ __forceinline__ uint32_t flags4(uint32_t w, uint32_t a0) {  // byte j
     return (__vcmpne4(w, 0u) & 0x01010101u) ^ (a0 * 0x01010101u);
 }
 
+// info: accumulators {min acc, min rej, #acc, #rej} at words 0-3 and a CTA
+// counter at word 12, armed at context creation; the last CTA copies the
+// totals to `out` (device memory or mapped pinned host memory) and re-arms
+// them -- no memsets before and no copy-engine readback after the kernel.
 __global__ void __launch_bounds__(kThreads) leader_info_kernel(const uint8_t* __restrict__ acc, uint32_t n,
                                                                uint32_t* __restrict__ info,
-                                                               uint8_t* __restrict__ dense2) {
+                                                               uint8_t* __restrict__ dense2, uint32_t* out) {
     __shared__ uint32_t red[4][kThreads / 32];
     uint32_t mina = kNone, minr = kNone, ca = 0, cr = 0;
     const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
@@ -131,6 +135,25 @@ __global__ void __launch_bounds__(kThreads) leader_info_kernel(const uint8_t* __
             if (minr != kNone) atomicMin(&info[1], minr);
             if (ca) atomicAdd(&info[2], ca);
             if (cr) atomicAdd(&info[3], cr);
+        }
+    }
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(&info[12], 1u) == gridDim.x - 1) {  // last CTA: publish and re-arm
+            __threadfence();
+            volatile uint32_t* vi = info;
+            volatile uint32_t* o = out;
+            const uint32_t r0 = vi[0], r1 = vi[1], r2 = vi[2], r3 = vi[3];
+            o[0] = r0;
+            o[1] = r1;
+            o[2] = r2;
+            o[3] = r3;
+            vi[0] = kNone;
+            vi[1] = kNone;
+            vi[2] = 0;
+            vi[3] = 0;
+            vi[12] = 0;
+            __threadfence_system();
         }
     }
 }
@@ -1240,29 +1263,28 @@ __global__ void __launch_bounds__(kThreads) small_persistent_kernel(SmallArgs A)
 
 LeaderInfo leader_info(Ctx* ctx, const DevDfa& d, cudaStream_t s) {
     uint32_t* info = reinterpret_cast<uint32_t*>(ctx->dmailbox);
-    const uint32_t init[4] = {kNone, kNone, 0, 0};
-    DK_CUDA(cudaMemcpyAsync(info, init, sizeof(init), cudaMemcpyHostToDevice, s));
     DK_LAUNCH(ctx, leader_info_kernel, grid_for(d.n, kThreads, (unsigned)ctx->num_sms * 8u), kThreads, 0, s, d.acc,
-              d.n, info, (uint8_t*)nullptr);
+              d.n, info, (uint8_t*)nullptr, info + 16);
     LeaderInfo li;
-    read_words(ctx, info, sizeof(li), &li, s);
+    read_words(ctx, info + 16, sizeof(li), &li, s);
     return li;
 }
 
 void leader_info_async(Ctx* ctx, const DevDfa& d, cudaStream_t s, uint8_t* dense2) {
     uint32_t* info = reinterpret_cast<uint32_t*>(ctx->dmailbox);
-    DK_CUDA(cudaMemsetAsync(info, 0xff, 2 * sizeof(uint32_t), s));
-    DK_CUDA(cudaMemsetAsync(info + 2, 0, 2 * sizeof(uint32_t), s));
     DK_LAUNCH(ctx, leader_info_kernel, grid_for(d.n, kThreads, (unsigned)ctx->num_sms * 8u), kThreads, 0, s, d.acc,
-              d.n, info, dense2);
-    DK_CUDA(cudaMemcpyAsync(ctx->mailbox + 56, info, sizeof(LeaderInfo), cudaMemcpyDeviceToHost, s));
+              d.n, info, dense2, ctx->fastbox + 120);  // straight into mapped pinned memory
     DK_CUDA(cudaEventRecord(ctx->info_ev, s));
 }
 
 LeaderInfo leader_info_wait(Ctx* ctx) {
     DK_CUDA(cudaEventSynchronize(ctx->info_ev));
     LeaderInfo li;
-    std::memcpy(&li, ctx->mailbox + 56, sizeof(li));
+    const volatile uint32_t* v = ctx->fastbox + 120;
+    li.min_acc = v[0];
+    li.min_rej = v[1];
+    li.cnt_acc = v[2];
+    li.cnt_rej = v[3];
     return li;
 }
 
