@@ -410,12 +410,28 @@ __global__ void __launch_bounds__(kThreads) table_apply_vec_kernel(const uint32_
         for (uint32_t i = threadIdx.x; i < tsize; i += blockDim.x) {
             s_min[i] = tmin_g[i];
             s_cnt[i] = tcnt_g[i];
-            if (rank_g) s_rank[i] = rank_g[i];
         }
         __syncthreads();
         tmin = s_min;
         tcnt = s_cnt;
-        rank = rank_g ? s_rank : nullptr;
+        if (rank_g) {  // the ranks of the occupied entries, computed here (no rank kernel)
+            __shared__ uint32_t ws[kThreads / 32];
+            constexpr uint32_t per = kApplyStageMax / kThreads;  // entries per thread
+            const uint32_t e0 = threadIdx.x * per;
+            uint32_t c = 0;
+#pragma unroll
+            for (uint32_t j = 0; j < per; ++j) c += e0 + j < tsize && s_cnt[e0 + j] != 0;
+            uint32_t tot;
+            uint32_t r = block_exclusive_scan<kThreads>(c, &tot, ws);
+#pragma unroll
+            for (uint32_t j = 0; j < per; ++j)
+                if (e0 + j < tsize) {
+                    s_rank[e0 + j] = r;
+                    r += s_cnt[e0 + j] != 0;
+                }
+            __syncthreads();
+            rank = s_rank;
+        }
     }
     uint32_t heads = 0, ablk = 0, surv = 0;
     const uint64_t nv = m / 4;
@@ -1623,22 +1639,27 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
             // partition as one table key: the ranks of the occupied entries
             // are compact block ids, the next pass's key labels (no O(n) scan)
             const bool full = list == nullptr;
+            auto a16 = [](const void* x) { return ((uintptr_t)x & 15u) == 0; };
+            if (full) {
+                if (nbits <= 16 && !w.next16.get()) w.next16.alloc(n, s);
+                if (nbits > 16 && !w.next32.get()) w.next32.alloc(n, s);
+            }
+            const bool vec = full && a16(w.heads.get()) && a16(w.lab.get()) && a16(w.keep.get()) &&
+                             a16(nbits <= 16 ? (void*)w.next16.get() : (void*)w.next32.get());
+            const bool staged = vec && tsize <= kApplyStageMax;  // ranks computed by the apply kernel
             if (full) {
                 if (w.trank.n < tsize) w.trank.alloc(tsize, s);
-                if (tsize <= (1u << 14)) {
+                if (staged) {
+                    // ranks computed inside the apply kernel (w.trank only flags "full")
+                } else if (tsize <= (1u << 14)) {
                     DK_LAUNCH(ctx, table_rank_one_kernel, 1, 1024, 0, s, w.tcnt.get(), (uint32_t)tsize, w.trank.get());
                 } else {
                     DK_LAUNCH(ctx, table_occupied_kernel, grid_for(tsize), kThreads, 0, s, w.tcnt.get(),
                               (uint32_t)tsize, w.trank.get());
                     exclusive_scan_u32(ctx, w.trank.get(), w.trank.get(), tsize, nullptr, s);
                 }
-                if (nbits <= 16 && !w.next16.get()) w.next16.alloc(n, s);
-                if (nbits > 16 && !w.next32.get()) w.next32.alloc(n, s);
             }
-            auto a16 = [](const void* x) { return ((uintptr_t)x & 15u) == 0; };
-            const bool vec = full && a16(w.heads.get()) && a16(w.lab.get()) && a16(w.keep.get()) &&
-                             a16(nbits <= 16 ? (void*)w.next16.get() : (void*)w.next32.get());
-            if (vec && tsize <= kApplyStageMax)  // identity list, four states per thread, tables in smem
+            if (staged)  // identity list, four states per thread, tables in smem
                 DK_LAUNCH_B(ctx, (double)m * (9.0 + (nbits <= 16 ? 2.0 : 4.0)), table_apply_vec_kernel<true>,
                             grid_for((m + 3) / 4, kThreads, (unsigned)ctx->num_sms * 4u), kThreads, 0, s,
                             w.heads.get(), m, w.tmin.get(), w.tcnt.get(), w.lab.get(), w.keep.get(), w.trank.get(),
