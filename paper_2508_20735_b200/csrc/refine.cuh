@@ -50,7 +50,7 @@ struct ShardInit {
     uint64_t active_states;
 };
 ShardInit shard_init(Ctx* ctx, const DevDfa& d, uint32_t lo, uint32_t hi, uint32_t* lab, uint8_t* act,
-                     cudaStream_t s);
+                     cudaStream_t s, bool lazy = false);
 void shard_keylab(Ctx* ctx, const uint32_t* lab, uint32_t n, uint32_t num_blocks, const PassPlan& plan, void* out,
                   uint32_t* scratch, cudaStream_t s,
                   const uint8_t* initial_acc = nullptr);

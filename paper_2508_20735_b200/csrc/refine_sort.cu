@@ -2054,15 +2054,23 @@ SigParams sig_params(const PassPlan& plan, uint32_t k, uint64_t salt) {
 
 }  // namespace
 
+// lazy: skip the initial labels and survivor flags when the first pass will
+// overwrite them -- every state active and a counting-table pass whose key
+// labels come from the flags (its apply writes every label and flag of the
+// rank's range), as in the single-GPU engine.
 ShardInit shard_init(Ctx* ctx, const DevDfa& d, uint32_t lo, uint32_t hi, uint32_t* lab, uint8_t* act,
-                     cudaStream_t s) {
+                     cudaStream_t s, bool lazy) {
     ShardInit r{};
     if (d.n == 0) return r;
     LeaderInfo li = leader_info(ctx, d, s);
-    init_leader_labels(ctx, d, li, lab, s);
     r.num_blocks = (li.min_acc != kNone) + (li.min_rej != kNone);
     r.active_blocks = (li.cnt_acc >= 2) + (li.cnt_rej >= 2);
     r.active_states = (li.cnt_acc >= 2 ? li.cnt_acc : 0) + (li.cnt_rej >= 2 ? li.cnt_rej : 0);
+    if (lazy && r.active_states == d.n) {
+        const PassPlan p0 = plan_pass(d.n, d.k, r.num_blocks, r.active_states, 0, false);
+        if (p0.strategy == kPlanTable && p0.keylab_bytes != 0) return r;
+    }
+    init_leader_labels(ctx, d, li, lab, s);
     if (hi > lo)
         DK_LAUNCH(ctx, init_act_range_kernel, grid_for(hi - lo), kThreads, 0, s, d.acc, lo, hi,
                   (uint8_t)(li.cnt_acc >= 2), (uint8_t)(li.cnt_rej >= 2), act);

@@ -287,7 +287,7 @@ RefineResult sort_pr_sharded_device(Ctx* ctx, NcclComm* cm, const DevDfa& d, uin
             read_words(ctx, p + i, std::min<size_t>(112, count - i) * sizeof(uint32_t), out + i, s);
     };
 
-    const ShardInit si = shard_init(ctx, d, lo, hi, lab.get(), act.get(), s);
+    const ShardInit si = shard_init(ctx, d, lo, hi, lab.get(), act.get(), s, /*lazy=*/true);
     uint32_t B = si.num_blocks, A = si.active_blocks;
     uint64_t m_total = si.active_states;
     uint32_t m = 0;
@@ -435,7 +435,7 @@ RefineResult sort_pr_sharded_device(Ctx* ctx, NcclComm* cm, const DevDfa& d, uin
             lab_stale = true;  // all singletons: the numbering needs no labels
         }
         if (m_total == n) m = hi - lo;  // every state survives: the identity range, no compaction
-        else compact();
+        else if (m_total) compact();     // (none left: the loop ends, nothing to compact)
     }
     // an all-singleton partition is numbered by identity (no label exchange)
     if (lab_stale && B < n) cm->allgather(lab.get(), (size_t)shard * sizeof(uint32_t), s);
