@@ -1381,7 +1381,10 @@ SmallRun run_small_persistent(Ctx* ctx, const DevDfa& d, uint32_t* lab, uint32_t
     DK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, small_persistent_kernel, kThreads, 0));
     if (per_sm < 1) throw Error(DFAKIT_E_RESOURCE, "persistent sort_pr kernel does not fit an SM");
     const uint64_t want = (m + kThreads - 1) / kThreads;
-    const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)ctx->num_sms));
+    // one state per thread up to every resident CTA (a pass is a dependent
+    // chain per state: more CTAs beat the cheaper barrier of a smaller grid)
+    const unsigned grid =
+        (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)ctx->num_sms * (uint64_t)per_sm));
     void* kargs[] = {(void*)&args};
     prof_begin_launch(ctx, s);
     DK_CUDA(cudaLaunchCooperativeKernel((const void*)small_persistent_kernel, grid, kThreads, kargs, 0, s));
