@@ -400,7 +400,9 @@ __global__ void __launch_bounds__(kThreads) table_apply_vec_kernel(const uint32_
                                                                    const uint32_t* __restrict__ rank_g,
                                                                    uint16_t* __restrict__ next16,
                                                                    uint32_t* __restrict__ next32,
-                                                                   IterCounters* __restrict__ ctr, uint32_t tsize) {
+                                                                   IterCounters* __restrict__ ctr, uint32_t tsize,
+                                                                   uint8_t* __restrict__ act = nullptr,
+                                                                   uint32_t q0 = 0) {
     __shared__ uint32_t s_min[STAGE ? kApplyStageMax : 1], s_cnt[STAGE ? kApplyStageMax : 1],
         s_rank[STAGE ? kApplyStageMax : 1];
     const uint32_t* tmin = tmin_g;
@@ -443,7 +445,7 @@ __global__ void __launch_bounds__(kThreads) table_apply_vec_kernel(const uint32_
             uint32_t rep[4], rk[4], kp = 0;
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-                const uint32_t q = (uint32_t)(4 * v + j);
+                const uint32_t q = q0 + (uint32_t)(4 * v + j);
                 rep[j] = tmin[key[j]];
                 const bool multi = tcnt[key[j]] >= 2;
                 if (rank) rk[j] = rank[key[j]];
@@ -454,18 +456,20 @@ __global__ void __launch_bounds__(kThreads) table_apply_vec_kernel(const uint32_
             }
             __stcs(reinterpret_cast<uint4*>(lab) + v, make_uint4(rep[0], rep[1], rep[2], rep[3]));
             if (keep) reinterpret_cast<uint32_t*>(keep)[v] = kp;
+            if (act) reinterpret_cast<uint32_t*>(act)[v] = kp;  // survivor flags of a state range
             if (next16)
                 reinterpret_cast<uint2*>(next16)[v] = make_uint2((rk[0] & 0xffffu) | (rk[1] << 16),
                                                                  (rk[2] & 0xffffu) | (rk[3] << 16));
             if (next32) reinterpret_cast<uint4*>(next32)[v] = make_uint4(rk[0], rk[1], rk[2], rk[3]);
         } else {  // tail: m % 4 states, one per thread
             const uint64_t i = 4 * nv + (v - nv);
-            const uint32_t key = keys32[i], q = (uint32_t)i;
+            const uint32_t key = keys32[i], q = q0 + (uint32_t)i;
             const uint32_t rep = tmin[key];
             const bool multi = tcnt[key] >= 2;
-            lab[q] = rep;
-            if (next16) next16[q] = (uint16_t)rank[key];
-            if (next32) next32[q] = rank[key];
+            lab[i] = rep;
+            if (next16) next16[i] = (uint16_t)rank[key];
+            if (next32) next32[i] = rank[key];
+            if (act) act[i] = multi;
             if (keep) keep[i] = multi;
             heads += rep == q;
             ablk += (rep == q) && multi;
@@ -2133,12 +2137,27 @@ void shard_table_apply(Ctx* ctx, const PassPlan& plan, const uint32_t* list, uin
     // compact block ids of the next partition when the pass covered every state
     DBuf<uint32_t> rank;
     const uint32_t tsize = 1u << plan.key_bits;
+    const bool narrow = plan.key_bits <= 16;
+    // a state range starting at a multiple of four with a small table: the
+    // vectorised apply with the table (and its ranks) staged in shared memory
+    auto a16 = [](const void* x) { return ((uintptr_t)x & 15u) == 0; };
+    uint32_t* lab_r = lab + list_base;
+    void* next_r = next_keylab ? static_cast<char*>(next_keylab) + (size_t)list_base * (narrow ? 2 : 4) : nullptr;
+    if (!list && list_base % 4 == 0 && tsize <= kApplyStageMax && a16(keys32) && a16(lab_r) &&
+        (!next_r || (narrow ? ((uintptr_t)next_r & 7u) == 0 : a16(next_r)))) {
+        DK_LAUNCH_B(ctx, (double)m * 13.0, table_apply_vec_kernel<true>,
+                    grid_for((m + 3) / 4, kThreads, (unsigned)ctx->num_sms * 4u), kThreads, 0, s, keys32, m, tmin,
+                    tcnt, lab_r, (uint8_t*)nullptr, next_r ? tcnt : nullptr /* ranks: computed in the kernel */,
+                    next_r && narrow ? static_cast<uint16_t*>(next_r) : nullptr,
+                    next_r && !narrow ? static_cast<uint32_t*>(next_r) : nullptr, reinterpret_cast<IterCounters*>(counters),
+                    tsize, act + list_base, list_base);
+        return;
+    }
     if (next_keylab) {
         rank.alloc(tsize, s);
         DK_LAUNCH(ctx, table_occupied_kernel, grid_for(tsize), kThreads, 0, s, tcnt, tsize, rank.get());
         exclusive_scan_u32(ctx, rank.get(), rank.get(), tsize, nullptr, s);
     }
-    const bool narrow = plan.key_bits <= 16;
     DK_LAUNCH_B(ctx, (double)m * 13.0, table_apply_kernel, grid_for(m), kThreads, 0, s, list, keys32, m, tmin, tcnt,
                 lab, nullptr, act, rank.get(), next_keylab && narrow ? static_cast<uint16_t*>(next_keylab) : nullptr,
                 next_keylab && !narrow ? static_cast<uint32_t*>(next_keylab) : nullptr, list_base,

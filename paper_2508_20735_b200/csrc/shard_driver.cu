@@ -272,7 +272,8 @@ RefineResult sort_pr_sharded_device(Ctx* ctx, NcclComm* cm, const DevDfa& d, uin
     const int world = cm->world, rank = cm->rank;
     if (n == 0) return res;
     if (n > 0x7fffffffu) throw Error(DFAKIT_E_INVALID, "sharded sort_pr: at most 2^31 - 1 states");
-    const uint32_t shard = (uint32_t)(((uint64_t)n + world - 1) / world);
+    // ranges start at multiples of four (the vectorised table apply)
+    const uint32_t shard = (uint32_t)((((uint64_t)n + world - 1) / world + 3) / 4 * 4);
     const uint32_t lo = std::min<uint64_t>(n, (uint64_t)rank * shard);
     const uint32_t hi = std::min<uint64_t>(n, (uint64_t)(rank + 1) * shard);
     DBuf<uint32_t> lab((uint64_t)world * shard, s), list(std::max(1u, hi - lo), s), scratch((uint64_t)n + 1, s);
