@@ -26,6 +26,7 @@ def main():
     p.add_argument("--algo", default=None)
     p.add_argument("--reps", type=int, default=3)
     p.add_argument("--grouping", type=int, default=0, help="dfakit_options.grouping (1 = radix_sort)")
+    p.add_argument("--host", action="store_true", help="synth: through dfakit_minimize with pinned host buffers")
     a = p.parse_args()
     import torch
     import paper_2508_20735_b200 as dk
@@ -60,6 +61,21 @@ def main():
         nat.check(nat.lib.dfakit_minimize_device(ctx.handle, C.byref(view), int(dk.Algorithm[algo]), C.byref(opts),
                                                  out.data_ptr(), C.byref(rep), ctx.stream))
         return rep
+
+    if a.host and w == "synth":
+        hd = torch.empty(k * n, dtype=torch.int32, pin_memory=True)
+        ha = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+        hb = torch.empty(n, dtype=torch.int32, pin_memory=True)
+        hd.copy_(delta.cpu())
+        ha.copy_(accd.cpu())
+        hview = nat.CDfa(n, k, hd.data_ptr(), ha.data_ptr(), -1)
+
+        def run():  # noqa: F811
+            rep = nat.CReport()
+            opts = nat.COptions(0, 0, 0, 1 << 40, 1 << 24, 64, a.grouping)
+            nat.check(nat.lib.dfakit_minimize(ctx.handle, C.byref(hview), int(dk.Algorithm[algo]), C.byref(opts),
+                                              hb.data_ptr(), C.byref(rep)))
+            return rep
 
     if w == "equiv":
         d2 = torch.empty(k * n, dtype=torch.int32, device="cuda")
