@@ -519,13 +519,36 @@ __global__ void dense2_kernel(const uint32_t* __restrict__ lab, uint32_t n, uint
 }
 
 // delta targets of states [q0, q1) must be < n (reference dfa.cpp validation)
-__global__ void range_check_rows_kernel(const uint32_t* __restrict__ delta, uint32_t n, uint32_t k, uint32_t q0,
+// (letter a0 + blockIdx.y; 16-byte loads where the row segment allows: a
+// 64-bit division per element made the check of a streamed chunk cost more
+// than the chunk's signature pass)
+__global__ void range_check_rows_kernel(const uint32_t* __restrict__ delta, uint32_t n, uint32_t a0, uint32_t q0,
                                         uint32_t q1, uint32_t* __restrict__ bad) {
-    const uint64_t w = q1 - q0, total = w * k;
+    const uint32_t* row = delta + (uint64_t)(a0 + blockIdx.y) * n;
+    const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
+    uint32_t lo = q0;
     bool b = false;
-    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total; t += (uint64_t)gridDim.x * blockDim.x)
-        b |= __ldcs(delta + (t / w) * n + q0 + t % w) >= n;
+    // scalar head up to a 16-byte boundary, then four per load
+    const uint32_t head = min(q1 - q0, (uint32_t)((4u - ((uintptr_t)(row + q0) >> 2)) & 3u));
+    for (uint32_t q = q0 + tid; q < q0 + head; q += stride) b |= __ldcs(row + q) >= n;
+    lo = q0 + head;
+    const uint32_t nv = (q1 - lo) / 4;
+    const uint4* v4 = reinterpret_cast<const uint4*>(row + lo);
+    for (uint32_t v = tid; v < nv; v += stride) {
+        const uint4 x = __ldcs(v4 + v);
+        b |= (x.x >= n) | (x.y >= n) | (x.z >= n) | (x.w >= n);
+    }
+    for (uint32_t q = lo + 4 * nv + tid; q < q1; q += stride) b |= __ldcs(row + q) >= n;
     if (__syncthreads_or(b) && threadIdx.x == 0) atomicOr(bad, 1u);
+}
+
+void range_check_rows(Ctx* ctx, const uint32_t* delta, uint32_t n, uint32_t k, uint32_t q0, uint32_t q1, uint32_t* bad,
+                      cudaStream_t s) {
+    if (q1 <= q0) return;
+    const unsigned gx = grid_for((uint64_t)(q1 - q0) / 4 + 1, kThreads, 148u * 4u);
+    for (uint32_t a0 = 0; a0 < k; a0 += 65535u)
+        DK_LAUNCH_B(ctx, 4.0 * (q1 - q0) * std::min(k - a0, 65535u), range_check_rows_kernel,
+                    dim3(gx, std::min(k - a0, 65535u)), kThreads, 0, s, delta, n, a0, q0, q1, bad);
 }
 
 // bitmap of a two-block partition: bit q = (lab[q] != lab[0]); one warp per word
@@ -1519,7 +1542,7 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
         if (!streamed) return;
         for (uint32_t c = 0; c < ds->chunks; ++c) DK_CUDA(cudaStreamWaitEvent(s, ds->ready[c], 0));
         DK_CUDA(cudaMemsetAsync(bad, 0, 4, s));
-        DK_LAUNCH(ctx, range_check_rows_kernel, grid_for((uint64_t)n * k), kThreads, 0, s, d.delta, n, k, 0u, n, bad);
+        range_check_rows(ctx, d.delta, n, k, 0u, n, bad, s);
         check_streamed();
     };
     while (m > 0) {
@@ -1634,8 +1657,7 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
                     const uint32_t q0 = ds->bounds[c], q1 = ds->bounds[c + 1];
                     DK_CUDA(cudaStreamWaitEvent(s, ds->ready[c], 0));
                     if (q1 == q0) continue;
-                    DK_LAUNCH(ctx, range_check_rows_kernel, grid_for((uint64_t)(q1 - q0) * k), kThreads, 0, s,
-                              d.delta, n, k, q0, q1, bad);
+                    range_check_rows(ctx, d.delta, n, k, q0, q1, bad, s);
                     sig_table(q0, q1 - q0, true);
                 }
             } else {
