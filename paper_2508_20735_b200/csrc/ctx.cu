@@ -95,6 +95,7 @@ void read_words(Ctx* ctx, const void* dsrc, size_t bytes, void* hdst, cudaStream
     const uint32_t seq = ++ctx->fast_seq;
     mailbox_kernel<<<1, 128, 0, s>>>(static_cast<const uint8_t*>(dsrc), (uint32_t)bytes, ctx->fastbox, seq);
     DK_CUDA(cudaGetLastError());
+    note_launch(ctx);
     // spin for short waits (the pass loop's readbacks follow sub-millisecond
     // kernels); past ~200 us block in cudaStreamSynchronize instead of
     // burning a core behind a long kernel
