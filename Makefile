@@ -16,7 +16,7 @@ CU_OBJS  := $(patsubst $(CSRC)/%.cu,$(BUILD)/%.o,$(CU_SRCS))
 HOST_SRCS:= $(wildcard $(CSRC)/host/*.cpp)
 HOST_OBJS:= $(patsubst $(CSRC)/host/%.cpp,$(BUILD)/host_%.o,$(HOST_SRCS))
 
-all: $(LIB) bin/dfakit oracle
+all: $(LIB) bin/dfakit oracle refsuites
 
 $(BUILD)/%.o: $(CSRC)/%.cu $(wildcard $(CSRC)/*.cuh) include/dfakit_b200.h
 	@mkdir -p $(BUILD)
@@ -37,8 +37,14 @@ bin/dfakit: $(CSRC)/cli/dfakit_cli.cpp $(LIB) include/dfakit_b200.hpp
 oracle:
 	$(MAKE) -s -C oracle
 
+# the reference's own unit suites + acceptance harness, compiled unchanged
+# against include/ and the library (needs /root/reference; no-op without it)
+refsuites: $(LIB) bin/dfakit
+	$(MAKE) -s -C tests/refsuites
+
 clean:
 	rm -rf $(BUILD) $(PKG)/lib bin
 	$(MAKE) -s -C oracle clean
+	$(MAKE) -s -C tests/refsuites clean
 
-.PHONY: all oracle clean
+.PHONY: all oracle refsuites clean

@@ -8,12 +8,14 @@ Default workload (BASELINE.json configs[1]): 10M states x |Sigma| = 10 =
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
-N = 1: the single-GPU engine (dfakit_minimize_device).  N > 1 (torchrun, one
-rank per GPU, NCCL): the sharded engine (paper_2508_20735_b200/sharded.py)
-on ONE automaton of N x 10M states (weak scaling: 100M transitions per GPU;
-N = 8 is the 800M-transition neighbourhood of configs[4]); per pass the
-label slices are allgathered and the wide-key entries exchanged all-to-all
-over NVLink; the step time is the max over ranks.
+N = 1: the single-GPU engine (dfakit_minimize_device).  N > 1: one rank per
+GPU over NCCL -- launched by the driver under torchrun, or, when WORLD_SIZE
+is unset, by this script re-executing itself under torch.distributed.run --
+the native sharded engine on ONE automaton of N x 10M states (weak scaling:
+100M transitions per GPU); per pass the label slices are allgathered and the
+wide-key entries exchanged all-to-all over NVLink; the step time is the max
+over ranks.  Beside the headline, `strong_scaling` times BASELINE configs[4]:
+one fixed 100M x 10 (1B-transition) automaton on all N GPUs.
 
 --impl reference times the reference's own CPU sort_pr (oracle/_ref, the
 unmodified reference sources compiled in place) on a bounded sample of the
@@ -27,6 +29,7 @@ import json
 import re
 import os
 import socket
+import subprocess
 import sys
 import threading
 import time
@@ -53,7 +56,26 @@ def parse_args():
     p.add_argument("--seed", type=int, default=1)
     p.add_argument("--no-extras", action="store_true", help="skip the secondary configs")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-strong", action="store_true", help="skip the configs[4] strong-scaling record")
+    p.add_argument("--dry-run", action="store_true",
+                   help="launcher check only (CPU, gloo): spawn / rendezvous / max-over-ranks, no device work")
     return p.parse_args()
+
+
+def ensure_ranks(args):
+    """`bench.py --gpus N` outside torchrun re-executes itself under
+    torch.distributed.run with N ranks (one per GPU); under torchrun the
+    world size must equal --gpus.  Returns only in a correctly sized rank."""
+    world_env = os.environ.get("WORLD_SIZE")
+    if world_env is None:
+        if args.gpus <= 1:
+            return
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+        env = dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "1"))
+        sys.exit(subprocess.call(cmd, env=env))
+    if int(world_env) != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world_env} (launch one rank per GPU)")
 
 
 def dist_env():
@@ -289,6 +311,8 @@ def run_b200(args, rank, world, local):
     from paper_2508_20735_b200 import _native as nat
     from paper_2508_20735_b200 import sharded
 
+    if torch.cuda.device_count() < world:
+        raise SystemExit(f"bench.py: --gpus {world} needs {world} visible devices, found {torch.cuda.device_count()}")
     torch.cuda.set_device(local)
     engine = args.engine if args.engine != "auto" else ("single" if world == 1 else "sharded")
     import torch.distributed as dist
@@ -444,6 +468,17 @@ def run_b200(args, rank, world, local):
             "vs_baseline": None, "dtype": "u32", "data": "synthetic", "config": cfg, "roofline": roofline, "e2e": e2e,
             "gpu_launches": int(launches), "clocks": clocks.summary()}
 
+    # free the headline automaton before the configs[4] record
+    del delta, acc, blocks, h_delta, h_acc, h_blocks
+    if sharded_engine:
+        state.pop("out", None)
+    if engine == "sharded":
+        ncomm.close()
+    torch.cuda.empty_cache()
+    if not args.no_strong:
+        line["strong_scaling"] = strong_scaling_1b(args, dk, nat, sharded, torch, ctx, rank, world, barrier,
+                                                   max_over_ranks)
+
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(k, args.seed)
     if rank == 0 and world == 1 and not args.no_extras:
@@ -452,6 +487,80 @@ def run_b200(args, rank, world, local):
         print(json.dumps(line), flush=True)
     if use_dist:
         dist.destroy_process_group()
+
+
+def strong_scaling_1b(args, dk, nat, sharded, torch, ctx, rank, world, barrier, max_over_ranks):
+    """BASELINE configs[4]: ONE fixed 1B-transition automaton (100M states x
+    |Sigma| = 10, the bench generator) minimised on all N GPUs -- strong
+    scaling.  N = 1: the single-GPU engine (and the native sharded engine at
+    world size 1 beside it); N > 1: the native sharded engine over NCCL, the
+    automaton replicated on every rank, states sharded in contiguous ranges.
+    Device time with CUDA events, max over ranks."""
+    n, k = 100_000_000, 10
+    steps = max(1, min(args.steps, 5))
+    d = torch.empty(k * n, dtype=torch.int32, device="cuda")
+    a = torch.empty(n, dtype=torch.uint8, device="cuda")
+    b = torch.empty(n, dtype=torch.int32, device="cuda")
+    nat.check(nat.lib.dfakit_gen_synth_device(ctx.handle, n, k, args.seed, d.data_ptr(), a.data_ptr(), ctx.stream))
+    torch.cuda.synchronize()
+    st = {}
+    rep = nat.CReport()
+    opts = nat.COptions(0, 0, 0, 0, 0, 64, 0)
+    view = nat.CDfa(n, k, d.data_ptr(), a.data_ptr(), -1)
+
+    def single():
+        nat.check(nat.lib.dfakit_minimize_device(ctx.handle, C.byref(view), int(dk.Algorithm.sort_pr), C.byref(opts),
+                                                 b.data_ptr(), C.byref(rep), ctx.stream))
+        st["passes"], st["iters"], st["blocks"] = int(rep.passes), int(rep.refining_iterations), int(rep.num_blocks)
+
+    ncomm = sharded.NativeComm(ctx) if world > 1 else None
+
+    def shard(comm):
+        def f():
+            _, r = sharded.sort_pr_sharded_native(ctx, comm, d, a, n, k, out=b)
+            st["passes"], st["iters"], st["blocks"] = r.passes, r.refining_iterations, r.num_blocks
+            st["exchanged"] = r.exchanged_entries
+        return f
+
+    stream = torch.cuda.ExternalStream(ctx.stream)
+
+    def timeit(fn):
+        for _ in range(2):
+            fn()
+        torch.cuda.synchronize()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            fn()
+        e1.record(stream)
+        e1.synchronize()
+        torch.cuda.synchronize()
+        barrier()
+        return max_over_ranks(e0.elapsed_time(e1)) / steps
+
+    out = {"workload": "sort_pr random DFA 100M states x |Sigma|=10 (1000M transitions), BASELINE configs[4]",
+           "scaling": "strong", "n_gpus": world, "steps": steps, "warmup": 2}
+    if world == 1:
+        ms = timeit(single)
+        out["engine"] = "single"
+        c1 = sharded.NativeComm(ctx)
+        out["sharded_native_world1_ms"] = timeit(shard(c1))
+        c1.close()
+    else:
+        ms = timeit(shard(ncomm))
+        out["engine"] = "sharded (native, NCCL)"
+        ex = st.get("exchanged", 0)
+        nv = 20 * ex + 4 * n * (world - 1) / world * max(st["iters"], 1)
+        out["nvlink"] = {"bytes_per_rank_per_step": nv, "GBps_per_rank": nv / (ms / 1000.0) / 1e9, "peak_GBps": 770.0,
+                         "frac": nv / (ms / 1000.0) / 1e9 / 770.0,
+                         "peak_source": "B200_PROFILING.md measured peer copy per direction"}
+        ncomm.close()
+    out.update({"ms_per_step": ms, "passes": st["passes"], "refining_iterations": st["iters"],
+                "num_blocks": st["blocks"], "value": n * k * st["passes"] / (ms / 1000.0), "unit": UNIT})
+    del d, a, b
+    torch.cuda.empty_cache()
+    return out
 
 
 def pcie_bound(torch, h_in, d_in, h_out, d_out, h2d, d2h, e2e_s):
@@ -561,22 +670,6 @@ def extras(dk, nat, ctx, torch, sharded, args):
                                                     "transitions_per_s": n * k * rr.passes / s}
     ncomm.close()
     del d, a, b
-    # configs[4] size on one GPU: 1B transitions (100M states x |Sigma| = 10),
-    # single-GPU engine and the native sharded engine at world size 1
-    n, k = 100_000_000, 10
-    d = torch.empty(k * n, dtype=torch.int32, device="cuda")
-    a = torch.empty(n, dtype=torch.uint8, device="cuda")
-    b = torch.empty(n, dtype=torch.int32, device="cuda")
-    nat.check(nat.lib.dfakit_gen_synth_device(ctx.handle, n, k, args.seed, d.data_ptr(), a.data_ptr(), ctx.stream))
-    view = nat.CDfa(n, k, d.data_ptr(), a.data_ptr(), -1)
-    s, r = timed(minimize(view, "sort_pr", b, nat.COptions(0, 0, 0, 0, 0, 64, 0)), 2)
-    out["sort_pr_1B_transitions_single"] = {"ms": s * 1000, "passes": int(r.passes), "blocks": int(r.num_blocks),
-                                            "transitions_per_s": n * k * int(r.passes) / s}
-    ncomm = sharded.NativeComm(ctx)
-    s, (bl, rr) = timed(lambda: sharded.sort_pr_sharded_native(ctx, ncomm, d, a, n, k, out=b), 2)
-    out["sort_pr_1B_transitions_sharded_native_world1"] = {"ms": s * 1000, "passes": rr.passes,
-                                                           "transitions_per_s": n * k * rr.passes / s}
-    ncomm.close()
     if own_pg:
         dist.destroy_process_group()
     del d, a, b
@@ -729,12 +822,35 @@ def extras(dk, nat, ctx, torch, sharded, args):
     return out
 
 
+def run_dry(args, rank, world):
+    """Launcher check without a device: every rank joins a gloo group, the
+    step time is reduced MAX over ranks, rank 0 prints the line skeleton."""
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        dist.init_process_group("gloo")
+    t0 = time.perf_counter()
+    time.sleep(0.01 * (rank + 1))
+    ms = torch.tensor([(time.perf_counter() - t0) * 1000.0], dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": None, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                          "warmup": args.warmup, "ms_per_step": float(ms[0]), "impl": args.impl, "dry_run": True}),
+              flush=True)
+
+
 def main():
     # one JSON line on stdout: keep NCCL's version banner off it
     if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
         os.environ["NCCL_DEBUG"] = "WARN"
     args = parse_args()
+    ensure_ranks(args)
     rank, world, local = dist_env()
+    if args.dry_run:
+        run_dry(args, rank, world)
+        return
     if args.impl == "reference":
         run_reference_arm(args, rank, world)
         return

@@ -227,6 +227,13 @@ struct ArrLab {
     const T* p;
     __device__ __forceinline__ uint32_t operator[](uint32_t i) const { return (uint32_t)__ldg(p + i); }
 };
+// Labels rewritten inside the same launch (the persistent small-m engine):
+// plain coherent loads, ordered by grid.sync().  __ldg's non-coherent path is
+// only defined for data that stays read-only for the whole kernel.
+struct CohLab {
+    const uint32_t* p;
+    __device__ __forceinline__ uint32_t operator[](uint32_t i) const { return p[i]; }
+};
 struct BitLab {
     const uint32_t* w;
     __device__ __forceinline__ uint32_t operator[](uint32_t i) const { return (__ldg(w + (i >> 5)) >> (i & 31u)) & 1u; }
@@ -1190,7 +1197,7 @@ __global__ void __launch_bounds__(kThreads) small_persistent_kernel(SmallArgs A)
         // keys, insert, elect the run minimum, count the run (slot T: a ~0 key)
         for (uint32_t i = tid; i < m; i += stride) {
             const uint32_t q = list[i];
-            const uint64_t key = tuple_key<ArrLab<uint32_t>, 8>(q, A.lab[q], A.delta, A.n, ArrLab<uint32_t>{A.lab}, p);
+            const uint64_t key = tuple_key<CohLab, 8>(q, A.lab[q], A.delta, A.n, CohLab{A.lab}, p);
             const unsigned long long hk = p.kind == kKeyPacked ? mix64(key) : key;
             uint32_t sl;
             if (hk == kEmptyKey) {
@@ -1227,7 +1234,7 @@ __global__ void __launch_bounds__(kThreads) small_persistent_kernel(SmallArgs A)
                 A.lab[q] = r;
                 const uint32_t at = warp_append(&c->listed, multi);
                 if (multi) next[at] = q;
-            } else if (!head && !same_tuple(q, r, A.delta, A.n, A.k, ArrLab<uint32_t>{A.lab})) {
+            } else if (!head && !same_tuple(q, r, A.delta, A.n, A.k, CohLab{A.lab})) {
                 clash = true;
             }
         }

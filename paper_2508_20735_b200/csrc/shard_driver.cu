@@ -371,6 +371,10 @@ RefineResult sort_pr_sharded_device(Ctx* ctx, NcclComm* cm, const DevDfa& d, uin
             }
             shard_table_apply(ctx, plan, lst, lo, keys32.get(), m, tmin.get(), tcnt.get(), lab.get(), act.get(),
                               next_kl, dctr.get(), s);
+            // only this rank's slice of `lab` was written (after a lazy
+            // shard_init the other slices were never initialised): a fixed
+            // point reached here must still exchange them before numbering
+            lab_stale = true;
             cm->allreduce_u32(dctr.get(), 4, false, s);
             read_u32(dctr.get(), 4, ctr);
         } else {

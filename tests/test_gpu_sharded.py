@@ -27,6 +27,10 @@ CASES = [
     ("family", 7, 0, 0.0, 0),
     ("family", 12, 0, 0.0, 1),
     ("synth", 1_000_000, 10, 0.0, 3),
+    # stable initial split {F, Q \ F}: refine_iters == 0 (the first pass is a
+    # table pass that reaches the fixed point before any label exchange)
+    ("random", 5000, 3, 1.0, 16),
+    ("parity", 3000, 4, 0.0, 0),
 ]
 
 
@@ -39,6 +43,11 @@ def make_case(case):
         d, a, _ = o.gen_random(n, k, frac, seed)
     elif kind == "synth":
         d, a, _ = o.gen_synth(n, k, seed)
+    elif kind == "parity":  # n copies of the 2-state parity automaton over k letters
+        q = np.arange(2 * n, dtype=np.uint32)
+        d = np.tile(q, (k, 1))
+        d[0] ^= 1
+        a = (q & 1).astype(np.uint8)
     elif kind == "copies":
         base, acc0, _ = o.gen_random(n, k, frac, seed)
         c = 30
