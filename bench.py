@@ -544,9 +544,17 @@ def strong_scaling_1b(args, dk, nat, sharded, torch, ctx, rank, world, barrier, 
     if world == 1:
         ms = timeit(single)
         out["engine"] = "single"
+        import torch.distributed as dist
+        own_pg = not dist.is_initialized()
+        if own_pg:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ["MASTER_PORT"] = str(free_port())
+            dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", ctx.device))
         c1 = sharded.NativeComm(ctx)
         out["sharded_native_world1_ms"] = timeit(shard(c1))
         c1.close()
+        if own_pg:
+            dist.destroy_process_group()
     else:
         ms = timeit(shard(ncomm))
         out["engine"] = "sharded (native, NCCL)"

@@ -290,7 +290,9 @@ __global__ void __launch_bounds__(kThreads) signature_kernel(const uint32_t* __r
 // ---- table strategy -----------------------------------------------------------------
 
 // step 1: signature + table of (run minimum, run size), in shared memory
-// when <= 13 bits; equal keys of a warp are combined first (match_any)
+// when <= 13 bits; equal keys of a warp are combined first (match_any).
+// Run sizes are only compared with 0 and 2: the shared-memory path keeps
+// them saturated (any value >= 2 means "two or more").
 template <typename LR, bool CLAMP = false>
 __global__ void __launch_bounds__(512, 3) sig_table_kernel(const uint32_t* __restrict__ list, uint64_t m,
                                                         const uint32_t* __restrict__ delta, uint32_t n,
@@ -316,15 +318,23 @@ __global__ void __launch_bounds__(512, 3) sig_table_kernel(const uint32_t* __res
         const unsigned peers = __match_any_sync(__activemask(), key);
         const uint32_t mq = __reduce_min_sync(peers, q);
         if ((threadIdx.x & 31u) == (unsigned)(__ffs(peers) - 1)) {
-            atomicMin(local ? &smin[key] : &tmin[key], mq);
-            atomicAdd(local ? &scnt[key] : &tcnt[key], (uint32_t)__popc(peers));
+            if (local) {
+                // counts are only ever tested for 0 / 1 / >= 2: one shared
+                // atomic per warp-distinct key (the minimum's old value says
+                // whether the key was seen before), the count saturates at 2
+                const uint32_t old = atomicMin(&smin[key], mq);
+                if (old != kNone || __popc(peers) >= 2) scnt[key] = 2u;
+            } else {
+                atomicMin(&tmin[key], mq);
+                atomicAdd(&tcnt[key], (uint32_t)__popc(peers));
+            }
         }
     }
     if (local) {
         __syncthreads();
         for (uint32_t e = threadIdx.x; e < tsize; e += blockDim.x)
-            if (scnt[e]) {
-                atomicAdd(&tcnt[e], scnt[e]);
+            if (smin[e] != kNone) {
+                atomicAdd(&tcnt[e], scnt[e] ? 2u : 1u);
                 atomicMin(&tmin[e], smin[e]);
             }
     }
