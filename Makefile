@@ -42,9 +42,19 @@ oracle:
 refsuites: $(LIB) bin/dfakit
 	$(MAKE) -s -C tests/refsuites
 
+# tuning experiments: make variant V=name DEFS="-DDFAKIT_X=Y" builds
+# $(PKG)/lib/variants/libdfakit_b200_name.so (loaded with DFAKIT_LIB_VARIANT=name)
+VOBJS = $(patsubst $(CSRC)/%.cu,$(BUILD)/v_$(V)/%.o,$(CU_SRCS))
+$(BUILD)/v_$(V)/%.o: $(CSRC)/%.cu $(wildcard $(CSRC)/*.cuh) include/dfakit_b200.h
+	@mkdir -p $(BUILD)/v_$(V)
+	$(NVCC) $(NVFLAGS) $(DEFS) -c $< -o $@ 2> $(BUILD)/v_$(V)/$*.ptxas.log || (cat $(BUILD)/v_$(V)/$*.ptxas.log; false)
+variant: $(VOBJS) $(HOST_OBJS)
+	@mkdir -p $(PKG)/lib/variants
+	$(NVCC) $(ARCH) -shared -o $(PKG)/lib/variants/libdfakit_b200_$(V).so $^ -Xcompiler -fPIC -lcudart_static -lpthread -ldl -lrt
+
 clean:
 	rm -rf $(BUILD) $(PKG)/lib bin
 	$(MAKE) -s -C oracle clean
 	$(MAKE) -s -C tests/refsuites clean
 
-.PHONY: all oracle refsuites clean
+.PHONY: all oracle refsuites clean variant

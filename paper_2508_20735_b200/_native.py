@@ -12,6 +12,10 @@ import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "lib", "libdfakit_b200.so")
+# development only: DFAKIT_LIB_VARIANT=name loads lib/variants/libdfakit_b200_<name>.so
+# (the same sources built with different compile-time tuning, `make variant`)
+if os.environ.get("DFAKIT_LIB_VARIANT"):
+    LIB_PATH = os.path.join(_HERE, "lib", "variants", f"libdfakit_b200_{os.environ['DFAKIT_LIB_VARIANT']}.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

@@ -214,16 +214,24 @@ struct SigParams {
     uint32_t q0;          // list == nullptr: the active states are q0, q0 + 1, ...
 };
 
-__device__ __forceinline__ uint64_t fp_step(uint64_t h, uint32_t x) {
-    return mix64(h ^ ((uint64_t)x * 0xD6E8FEB86659FD93ull));
-}
+#ifndef DFAKIT_SIGB_MINB
+#define DFAKIT_SIGB_MINB 5
+#endif
+#ifndef DFAKIT_SIGB_CH
+#define DFAKIT_SIGB_CH 16
+#endif
+// one fingerprint round over a 64-bit word of packed labels
+__device__ __forceinline__ uint64_t fp_word(uint64_t h, uint64_t w) { return mix64(h ^ w); }
 
 // Key-label readers: a dense / min-state label array of T, or one bit per
 // state (a two-block partition: the initial {F, Q \ F} of every run -- a
 // 10M-state automaton's bitmap is 1.25 MB and stays L2-resident where a byte
 // array of a 100M-state one does not).
+// kBits: the reader's label width (fingerprints pack 64 / kBits labels per
+// hashed word).
 template <typename T>
 struct ArrLab {
+    static constexpr int kBits = 8 * (int)sizeof(T);
     const T* p;
     __device__ __forceinline__ uint32_t operator[](uint32_t i) const { return (uint32_t)__ldg(p + i); }
 };
@@ -231,10 +239,12 @@ struct ArrLab {
 // plain coherent loads, ordered by grid.sync().  __ldg's non-coherent path is
 // only defined for data that stays read-only for the whole kernel.
 struct CohLab {
+    static constexpr int kBits = 32;
     const uint32_t* p;
     __device__ __forceinline__ uint32_t operator[](uint32_t i) const { return p[i]; }
 };
 struct BitLab {
+    static constexpr int kBits = 1;
     const uint32_t* w;
     __device__ __forceinline__ uint32_t operator[](uint32_t i) const { return (__ldg(w + (i >> 5)) >> (i & 31u)) & 1u; }
 };
@@ -252,8 +262,15 @@ constexpr int kLetterChunk = 16;  // default; the counting-table kernel runs bes
 template <typename LR, int CH = kLetterChunk, bool CLAMP = false>
 __device__ __forceinline__ uint64_t tuple_key(uint32_t q, uint32_t lead, const uint32_t* __restrict__ delta,
                                               uint32_t n, LR lab, const SigParams& p) {
+    // fingerprints: the tuple's labels are packed LR::kBits apiece into
+    // 64-bit words (an injective layout: every tuple of a pass has k + 1
+    // labels) and each full word is hashed in -- ceil((k + 1) / (64 / kBits))
+    // mix rounds instead of one per letter (the per-letter rounds were ~40 %
+    // of the signature kernels' instructions)
+    constexpr int W = LR::kBits >= 64 ? 32 : LR::kBits;
+    constexpr uint32_t PER = 64u / (uint32_t)W;
     const bool packed = p.kind == kKeyPacked;
-    uint64_t key = packed ? (uint64_t)lead : fp_step(p.salt, lead);
+    uint64_t key = lead, h = p.salt;
     for (uint32_t a = p.a0; a < p.a1; a += CH) {
         uint32_t t[CH];
 #pragma unroll
@@ -267,9 +284,19 @@ __device__ __forceinline__ uint64_t tuple_key(uint32_t q, uint32_t lead, const u
             if (a + j < p.a1) t[j] = lab[t[j]];
 #pragma unroll
         for (int j = 0; j < CH; ++j)
-            if (a + j < p.a1) key = packed ? (key << p.field_bits) | t[j] : fp_step(key + a + j, t[j]);
+            if (a + j < p.a1) {
+                if (packed) {
+                    key = (key << p.field_bits) | t[j];
+                } else {
+                    key = (key << W) | t[j];
+                    if (((a + j + 1) & (PER - 1)) == PER - 1) {  // label a+j+1 of the tuple fills the word
+                        h = fp_word(h, key);
+                        key = 0;
+                    }
+                }
+            }
     }
-    return packed ? key : key & p.fp_mask;
+    return packed ? key : fp_word(h, key) & p.fp_mask;
 }
 
 // Plain signature kernel (radix-sort grouping and the exact chunked path):
@@ -298,7 +325,7 @@ __global__ void __launch_bounds__(512, 3) sig_table_kernel(const uint32_t* __res
                                                         const uint32_t* __restrict__ delta, uint32_t n,
                                                         LR lab, SigParams p, uint32_t nbits,
                                                         uint32_t* __restrict__ keys32, uint32_t* __restrict__ tmin,
-                                                        uint32_t* __restrict__ tcnt) {
+                                                        uint32_t* __restrict__ tcnt, int inc) {
     extern __shared__ uint32_t st[];  // [tsize] minima, then [tsize] counts (shared mode only)
     const bool local = nbits <= kSmemTableBits;
     const uint32_t tsize = 1u << nbits;
@@ -316,7 +343,10 @@ __global__ void __launch_bounds__(512, 3) sig_table_kernel(const uint32_t* __res
         const uint32_t key = (uint32_t)tuple_key<LR, 8, CLAMP>(q, lab[q], delta, n, lab, p);
         keys32[i] = key;
         const unsigned peers = __match_any_sync(__activemask(), key);
-        const uint32_t mq = __reduce_min_sync(peers, q);
+        // inc: states increase with the lane (identity / increasing list), so
+        // the lowest peer lane -- the one that updates the table -- holds the
+        // minimum (the masked reduction compiles to a loop)
+        const uint32_t mq = inc ? q : __reduce_min_sync(peers, q);
         if ((threadIdx.x & 31u) == (unsigned)(__ffs(peers) - 1)) {
             if (local) {
                 // counts are only ever tested for 0 / 1 / >= 2: one shared
@@ -581,8 +611,15 @@ __global__ void dense2_bits_kernel(const uint32_t* __restrict__ lab, uint32_t n,
 
 // ---- bucket strategy -----------------------------------------------------------------
 
-constexpr int kGrpThreads = 256;
-constexpr int kGrpItems = 8;
+#ifndef DFAKIT_GRP_THREADS
+#define DFAKIT_GRP_THREADS 256
+#endif
+#ifndef DFAKIT_GRP_MINB
+#define DFAKIT_GRP_MINB 4
+#endif
+constexpr int kGrpThreads = DFAKIT_GRP_THREADS;
+constexpr unsigned kGrpCtasPerSm = DFAKIT_GRP_MINB;
+constexpr int kGrpItems = 2048 / kGrpThreads;
 constexpr uint32_t kGrpCap = kGrpThreads * kGrpItems;  // bucket capacity (slots per bucket)
 constexpr uint32_t kGrpSlots = 2 * kGrpCap;            // shared hash table (load <= 1/2)
 constexpr unsigned long long kEmptyKey = ~0ull;         // a real ~0 key takes the extra slot
@@ -654,7 +691,7 @@ __device__ __forceinline__ void bucket_append(unsigned long long hk, uint32_t q,
 // hkey >> shift.  Slots b*cap .. b*cap+cap-1; the excess goes to the
 // overflow region at nb*cap (counted in ctr->overflow).
 template <typename LR>
-__global__ void __launch_bounds__(kThreads, 5) sig_bucket_kernel(const uint32_t* __restrict__ list, uint64_t m,
+__global__ void __launch_bounds__(kThreads, DFAKIT_SIGB_MINB) sig_bucket_kernel(const uint32_t* __restrict__ list, uint64_t m,
                                                               const uint32_t* __restrict__ delta, uint32_t n,
                                                               LR lab, SigParams p,
                                                               uint32_t nb, uint32_t* __restrict__ bcnt,
@@ -662,16 +699,16 @@ __global__ void __launch_bounds__(kThreads, 5) sig_bucket_kernel(const uint32_t*
                                                               IterCounters* __restrict__ ctr) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t q = list ? list[i] : p.q0 + (uint32_t)i;
-        const uint64_t key = tuple_key<LR>(q, lab[q], delta, n, lab, p);
+        const uint64_t key = tuple_key<LR, DFAKIT_SIGB_CH>(q, lab[q], delta, n, lab, p);
         const unsigned long long hk = p.kind == kKeyPacked ? mix64(key) : key;
         bucket_append(hk, q, 0u, nb, bcnt, bent, ctr);
     }
 }
 
-struct GroupSmem {
-    unsigned long long key[kGrpSlots + 1];
-    uint32_t rep[kGrpSlots + 1];
-    uint8_t multi[kGrpSlots + 1];
+struct GroupSmem {  // slot kGrpSlots: the ~0 key's own slot
+    alignas(16) unsigned long long key[kGrpSlots + 2];
+    alignas(16) uint32_t rep[kGrpSlots + 4];
+    alignas(16) uint8_t multi[kGrpSlots + 16];
 };
 
 __device__ __forceinline__ uint32_t pow2_at_least(uint32_t x) { return x <= 1 ? 1u : 1u << (32 - __clz(x - 1)); }
@@ -685,12 +722,15 @@ struct GroupOut {
     uint32_t* rep_slot;
     uint8_t* keep_slot;
     uint32_t* res;     // sharded engine: res[entry index] = rep | multi << 31
+    uint2* rec;        // deferred: rec[slot] = {state, rep | multi << 31}, applied once verified
 };
 
 __device__ __forceinline__ void emit(const GroupOut& o, uint64_t slot, uint32_t q, uint32_t r, bool multi,
                                      uint32_t idx) {
     if (o.res) {
         o.res[idx] = r | (multi ? 0x80000000u : 0u);
+    } else if (o.rec) {
+        o.rec[slot] = make_uint2(q, r | (multi ? 0x80000000u : 0u));
     } else if (o.direct) {
         o.lab[q] = r;
         if (o.state_order) {
@@ -707,7 +747,7 @@ __device__ __forceinline__ void emit(const GroupOut& o, uint64_t slot, uint32_t 
 // One CTA per bucket (persistent over buckets).  Buckets whose count
 // exceeds the capacity are left to the ghash fallback.
 template <typename LR>
-__global__ void __launch_bounds__(kGrpThreads) bucket_group_kernel(
+__global__ void __launch_bounds__(kGrpThreads, DFAKIT_GRP_MINB) bucket_group_kernel(
     const uint32_t* __restrict__ bcnt, uint32_t nb, const uint4* __restrict__ bent, int fingerprint,
     const uint32_t* __restrict__ delta, uint32_t n, uint32_t k, LR lab_in, GroupOut o,
     IterCounters* __restrict__ ctr) {
@@ -731,10 +771,15 @@ __global__ void __launch_bounds__(kGrpThreads) bucket_group_kernel(
         }
         if (len == 0 || len > kGrpCap) continue;  // uniform across the CTA
         const uint32_t T = max(64u, pow2_at_least(2 * len));
-        for (uint32_t e = tid; e <= T; e += kGrpThreads) {
-            sm.key[e == T ? kGrpSlots : e] = kEmptyKey;
-            sm.rep[e == T ? kGrpSlots : e] = kNone;
-            sm.multi[e == T ? kGrpSlots : e] = 0;
+        // rep needs no reset: every claimed slot's rep is written by its
+        // claimer; keys and flags are reset with 16-byte stores (T >= 64)
+        for (uint32_t e = tid; e < T / 2; e += kGrpThreads)
+            reinterpret_cast<ulonglong2*>(sm.key)[e] = make_ulonglong2(kEmptyKey, kEmptyKey);
+        for (uint32_t e = tid; e < T / 16; e += kGrpThreads)
+            reinterpret_cast<uint4*>(sm.multi)[e] = make_uint4(0, 0, 0, 0);
+        if (tid == 0) {
+            sm.key[kGrpSlots] = kEmptyKey;
+            sm.multi[kGrpSlots] = 0;
         }
         __syncthreads();
         const uint64_t s0 = (uint64_t)b * kGrpCap;
@@ -750,28 +795,38 @@ __global__ void __launch_bounds__(kGrpThreads) bucket_group_kernel(
                 ix[j] = e.w;
             }
         }
+        // claim: the member whose CAS takes the empty slot writes the run's
+        // rep with a plain store; a member that finds its key already there
+        // makes the run multi-member and joins the minimum after the barrier
+        // (one shared atomic per entry instead of two when keys are distinct).
+        // The ~0 key takes its own slot, where the first claimer writes 0.
+        unsigned dup = 0;
 #pragma unroll
         for (int j = 0; j < kGrpItems; ++j) {
             const uint32_t idx = j * kGrpThreads + tid;
             if (idx < len) {
-                uint32_t s;
-                if (hk[j] == kEmptyKey) {
-                    s = kGrpSlots;
-                } else {
-                    s = (uint32_t)hk[j] & (T - 1);
-                    for (;;) {
-                        const unsigned long long old = atomicCAS(&sm.key[s], kEmptyKey, hk[j]);
-                        if (old == kEmptyKey || old == hk[j]) break;
-                        s = (s + 1) & (T - 1);
-                    }
+                const unsigned long long want = hk[j] == kEmptyKey ? 0ull : hk[j];
+                uint32_t s = hk[j] == kEmptyKey ? kGrpSlots : (uint32_t)hk[j] & (T - 1);
+                unsigned long long o = atomicCAS(&sm.key[s], kEmptyKey, want);
+                while (o != kEmptyKey && o != want) {
+                    s = (s + 1) & (T - 1);
+                    o = atomicCAS(&sm.key[s], kEmptyKey, want);
                 }
                 slot[j] = s;
-                // a member that finds the slot already claimed makes the run
-                // multi-member (whoever came first): no separate marking sweep
-                if (atomicMin(&sm.rep[s], q[j]) != kNone) sm.multi[s] = 1;
+                if (o == kEmptyKey) {
+                    sm.rep[s] = q[j];
+                } else {
+                    sm.multi[s] = 1;
+                    dup |= 1u << j;
+                }
             }
         }
-        __syncthreads();
+        if (__syncthreads_or(dup != 0)) {
+#pragma unroll
+            for (int j = 0; j < kGrpItems; ++j)
+                if (dup & (1u << j)) atomicMin(&sm.rep[slot[j]], q[j]);
+            __syncthreads();
+        }
 #pragma unroll
         for (int j = 0; j < kGrpItems; ++j) {
             const uint32_t idx = j * kGrpThreads + tid;
@@ -880,6 +935,22 @@ __global__ void slot_apply_kernel(const uint32_t* __restrict__ bcnt, uint32_t nb
         const uint32_t q = bent[e].z;
         lab[q] = rep_slot[e];
         if (act) act[q] = keep_slot[e];
+    }
+}
+
+// deferred big fingerprint passes: the packed per-slot records of a verified
+// pass become labels (and survivor flags; act was zeroed) -- skipped when the
+// pass left every block a singleton (the numbering is then the identity)
+__global__ void rec_apply_kernel(const uint32_t* __restrict__ bcnt, uint32_t nb, uint32_t ovf,
+                                 const uint2* __restrict__ rec, uint32_t* __restrict__ lab,
+                                 uint8_t* __restrict__ act) {
+    const uint64_t bspace = (uint64_t)nb * kGrpCap, total = bspace + ovf;
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        if (e < bspace && (uint32_t)(e % kGrpCap) >= min(bcnt[(e / kGrpCap) * kCntStride], kGrpCap)) continue;
+        const uint2 r = __ldcs(rec + e);
+        lab[r.x] = r.y & 0x7fffffffu;
+        if (r.y >> 31) act[r.x] = 1;
     }
 }
 
@@ -1102,6 +1173,7 @@ struct Workspace {
     DBuf<uint8_t> keep, act;
     // bucket strategy
     DBuf<uint32_t> bcnt, rep_slot, gslot, grep, eval;
+    DBuf<uint2> rec;
     DBuf<uint4> bent;
     DBuf<unsigned long long> gkey;
     DBuf<uint8_t> keep_slot, gmul;
@@ -1646,6 +1718,7 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
             fills.flush(ctx, s);
             const bool local = nbits <= kSmemTableBits;
             const size_t smem = local ? (size_t)(2u << nbits) * 4 : 0;
+            const int inc = list == nullptr || list_inc ? 1 : 0;
             auto sig_table = [&](uint32_t q0, uint64_t mm, bool clamp) {
                 const unsigned tg = (unsigned)std::min<uint64_t>((mm + 511) / 512, (uint64_t)ctx->num_sms * 3);
                 SigParams pc = p;
@@ -1660,10 +1733,12 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
                                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                      (int)(2u << kSmemTableBits) * 4));
                         DK_LAUNCH_BU(ctx, bytes, (double)mm * k, sig_table_clamped_kernel, tg, 512, smem, s, list,
-                                     mm, d.delta, n, lab, pc, nbits, w.heads.get() + q0, w.tmin.get(), w.tcnt.get());
+                                     mm, d.delta, n, lab, pc, nbits, w.heads.get() + q0, w.tmin.get(), w.tcnt.get(),
+                                     inc);
                     } else {
                         DK_LAUNCH_BU(ctx, bytes, (double)mm * k, sig_table_kernel<LR>, tg, 512, smem, s, list, mm,
-                                     d.delta, n, lab, pc, nbits, w.heads.get() + q0, w.tmin.get(), w.tcnt.get());
+                                     d.delta, n, lab, pc, nbits, w.heads.get() + q0, w.tmin.get(), w.tcnt.get(),
+                                     inc);
                     }
                 });
             };
@@ -1755,8 +1830,15 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
             // discarded if verification finds a collision); small passes
             // keep per-slot outputs and apply fingerprint labels afterwards
             const bool state_order = m >= (uint64_t)n / 16;
-            const bool direct = !fingerprint || state_order;
-            if (!direct && w.rep_slot.n < espace) w.rep_slot.alloc(espace, s);
+            // big fingerprint passes defer their labels: packed per-slot
+            // records (coalesced) are applied after verification -- and not at
+            // all when every block came out a singleton (the usual last pass:
+            // 4-byte label stores to random states cost as much as the rest
+            // of the grouping)
+            const bool defer = fingerprint && state_order && n < 0x80000000u;
+            const bool direct = (!fingerprint || state_order) && !defer;
+            if (!direct && !defer && w.rep_slot.n < espace) w.rep_slot.alloc(espace, s);
+            if (defer && w.rec.n < espace) w.rec.alloc(espace, s);
             if (state_order && !w.act.get()) w.act.alloc(n, s);
             if (fingerprint && direct) {
                 if (!w.lab2.get()) w.lab2.alloc(n, s);
@@ -1776,8 +1858,9 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
                             lab, p, nb, w.bcnt.get(), w.bent.get(), dctr);
             });
             GroupOut go{direct ? 1 : 0, state_order ? 1 : 0, out_lab, w.act.get(),
-                        direct ? nullptr : w.rep_slot.get(), w.keep_slot.get(), nullptr};
-            const unsigned gg = (unsigned)std::min<uint64_t>(nb, (uint64_t)ctx->num_sms * 4);
+                        direct || defer ? nullptr : w.rep_slot.get(), w.keep_slot.get(), nullptr,
+                        defer ? w.rec.get() : nullptr};
+            const unsigned gg = (unsigned)std::min<uint64_t>(nb, (uint64_t)ctx->num_sms * kGrpCtasPerSm);
             // algorithmic HBM bytes: (hkey, state) in, label + survivor flag out
             DK_LAUNCH_B(ctx, (double)m * (16.0 + 4.0 + 1.0 + (direct ? 0.0 : 4.0)), bucket_group_kernel, gg,
                         kGrpThreads, sizeof(GroupSmem), s, w.bcnt.get(), nb, w.bent.get(), fingerprint ? 1 : 0,
@@ -1819,7 +1902,11 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
             collisions_this_pass = 0;
             if (B - A + c.runs == B) break;  // fixed point (reference l.411)
             if (fingerprint && direct) std::swap(w.lab, w.lab2);
-            if (!direct)
+            if (defer) {
+                if (B - A + c.runs != n)
+                    DK_LAUNCH_B(ctx, (double)m * 12.0, rec_apply_kernel, grid_for(bspace + c.overflow), kThreads, 0,
+                                s, w.bcnt.get(), nb, c.overflow, w.rec.get(), w.lab.get(), w.act.get());
+            } else if (!direct)
                 DK_LAUNCH_B(ctx, (double)m * 13.0, slot_apply_kernel, grid_for(bspace + c.overflow), kThreads, 0, s,
                             w.bcnt.get(), nb, c.overflow, w.bent.get(), w.rep_slot.get(), w.keep_slot.get(),
                             w.lab.get(), state_order ? w.act.get() : nullptr);
@@ -2163,7 +2250,7 @@ void shard_table_signature(Ctx* ctx, const DevDfa& d, const void* keylab, const 
         using LR = decltype(lab);
         DK_CUDA(cudaFuncSetAttribute(sig_table_kernel<LR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_table));
         DK_LAUNCH_BU(ctx, (double)m * (8.0 + 4.0 * d.k), (double)m * d.k, sig_table_kernel<LR>, tg, 512, smem, s, list, m, d.delta,
-                    d.n, lab, p, nbits, keys32, tmin, tcnt);
+                    d.n, lab, p, nbits, keys32, tmin, tcnt, 1 /* local lists are compacted in state order */);
     });
 }
 
@@ -2239,8 +2326,8 @@ void shard_group(Ctx* ctx, const DevDfa& d, const void* verify_lab, uint32_t ver
         DK_LAUNCH_B(ctx, 32.0 * count, entry_bucket_kernel, grid_for(count), kThreads, 0, s, recv, count, nb,
                     bcnt.get(), bent.get(), dctr);
         const int fp = plan.strategy == kPlanFingerprint ? 1 : 0;
-        GroupOut go{0, 0, nullptr, nullptr, nullptr, nullptr, results};
-        const unsigned gg = (unsigned)std::min<uint64_t>(nb, (uint64_t)ctx->num_sms * 4);
+        GroupOut go{0, 0, nullptr, nullptr, nullptr, nullptr, results, nullptr};
+        const unsigned gg = (unsigned)std::min<uint64_t>(nb, (uint64_t)ctx->num_sms * kGrpCtasPerSm);
         const KeyLab vl{verify_lab, (int)verify_bytes};
         with_lab_type(vl, [&](auto lab) {
             using LR = decltype(lab);

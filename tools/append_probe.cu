@@ -1,0 +1,202 @@
+// append_probe.cu -- experiment: what the (hkey, state) append of the bucket
+// signature pass costs next to its label gathers, and which output shapes
+// are cheaper.  A signature pass over a random 10M x 10 automaton with
+// 16-bit key labels (the bench's second pass) followed by one of:
+//   0 nothing (the gathers + hashing alone)
+//   1 bucket append: warp-aggregated cursor atomic + 16-byte entry store
+//   2 cursor atomic + 8-byte store          3 cursor atomic + 32-byte store
+//   4 coalesced 8-byte key store (state order)
+//   5 cursor atomic only                    6 16-byte store at a random slot
+//   7 global hash-table CAS (2^25 8-byte slots)
+//   8 bucket append staged per CTA in shared memory, flushed 2 entries
+//     (one 32-byte sector) at a time per bucket
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o bin/append_probe tools/append_probe.cu
+#include <cstdint>
+#include <cstdio>
+#include <cuda_runtime.h>
+
+#define CK(x)                                                                              \
+    do {                                                                                   \
+        cudaError_t e = (x);                                                               \
+        if (e != cudaSuccess) {                                                            \
+            printf("CUDA %s at %s:%d\n", cudaGetErrorString(e), __FILE__, __LINE__);       \
+            return 1;                                                                      \
+        }                                                                                  \
+    } while (0)
+
+constexpr uint32_t kCap = 2048, kStride = 8, kShift = 20;
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z += 0x9e3779b97f4a7c15ull;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+
+__global__ void init_kernel(uint32_t* delta, uint16_t* lab, uint32_t n, uint32_t k) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < (uint64_t)n * k;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        delta[i] = (uint32_t)(mix64(i * 3 + 1) % n);
+        if (i < n) lab[i] = (uint16_t)(mix64(i * 7 + 5) & 2047);
+    }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256, 5) sig_kernel(const uint32_t* __restrict__ delta, const uint16_t* __restrict__ lab,
+                                                     uint32_t n, uint32_t k, uint32_t nb, uint32_t* __restrict__ bcnt,
+                                                     uint4* __restrict__ bent, unsigned long long* __restrict__ gtab,
+                                                     uint32_t* sink) {
+    __shared__ uint4 stage[MODE == 8 ? 1024 * 2 : 1];  // 2 entries per bucket slot group (sector)
+    __shared__ uint32_t scnt[MODE == 8 ? 1024 : 1];
+    if (MODE == 8) {
+        for (uint32_t i = threadIdx.x; i < 1024; i += blockDim.x) scnt[i] = 0;
+        __syncthreads();
+    }
+    uint64_t acc = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t q = (uint32_t)i;
+        uint32_t t[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            if (j < (int)k) t[j] = __ldcs(delta + (uint64_t)j * n + q);
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            if (j < (int)k) t[j] = __ldg(lab + t[j]);
+        uint64_t key = __ldg(lab + q), h = 0x1234567;
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            if (j < (int)k) {
+                key = (key << 16) | t[j];
+                if (((j + 1) & 3) == 3) {
+                    h = mix64(h ^ key);
+                    key = 0;
+                }
+            }
+        const uint64_t hk = mix64(h ^ key);
+        const uint32_t b = (uint32_t)(hk >> kShift) & (nb - 1);
+        const unsigned lane = threadIdx.x & 31u, lt = (1u << lane) - 1u, act = __activemask();
+        if (MODE == 0) {
+            acc ^= hk;
+        } else if (MODE == 4) {
+            reinterpret_cast<unsigned long long*>(bent)[i] = hk;
+        } else if (MODE == 6) {
+            bent[(hk & 0xffffff) % ((uint64_t)nb * kCap)] = make_uint4((uint32_t)hk, (uint32_t)(hk >> 32), q, 0);
+        } else if (MODE == 7) {
+            uint64_t s = hk & ((1u << 25) - 1);
+            for (;;) {
+                const unsigned long long old = atomicCAS(gtab + s, ~0ull, hk);
+                if (old == ~0ull || old == hk) break;
+                s = (s + 1) & ((1u << 25) - 1);
+            }
+        } else if (MODE == 8) {
+            // stage by bucket group (nb / 2048 buckets share a smem slot pair... use the low 11 bits)
+            const uint32_t g = b & 1023;
+            const uint32_t pos = atomicAdd(&scnt[g], 1u);
+            if (pos < 2) stage[g * 2 + pos] = make_uint4((uint32_t)hk, (uint32_t)(hk >> 32), q, b);
+            if (pos == 1) {
+                // the pair is complete: flush both if they share the bucket, else one by one
+                const uint4 e0 = stage[g * 2], e1 = stage[g * 2 + 1];
+                scnt[g] = 0;
+                if (e0.w == e1.w) {
+                    const uint32_t base = atomicAdd(&bcnt[e0.w * kStride], 2u);
+                    if (base + 1 < kCap) {
+                        asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(bent + (uint64_t)e0.w * kCap + base),
+                                     "r"(e0.x), "r"(e0.y), "r"(e0.z), "r"(0u), "r"(e1.x), "r"(e1.y), "r"(e1.z), "r"(0u)
+                                     : "memory");
+                    }
+                } else {
+                    uint32_t p0 = atomicAdd(&bcnt[e0.w * kStride], 1u), p1 = atomicAdd(&bcnt[e1.w * kStride], 1u);
+                    if (p0 < kCap) bent[(uint64_t)e0.w * kCap + p0] = make_uint4(e0.x, e0.y, e0.z, 0);
+                    if (p1 < kCap) bent[(uint64_t)e1.w * kCap + p1] = make_uint4(e1.x, e1.y, e1.z, 0);
+                }
+            } else if (pos >= 2) {
+                const uint32_t p0 = atomicAdd(&bcnt[b * kStride], 1u);
+                if (p0 < kCap) bent[(uint64_t)b * kCap + p0] = make_uint4((uint32_t)hk, (uint32_t)(hk >> 32), q, 0);
+            }
+        } else {
+            const unsigned peers = __match_any_sync(act, b);
+            const unsigned leader = __ffs(peers) - 1;
+            uint32_t base = 0;
+            if (lane == leader) base = atomicAdd(&bcnt[b * kStride], (uint32_t)__popc(peers));
+            base = __shfl_sync(act, base, leader);
+            const uint32_t pos = min(base + (uint32_t)__popc(peers & lt), kCap - 1);
+            const uint64_t slot = (uint64_t)b * kCap + pos;
+            if (MODE == 1) {
+                bent[slot] = make_uint4((uint32_t)hk, (uint32_t)(hk >> 32), q, 0);
+            } else if (MODE == 2) {
+                reinterpret_cast<unsigned long long*>(bent)[slot] = hk;
+            } else if (MODE == 3) {
+                asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(bent + 2 * slot),
+                             "r"((uint32_t)hk), "r"((uint32_t)(hk >> 32)), "r"(q), "r"(0u), "r"(0u), "r"(0u), "r"(0u),
+                             "r"(0u)
+                             : "memory");
+            } else {
+                acc ^= base;
+            }
+        }
+    }
+    if (MODE == 8) {  // leftovers
+        __syncthreads();
+        for (uint32_t g = threadIdx.x; g < 1024; g += blockDim.x)
+            if (scnt[g] == 1) {
+                const uint4 e = stage[g * 2];
+                const uint32_t p0 = atomicAdd(&bcnt[e.w * kStride], 1u);
+                if (p0 < kCap) bent[(uint64_t)e.w * kCap + p0] = make_uint4(e.x, e.y, e.z, 0);
+            }
+    }
+    if (acc == 0x12345ull) sink[0] = (uint32_t)acc;
+}
+
+template <int MODE>
+float run(const uint32_t* delta, const uint16_t* lab, uint32_t n, uint32_t k, uint32_t nb, uint32_t* bcnt, uint4* bent,
+          unsigned long long* gtab, uint32_t* sink, int sms) {
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    float best = 1e9f;
+    for (int r = 0; r < 6; ++r) {
+        cudaMemset(bcnt, 0, (size_t)nb * kStride * 4);
+        if (MODE == 7) cudaMemset(gtab, 0xff, (size_t)8 << 25);
+        cudaEventRecord(e0);
+        sig_kernel<MODE><<<sms * 8, 256>>>(delta, lab, n, k, nb, bcnt, bent, gtab, sink);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (r) best = ms < best ? ms : best;
+    }
+    return best;
+}
+
+int main() {
+    const uint32_t n = 10000000, k = 10, nb = 8192;
+    int sms;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    uint32_t *delta, *bcnt, *sink;
+    uint16_t* lab;
+    uint4* bent;
+    unsigned long long* gtab;
+    CK(cudaMalloc(&delta, (size_t)n * k * 4));
+    CK(cudaMalloc(&lab, (size_t)n * 2));
+    CK(cudaMalloc(&bcnt, (size_t)nb * kStride * 4));
+    CK(cudaMalloc(&bent, (size_t)nb * kCap * 32));
+    CK(cudaMalloc(&gtab, (size_t)8 << 25));
+    CK(cudaMalloc(&sink, 4));
+    init_kernel<<<sms * 8, 256>>>(delta, lab, n, k);
+    CK(cudaDeviceSynchronize());
+    const char* names[] = {"gathers only", "atomic + 16B store (bucket append)", "atomic + 8B store",
+                           "atomic + 32B store", "coalesced 8B store", "atomic only", "16B store, random slot",
+                           "global hash CAS (2^25 slots)", "smem-staged pairs, 32B flush"};
+    float t[8];
+    t[0] = run<0>(delta, lab, n, k, nb, bcnt, bent, gtab, sink, sms);
+    t[1] = run<1>(delta, lab, n, k, nb, bcnt, bent, gtab, sink, sms);
+    t[2] = run<2>(delta, lab, n, k, nb, bcnt, bent, gtab, sink, sms);
+    t[3] = run<3>(delta, lab, n, k, nb, bcnt, bent, gtab, sink, sms);
+    t[4] = run<4>(delta, lab, n, k, nb, bcnt, bent, gtab, sink, sms);
+    t[5] = run<5>(delta, lab, n, k, nb, bcnt, bent, gtab, sink, sms);
+    t[6] = run<6>(delta, lab, n, k, nb, bcnt, bent, gtab, sink, sms);
+    t[7] = run<7>(delta, lab, n, k, nb, bcnt, bent, gtab, sink, sms);
+    CK(cudaDeviceSynchronize());
+    for (int i = 0; i < 8; ++i) printf("mode %d  %-40s %.3f ms\n", i, names[i], t[i]);
+    return 0;
+}
