@@ -409,7 +409,13 @@ constexpr int kRadixBits = 8;
 constexpr int kRadix = 1 << kRadixBits;
 constexpr int kSortThreads = 256;
 constexpr int kSortWarps = kSortThreads / 32;
-constexpr int kSortItems = 12;
+#ifndef DFAKIT_SORT_ITEMS
+#define DFAKIT_SORT_ITEMS 12
+#endif
+#ifndef DFAKIT_SORT_MINB
+#define DFAKIT_SORT_MINB 3
+#endif
+constexpr int kSortItems = DFAKIT_SORT_ITEMS;
 constexpr int kSortTile = kSortThreads * kSortItems;  // 3072 keys
 constexpr int kWarpSpan = 32 * kSortItems;            // keys per warp segment
 constexpr int kMaxDigits = 8;
@@ -454,6 +460,7 @@ struct OnesweepSmem {
     uint64_t keys[kSortTile];
     uint32_t vals[kSortTile];
     uint32_t warp_hist[kSortWarps][kRadix];
+    uint32_t match[kSortWarps][kRadix];  // per-warp digit -> lane mask (atomicOr ranking)
     uint32_t digit_start[kRadix];
     uint32_t global_base[kRadix];
     uint32_t tile_hist[kRadix];
@@ -462,7 +469,7 @@ struct OnesweepSmem {
 };
 
 template <int W>
-__global__ void __launch_bounds__(kSortThreads, 3) radix_onesweep_kernel(
+__global__ void __launch_bounds__(kSortThreads, DFAKIT_SORT_MINB) radix_onesweep_kernel(
     const uint64_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in, uint64_t m, uint32_t shift,
     const uint32_t* __restrict__ bins, unsigned long long* __restrict__ look, uint32_t* __restrict__ tile_ctr,
     uint32_t tag, uint64_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out) {
@@ -470,7 +477,10 @@ __global__ void __launch_bounds__(kSortThreads, 3) radix_onesweep_kernel(
     OnesweepSmem& sm = *reinterpret_cast<OnesweepSmem*>(smem_raw);
     const unsigned lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
     if (threadIdx.x == 0) sm.tile = atomicAdd(tile_ctr, 1u);
-    for (int i = threadIdx.x; i < kSortWarps * kRadix; i += kSortThreads) (&sm.warp_hist[0][0])[i] = 0;
+    for (int i = threadIdx.x; i < kSortWarps * kRadix; i += kSortThreads) {
+        (&sm.warp_hist[0][0])[i] = 0;
+        (&sm.match[0][0])[i] = 0;
+    }
     sm.tile_hist[threadIdx.x] = 0;
     __syncthreads();
     const uint32_t tile = sm.tile;
@@ -497,19 +507,30 @@ __global__ void __launch_bounds__(kSortThreads, 3) radix_onesweep_kernel(
         const uint32_t d = threadIdx.x, c = sm.tile_hist[d];
         lk[(uint64_t)tile * kRadix + d] = hi | ((tile == 0 ? kFlagPre : kFlagAgg) << 32) | c;
     }
+    // stable warp ranking: the lanes of a digit find each other through a
+    // shared lane mask (atomicOr, read back after a warp barrier -- cheaper
+    // than match.any, whose latency bound this loop); the lowest lane of the
+    // group owns the digit's warp counter for this item, bumps it and clears
+    // the mask, and the peers take their offsets from it
+    uint32_t* wmatch = sm.match[wid];
+    uint32_t* whist = sm.warp_hist[wid];
 #pragma unroll
     for (int j = 0; j < kSortItems; ++j) {
         const uint64_t i = seg + (uint64_t)j * 32 + lane;
         const bool valid = i < m;
-        const unsigned vmask = __ballot_sync(0xffffffffu, valid);
         const uint32_t d = digit_of(key[j], shift);
-        // the lowest lane of each digit group bumps the warp's counter of
-        // the digit (one shared atomic round trip); its peers read the old
-        // count from it
-        const unsigned peers = valid ? __match_any_sync(vmask, d) : 0u;
+        if (valid) atomicOr(&wmatch[d], 1u << lane);
+        __syncwarp();
+        const unsigned peers = valid ? wmatch[d] : 0u;
         const unsigned leader = valid ? (unsigned)(__ffs(peers) - 1) : lane;
         uint32_t base = 0;
-        if (valid && lane == leader) base = atomicAdd(&sm.warp_hist[wid][d], (uint32_t)__popc(peers));
+        __syncwarp();
+        if (valid && lane == leader) {
+            base = whist[d];
+            whist[d] = base + (uint32_t)__popc(peers);
+            wmatch[d] = 0;
+        }
+        __syncwarp();  // the clears land before the next item's atomicOr
         base = __shfl_sync(0xffffffffu, base, leader);
         rank[j] = valid ? base + (uint32_t)__popc(peers & lt_mask) : kNone;
     }

@@ -19,7 +19,7 @@ sys.path.insert(0, os.path.join(ROOT, "oracle"))
 
 def main():
     p = argparse.ArgumentParser()
-    p.add_argument("workload", choices=["synth", "chain", "fib", "naive", "equiv"])
+    p.add_argument("workload", choices=["synth", "chain", "fib", "naive", "equiv", "sharded"])
     p.add_argument("--states", type=int, default=None)
     p.add_argument("--alphabet", type=int, default=10)
     p.add_argument("--param", type=int, default=19)
@@ -75,6 +75,24 @@ def main():
             opts = nat.COptions(0, 0, 0, 1 << 40, 1 << 24, 64, a.grouping)
             nat.check(nat.lib.dfakit_minimize(ctx.handle, C.byref(hview), int(dk.Algorithm[algo]), C.byref(opts),
                                               hb.data_ptr(), C.byref(rep)))
+            return rep
+
+    if w == "sharded":  # the native sharded engine at world size 1 (NCCL)
+        import socket
+        import torch.distributed as dist
+        from paper_2508_20735_b200 import sharded
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ["MASTER_PORT"] = str(sk.getsockname()[1])
+        sk.close()
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+        ncomm = sharded.NativeComm(ctx)
+
+        def run():  # noqa: F811
+            _, r = sharded.sort_pr_sharded_native(ctx, ncomm, delta, accd, n, k, out=out)
+            rep = nat.CReport()
+            rep.passes, rep.num_blocks = r.passes, r.num_blocks
             return rep
 
     if w == "equiv":
