@@ -215,6 +215,108 @@ __device__ __forceinline__ bool item_wins(const Slot* __restrict__ table, const 
     return __ldcg(&table[s].disc) == disc;
 }
 
+// Levels of at most kSoloItems (frontier records x letters) run on CTA 0
+// alone, one after another, with block barriers between the phases; the
+// other CTAs wait at ONE grid barrier for the whole run of small levels
+// (the ~30 small levels of a 10M-state exploration otherwise paid three grid
+// barriers each).  Same table, same winner rule, same record order.
+#ifndef DFAKIT_BFS_SOLO
+#define DFAKIT_BFS_SOLO 1024
+#endif
+constexpr uint64_t kSoloItems = DFAKIT_BFS_SOLO;
+
+struct SoloOut {
+    uint64_t wb, we;
+    unsigned long long first_fail_all;
+    uint32_t levels, status;
+};
+
+__device__ void solo_levels(const BfsArgs& A, SoloOut& o) {
+    auto tile = cg::tiled_partition<kTile>(cg::this_thread_block());
+    __shared__ uint32_t ws[kThreads / 32];
+    __shared__ uint32_t s_fail;
+    BfsState* st = A.st;
+    const uint64_t mask = A.cap - 1;
+    uint64_t wb = o.wb, we = o.we;
+    uint32_t levels = o.levels;
+    uint32_t status = kBfsRunning;
+    while (wb < we) {
+        const uint64_t items = (we - wb) * A.k;
+        if (items > kSoloItems) break;  // back to the whole grid
+        if (items > A.item_cap || we + items > A.rec_cap || 2 * (we + items) + 64 > A.cap) {
+            status = kBfsGrow;
+            break;
+        }
+        if (threadIdx.x == 0) s_fail = kNone;
+        for (uint64_t base = 0; base < items; base += blockDim.x) {
+            const uint64_t t = base + threadIdx.x;
+            const bool valid = t < items;
+            unsigned long long key = 0, disc = 0;
+            if (valid) {
+                const uint64_t i = wb + t / A.k;
+                const uint32_t la = (uint32_t)(t % A.k);
+                const unsigned long long pk = __ldcg(A.rec.key + i);
+                const uint32_t pa = A.da[(uint64_t)la * A.na + (uint32_t)(pk >> 32)];
+                const uint32_t pb = A.db[(uint64_t)A.to_b[la] * A.nb + (uint32_t)pk];
+                key = ((unsigned long long)pa << 32) | pb;
+                disc = ((unsigned long long)(i + 1) << 32) | la;
+            }
+            const uint32_t sl = tile_find_or_insert(tile, valid, key, A.table, mask);
+            if (valid) {
+                const unsigned long long old = atomicMin(&A.table[sl].disc, disc);
+                A.item_slot[t] = (old >= ((unsigned long long)(wb + 1) << 32)) ? sl : kNone;
+                A.item_key[t] = key;
+            }
+        }
+        __syncthreads();
+        uint32_t run = 0;
+        for (uint64_t base = 0; base < items; base += blockDim.x) {
+            const uint64_t t = base + threadIdx.x;
+            const bool win = t < items && item_wins(A.table, A.item_slot, wb, t, A.k);
+            uint32_t tot;
+            const uint32_t e = block_exclusive_scan<kThreads>(win ? 1u : 0u, &tot, ws);
+            if (win) {
+                const uint32_t posn = run + e;
+                const uint64_t r = we + posn;
+                const unsigned long long key = A.item_key[t];
+                A.rec.key[r] = key;
+                A.rec.parent[r] = (uint32_t)(wb + t / A.k);
+                A.rec.letter[r] = (uint32_t)(t % A.k);
+                const bool fa = A.acc_a[key >> 32], fb = A.acc_b[(uint32_t)key];
+                const bool fails = A.mode == DFAKIT_MODE_INCLUSION ? (fa && !fb) : (fa != fb);
+                if (fails) atomicMin(&s_fail, posn);
+            }
+            run += tot;
+        }
+        __syncthreads();
+        const uint32_t ff = s_fail, total = run;
+        __syncthreads();  // s_fail is reset by the next level
+        if (ff != kNone && A.mode != DFAKIT_MODE_FULL) {
+            if (we + ff >= A.max_visited) {
+                status = kBfsBudget;
+            } else {
+                status = kBfsFail;
+                if (threadIdx.x == 0) st->fail_rec = (uint32_t)(we + ff);
+            }
+            we = we + ff + 1;
+            break;
+        }
+        if (we + total > A.max_visited) {
+            status = kBfsBudget;
+            break;
+        }
+        if (ff != kNone && o.first_fail_all == ~0ull) o.first_fail_all = we + ff;
+        ++levels;
+        wb = we;
+        we += total;
+    }
+    if (status == kBfsRunning && wb >= we) status = kBfsDone;
+    o.wb = wb;
+    o.we = we;
+    o.levels = levels;
+    o.status = status;
+}
+
 __global__ void __launch_bounds__(kThreads) bfs_persistent_kernel(BfsArgs A) {
     cg::grid_group grid = cg::this_grid();
     auto tile = cg::tiled_partition<kTile>(cg::this_thread_block());
@@ -228,8 +330,42 @@ __global__ void __launch_bounds__(kThreads) bfs_persistent_kernel(BfsArgs A) {
     const uint64_t mask = A.cap - 1;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     const uint64_t gtid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    __shared__ SoloOut s_solo;
     while (wb < we) {
         const uint64_t items = (we - wb) * A.k;
+        if (items <= kSoloItems) {
+            // a run of small levels on CTA 0; everyone else waits at one barrier
+            if (blockIdx.x == 0) {
+                if (threadIdx.x == 0) s_solo = SoloOut{wb, we, first_fail_all, levels, kBfsRunning};
+                __syncthreads();
+                SoloOut o = s_solo;
+                solo_levels(A, o);
+                if (threadIdx.x == 0) {
+                    st->wb = o.wb;
+                    st->we = o.we;
+                    st->levels = o.levels;
+                    st->status = o.status;
+                    st->first_fail_all = o.first_fail_all;
+                }
+            }
+            grid.sync();
+            if (threadIdx.x == 0) {
+                volatile BfsState* vs = st;
+                s_solo = SoloOut{vs->wb, vs->we, vs->first_fail_all, vs->levels, vs->status};
+            }
+            __syncthreads();
+            const SoloOut o = s_solo;
+            __syncthreads();
+            wb = o.wb;
+            we = o.we;
+            levels = o.levels;
+            first_fail_all = o.first_fail_all;
+            if (o.status != kBfsRunning) {
+                status = o.status;
+                break;
+            }
+            continue;
+        }
         if (items > A.item_cap || we + items > A.rec_cap || 2 * (we + items) + 64 > A.cap) {
             status = kBfsGrow;
             break;
@@ -237,7 +373,10 @@ __global__ void __launch_bounds__(kThreads) bfs_persistent_kernel(BfsArgs A) {
         // three slots: threads may still read level L-1's slot while level L
         // starts; level L-2's slot (= level L+1's) is free
         const uint32_t par = levels % 3;
-        if (gtid == 0) st->fail[(levels + 1) % 3] = kNone;
+        if (gtid == 0) {
+            st->fail[par] = kNone;  // (a preceding run of solo levels did not reset it)
+            st->fail[(levels + 1) % 3] = kNone;
+        }
         // expand
         const uint64_t trips = (items + stride - 1) / stride;
         for (uint64_t it = 0; it < trips; ++it) {
