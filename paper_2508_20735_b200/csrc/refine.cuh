@@ -100,6 +100,9 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
                             const DeltaStream* ds = nullptr);
 RefineResult naive_pr_device(Ctx* ctx, const DevDfa& d, int policy, uint64_t seed, uint32_t* block_out,
                              cudaStream_t s);
+// ElectionPolicy::arbitrary(seed) with the reference's exact winner stream
+RefineResult naive_pr_arbitrary_device(Ctx* ctx, const DevDfa& d, uint64_t seed, uint32_t* block_out,
+                                       cudaStream_t s);
 RefineResult naive_pr_fused_device(Ctx* ctx, const DevDfa& d, uint32_t* block_out, cudaStream_t s);
 uint32_t floor_log2_u32(uint32_t n);
 // out: k * (floor_log2(n)+1) * n entries (device)
