@@ -288,6 +288,11 @@ dfakit_status dfakit_comm_init(dfakit_ctx* ctx, const uint8_t* id128, int world,
 void dfakit_comm_destroy(dfakit_comm* comm);
 dfakit_status dfakit_sort_pr_sharded(dfakit_ctx* ctx, dfakit_comm* comm, const dfakit_dfa* dfa, uint32_t* block_of,
                                      dfakit_report* report, uint64_t* exchanged, void* stream);
+/* Same with the automaton in host memory (copied to this rank's device and
+ * validated) and block_of in host memory: the C++ extension
+ * dfakit::b200::sort_pr_sharded uses it. */
+dfakit_status dfakit_sort_pr_sharded_host(dfakit_ctx* ctx, dfakit_comm* comm, const dfakit_dfa* dfa,
+                                          uint32_t* block_of, dfakit_report* report);
 /* In-process communicator: `world` ranks as threads of one process, each
  * with its own context (on any devices, e.g. all on one GPU), collectives
  * staged through host memory.  Runs the native driver's multi-rank path

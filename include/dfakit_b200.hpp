@@ -11,6 +11,7 @@
 #pragma once
 
 #include <cstddef>
+#include <array>
 #include <cstdint>
 #include <optional>
 #include <span>
@@ -207,5 +208,44 @@ struct DeterminizeOptions {
 };
 Lts determinize(const Lts& lts, const DeterminizeOptions& opts = {});
 Dfa complete_to_dfa(const Lts& deterministic);
+
+// ---- B200 extensions (no reference counterpart) ------------------------------------------
+//
+// Every calling thread runs on its own device context (its own stream and
+// memory pool): concurrent callers proceed in parallel.  A thread's context
+// is created on its first call -- on device DFAKIT_DEVICE when set, else
+// round-robin over the visible devices -- and destroyed when the thread ends.
+namespace b200 {
+
+// Device the calling thread's context runs on (creates the context).
+int current_device();
+
+// Multi-GPU sortPR (one process per GPU, NCCL): rank 0 creates the id,
+// shares its 128 bytes with every rank out of band, every rank constructs a
+// ShardedComm on its own device and calls sort_pr_sharded with the same
+// automaton; every rank receives the whole canonical partition.
+using CommId = std::array<std::uint8_t, 128>;
+CommId sharded_unique_id();
+
+class ShardedComm {
+public:
+    ShardedComm(const CommId& id, int world, int rank, int device);
+    ~ShardedComm();
+    ShardedComm(const ShardedComm&) = delete;
+    ShardedComm& operator=(const ShardedComm&) = delete;
+    int world() const { return world_; }
+    int rank() const { return rank_; }
+    void* ctx() const { return ctx_; }
+    void* comm() const { return comm_; }
+
+private:
+    int world_, rank_;
+    void* ctx_ = nullptr;
+    void* comm_ = nullptr;
+};
+
+RefinementReport sort_pr_sharded(const Dfa& dfa, ShardedComm& comm);
+
+}  // namespace b200
 
 }  // namespace dfakit

@@ -575,6 +575,30 @@ dfakit_status dfakit_sort_pr_sharded(dfakit_ctx* ctx, dfakit_comm* comm, const d
     });
 }
 
+dfakit_status dfakit_sort_pr_sharded_host(dfakit_ctx* ctx, dfakit_comm* comm, const dfakit_dfa* dfa,
+                                          uint32_t* block_of, dfakit_report* report) {
+    return guard([&] {
+        if (!ctx) throw dk::Error(DFAKIT_E_INVALID, "null context");
+        if (!comm) throw dk::Error(DFAKIT_E_INVALID, "null communicator");
+        check_view(dfa, "sort_pr_sharded");
+        dk::Ctx* c = ctx->c;
+        DK_CUDA(cudaSetDevice(c->device));
+        cudaStream_t s = c->stream;
+        Staged st;
+        stage(c, dfa, st, s);
+        const uint32_t n = dfa->num_states;
+        dk::DBuf<uint32_t> blocks(n ? n : 1, s);
+        DK_CUDA(cudaEventRecord(c->ev0, s));
+        const dk::RefineResult rr = dk::sort_pr_sharded_device(c, comm->c, st.view, blocks.get(), s, nullptr);
+        DK_CUDA(cudaEventRecord(c->ev1, s));
+        if (n && block_of) DK_CUDA(cudaMemcpyAsync(block_of, blocks.get(), (size_t)n * 4, cudaMemcpyDeviceToHost, s));
+        DK_CUDA(cudaStreamSynchronize(s));
+        float ms = 0;
+        DK_CUDA(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+        fill_report(report, rr, DFAKIT_ALGO_SORT_PR, n, dfa->alphabet_size, ms);
+    });
+}
+
 dfakit_status dfakit_calibrate_gather(dfakit_ctx* ctx, uint64_t table_words, uint32_t elem_bytes, uint64_t gathers,
                                       double* gathers_per_s) {
     return on_device(ctx, nullptr, [&](dk::Ctx* c, cudaStream_t s) {

@@ -1,11 +1,13 @@
 // engine_api.cpp -- the GPU-backed part of the drop-in API: minimisers and
-// product exploration forward to the C ABI (dfakit_b200.h).  One process-wide
-// context on device 0 (override with DFAKIT_DEVICE); calls are serialised on
-// it.  Errors map back to the reference's exception types.
+// product exploration forward to the C ABI (dfakit_b200.h).  Every calling
+// thread has its own context (stream + memory pool) on device DFAKIT_DEVICE
+// or, without it, on the visible devices round-robin: concurrent callers run
+// in parallel instead of queueing on one process-wide context.  Errors map
+// back to the reference's exception types.
+#include <atomic>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
-#include <mutex>
 #include <unordered_map>
 
 #include "dfakit_b200.h"
@@ -15,9 +17,6 @@ namespace dfakit {
 
 namespace {
 
-std::mutex g_mu;
-dfakit_ctx* g_ctx = nullptr;
-
 void raise(dfakit_status s) {
     if (s == DFAKIT_OK) return;
     const std::string msg = dfakit_last_error();
@@ -26,13 +25,32 @@ void raise(dfakit_status s) {
     throw std::runtime_error("libdfakit_b200: " + msg);
 }
 
-dfakit_ctx* context() {
-    if (!g_ctx) {
-        const char* env = std::getenv("DFAKIT_DEVICE");
-        raise(dfakit_ctx_create(env ? std::atoi(env) : 0, &g_ctx));
-    }
-    return g_ctx;
+int pick_device() {
+    if (const char* env = std::getenv("DFAKIT_DEVICE")) return std::atoi(env);
+    static std::atomic<unsigned> next{0};
+    const int nd = dfakit_device_count();
+    return nd > 0 ? (int)(next.fetch_add(1) % (unsigned)nd) : 0;
 }
+
+struct ThreadCtx {
+    dfakit_ctx* c = nullptr;
+    int device = -1;
+    ~ThreadCtx() {
+        if (c) dfakit_ctx_destroy(c);
+    }
+};
+
+ThreadCtx& thread_ctx() {
+    thread_local ThreadCtx t;
+    if (!t.c) {
+        const int dev = pick_device();
+        raise(dfakit_ctx_create(dev, &t.c));
+        t.device = dev;
+    }
+    return t;
+}
+
+dfakit_ctx* context() { return thread_ctx().c; }
 
 // contiguous letter-major copy of a Dfa
 struct Flat {
@@ -59,7 +77,6 @@ struct Flat {
 };
 
 RefinementReport run(const Dfa& d, Algorithm algo, const dfakit_options* o) {
-    std::lock_guard<std::mutex> lk(g_mu);
     Flat f(d);
     RefinementReport r;
     r.algorithm = algo;
@@ -111,7 +128,6 @@ RefinementReport trans_pr(const Dfa& dfa, const ElectionPolicy& policy, std::uin
 }
 
 TransResult trans_minimize(const Dfa& dfa, std::uint64_t max_pair_nodes) {
-    std::lock_guard<std::mutex> lk(g_mu);
     Flat f(dfa);
     const StateId n = dfa.num_states;
     if ((std::uint64_t)n * n > max_pair_nodes) {
@@ -136,7 +152,6 @@ TransResult trans_minimize(const Dfa& dfa, std::uint64_t max_pair_nodes) {
 }
 
 Dfa build_transitive_alphabet(const Dfa& dfa, std::uint64_t max_transitions) {
-    std::lock_guard<std::mutex> lk(g_mu);
     Flat f(dfa);
     uint32_t k2 = 0;
     raise(dfakit_build_transitive_alphabet(context(), &f.view, max_transitions, nullptr, &k2));
@@ -203,7 +218,6 @@ ProductResult explore_product(const Dfa& a, const Dfa& b, ExploreMode mode, cons
     if (!a.initial || !b.initial)
         throw std::invalid_argument("product exploration requires initial states on both inputs");
     std::vector<uint32_t> map = letter_map(a, b, opts);
-    std::lock_guard<std::mutex> lk(g_mu);
     Flat fa(a), fb(b);
     dfakit_product p{};
     std::vector<uint32_t> word(1u << 16);
@@ -229,7 +243,6 @@ ProductResult check_inclusion(const Dfa& a, const Dfa& b, const ExploreOptions& 
 ProductResult check_equiv_union_find(const Dfa& a, const Dfa& b) {
     if (!a.initial || !b.initial)
         throw std::invalid_argument("equivalence checking requires initial states on both inputs");
-    std::lock_guard<std::mutex> lk(g_mu);
     Flat fa(a), fb(b);
     dfakit_product p{};
     std::vector<uint32_t> word(1u << 16);
@@ -240,5 +253,49 @@ ProductResult check_equiv_union_find(const Dfa& a, const Dfa& b) {
     }
     return finish(p, word);
 }
+
+namespace b200 {
+
+int current_device() { return thread_ctx().device; }
+
+CommId sharded_unique_id() {
+    CommId id{};
+    raise(dfakit_comm_unique_id(id.data()));
+    return id;
+}
+
+ShardedComm::ShardedComm(const CommId& id, int world, int rank, int device) : world_(world), rank_(rank) {
+    dfakit_ctx* c = nullptr;
+    raise(dfakit_ctx_create(device, &c));
+    dfakit_comm* m = nullptr;
+    const dfakit_status st = dfakit_comm_init(c, id.data(), world, rank, &m);
+    if (st != DFAKIT_OK) {
+        dfakit_ctx_destroy(c);
+        raise(st);
+    }
+    ctx_ = c;
+    comm_ = m;
+}
+
+ShardedComm::~ShardedComm() {
+    if (comm_) dfakit_comm_destroy(static_cast<dfakit_comm*>(comm_));
+    if (ctx_) dfakit_ctx_destroy(static_cast<dfakit_ctx*>(ctx_));
+}
+
+RefinementReport sort_pr_sharded(const Dfa& dfa, ShardedComm& comm) {
+    Flat f(dfa);
+    RefinementReport r;
+    r.algorithm = Algorithm::sort_pr;
+    r.partition.block_of.resize(dfa.num_states);
+    dfakit_report rep{};
+    raise(dfakit_sort_pr_sharded_host(static_cast<dfakit_ctx*>(comm.ctx()), static_cast<dfakit_comm*>(comm.comm()),
+                                      &f.view, r.partition.block_of.data(), &rep));
+    r.partition.num_blocks = rep.num_blocks;
+    r.refining_iterations = rep.refining_iterations;
+    r.closure_iterations = rep.closure_iterations;
+    return r;
+}
+
+}  // namespace b200
 
 }  // namespace dfakit
