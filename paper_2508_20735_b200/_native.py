@@ -112,6 +112,7 @@ _sig = {
     "dfakit_comm_init": (C.c_int, [_V, _V, C.c_int, C.c_int, _P(C.c_void_p)]),
     "dfakit_comm_destroy": (None, [_V]),
     "dfakit_sort_pr_sharded": (C.c_int, [_V, _V, _P(CDfa), _V, _P(CReport), _P(C.c_uint64), _V]),
+    "dfakit_sort_pr_sharded_host": (C.c_int, [_V, _V, _P(CDfa), _V, _P(CReport)]),
     "dfakit_local_hub_create": (C.c_int, [C.c_int, _P(C.c_void_p)]),
     "dfakit_local_hub_destroy": (None, [_V]),
     "dfakit_comm_init_local": (C.c_int, [_V, C.c_int, _P(C.c_void_p)]),
