@@ -302,6 +302,17 @@ dfakit_status dfakit_local_hub_create(int world, dfakit_local_hub** out);
 void dfakit_local_hub_destroy(dfakit_local_hub* hub);
 dfakit_status dfakit_comm_init_local(dfakit_local_hub* hub, int rank, dfakit_comm** out);
 
+/* ---- primitives -----------------------------------------------------------------
+ * The LSD radix sort of sortPR's literal Alg. 4 grouping (one sweep per 8-bit
+ * digit, decoupled look-back): stable sort of (key, value) pairs on key bits
+ * [0, key_bits), device buffers, ping-ponging between (keys, vals) and the
+ * alternates; *result_in_alt = 1 when the sorted pairs ended in the
+ * alternates.  Replaces the reference's std::stable_sort of (block,
+ * signature) tuples (src/minimize.cpp:392). */
+dfakit_status dfakit_radix_sort_pairs_device(dfakit_ctx* ctx, uint64_t* keys, uint32_t* vals, uint64_t* keys_alt,
+                                             uint32_t* vals_alt, uint64_t count, uint32_t key_bits,
+                                             int32_t* result_in_alt, void* stream);
+
 /* ---- calibration ---------------------------------------------------------------
  * Measured ceiling of the signature kernels' random block-label gathers:
  * independent random gathers of elem_bytes (1, 2, 4) from a table of

@@ -108,6 +108,7 @@ _sig = {
     "dfakit_permute_states_device": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint64, C.c_void_p,
                                                C.c_void_p, C.c_void_p, C.c_void_p, _P(C.c_uint32), C.c_void_p]),
     "dfakit_calibrate_gather": (C.c_int, [_V, C.c_uint64, C.c_uint32, C.c_uint64, _P(C.c_double)]),
+    "dfakit_radix_sort_pairs_device": (C.c_int, [_V, _V, _V, _V, _V, C.c_uint64, C.c_uint32, _P(C.c_int32), _V]),
     "dfakit_comm_unique_id": (C.c_int, [_V]),
     "dfakit_comm_init": (C.c_int, [_V, _V, C.c_int, C.c_int, _P(C.c_void_p)]),
     "dfakit_comm_destroy": (None, [_V]),

@@ -599,6 +599,18 @@ dfakit_status dfakit_sort_pr_sharded_host(dfakit_ctx* ctx, dfakit_comm* comm, co
     });
 }
 
+dfakit_status dfakit_radix_sort_pairs_device(dfakit_ctx* ctx, uint64_t* keys, uint32_t* vals, uint64_t* keys_alt,
+                                             uint32_t* vals_alt, uint64_t count, uint32_t key_bits,
+                                             int32_t* result_in_alt, void* stream) {
+    return on_device(ctx, stream, [&](dk::Ctx* c, cudaStream_t s) {
+        if (key_bits > 64) throw dk::Error(DFAKIT_E_INVALID, "radix_sort_pairs: key_bits > 64");
+        if (count && (!keys || !vals || !keys_alt || !vals_alt))
+            throw dk::Error(DFAKIT_E_INVALID, "radix_sort_pairs: null buffer");
+        const bool flipped = dk::radix_sort_pairs(c, dk::RadixBuffers{keys, vals, keys_alt, vals_alt}, count, key_bits, s);
+        if (result_in_alt) *result_in_alt = flipped ? 1 : 0;
+    });
+}
+
 dfakit_status dfakit_calibrate_gather(dfakit_ctx* ctx, uint64_t table_words, uint32_t elem_bytes, uint64_t gathers,
                                       double* gathers_per_s) {
     return on_device(ctx, nullptr, [&](dk::Ctx* c, cudaStream_t s) {
