@@ -514,30 +514,6 @@ __global__ void __launch_bounds__(kSortThreads, DFAKIT_SORT_MINB) radix_onesweep
     // the mask, and the peers take their offsets from it
     uint32_t* wmatch = sm.match[wid];
     uint32_t* whist = sm.warp_hist[wid];
-        unsigned pe = vmask;
-#pragma unroll
-        for (int b = 0; b < kRadixBits; ++b) {
-            const unsigned bal = __ballot_sync(0xffffffffu, (d >> b) & 1u);
-            pe &= ((d >> b) & 1u) ? bal : ~bal;
-        }
-        pm[j] = valid ? pe : 0u;
-#endif
-    }
-#pragma unroll
-    for (int j = 0; j < kSortItems; ++j) {
-        const unsigned peers = pm[j];
-        const uint32_t d = digit_of(key[j], shift);
-        const unsigned leader = peers ? (unsigned)(__ffs(peers) - 1) : lane;
-        uint32_t base = 0;
-        if (peers && lane == leader) {
-            base = whist[d];
-            whist[d] = base + (uint32_t)__popc(peers);
-        }
-        __syncwarp();
-        base = __shfl_sync(0xffffffffu, base, leader);
-        rank[j] = peers ? base + (uint32_t)__popc(peers & lt_mask) : kNone;
-    }
-#else
 #pragma unroll
     for (int j = 0; j < kSortItems; ++j) {
         const uint64_t i = seg + (uint64_t)j * 32 + lane;
