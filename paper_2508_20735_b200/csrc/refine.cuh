@@ -68,6 +68,20 @@ void shard_sig_partition(Ctx* ctx, const DevDfa& d, const void* keylab, const Pa
 // 4 / 2 / 1 / kKeylabBits) -- the min-state labels, or the pass's key labels
 void shard_group(Ctx* ctx, const DevDfa& d, const void* verify_lab, uint32_t verify_bytes, const PassPlan& plan,
                  const uint4* recv, uint64_t count, uint32_t* results, uint32_t* counters, cudaStream_t s);
+// The same in two steps (the native driver): grouping into a workspace that
+// keeps slot-ordered records, and the per-entry results from them -- needed
+// only when the pass is not the last.
+struct ShardGroupWs {
+    DBuf<uint32_t> bcnt;
+    DBuf<uint4> bent;
+    DBuf<uint2> rec;
+    uint32_t nb = 0, ovf = 0;
+    uint64_t count = 0;
+};
+void shard_group_deferred(Ctx* ctx, const DevDfa& d, const void* verify_lab, uint32_t verify_bytes,
+                          const PassPlan& plan, const uint4* recv, uint64_t count, ShardGroupWs& ws,
+                          uint32_t* counters, cudaStream_t s);
+void shard_group_results(Ctx* ctx, const ShardGroupWs& ws, uint32_t* results, cudaStream_t s);
 void shard_apply(Ctx* ctx, const uint4* send, const uint32_t* results, uint64_t count, uint32_t* lab, uint8_t* act,
                  cudaStream_t s);
 void shard_compact(Ctx* ctx, const uint8_t* act, uint32_t lo, uint32_t hi, uint32_t* list, uint32_t* count_dev,

@@ -723,6 +723,7 @@ struct GroupOut {
     uint8_t* keep_slot;
     uint32_t* res;     // sharded engine: res[entry index] = rep | multi << 31
     uint2* rec;        // deferred: rec[slot] = {state, rep | multi << 31}, applied once verified
+    int rec_index;     // rec[slot].x = the entry index instead of the state (sharded owners)
 };
 
 __device__ __forceinline__ void emit(const GroupOut& o, uint64_t slot, uint32_t q, uint32_t r, bool multi,
@@ -730,7 +731,7 @@ __device__ __forceinline__ void emit(const GroupOut& o, uint64_t slot, uint32_t 
     if (o.res) {
         o.res[idx] = r | (multi ? 0x80000000u : 0u);
     } else if (o.rec) {
-        o.rec[slot] = make_uint2(q, r | (multi ? 0x80000000u : 0u));
+        o.rec[slot] = make_uint2(o.rec_index ? idx : q, r | (multi ? 0x80000000u : 0u));
     } else if (o.direct) {
         o.lab[q] = r;
         if (o.state_order) {
@@ -951,6 +952,19 @@ __global__ void rec_apply_kernel(const uint32_t* __restrict__ bcnt, uint32_t nb,
         const uint2 r = __ldcs(rec + e);
         lab[r.x] = r.y & 0x7fffffffu;
         if (r.y >> 31) act[r.x] = 1;
+    }
+}
+
+// sharded owners: slot-ordered records -> per-entry results (for the trip
+// back to the senders); only when the pass is not the last
+__global__ void rec_results_kernel(const uint32_t* __restrict__ bcnt, uint32_t nb, uint32_t ovf,
+                                   const uint2* __restrict__ rec, uint32_t* __restrict__ results) {
+    const uint64_t bspace = (uint64_t)nb * kGrpCap, total = bspace + ovf;
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        if (e < bspace && (uint32_t)(e % kGrpCap) >= min(bcnt[(e / kGrpCap) * kCntStride], kGrpCap)) continue;
+        const uint2 r = __ldcs(rec + e);
+        results[r.x] = r.y;
     }
 }
 
@@ -1859,7 +1873,7 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
             });
             GroupOut go{direct ? 1 : 0, state_order ? 1 : 0, out_lab, w.act.get(),
                         direct || defer ? nullptr : w.rep_slot.get(), w.keep_slot.get(), nullptr,
-                        defer ? w.rec.get() : nullptr};
+                        defer ? w.rec.get() : nullptr, 0};
             const unsigned gg = (unsigned)std::min<uint64_t>(nb, (uint64_t)ctx->num_sms * kGrpCtasPerSm);
             // algorithmic HBM bytes: (hkey, state) in, label + survivor flag out
             DK_LAUNCH_B(ctx, (double)m * (16.0 + 4.0 + 1.0 + (direct ? 0.0 : 4.0)), bucket_group_kernel, gg,
@@ -2311,34 +2325,46 @@ void shard_sig_partition(Ctx* ctx, const DevDfa& d, const void* keylab, const Pa
                 send);
 }
 
-void shard_group(Ctx* ctx, const DevDfa& d, const void* verify_lab, uint32_t verify_bytes, const PassPlan& plan,
-                 const uint4* recv, uint64_t count, uint32_t* results, uint32_t* counters, cudaStream_t s) {
+// Owner-side grouping of received entries into the workspace: per-slot
+// records {entry index, rep | multi << 31} (coalesced), counters.  The
+// per-entry results for the trip back are scattered from the records by
+// shard_group_results, which the driver skips after the last pass.
+void shard_group_deferred(Ctx* ctx, const DevDfa& d, const void* verify_lab, uint32_t verify_bytes,
+                          const PassPlan& plan, const uint4* recv, uint64_t count, ShardGroupWs& ws,
+                          uint32_t* counters, cudaStream_t s) {
     IterCounters* dctr = reinterpret_cast<IterCounters*>(ctx->dmailbox) + 4;
     DK_CUDA(cudaMemsetAsync(dctr, 0, sizeof(IterCounters), s));
+    ws.count = count;
+    ws.ovf = 0;
     if (count) {
         uint32_t D = 1;
         while (D < 24 && ((uint64_t)1 << D) * (kGrpCap * 3 / 4) < count) ++D;
         const uint32_t nb = 1u << D;
         const uint64_t bspace = (uint64_t)nb * kGrpCap, espace = bspace + count;
-        DBuf<uint32_t> bcnt((uint64_t)nb * kCntStride, s);
-        DBuf<uint4> bent(espace, s);
-        DK_CUDA(cudaMemsetAsync(bcnt.get(), 0, (size_t)nb * kCntStride * 4, s));
+        ws.nb = nb;
+        if (ws.bcnt.n < (uint64_t)nb * kCntStride) ws.bcnt.alloc((uint64_t)nb * kCntStride, s);
+        if (ws.bent.n < espace) {
+            ws.bent.alloc(espace, s);
+            ws.rec.alloc(espace, s);
+        }
+        DK_CUDA(cudaMemsetAsync(ws.bcnt.get(), 0, (size_t)nb * kCntStride * 4, s));
         DK_LAUNCH_B(ctx, 32.0 * count, entry_bucket_kernel, grid_for(count), kThreads, 0, s, recv, count, nb,
-                    bcnt.get(), bent.get(), dctr);
+                    ws.bcnt.get(), ws.bent.get(), dctr);
         const int fp = plan.strategy == kPlanFingerprint ? 1 : 0;
-        GroupOut go{0, 0, nullptr, nullptr, nullptr, nullptr, results, nullptr};
+        GroupOut go{0, 0, nullptr, nullptr, nullptr, nullptr, nullptr, ws.rec.get(), 1};
         const unsigned gg = (unsigned)std::min<uint64_t>(nb, (uint64_t)ctx->num_sms * kGrpCtasPerSm);
         const KeyLab vl{verify_lab, (int)verify_bytes};
         with_lab_type(vl, [&](auto lab) {
             using LR = decltype(lab);
             DK_CUDA(cudaFuncSetAttribute(bucket_group_kernel<LR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)sizeof(GroupSmem)));
-            DK_LAUNCH_B(ctx, 20.0 * count, bucket_group_kernel, gg, kGrpThreads, sizeof(GroupSmem), s, bcnt.get(),
-                        nb, bent.get(), fp, d.delta, d.n, d.k, lab, go, dctr);
+            DK_LAUNCH_B(ctx, 24.0 * count, bucket_group_kernel, gg, kGrpThreads, sizeof(GroupSmem), s,
+                        ws.bcnt.get(), nb, ws.bent.get(), fp, d.delta, d.n, d.k, lab, go, dctr);
         });
         IterCounters c{};
         read_words(ctx, dctr, sizeof(c), &c, s);
         if (c.overflow) {
+            ws.ovf = c.overflow;
             uint64_t T = 2;
             while (T < 2 * count) T <<= 1;
             DBuf<unsigned long long> gkey(T + 1, s);
@@ -2348,17 +2374,31 @@ void shard_group(Ctx* ctx, const DevDfa& d, const void* verify_lab, uint32_t ver
             DK_CUDA(cudaMemsetAsync(grep.get(), 0xff, (T + 1) * 4, s));
             DK_CUDA(cudaMemsetAsync(gmul.get(), 0, T + 1, s));
             const unsigned eg = grid_for(bspace + c.overflow);
-            DK_LAUNCH(ctx, ghash_insert_kernel, eg, kThreads, 0, s, bcnt.get(), nb, c.overflow, bent.get(), T,
+            DK_LAUNCH(ctx, ghash_insert_kernel, eg, kThreads, 0, s, ws.bcnt.get(), nb, c.overflow, ws.bent.get(), T,
                       gkey.get(), grep.get(), gslot.get());
-            DK_LAUNCH(ctx, ghash_multi_kernel, eg, kThreads, 0, s, bcnt.get(), nb, c.overflow, bent.get(), grep.get(),
-                      gslot.get(), gmul.get());
+            DK_LAUNCH(ctx, ghash_multi_kernel, eg, kThreads, 0, s, ws.bcnt.get(), nb, c.overflow, ws.bent.get(),
+                      grep.get(), gslot.get(), gmul.get());
             with_lab_type(vl, [&](auto lab) {
-                DK_LAUNCH(ctx, ghash_out_kernel, eg, kThreads, 0, s, bcnt.get(), nb, c.overflow, bent.get(),
+                DK_LAUNCH(ctx, ghash_out_kernel, eg, kThreads, 0, s, ws.bcnt.get(), nb, c.overflow, ws.bent.get(),
                           grep.get(), gslot.get(), gmul.get(), fp, d.delta, d.n, d.k, lab, go, dctr);
             });
         }
     }
     DK_CUDA(cudaMemcpyAsync(counters, dctr, 4 * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+}
+
+void shard_group_results(Ctx* ctx, const ShardGroupWs& ws, uint32_t* results, cudaStream_t s) {
+    if (!ws.count) return;
+    const uint64_t total = (uint64_t)ws.nb * kGrpCap + ws.ovf;
+    DK_LAUNCH_B(ctx, 12.0 * ws.count, rec_results_kernel, grid_for(total), kThreads, 0, s, ws.bcnt.get(), ws.nb,
+                ws.ovf, ws.rec.get(), results);
+}
+
+void shard_group(Ctx* ctx, const DevDfa& d, const void* verify_lab, uint32_t verify_bytes, const PassPlan& plan,
+                 const uint4* recv, uint64_t count, uint32_t* results, uint32_t* counters, cudaStream_t s) {
+    ShardGroupWs ws;
+    shard_group_deferred(ctx, d, verify_lab, verify_bytes, plan, recv, count, ws, counters, s);
+    shard_group_results(ctx, ws, results, s);
 }
 
 void shard_apply(Ctx* ctx, const uint4* send, const uint32_t* results, uint64_t count, uint32_t* lab, uint8_t* act,

@@ -283,6 +283,7 @@ RefineResult sort_pr_sharded_device(Ctx* ctx, NcclComm* cm, const DevDfa& d, uin
     DBuf<uint16_t> kl16, next16;
     DBuf<uint32_t> kl32, next32, tmin, tcnt, results, back, bits;
     DBuf<uint4> send, recv;
+    ShardGroupWs gws;  // owner-side grouping workspace (slot-ordered records)
     auto read_u32 = [&](const uint32_t* p, size_t count, uint32_t* out) {
         for (size_t i = 0; i < count; i += 112)  // read_words moves at most 112 words
             read_words(ctx, p + i, std::min<size_t>(112, count - i) * sizeof(uint32_t), out + i, s);
@@ -397,10 +398,10 @@ RefineResult sort_pr_sharded_device(Ctx* ctx, NcclComm* cm, const DevDfa& d, uin
             // verification compares any injective labelling: the key labels when
             // the min-state labels of other ranks are stale
             if (lab_stale)
-                shard_group(ctx, d, keylab, plan.keylab_bytes ? plan.keylab_bytes : 4, plan, recv.get(), rtotal,
-                            results.get(), dctr.get(), s);
+                shard_group_deferred(ctx, d, keylab, plan.keylab_bytes ? plan.keylab_bytes : 4, plan, recv.get(),
+                                     rtotal, gws, dctr.get(), s);
             else
-                shard_group(ctx, d, lab.get(), 4, plan, recv.get(), rtotal, results.get(), dctr.get(), s);
+                shard_group_deferred(ctx, d, lab.get(), 4, plan, recv.get(), rtotal, gws, dctr.get(), s);
             cm->allreduce_u32(dctr.get(), 4, false, s);
             read_u32(dctr.get(), 4, ctr);
             if (ctr[3]) {
@@ -412,6 +413,15 @@ RefineResult sort_pr_sharded_device(Ctx* ctx, NcclComm* cm, const DevDfa& d, uin
                 continue;
             }
             if (B - A + ctr[0] == B) break;  // fixed point (reference l.411)
+            if (B - A + ctr[0] == n) {
+                // every block a singleton (the usual last pass): the numbering
+                // is the identity, so the results need not travel back nor
+                // become labels (a random 4-byte store per state)
+                ++res.iters;
+                B = n;
+                break;
+            }
+            shard_group_results(ctx, gws, results.get(), s);
             if (back.n < std::max(1u, m)) back.alloc(std::max(1u, hi - lo), s);
             cm->all_to_all_v(results.get(), rcount, back.get(), scount, sizeof(uint32_t), s);
             if (hi > lo) DK_CUDA(cudaMemsetAsync(act.get() + lo, 0, hi - lo, s));
