@@ -82,6 +82,39 @@ void shard_group_deferred(Ctx* ctx, const DevDfa& d, const void* verify_lab, uin
                           const PassPlan& plan, const uint4* recv, uint64_t count, ShardGroupWs& ws,
                           uint32_t* counters, cudaStream_t s);
 void shard_group_results(Ctx* ctx, const ShardGroupWs& ws, uint32_t* results, cudaStream_t s);
+// Owner-bucket layout of the native driver's wide passes: the sender's
+// signature kernel appends straight into (owner, bucket) sub-buckets of cs
+// slots (nb buckets per owner), which travel as they are; the owner groups
+// the W senders' parts of each bucket together (no staging / partition /
+// re-bucketing passes).  Sub-bucket overflow goes through a compact list and
+// the global-table fallback.
+struct OwnerPlan {
+    uint32_t world = 1, nb = 1, cs = 0;
+};
+OwnerPlan owner_plan(uint64_t m_total, uint32_t world);
+struct OwnerSend {
+    DBuf<uint4> send;        // world * nb * cs slots: region o = nb sub-buckets of owner o
+    DBuf<uint32_t> scur;     // sub-bucket cursors (kCntStride apart)
+    DBuf<uint4> ovf, ovf_sorted;  // overflow entries, then sorted by owner
+    DBuf<uint32_t> ovf_cnt;  // per owner, then the total
+    DBuf<uint32_t> ovf_cur;
+    DBuf<uint32_t> msg;      // per owner: nb counts + overflow count
+};
+struct OwnerSources {
+    const uint4* base[8];
+    const uint32_t* cnt[8];
+};
+void shard_sig_owner(Ctx* ctx, const DevDfa& d, const void* keylab, const PassPlan& plan, uint64_t salt,
+                     const uint32_t* list, uint32_t list_base, uint64_t m, const OwnerPlan& op, OwnerSend& ws,
+                     cudaStream_t s);
+void shard_sort_overflow(Ctx* ctx, const OwnerPlan& op, OwnerSend& ws, uint32_t ovf_total, cudaStream_t s);
+void shard_owner_ovf_counts(Ctx* ctx, const OwnerPlan& op, const uint32_t* recv_msg, uint32_t* out, cudaStream_t s);
+void shard_group_owner(Ctx* ctx, const DevDfa& d, const void* verify_lab, uint32_t verify_bytes, const PassPlan& plan,
+                       const OwnerPlan& op, const OwnerSources& in, const uint4* ovf_in, uint32_t ovf_total,
+                       uint32_t* results, uint32_t* counters, cudaStream_t s);
+void shard_apply_owner(Ctx* ctx, const OwnerPlan& op, const OwnerSend& ws, uint32_t rank, const uint32_t* own_res,
+                       const uint32_t* back, const uint32_t* back_ovf, uint32_t ovf_total, uint32_t* lab,
+                       uint8_t* act, cudaStream_t s);
 void shard_apply(Ctx* ctx, const uint4* send, const uint32_t* results, uint64_t count, uint32_t* lab, uint8_t* act,
                  cudaStream_t s);
 void shard_compact(Ctx* ctx, const uint8_t* act, uint32_t lo, uint32_t hi, uint32_t* list, uint32_t* count_dev,

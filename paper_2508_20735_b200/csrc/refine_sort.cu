@@ -745,30 +745,102 @@ __device__ __forceinline__ void emit(const GroupOut& o, uint64_t slot, uint32_t 
     }
 }
 
+// Bucket sources of the grouping kernel.  OneSrc: the single-GPU layout --
+// bucket b's entries at bent + b * kGrpCap, its count at bcnt[b * stride].
+// MultiSrc (sharded owners): bucket b is the concatenation of one sub-bucket
+// per sender s (capacity cs, count cnt[s][b]); a count above cs on any
+// sender sends the whole bucket to the ghash fallback.  The view of a bucket
+// loads its idx-th entry and names the output index of that entry.
+struct OneSrc {
+    const uint32_t* __restrict__ bcnt;
+    const uint4* __restrict__ bent;
+    struct View {
+        const uint4* base;
+        __device__ __forceinline__ uint4 load(uint32_t idx) const { return __ldcs(base + idx); }
+        __device__ __forceinline__ uint32_t index(uint32_t, const uint4& e) const { return e.w; }
+    };
+    __device__ __forceinline__ uint32_t count(uint32_t b) const { return bcnt[b * kCntStride]; }
+    __device__ __forceinline__ View view(uint32_t b) const { return View{bent + (uint64_t)b * kGrpCap}; }
+    __device__ __forceinline__ uint64_t slot0(uint32_t b) const { return (uint64_t)b * kGrpCap; }
+    __device__ __forceinline__ void prefetch(uint32_t b, uint32_t len, unsigned tid, unsigned nt) const {
+        const uint32_t lines = (min(len, kGrpCap) * 16u + 127u) / 128u;
+        const char* base = reinterpret_cast<const char*>(bent + (uint64_t)b * kGrpCap);
+        for (uint32_t l = tid; l < lines; l += nt) asm volatile("prefetch.global.L2 [%0];" ::"l"(base + 128ull * l));
+    }
+};
+
+constexpr int kMaxSrc = 8;
+struct MultiSrc {
+    const uint4* base[kMaxSrc];     // sender s's sub-buckets for this owner: nb * cs slots
+    const uint32_t* cnt[kMaxSrc];   // sender s's counts (nb words, unclamped)
+    uint32_t nsrc, nb, cs;
+    struct View {
+        const MultiSrc* src;
+        uint32_t b;
+        uint32_t pre[kMaxSrc + 1];
+        __device__ __forceinline__ uint32_t source(uint32_t idx) const {
+            uint32_t s = 0;
+#pragma unroll
+            for (int t = 1; t < kMaxSrc; ++t) s += (uint32_t)t < src->nsrc && idx >= pre[t];
+            return s;
+        }
+        __device__ __forceinline__ uint4 load(uint32_t idx) const {
+            const uint32_t s = source(idx);
+            return __ldcs(src->base[s] + (uint64_t)b * src->cs + (idx - pre[s]));
+        }
+        // output index: sender s's padded slot, in the layout the results travel back in
+        __device__ __forceinline__ uint32_t index(uint32_t idx, const uint4&) const {
+            const uint32_t s = source(idx);
+            return (s * src->nb + b) * src->cs + (idx - pre[s]);
+        }
+    };
+    __device__ __forceinline__ uint32_t count(uint32_t b) const {
+        uint32_t t = 0;
+        bool over = false;
+#pragma unroll
+        for (int s = 0; s < kMaxSrc; ++s)
+            if ((uint32_t)s < nsrc) {
+                const uint32_t c = cnt[s][b];
+                over |= c > cs;
+                t += c;
+            }
+        return over ? kGrpCap + 1 : t;
+    }
+    __device__ __forceinline__ View view(uint32_t b) const {
+        View v{this, b, {}};
+        uint32_t t = 0;
+#pragma unroll
+        for (int s = 0; s < kMaxSrc; ++s) {
+            v.pre[s] = t;
+            if ((uint32_t)s < nsrc) t += min(cnt[s][b], cs);
+        }
+        v.pre[kMaxSrc] = t;
+        return v;
+    }
+    __device__ __forceinline__ uint64_t slot0(uint32_t b) const { return (uint64_t)b * kGrpCap; }
+    __device__ __forceinline__ void prefetch(uint32_t, uint32_t, unsigned, unsigned) const {}
+};
+
 // One CTA per bucket (persistent over buckets).  Buckets whose count
 // exceeds the capacity are left to the ghash fallback.
-template <typename LR>
+template <typename LR, typename Src = OneSrc>
 __global__ void __launch_bounds__(kGrpThreads, DFAKIT_GRP_MINB) bucket_group_kernel(
-    const uint32_t* __restrict__ bcnt, uint32_t nb, const uint4* __restrict__ bent, int fingerprint,
-    const uint32_t* __restrict__ delta, uint32_t n, uint32_t k, LR lab_in, GroupOut o,
-    IterCounters* __restrict__ ctr) {
+    Src src, uint32_t nb, int fingerprint, const uint32_t* __restrict__ delta, uint32_t n, uint32_t k, LR lab_in,
+    GroupOut o, IterCounters* __restrict__ ctr) {
     extern __shared__ __align__(16) unsigned char grp_raw[];
     GroupSmem& sm = *reinterpret_cast<GroupSmem*>(grp_raw);
     const unsigned tid = threadIdx.x;
     uint32_t heads = 0, ablk = 0, surv = 0;
     bool clash = false;
-    uint32_t len_next = blockIdx.x < nb ? bcnt[blockIdx.x * kCntStride] : 0u;
+    uint32_t len_next = blockIdx.x < nb ? src.count(blockIdx.x) : 0u;
     for (uint32_t b = blockIdx.x; b < nb; b += gridDim.x) {
         const uint32_t len = len_next;
         // the next bucket's length now, its entries into L2 while this one
         // is grouped (one prefetch per 128-byte line)
         const uint32_t bn = b + gridDim.x;
         if (bn < nb) {
-            len_next = bcnt[bn * kCntStride];
-            const uint32_t lines = (min(len_next, kGrpCap) * 16u + 127u) / 128u;
-            const char* base = reinterpret_cast<const char*>(bent + (uint64_t)bn * kGrpCap);
-            for (uint32_t l = tid; l < lines; l += kGrpThreads)
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(base + 128ull * l));
+            len_next = src.count(bn);
+            src.prefetch(bn, len_next, tid, kGrpThreads);
         }
         if (len == 0 || len > kGrpCap) continue;  // uniform across the CTA
         const uint32_t T = max(64u, pow2_at_least(2 * len));
@@ -783,17 +855,18 @@ __global__ void __launch_bounds__(kGrpThreads, DFAKIT_GRP_MINB) bucket_group_ker
             sm.multi[kGrpSlots] = 0;
         }
         __syncthreads();
-        const uint64_t s0 = (uint64_t)b * kGrpCap;
+        const uint64_t s0 = src.slot0(b);
+        const auto view = src.view(b);
         unsigned long long hk[kGrpItems];
         uint32_t q[kGrpItems], slot[kGrpItems], ix[kGrpItems];
 #pragma unroll
         for (int j = 0; j < kGrpItems; ++j) {
             const uint32_t idx = j * kGrpThreads + tid;
             if (idx < len) {
-                const uint4 e = __ldcs(bent + s0 + idx);
+                const uint4 e = view.load(idx);
                 hk[j] = entry_key(e);
                 q[j] = e.z;
-                ix[j] = e.w;
+                ix[j] = view.index(idx, e);
             }
         }
         // claim: the member whose CAS takes the empty slot writes the run's
@@ -1540,7 +1613,7 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
     w.scratch.alloc((uint64_t)n + 1, s);
     w.keep.alloc(n, s);
     w.ctr.alloc(1, s);
-    DK_CUDA(cudaFuncSetAttribute(bucket_group_kernel<ArrLab<uint32_t>>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    DK_CUDA(cudaFuncSetAttribute(bucket_group_kernel<ArrLab<uint32_t>, OneSrc>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)sizeof(GroupSmem)));
     const int smem_table = (int)(2u << kSmemTableBits) * 4;
     DK_CUDA(cudaFuncSetAttribute(sig_table_kernel<BitLab>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_table));
@@ -1876,9 +1949,10 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
                         defer ? w.rec.get() : nullptr, 0};
             const unsigned gg = (unsigned)std::min<uint64_t>(nb, (uint64_t)ctx->num_sms * kGrpCtasPerSm);
             // algorithmic HBM bytes: (hkey, state) in, label + survivor flag out
-            DK_LAUNCH_B(ctx, (double)m * (16.0 + 4.0 + 1.0 + (direct ? 0.0 : 4.0)), bucket_group_kernel, gg,
-                        kGrpThreads, sizeof(GroupSmem), s, w.bcnt.get(), nb, w.bent.get(), fingerprint ? 1 : 0,
-                        d.delta, n, k, ArrLab<uint32_t>{w.lab.get()}, go, dctr);
+            DK_LAUNCH_B(ctx, (double)m * (16.0 + 4.0 + 1.0 + (direct ? 0.0 : 4.0)),
+                        bucket_group_kernel, gg, kGrpThreads, sizeof(GroupSmem), s,
+                        OneSrc{w.bcnt.get(), w.bent.get()}, nb, fingerprint ? 1 : 0, d.delta, n, k,
+                        ArrLab<uint32_t>{w.lab.get()}, go, dctr);
             read_words(ctx, dctr, sizeof(c), &c, s);
             if (c.overflow) {
                 // heavy duplication: overflowed buckets through a global table
@@ -2188,6 +2262,95 @@ __global__ void init_act_range_kernel(const uint8_t* __restrict__ acc, uint32_t 
         act[q] = acc[q] ? keep_acc : keep_rej;
 }
 
+// ---- owner-bucket layout (native driver) --------------------------------------------
+//
+// The sender's signature kernel appends (hkey, state) straight into
+// sub-bucket (owner o, bucket b) of its send regions -- region o holds nb
+// sub-buckets of cs slots, b from the same hash bits as the single-GPU
+// buckets -- so the owner groups what it receives as is (MultiSrc): no
+// staging pass, no partition pass, no re-bucketing at the owner.  Past cs a
+// sub-bucket's entries go to an overflow list {hk lo, hk hi, state, owner}.
+template <typename LR>
+__global__ void __launch_bounds__(kThreads, DFAKIT_SIGB_MINB) sig_owner_kernel(
+    const uint32_t* __restrict__ list, uint64_t m, const uint32_t* __restrict__ delta, uint32_t n, LR lab, SigParams p,
+    uint32_t world, uint32_t nb, uint32_t cs, uint32_t* __restrict__ scur, uint4* __restrict__ send,
+    uint4* __restrict__ ovf, uint32_t* __restrict__ ovf_cnt) {
+    const unsigned lane = threadIdx.x & 31u, lt = (1u << lane) - 1u;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t q = list ? list[i] : p.q0 + (uint32_t)i;
+        const uint64_t key = tuple_key<LR, DFAKIT_SIGB_CH>(q, lab[q], delta, n, lab, p);
+        const unsigned long long hk = p.kind == kKeyPacked ? mix64(key) : key;
+        const uint32_t o = owner_of(hk, world);
+        const uint32_t g = o * nb + ((uint32_t)(hk >> kBucketShift) & (nb - 1));
+        const unsigned act = __activemask();
+        const unsigned peers = __match_any_sync(act, g);
+        const unsigned leader = __ffs(peers) - 1;
+        uint32_t base = 0;
+        if (lane == leader) base = atomicAdd(&scur[g * kCntStride], (uint32_t)__popc(peers));
+        base = __shfl_sync(act, base, leader);
+        const uint32_t pos = base + (uint32_t)__popc(peers & lt);
+        const uint4 e = make_uint4((uint32_t)hk, (uint32_t)(hk >> 32), q, o);
+        if (pos < cs) {
+            send[(uint64_t)g * cs + pos] = e;
+        } else {
+            ovf[atomicAdd(&ovf_cnt[world], 1u)] = e;
+            atomicAdd(&ovf_cnt[o], 1u);
+        }
+    }
+}
+
+// per owner o: the nb sub-bucket counts then its overflow count (nb + 1 words)
+__global__ void owner_counts_kernel(const uint32_t* __restrict__ scur, const uint32_t* __restrict__ ovf_cnt,
+                                    uint32_t world, uint32_t nb, uint32_t* __restrict__ msg) {
+    const uint64_t total = (uint64_t)world * (nb + 1);
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t o = (uint32_t)(i / (nb + 1)), b = (uint32_t)(i % (nb + 1));
+        msg[i] = b < nb ? scur[((uint64_t)o * nb + b) * kCntStride] : ovf_cnt[o];
+    }
+}
+
+// received overflow counts of every sender (for the host readback)
+__global__ void owner_ovf_gather_kernel(const uint32_t* __restrict__ recv_msg, uint32_t world, uint32_t nb,
+                                        uint32_t* __restrict__ out) {
+    for (uint32_t s = threadIdx.x; s < world; s += blockDim.x) out[s] = recv_msg[(uint64_t)s * (nb + 1) + nb];
+}
+
+// the ghash fallback's elements: every entry of a bucket that overflowed on
+// some sender, then every received overflow entry; .w = the output index
+__global__ void owner_collect_kernel(MultiSrc src, const uint4* __restrict__ ovf_in, uint32_t ovf_total,
+                                     uint4* __restrict__ out, uint32_t* __restrict__ out_count) {
+    const uint64_t region = (uint64_t)src.nb * src.cs, total = region * src.nsrc + ovf_total;
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total; e += (uint64_t)gridDim.x * blockDim.x) {
+        uint4 v;
+        if (e < region * src.nsrc) {
+            const uint32_t sidx = (uint32_t)(e / region), r = (uint32_t)(e % region), b = r / src.cs, off = r % src.cs;
+            if (src.count(b) <= kGrpCap || off >= min(src.cnt[sidx][b], src.cs)) continue;
+            v = src.base[sidx][(uint64_t)b * src.cs + off];
+            v.w = (uint32_t)e;
+        } else {
+            v = ovf_in[e - region * src.nsrc];
+            v.w = (uint32_t)e;
+        }
+        out[atomicAdd(out_count, 1u)] = v;
+    }
+}
+
+// sender: results of its sub-bucket entries (padded layout) -> labels
+__global__ void owner_apply_kernel(const uint4* __restrict__ send, const uint32_t* __restrict__ scur, uint32_t world,
+                                   uint32_t nb, uint32_t cs, uint32_t rank, const uint32_t* __restrict__ own_res,
+                                   const uint32_t* __restrict__ back, uint32_t* __restrict__ lab,
+                                   uint8_t* __restrict__ act) {
+    const uint64_t region = (uint64_t)nb * cs, total = region * world;
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total; e += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t o = (uint32_t)(e / region), r = (uint32_t)(e % region);
+        if (r % cs >= min(scur[((uint64_t)o * nb + r / cs) * kCntStride], cs)) continue;
+        const uint32_t q = send[e].z;
+        const uint32_t v = o == rank ? own_res[r] : back[(uint64_t)(o - (o > rank)) * region + r];
+        lab[q] = v & 0x7fffffffu;
+        if (v >> 31) act[q] = 1;  // act zeroed by the caller
+    }
+}
+
 SigParams sig_params(const PassPlan& plan, uint32_t k, uint64_t salt) {
     SigParams p{};
     p.kind = plan.strategy == kPlanFingerprint ? kKeyFingerprint : kKeyPacked;
@@ -2356,10 +2519,10 @@ void shard_group_deferred(Ctx* ctx, const DevDfa& d, const void* verify_lab, uin
         const KeyLab vl{verify_lab, (int)verify_bytes};
         with_lab_type(vl, [&](auto lab) {
             using LR = decltype(lab);
-            DK_CUDA(cudaFuncSetAttribute(bucket_group_kernel<LR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            DK_CUDA(cudaFuncSetAttribute(bucket_group_kernel<LR, OneSrc>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)sizeof(GroupSmem)));
             DK_LAUNCH_B(ctx, 24.0 * count, bucket_group_kernel, gg, kGrpThreads, sizeof(GroupSmem), s,
-                        ws.bcnt.get(), nb, ws.bent.get(), fp, d.delta, d.n, d.k, lab, go, dctr);
+                        OneSrc{ws.bcnt.get(), ws.bent.get()}, nb, fp, d.delta, d.n, d.k, lab, go, dctr);
         });
         IterCounters c{};
         read_words(ctx, dctr, sizeof(c), &c, s);
@@ -2411,6 +2574,133 @@ void shard_apply(Ctx* ctx, const uint4* send, const uint32_t* results, uint64_t 
 void shard_compact(Ctx* ctx, const uint8_t* act, uint32_t lo, uint32_t hi, uint32_t* list, uint32_t* count_dev,
                    cudaStream_t s) {
     compact_flags(ctx, nullptr, act + lo, hi > lo ? hi - lo : 0, list, count_dev, s, lo);
+}
+
+// ---- owner-bucket layout: host side --------------------------------------------------
+
+OwnerPlan owner_plan(uint64_t m_total, uint32_t world) {
+    OwnerPlan op;
+    op.world = world;
+    op.cs = (kGrpCap / world) & ~3u;  // every sender's share of a bucket: merged buckets fit kGrpCap
+    // buckets of ~768..1536 expected entries over all senders, as on one GPU
+    const uint64_t per_owner = (m_total + world - 1) / world;
+    uint32_t D = 1;
+    while (D < 22 && ((uint64_t)1 << D) * (kGrpCap * 3 / 4) < per_owner) ++D;
+    op.nb = 1u << D;
+    return op;
+}
+
+void shard_sig_owner(Ctx* ctx, const DevDfa& d, const void* keylab, const PassPlan& plan, uint64_t salt,
+                     const uint32_t* list, uint32_t list_base, uint64_t m, const OwnerPlan& op, OwnerSend& ws,
+                     cudaStream_t s) {
+    const uint32_t W = op.world, nb = op.nb, cs = op.cs;
+    const uint64_t slots = (uint64_t)W * nb * cs;
+    if (ws.send.n < std::max<uint64_t>(1, slots)) ws.send.alloc(std::max<uint64_t>(1, slots), s);
+    if (ws.scur.n < (uint64_t)W * nb * kCntStride) ws.scur.alloc((uint64_t)W * nb * kCntStride, s);
+    if (ws.ovf.n < std::max<uint64_t>(1, m)) {
+        ws.ovf.alloc(std::max<uint64_t>(1, m), s);
+        ws.ovf_sorted.alloc(std::max<uint64_t>(1, m), s);
+    }
+    if (ws.ovf_cnt.n < (uint64_t)W + 1) {
+        ws.ovf_cnt.alloc(W + 1, s);
+        ws.ovf_cur.alloc(W, s);
+    }
+    if (ws.msg.n < (uint64_t)W * (nb + 1)) ws.msg.alloc((uint64_t)W * (nb + 1), s);
+    Fills f;
+    f.add(ws.scur.get(), (size_t)W * nb * kCntStride * 4, 0);
+    f.add(ws.ovf_cnt.get(), (size_t)(W + 1) * 4, 0);
+    f.flush(ctx, s);
+    if (m) {
+        SigParams p = sig_params(plan, d.k, salt);
+        p.q0 = list_base;
+        with_lab_type(KeyLab{keylab, plan.keylab_bytes ? (int)plan.keylab_bytes : 4}, [&](auto lab) {
+            DK_LAUNCH_BU(ctx, (double)m * (4.0 * d.k + 16.0), (double)m * d.k, sig_owner_kernel,
+                         grid_for(m, kThreads, (unsigned)ctx->num_sms * 8u), kThreads, 0, s, list, m, d.delta, d.n,
+                         lab, p, W, nb, cs, ws.scur.get(), ws.send.get(), ws.ovf.get(), ws.ovf_cnt.get());
+        });
+    }
+    DK_LAUNCH(ctx, owner_counts_kernel, grid_for((uint64_t)W * (nb + 1)), kThreads, 0, s, ws.scur.get(),
+              ws.ovf_cnt.get(), W, nb, ws.msg.get());
+}
+
+void shard_sort_overflow(Ctx* ctx, const OwnerPlan& op, OwnerSend& ws, uint32_t ovf_total, cudaStream_t s) {
+    if (!ovf_total) return;
+    DK_LAUNCH(ctx, dest_offsets_kernel, 1, 32, 0, s, ws.ovf_cnt.get(), op.world, ws.ovf_cur.get());
+    const uint64_t tiles = (ovf_total + kPartThreads * kPartItems - 1) / (kPartThreads * kPartItems);
+    DK_LAUNCH(ctx, partition_kernel, (unsigned)tiles, kPartThreads, 0, s, ws.ovf.get(), (uint64_t)ovf_total, op.world,
+              ws.ovf_cur.get(), ws.ovf_sorted.get());
+}
+
+void shard_owner_ovf_counts(Ctx* ctx, const OwnerPlan& op, const uint32_t* recv_msg, uint32_t* out, cudaStream_t s) {
+    DK_LAUNCH(ctx, owner_ovf_gather_kernel, 1, 64, 0, s, recv_msg, op.world, op.nb, out);
+}
+
+void shard_group_owner(Ctx* ctx, const DevDfa& d, const void* verify_lab, uint32_t verify_bytes, const PassPlan& plan,
+                       const OwnerPlan& op, const OwnerSources& in, const uint4* ovf_in, uint32_t ovf_total,
+                       uint32_t* results, uint32_t* counters, cudaStream_t s) {
+    if (op.world > (uint32_t)kMaxSrc) throw Error(DFAKIT_E_INVALID, "owner buckets: at most 8 ranks");
+    IterCounters* dctr = reinterpret_cast<IterCounters*>(ctx->dmailbox) + 4;
+    DK_CUDA(cudaMemsetAsync(dctr, 0, sizeof(IterCounters), s));
+    MultiSrc src{};
+    for (uint32_t r = 0; r < op.world; ++r) {
+        src.base[r] = in.base[r];
+        src.cnt[r] = in.cnt[r];
+    }
+    src.nsrc = op.world;
+    src.nb = op.nb;
+    src.cs = op.cs;
+    const int fp = plan.strategy == kPlanFingerprint ? 1 : 0;
+    GroupOut go{0, 0, nullptr, nullptr, nullptr, nullptr, results, nullptr, 0};
+    const unsigned gg = (unsigned)std::min<uint64_t>(op.nb, (uint64_t)ctx->num_sms * kGrpCtasPerSm);
+    const KeyLab vl{verify_lab, (int)verify_bytes};
+    with_lab_type(vl, [&](auto lab) {
+        using LR = decltype(lab);
+        DK_CUDA(cudaFuncSetAttribute(bucket_group_kernel<LR, MultiSrc>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sizeof(GroupSmem)));
+        DK_LAUNCH_B(ctx, 20.0 * (double)op.nb * kGrpCap * 3 / 4, bucket_group_kernel, gg, kGrpThreads,
+                    sizeof(GroupSmem), s, src, op.nb, fp, d.delta, d.n, d.k, lab, go, dctr);
+    });
+    if (ovf_total) {
+        // some sub-bucket overflowed: its whole bucket (every sender's part)
+        // and the overflow entries through the global table
+        const uint64_t cap = (uint64_t)op.world * op.nb * op.cs + ovf_total;
+        DBuf<uint4> fl(cap, s);
+        DBuf<uint32_t> fc(1, s);
+        DK_CUDA(cudaMemsetAsync(fc.get(), 0, 4, s));
+        DK_LAUNCH(ctx, owner_collect_kernel, grid_for(cap), kThreads, 0, s, src, ovf_in, ovf_total, fl.get(), fc.get());
+        uint32_t count = 0;
+        read_words(ctx, fc.get(), 4, &count, s);
+        uint64_t T = 2;
+        while (T < 2 * (uint64_t)count) T <<= 1;
+        DBuf<unsigned long long> gkey(T + 1, s);
+        DBuf<uint32_t> grep(T + 1, s), gslot(count ? count : 1, s);
+        DBuf<uint8_t> gmul(T + 1, s);
+        DK_CUDA(cudaMemsetAsync(gkey.get(), 0xff, (T + 1) * 8, s));
+        DK_CUDA(cudaMemsetAsync(grep.get(), 0xff, (T + 1) * 4, s));
+        DK_CUDA(cudaMemsetAsync(gmul.get(), 0, T + 1, s));
+        const unsigned eg = grid_for(count ? count : 1);
+        // a compact element list: no buckets (nb = 0), every element a fallback one
+        DK_LAUNCH(ctx, ghash_insert_kernel, eg, kThreads, 0, s, nullptr, 0u, count, fl.get(), T, gkey.get(),
+                  grep.get(), gslot.get());
+        DK_LAUNCH(ctx, ghash_multi_kernel, eg, kThreads, 0, s, nullptr, 0u, count, fl.get(), grep.get(), gslot.get(),
+                  gmul.get());
+        with_lab_type(vl, [&](auto lab) {
+            DK_LAUNCH(ctx, ghash_out_kernel, eg, kThreads, 0, s, nullptr, 0u, count, fl.get(), grep.get(),
+                      gslot.get(), gmul.get(), fp, d.delta, d.n, d.k, lab, go, dctr);
+        });
+    }
+    DK_CUDA(cudaMemcpyAsync(counters, dctr, 4 * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+}
+
+void shard_apply_owner(Ctx* ctx, const OwnerPlan& op, const OwnerSend& ws, uint32_t rank, const uint32_t* own_res,
+                       const uint32_t* back, const uint32_t* back_ovf, uint32_t ovf_total, uint32_t* lab,
+                       uint8_t* act, cudaStream_t s) {
+    const uint64_t total = (uint64_t)op.world * op.nb * op.cs;
+    DK_LAUNCH_B(ctx, 25.0 * total * 3 / 4, owner_apply_kernel, grid_for(total), kThreads, 0, s, ws.send.get(),
+                ws.scur.get(), op.world, op.nb, op.cs, rank, own_res, back, lab, act);
+    if (ovf_total)
+        DK_LAUNCH(ctx, shard_apply_kernel, grid_for(ovf_total), kThreads, 0, s, ws.ovf_sorted.get(), back_ovf,
+                  (uint64_t)ovf_total, lab, act);
 }
 
 }  // namespace dk

@@ -20,6 +20,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <condition_variable>
 #include <mutex>
@@ -83,23 +84,22 @@ void nccl_check(ncclResult_t r, const char* what) {
 
 uint64_t mix64_host(uint64_t z) { return mix64(z); }
 
-// one grouped send/recv round: element_bytes-sized elements, counts per peer
-void grouped_all_to_all_v(const NcclApi& api, ncclComm_t comm, int world, const void* send,
-                  const std::vector<uint64_t>& scount, void* recv, const std::vector<uint64_t>& rcount,
-                  size_t element_bytes, cudaStream_t s) {
+// one grouped send/recv round: element_bytes-sized elements, offsets and
+// counts per peer
+void grouped_all_to_all(const NcclApi& api, ncclComm_t comm, int world, const void* send,
+                        const std::vector<uint64_t>& soff, const std::vector<uint64_t>& scount, void* recv,
+                        const std::vector<uint64_t>& roff, const std::vector<uint64_t>& rcount, size_t element_bytes,
+                        cudaStream_t s) {
     nccl_check(api.GroupStart(), "ncclGroupStart");
-    uint64_t so = 0, ro = 0;
     for (int r = 0; r < world; ++r) {
         if (scount[r])
-            nccl_check(api.Send(static_cast<const char*>(send) + so * element_bytes, scount[r] * element_bytes,
+            nccl_check(api.Send(static_cast<const char*>(send) + soff[r] * element_bytes, scount[r] * element_bytes,
                                 ncclUint8, r, comm, s),
                        "ncclSend");
         if (rcount[r])
-            nccl_check(api.Recv(static_cast<char*>(recv) + ro * element_bytes, rcount[r] * element_bytes, ncclUint8,
-                                r, comm, s),
+            nccl_check(api.Recv(static_cast<char*>(recv) + roff[r] * element_bytes, rcount[r] * element_bytes,
+                                ncclUint8, r, comm, s),
                        "ncclRecv");
-        so += scount[r];
-        ro += rcount[r];
     }
     nccl_check(api.GroupEnd(), "ncclGroupEnd");
 }
@@ -116,8 +116,19 @@ struct NcclComm {
     virtual void allreduce_u32(uint32_t* buf, size_t count, bool use_min, cudaStream_t s) = 0;
     // full holds world slices of `bytes`; this rank's slice is at rank * bytes
     virtual void allgather(void* full, size_t bytes, cudaStream_t s) = 0;
-    virtual void all_to_all_v(const void* send, const std::vector<uint64_t>& scount, void* recv,
-                              const std::vector<uint64_t>& rcount, size_t element_bytes, cudaStream_t s) = 0;
+    // element offsets per peer given explicitly (segments need not be packed)
+    virtual void all_to_all_off(const void* send, const std::vector<uint64_t>& soff,
+                                const std::vector<uint64_t>& scount, void* recv, const std::vector<uint64_t>& roff,
+                                const std::vector<uint64_t>& rcount, size_t element_bytes, cudaStream_t s) = 0;
+    void all_to_all_v(const void* send, const std::vector<uint64_t>& scount, void* recv,
+                      const std::vector<uint64_t>& rcount, size_t element_bytes, cudaStream_t s) {
+        std::vector<uint64_t> so(world), ro(world);
+        for (int r = 1; r < world; ++r) {
+            so[r] = so[r - 1] + scount[r - 1];
+            ro[r] = ro[r - 1] + rcount[r - 1];
+        }
+        all_to_all_off(send, so, scount, recv, ro, rcount, element_bytes, s);
+    }
 };
 
 namespace {
@@ -134,9 +145,10 @@ struct NcclImpl : NcclComm {
         nccl_check(nccl().AllGather(static_cast<char*>(full) + (uint64_t)rank * bytes, full, bytes, ncclUint8, comm, s),
                    "allgather");
     }
-    void all_to_all_v(const void* send, const std::vector<uint64_t>& scount, void* recv,
-                      const std::vector<uint64_t>& rcount, size_t element_bytes, cudaStream_t s) override {
-        grouped_all_to_all_v(nccl(), comm, world, send, scount, recv, rcount, element_bytes, s);
+    void all_to_all_off(const void* send, const std::vector<uint64_t>& soff, const std::vector<uint64_t>& scount,
+                        void* recv, const std::vector<uint64_t>& roff, const std::vector<uint64_t>& rcount,
+                        size_t element_bytes, cudaStream_t s) override {
+        grouped_all_to_all(nccl(), comm, world, send, soff, scount, recv, roff, rcount, element_bytes, s);
     }
 };
 
@@ -197,24 +209,34 @@ struct LocalImpl : NcclComm {
         DK_CUDA(cudaStreamSynchronize(s));
         hub->barrier();
     }
-    void all_to_all_v(const void* send, const std::vector<uint64_t>& scount, void* recv,
-                      const std::vector<uint64_t>& rcount, size_t element_bytes, cudaStream_t s) override {
+    void all_to_all_off(const void* send, const std::vector<uint64_t>& soff, const std::vector<uint64_t>& scount,
+                        void* recv, const std::vector<uint64_t>& roff, const std::vector<uint64_t>& rcount,
+                        size_t element_bytes, cudaStream_t s) override {
+        // stage every outgoing segment back to back; counts tell the peers where theirs is
         uint64_t total = 0;
         for (uint64_t c : scount) total += c;
-        publish(send, total * element_bytes, s);
+        auto& h = hub->host[rank];
+        h.resize(total * element_bytes);
+        uint64_t at = 0;
+        for (int r = 0; r < world; ++r) {
+            if (scount[r])
+                DK_CUDA(cudaMemcpyAsync(h.data() + at * element_bytes,
+                                        static_cast<const char*>(send) + soff[r] * element_bytes,
+                                        scount[r] * element_bytes, cudaMemcpyDeviceToHost, s));
+            at += scount[r];
+        }
+        DK_CUDA(cudaStreamSynchronize(s));
         hub->counts[rank] = scount;
         hub->barrier();
-        uint64_t ro = 0;
         for (int r = 0; r < world; ++r) {
             uint64_t off = 0;
             for (int j = 0; j < rank; ++j) off += hub->counts[r][j];
             const uint64_t c = hub->counts[r][rank];
             if (c != rcount[r]) throw Error(DFAKIT_E_INVALID, "local hub: receive count mismatch");
             if (c)
-                DK_CUDA(cudaMemcpyAsync(static_cast<char*>(recv) + ro * element_bytes,
+                DK_CUDA(cudaMemcpyAsync(static_cast<char*>(recv) + roff[r] * element_bytes,
                                         hub->host[r].data() + off * element_bytes, c * element_bytes,
                                         cudaMemcpyHostToDevice, s));
-            ro += c;
         }
         DK_CUDA(cudaStreamSynchronize(s));
         hub->barrier();
@@ -284,6 +306,13 @@ RefineResult sort_pr_sharded_device(Ctx* ctx, NcclComm* cm, const DevDfa& d, uin
     DBuf<uint32_t> kl32, next32, tmin, tcnt, results, back, bits;
     DBuf<uint4> send, recv;
     ShardGroupWs gws;  // owner-side grouping workspace (slot-ordered records)
+    // owner-bucket layout (up to 8 ranks; DFAKIT_SHARD_STAGED=1 forces the
+    // staged entries + partition + owner re-bucketing protocol of sharded.py)
+    const bool owner_layout = world <= 8 && !getenv("DFAKIT_SHARD_STAGED");
+    OwnerSend ows;
+    DBuf<uint32_t> rmsg, small(2 * (uint64_t)world + 2, s);
+    DBuf<uint4> rreg, rovf_buf;
+    DBuf<uint32_t> back_ovf;
     auto read_u32 = [&](const uint32_t* p, size_t count, uint32_t* out) {
         for (size_t i = 0; i < count; i += 112)  // read_words moves at most 112 words
             read_words(ctx, p + i, std::min<size_t>(112, count - i) * sizeof(uint32_t), out + i, s);
@@ -378,6 +407,80 @@ RefineResult sort_pr_sharded_device(Ctx* ctx, NcclComm* cm, const DevDfa& d, uin
             lab_stale = true;
             cm->allreduce_u32(dctr.get(), 4, false, s);
             read_u32(dctr.get(), 4, ctr);
+        } else if (owner_layout) {
+            // wide pass, owner-bucket layout: the signature kernel fills
+            // (owner, bucket) sub-buckets that travel as they are
+            const OwnerPlan op = owner_plan(m_total, (uint32_t)world);
+            shard_sig_owner(ctx, d, keylab, plan, salt, lst, lo, m, op, ows, s);
+            const uint64_t msgw = op.nb + 1, region = (uint64_t)op.nb * op.cs;
+            if (rmsg.n < world * msgw) rmsg.alloc(world * msgw, s);
+            const std::vector<uint64_t> mcount(world, msgw);
+            cm->all_to_all_v(ows.msg.get(), mcount, rmsg.get(), mcount, sizeof(uint32_t), s);
+            // overflow counts: received per sender, own per owner, own total
+            shard_owner_ovf_counts(ctx, op, rmsg.get(), small.get(), s);
+            DK_CUDA(cudaMemcpyAsync(small.get() + world, ows.ovf_cnt.get(), (world + 1) * sizeof(uint32_t),
+                                    cudaMemcpyDeviceToDevice, s));
+            std::vector<uint32_t> w32(2 * (size_t)world + 1);
+            read_u32(small.get(), w32.size(), w32.data());
+            std::vector<uint64_t> rovf(world), sovf(world);
+            uint64_t rovf_total = 0;
+            for (int r = 0; r < world; ++r) {
+                rovf_total += (rovf[r] = w32[r]);
+                sovf[r] = w32[world + r];
+            }
+            const uint32_t own_ovf = w32[2 * world];
+            shard_sort_overflow(ctx, op, ows, own_ovf, s);
+            // regions: every peer's region of this rank's send buffer; its own stays put
+            std::vector<uint64_t> soff(world), scnt(world), roff(world), rcnt(world);
+            for (int r = 0; r < world; ++r) {
+                soff[r] = (uint64_t)r * region;
+                scnt[r] = rcnt[r] = r == rank ? 0 : region;
+                roff[r] = r == rank ? 0 : (uint64_t)(r - (r > rank)) * region;
+            }
+            const uint64_t peers_slots = (uint64_t)(world - 1) * region;
+            if (peers_slots && rreg.n < peers_slots) rreg.alloc(peers_slots, s);
+            if (peers_slots) cm->all_to_all_off(ows.send.get(), soff, scnt, rreg.get(), roff, rcnt, sizeof(uint4), s);
+            if (rovf_buf.n < std::max<uint64_t>(1, rovf_total)) rovf_buf.alloc(std::max<uint64_t>(1, rovf_total), s);
+            cm->all_to_all_v(ows.ovf_sorted.get(), sovf, rovf_buf.get(), rovf, sizeof(uint4), s);
+            sent += m;
+            OwnerSources in{};
+            for (int r = 0; r < world; ++r) {
+                in.base[r] = r == rank ? ows.send.get() + (uint64_t)rank * region : rreg.get() + roff[r];
+                in.cnt[r] = rmsg.get() + (uint64_t)r * msgw;
+            }
+            const uint64_t rslots = (uint64_t)world * region + rovf_total;
+            if (results.n < rslots) results.alloc(rslots, s);
+            if (lab_stale)
+                shard_group_owner(ctx, d, keylab, plan.keylab_bytes ? plan.keylab_bytes : 4, plan, op, in,
+                                  rovf_buf.get(), (uint32_t)rovf_total, results.get(), dctr.get(), s);
+            else
+                shard_group_owner(ctx, d, lab.get(), 4, plan, op, in, rovf_buf.get(), (uint32_t)rovf_total,
+                                  results.get(), dctr.get(), s);
+            cm->allreduce_u32(dctr.get(), 4, false, s);
+            read_u32(dctr.get(), 4, ctr);
+            if (ctr[3]) {
+                ++res.collisions;
+                --res.passes;
+                if (++strikes > 16) throw Error(DFAKIT_E_RESOURCE, "sharded sort_pr: repeated fingerprint collisions");
+                salt = mix64_host(salt + 0x1234567ull);
+                continue;
+            }
+            if (B - A + ctr[0] == B) break;  // fixed point (reference l.411)
+            if (B - A + ctr[0] == n) {       // all singletons: nothing travels back
+                ++res.iters;
+                B = n;
+                break;
+            }
+            // results back: each sender's padded part of every region, then the overflow results
+            if (peers_slots && back.n < peers_slots) back.alloc(peers_slots, s);
+            if (peers_slots)
+                cm->all_to_all_off(results.get(), soff, scnt, back.get(), roff, rcnt, sizeof(uint32_t), s);
+            if (back_ovf.n < std::max<uint32_t>(1, own_ovf)) back_ovf.alloc(std::max<uint32_t>(1, own_ovf), s);
+            cm->all_to_all_v(results.get() + (uint64_t)world * region, rovf, back_ovf.get(), sovf, sizeof(uint32_t),
+                             s);
+            if (hi > lo) DK_CUDA(cudaMemsetAsync(act.get() + lo, 0, hi - lo, s));
+            shard_apply_owner(ctx, op, ows, (uint32_t)rank, results.get() + (uint64_t)rank * region, back.get(),
+                              back_ovf.get(), own_ovf, lab.get(), act.get(), s);
         } else {
             if (send.n < std::max(1u, m)) send.alloc(std::max(1u, hi - lo), s);
             shard_sig_partition(ctx, d, keylab, plan, salt, lst, lo, m, (uint32_t)world, send.get(), counts.get(), s);

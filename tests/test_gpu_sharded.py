@@ -31,6 +31,8 @@ CASES = [
     # table pass that reaches the fixed point before any label exchange)
     ("random", 5000, 3, 1.0, 16),
     ("parity", 3000, 4, 0.0, 0),
+    # classes of 3000 members: sub-buckets overflow (global-table fallback)
+    ("bigcopies", 40, 8, 0.5, 17),
 ]
 
 
@@ -48,9 +50,9 @@ def make_case(case):
         d = np.tile(q, (k, 1))
         d[0] ^= 1
         a = (q & 1).astype(np.uint8)
-    elif kind == "copies":
+    elif kind in ("copies", "bigcopies"):
         base, acc0, _ = o.gen_random(n, k, frac, seed)
-        c = 30
+        c = 30 if kind == "copies" else 3000
         d = np.empty((k, n * c), np.uint32)
         for j in range(c):
             d[:, j * n:(j + 1) * n] = base + ((j + 1) % c) * n
@@ -155,11 +157,15 @@ def test_sharded_world2_one_gpu(dk):
         check(res[r])
 
 
-def test_native_driver_multirank_local_hub(dk):
+@pytest.mark.parametrize("layout", ["owner", "staged"])
+def test_native_driver_multirank_local_hub(dk, layout, monkeypatch):
     """The native C++ pass loop with world sizes 2 and 3: ranks are threads of
     this process, each with its own context on the one GPU, collectives
     through the in-process hub (NCCL refuses two ranks on one device).  Every
-    rank must return the oracle's partition and pass count."""
+    rank must return the oracle's partition and pass count -- through the
+    owner-bucket layout (the default) and the staged-entries protocol."""
+    if layout == "staged":
+        monkeypatch.setenv("DFAKIT_SHARD_STAGED", "1")
     import ctypes as C
     import threading
     from paper_2508_20735_b200 import _native as nat
