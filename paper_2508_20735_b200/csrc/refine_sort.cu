@@ -757,8 +757,11 @@ struct OneSrc {
     struct View {
         const uint4* base;
         __device__ __forceinline__ uint4 load(uint32_t idx) const { return __ldcs(base + idx); }
-        __device__ __forceinline__ uint32_t index(uint32_t, const uint4& e) const { return e.w; }
+        // what the entry keeps for its output index, and the index
+        __device__ __forceinline__ uint32_t keep(const uint4& e) const { return e.w; }
+        __device__ __forceinline__ uint32_t index(uint32_t, uint32_t kept) const { return kept; }
     };
+    __device__ __forceinline__ void init() const {}
     __device__ __forceinline__ uint32_t count(uint32_t b) const { return bcnt[b * kCntStride]; }
     __device__ __forceinline__ View view(uint32_t b) const { return View{bent + (uint64_t)b * kGrpCap}; }
     __device__ __forceinline__ uint64_t slot0(uint32_t b) const { return (uint64_t)b * kGrpCap; }
@@ -774,64 +777,101 @@ struct MultiSrc {
     const uint4* base[kMaxSrc];     // sender s's sub-buckets for this owner: nb * cs slots
     const uint32_t* cnt[kMaxSrc];   // sender s's counts (nb words, unclamped)
     uint32_t nsrc, nb, cs;
+    // per-bucket view in shared memory (the CTA's current bucket): prefix of
+    // the senders' clamped counts and each sender's chunk pointer -- runtime
+    // indices into shared memory, not register arrays (which go to local
+    // memory); the per-sender pointers are staged in shared memory once per
+    // CTA too (hoisted into registers they crowded out the grouping's state)
     struct View {
-        const MultiSrc* src;
-        uint32_t b;
-        uint32_t pre[kMaxSrc + 1];
+        const uint32_t* pre;       // kMaxSrc + 1 prefix sums
+        const uint4* const* ptr;   // kMaxSrc chunk bases
+        uint32_t nsrc, b, nb, cs;
         __device__ __forceinline__ uint32_t source(uint32_t idx) const {
             uint32_t s = 0;
 #pragma unroll
-            for (int t = 1; t < kMaxSrc; ++t) s += (uint32_t)t < src->nsrc && idx >= pre[t];
+            for (int t = 1; t < kMaxSrc; ++t) s += (uint32_t)t < nsrc && idx >= pre[t];
             return s;
         }
         __device__ __forceinline__ uint4 load(uint32_t idx) const {
             const uint32_t s = source(idx);
-            return __ldcs(src->base[s] + (uint64_t)b * src->cs + (idx - pre[s]));
+            return __ldcs(ptr[s] + (idx - pre[s]));
         }
-        // output index: sender s's padded slot, in the layout the results travel back in
-        __device__ __forceinline__ uint32_t index(uint32_t idx, const uint4&) const {
+        // output index: sender s's padded slot, in the layout the results
+        // travel back in (recomputed at output time: nothing kept per item)
+        __device__ __forceinline__ uint32_t keep(const uint4&) const { return 0; }
+        __device__ __forceinline__ uint32_t index(uint32_t idx, uint32_t) const {
             const uint32_t s = source(idx);
-            return (s * src->nb + b) * src->cs + (idx - pre[s]);
+            return (s * nb + b) * cs + (idx - pre[s]);
         }
     };
+    struct Shared {
+        const uint4* base[kMaxSrc];
+        const uint32_t* cnt[kMaxSrc];
+        const uint4* ptr[kMaxSrc];
+        uint32_t pre[kMaxSrc + 1];
+    };
+    __device__ __forceinline__ Shared& sh() const {
+        __shared__ Shared s_multi;
+        return s_multi;
+    }
+    __device__ __forceinline__ void init() const {
+        if (threadIdx.x < kMaxSrc) {
+            sh().base[threadIdx.x] = threadIdx.x < nsrc ? base[threadIdx.x] : nullptr;
+            sh().cnt[threadIdx.x] = threadIdx.x < nsrc ? cnt[threadIdx.x] : nullptr;
+        }
+        __syncthreads();
+    }
     __device__ __forceinline__ uint32_t count(uint32_t b) const {
+        const Shared& m = sh();
         uint32_t t = 0;
         bool over = false;
-#pragma unroll
-        for (int s = 0; s < kMaxSrc; ++s)
-            if ((uint32_t)s < nsrc) {
-                const uint32_t c = cnt[s][b];
-                over |= c > cs;
-                t += c;
-            }
+        for (uint32_t s = 0; s < nsrc; ++s) {
+            const uint32_t c = m.cnt[s][b];
+            over |= c > cs;
+            t += c;
+        }
         return over ? kGrpCap + 1 : t;
     }
+    // every thread computes (and stores) the same values: the writes are
+    // identical, and the grouping kernel's end-of-bucket barrier orders them
+    // after the previous bucket's reads
     __device__ __forceinline__ View view(uint32_t b) const {
-        View v{this, b, {}};
+        Shared& m = sh();
         uint32_t t = 0;
-#pragma unroll
-        for (int s = 0; s < kMaxSrc; ++s) {
-            v.pre[s] = t;
-            if ((uint32_t)s < nsrc) t += min(cnt[s][b], cs);
+        for (uint32_t s = 0; s < kMaxSrc; ++s) {
+            m.pre[s] = t;
+            if (s < nsrc) {
+                m.ptr[s] = m.base[s] + (uint64_t)b * cs;
+                t += min(m.cnt[s][b], cs);
+            }
         }
-        v.pre[kMaxSrc] = t;
-        return v;
+        m.pre[kMaxSrc] = t;
+        return View{m.pre, m.ptr, nsrc, b, nb, cs};
     }
     __device__ __forceinline__ uint64_t slot0(uint32_t b) const { return (uint64_t)b * kGrpCap; }
-    __device__ __forceinline__ void prefetch(uint32_t, uint32_t, unsigned, unsigned) const {}
+    __device__ __forceinline__ void prefetch(uint32_t b, uint32_t, unsigned tid, unsigned nt) const {
+        const Shared& m = sh();
+        for (uint32_t s = 0; s < nsrc; ++s) {
+            const uint32_t lines = (min(m.cnt[s][b], cs) * 16u + 127u) / 128u;
+            const char* p = reinterpret_cast<const char*>(m.base[s] + (uint64_t)b * cs);
+            for (uint32_t l = tid; l < lines; l += nt) asm volatile("prefetch.global.L2 [%0];" ::"l"(p + 128ull * l));
+        }
+    }
 };
 
 // One CTA per bucket (persistent over buckets).  Buckets whose count
 // exceeds the capacity are left to the ghash fallback.
 template <typename LR, typename Src = OneSrc>
 __global__ void __launch_bounds__(kGrpThreads, DFAKIT_GRP_MINB) bucket_group_kernel(
-    Src src, uint32_t nb, int fingerprint, const uint32_t* __restrict__ delta, uint32_t n, uint32_t k, LR lab_in,
+    const __grid_constant__ Src src, uint32_t nb, int fingerprint, const uint32_t* __restrict__ delta, uint32_t n,
+    uint32_t k, LR lab_in,
     GroupOut o, IterCounters* __restrict__ ctr) {
     extern __shared__ __align__(16) unsigned char grp_raw[];
     GroupSmem& sm = *reinterpret_cast<GroupSmem*>(grp_raw);
     const unsigned tid = threadIdx.x;
     uint32_t heads = 0, ablk = 0, surv = 0;
     bool clash = false;
+    src.init();
     uint32_t len_next = blockIdx.x < nb ? src.count(blockIdx.x) : 0u;
     for (uint32_t b = blockIdx.x; b < nb; b += gridDim.x) {
         const uint32_t len = len_next;
@@ -866,7 +906,7 @@ __global__ void __launch_bounds__(kGrpThreads, DFAKIT_GRP_MINB) bucket_group_ker
                 const uint4 e = view.load(idx);
                 hk[j] = entry_key(e);
                 q[j] = e.z;
-                ix[j] = view.index(idx, e);
+                ix[j] = view.keep(e);
             }
         }
         // claim: the member whose CAS takes the empty slot writes the run's
@@ -912,7 +952,7 @@ __global__ void __launch_bounds__(kGrpThreads, DFAKIT_GRP_MINB) bucket_group_ker
                 ablk += head && multi;
                 surv += multi;
                 if (fingerprint && !head && !same_tuple(q[j], r, delta, n, k, lab_in)) clash = true;
-                emit(o, s0 + idx, q[j], r, multi, ix[j]);
+                emit(o, s0 + idx, q[j], r, multi, view.index(idx, ix[j]));
             }
         }
         __syncthreads();
@@ -2320,6 +2360,7 @@ __global__ void owner_ovf_gather_kernel(const uint32_t* __restrict__ recv_msg, u
 __global__ void owner_collect_kernel(MultiSrc src, const uint4* __restrict__ ovf_in, uint32_t ovf_total,
                                      uint4* __restrict__ out, uint32_t* __restrict__ out_count) {
     const uint64_t region = (uint64_t)src.nb * src.cs, total = region * src.nsrc + ovf_total;
+    src.init();  // count() reads the shared-memory copy of the pointers
     for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total; e += (uint64_t)gridDim.x * blockDim.x) {
         uint4 v;
         if (e < region * src.nsrc) {
