@@ -99,6 +99,7 @@ struct OwnerSend {
     DBuf<uint32_t> ovf_cnt;  // per owner, then the total
     DBuf<uint32_t> ovf_cur;
     DBuf<uint32_t> msg;      // per owner: nb counts + overflow count
+    DBuf<uint64_t> part;     // partial keys of a sliced signature pass
 };
 struct OwnerSources {
     const uint4* base[8];

@@ -220,9 +220,6 @@ struct SigParams {
 #ifndef DFAKIT_SIGB_CH
 #define DFAKIT_SIGB_CH 16
 #endif
-// one fingerprint round over a 64-bit word of packed labels
-__device__ __forceinline__ uint64_t fp_word(uint64_t h, uint64_t w) { return mix64(h ^ w); }
-
 // Key-label readers: a dense / min-state label array of T, or one bit per
 // state (a two-block partition: the initial {F, Q \ F} of every run -- a
 // 10M-state automaton's bitmap is 1.25 MB and stays L2-resident where a byte
@@ -259,14 +256,68 @@ struct BitLab {
 // memory latencies per letter).
 constexpr int kLetterChunk = 16;  // default; the counting-table kernel runs best with 8
 
+// Keys are built additively from one term per tuple position, so a pass can
+// gather its labels in several sweeps over slices of the label array (each
+// sweep L2-resident) and add the partial keys:
+//   packed keys   -- position p's field at its bit offset, ORed in (exact);
+//   fingerprints  -- fp_term(salt, p, label) summed mod 2^64, then mixed
+//                    (terms are a bijection of (p, label); collisions are
+//                    verified tuple by tuple like every fingerprint).
+// Position 0 is the lead (the state's own block), position a + 1 letter a.
+__device__ __forceinline__ uint64_t fp_term(uint64_t salt, uint32_t pos, uint32_t x) {
+    return mix64(salt ^ (((uint64_t)x << 24) | pos));
+}
+__device__ __forceinline__ uint64_t packed_field(uint64_t v, uint32_t shift) { return shift < 64 ? v << shift : 0ull; }
+
+// FILTER: only successors in [lo, hi) contribute (one slice of the labels)
+template <typename LR, int CH = kLetterChunk, bool CLAMP = false, bool FILTER = false>
+__device__ __forceinline__ uint64_t tuple_part(uint32_t q, uint32_t lead, bool with_lead,
+                                               const uint32_t* __restrict__ delta, uint32_t n, LR lab,
+                                               const SigParams& p, uint32_t lo = 0, uint32_t hi = 0) {
+    const bool packed = p.kind == kKeyPacked;
+    const uint32_t nl = p.a1 - p.a0;
+    uint64_t acc = 0;
+    if (with_lead) acc = packed ? packed_field(lead, p.field_bits * nl) : fp_term(p.salt, 0, lead);
+    for (uint32_t a = p.a0; a < p.a1; a += CH) {
+        uint32_t t[CH];
+        bool in[CH];
+#pragma unroll
+        for (int j = 0; j < CH; ++j)
+            if (a + j < p.a1) {
+                t[j] = ld_stream(delta + (uint64_t)(a + j) * n + q);
+                if (CLAMP) t[j] = min(t[j], n - 1);
+                in[j] = !FILTER || (t[j] >= lo && t[j] < hi);
+            }
+#pragma unroll
+        for (int j = 0; j < CH; ++j)
+            if (a + j < p.a1 && in[j]) t[j] = lab[t[j]];
+#pragma unroll
+        for (int j = 0; j < CH; ++j)
+            if (a + j < p.a1 && in[j]) {
+                const uint32_t r = a + j - p.a0;
+                if (packed) acc |= packed_field(t[j], p.field_bits * (nl - 1 - r));
+                else acc += fp_term(p.salt, r + 1, t[j]);
+            }
+    }
+    return acc;
+}
+
+__device__ __forceinline__ uint64_t key_of_part(const SigParams& p, uint64_t acc) {
+    return p.kind == kKeyPacked ? acc : mix64(acc) & p.fp_mask;
+}
+
+// one fingerprint round over a 64-bit word of packed labels
+__device__ __forceinline__ uint64_t fp_word(uint64_t h, uint64_t w) { return mix64(h ^ w); }
+
+// Key of a whole tuple in one sweep.  Fingerprints: the labels are packed
+// LR::kBits apiece into 64-bit words (an injective layout: every tuple of a
+// pass has k + 1 labels) and each full word is hashed in -- ceil((k + 1) /
+// (64 / kBits)) mix rounds instead of one per letter, and few live registers
+// (the signature kernels run at 48).  A sliced pass uses the additive terms
+// of tuple_part instead; a pass is either sliced or not, on every rank.
 template <typename LR, int CH = kLetterChunk, bool CLAMP = false>
 __device__ __forceinline__ uint64_t tuple_key(uint32_t q, uint32_t lead, const uint32_t* __restrict__ delta,
                                               uint32_t n, LR lab, const SigParams& p) {
-    // fingerprints: the tuple's labels are packed LR::kBits apiece into
-    // 64-bit words (an injective layout: every tuple of a pass has k + 1
-    // labels) and each full word is hashed in -- ceil((k + 1) / (64 / kBits))
-    // mix rounds instead of one per letter (the per-letter rounds were ~40 %
-    // of the signature kernels' instructions)
     constexpr int W = LR::kBits >= 64 ? 32 : LR::kBits;
     constexpr uint32_t PER = 64u / (uint32_t)W;
     const bool packed = p.kind == kKeyPacked;
@@ -297,6 +348,84 @@ __device__ __forceinline__ uint64_t tuple_key(uint32_t q, uint32_t lead, const u
             }
     }
     return packed ? key : fp_word(h, key) & p.fp_mask;
+}
+
+// Identity-list sweep, four consecutive states per thread: 16-byte delta
+// loads keep four times the bytes in flight (a sweep streams all of delta
+// for a slice's worth of gathers, so it is bound by the stream's latency).
+// Requires n % 4 == 0 (16-byte aligned rows) and q0 % 4 == 0.
+template <typename LR>
+__global__ void __launch_bounds__(kThreads, DFAKIT_SIGB_MINB) sig_part_vec_kernel(
+    uint64_t m, const uint32_t* __restrict__ delta, uint32_t n, LR lab, SigParams p, uint32_t lo, uint32_t hi,
+    int first, uint64_t* __restrict__ part) {
+    const bool packed = p.kind == kKeyPacked;
+    const uint32_t nl = p.a1 - p.a0;
+    constexpr int CH = 4;
+    for (uint64_t i4 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i4 * 4 < m;
+         i4 += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t i = i4 * 4;
+        const uint32_t q = p.q0 + (uint32_t)i;
+        const uint32_t cnt = m - i < 4 ? (uint32_t)(m - i) : 4u;
+        uint64_t acc[4] = {0, 0, 0, 0};
+        if (first)
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                if ((uint32_t)e < cnt) {
+                    const uint32_t lead = lab[q + e];
+                    acc[e] = packed ? packed_field(lead, p.field_bits * nl) : fp_term(p.salt, 0, lead);
+                }
+        for (uint32_t a = p.a0; a < p.a1; a += CH) {
+            uint4 t[CH];
+#pragma unroll
+            for (int j = 0; j < CH; ++j)
+                if (a + j < p.a1) t[j] = __ldcs(reinterpret_cast<const uint4*>(delta + (uint64_t)(a + j) * n + q));
+#pragma unroll
+            for (int j = 0; j < CH; ++j)
+                if (a + j < p.a1) {
+                    const uint32_t r = a + j - p.a0;
+                    const uint32_t tt[4] = {t[j].x, t[j].y, t[j].z, t[j].w};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+                        if ((uint32_t)e < cnt && tt[e] >= lo && tt[e] < hi) {
+                            const uint32_t l = lab[tt[e]];
+                            if (packed) acc[e] |= packed_field(l, p.field_bits * (nl - 1 - r));
+                            else acc[e] += fp_term(p.salt, r + 1, l);
+                        }
+                }
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+            if ((uint32_t)e < cnt) {
+                if (first) {
+                    __stcs(part + i + e, acc[e]);
+                } else {
+                    const uint64_t prev = __ldcs(part + i + e);
+                    __stcs(part + i + e, packed ? prev | acc[e] : prev + acc[e]);
+                }
+            }
+    }
+}
+
+// One sweep of a sliced signature pass: the partial keys of the active
+// states over successors in [lo, hi) (the lead in the first sweep), added
+// into part[] (written by the first sweep).
+template <typename LR>
+__global__ void __launch_bounds__(kThreads, DFAKIT_SIGB_MINB) sig_part_kernel(const uint32_t* __restrict__ list, uint64_t m,
+                                                            const uint32_t* __restrict__ delta, uint32_t n, LR lab,
+                                                            SigParams p, uint32_t lo, uint32_t hi, int first,
+                                                            uint64_t* __restrict__ part) {
+    const bool packed = p.kind == kKeyPacked;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t q = list ? list[i] : p.q0 + (uint32_t)i;
+        const uint64_t acc = tuple_part<LR, 8, false, true>(q, first ? lab[q] : 0u, first != 0, delta, n, lab, p, lo, hi);
+        // streaming accesses: the partial keys must not push the slice's labels out of the L2
+        if (first) {
+            __stcs(part + i, acc);
+        } else {
+            const uint64_t prev = __ldcs(part + i);
+            __stcs(part + i, packed ? prev | acc : prev + acc);
+        }
+    }
 }
 
 // Plain signature kernel (radix-sort grouping and the exact chunked path):
@@ -696,10 +825,13 @@ __global__ void __launch_bounds__(kThreads, DFAKIT_SIGB_MINB) sig_bucket_kernel(
                                                               LR lab, SigParams p,
                                                               uint32_t nb, uint32_t* __restrict__ bcnt,
                                                               uint4* __restrict__ bent,
-                                                              IterCounters* __restrict__ ctr) {
+                                                              IterCounters* __restrict__ ctr,
+                                                              const uint64_t* __restrict__ part) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t q = list ? list[i] : p.q0 + (uint32_t)i;
-        const uint64_t key = tuple_key<LR, DFAKIT_SIGB_CH>(q, lab[q], delta, n, lab, p);
+        // part: the keys were gathered by a sliced pass (sig_part_kernel sweeps)
+        const uint64_t key = part ? key_of_part(p, __ldcs(part + i))
+                                  : tuple_key<LR, DFAKIT_SIGB_CH>(q, lab[q], delta, n, lab, p);
         const unsigned long long hk = p.kind == kKeyPacked ? mix64(key) : key;
         bucket_append(hk, q, 0u, nb, bcnt, bent, ctr);
     }
@@ -1301,6 +1433,7 @@ struct Workspace {
     // bucket strategy
     DBuf<uint32_t> bcnt, rep_slot, gslot, grep, eval;
     DBuf<uint2> rec;
+    DBuf<uint64_t> part;  // partial keys of a sliced pass
     DBuf<uint4> bent;
     DBuf<unsigned long long> gkey;
     DBuf<uint8_t> keep_slot, gmul;
@@ -1325,6 +1458,46 @@ void with_lab_type(const KeyLab& kl, F&& f) {
 }
 
 double keylab_bytes_per_state(const KeyLab& kl) { return kl.bytes == kBitLabels ? 0.125 : (double)kl.bytes; }
+
+// Label arrays past the L2 (100M states' 16-bit key labels are 200 MB against
+// 126 MB of L2) make every gather of a signature pass a DRAM sector read.
+// Such passes gather in sweeps over slices of at most kSliceBytes of labels
+// (each L2-resident while its sweep runs), adding partial keys (tuple_part);
+// the bucket kernel then only finishes the keys.  DFAKIT_TEST_SLICE_BYTES
+// overrides the slice size (tests force slicing on small automata).
+constexpr double kSliceBytes = 72.0 * 1024 * 1024;  // 200 MB of labels: 3 slices (2: same time, 4: +10 %)
+
+uint32_t label_slices(const KeyLab& kl, uint32_t n) {
+    double slice = kSliceBytes;
+    if (const char* e = getenv("DFAKIT_TEST_SLICE_BYTES")) slice = std::max(1.0, atof(e));
+    const double bytes = keylab_bytes_per_state(kl) * n;
+    return bytes <= slice ? 1u : (uint32_t)std::min<double>(64.0, std::ceil(bytes / slice));
+}
+
+// The sweeps of a sliced pass into part[0, m): nullptr when one slice suffices.
+const uint64_t* sliced_parts(Ctx* ctx, const KeyLab& kl, const uint32_t* list, uint64_t m, const DevDfa& d,
+                             const SigParams& p, DBuf<uint64_t>& part, cudaStream_t s) {
+    const uint32_t slices = label_slices(kl, d.n);
+    if (slices <= 1 || m == 0) return nullptr;
+    if (part.n < m) part.alloc(m, s);
+    for (uint32_t j = 0; j < slices; ++j) {
+        const uint32_t lo = (uint32_t)((uint64_t)d.n * j / slices), hi = (uint32_t)((uint64_t)d.n * (j + 1) / slices);
+        const bool vec = !list && d.n % 4 == 0 && p.q0 % 4 == 0;
+        with_lab_type(kl, [&](auto lab) {
+            // algorithmic HBM bytes: delta rows, the slice's labels, the partial keys
+            const double bytes = (double)m * (4.0 * d.k + (j ? 16.0 : 8.0)) + keylab_bytes_per_state(kl) * (hi - lo);
+            if (vec)
+                DK_LAUNCH_BU(ctx, bytes, (double)m * d.k / slices, sig_part_vec_kernel,
+                             grid_for((m + 3) / 4, kThreads, (unsigned)ctx->num_sms * 5u), kThreads, 0, s, m, d.delta,
+                             d.n, lab, p, lo, hi, j == 0 ? 1 : 0, part.get());
+            else
+                DK_LAUNCH_BU(ctx, bytes, (double)m * d.k / slices, sig_part_kernel,
+                             grid_for(m, kThreads, (unsigned)ctx->num_sms * 8u), kThreads, 0, s, list, m, d.delta,
+                             d.n, lab, p, lo, hi, j == 0 ? 1 : 0, part.get());
+        });
+    }
+    return part.get();
+}
 
 // ---- persistent small-m engine ---------------------------------------------------
 //
@@ -1977,12 +2150,14 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
             if (state_order) fills.add(w.act.get(), n, 0);
             if (!state_order) fills.add(w.keep_slot.get(), espace, 0);
             fills.flush(ctx, s);
+            const uint64_t* part = sliced_parts(ctx, kl, list, m, d, p, w.part, s);
             with_lab_type(kl, [&](auto lab) {
                 // algorithmic HBM bytes: delta rows (+ list), (hkey, state) out, the key-label array once
-                DK_LAUNCH_BU(ctx, (double)m * (4.0 * k + 16.0 + list_b) + keylab_bytes_per_state(kl) * n, (double)m * k,
-                             sig_bucket_kernel,
-                            grid_for(m, kThreads, (unsigned)ctx->num_sms * 8u), kThreads, 0, s, list, m, d.delta, n,
-                            lab, p, nb, w.bcnt.get(), w.bent.get(), dctr);
+                // (a sliced pass: the partial keys in, hkey out)
+                DK_LAUNCH_BU(ctx, part ? (double)m * 24.0 : (double)m * (4.0 * k + 16.0 + list_b) + keylab_bytes_per_state(kl) * n,
+                             part ? 0.0 : (double)m * k, sig_bucket_kernel,
+                             grid_for(m, kThreads, (unsigned)ctx->num_sms * 8u), kThreads, 0, s, list, m, d.delta, n,
+                             lab, p, nb, w.bcnt.get(), w.bent.get(), dctr, part);
             });
             GroupOut go{direct ? 1 : 0, state_order ? 1 : 0, out_lab, w.act.get(),
                         direct || defer ? nullptr : w.rep_slot.get(), w.keep_slot.get(), nullptr,
@@ -2314,11 +2489,12 @@ template <typename LR>
 __global__ void __launch_bounds__(kThreads, DFAKIT_SIGB_MINB) sig_owner_kernel(
     const uint32_t* __restrict__ list, uint64_t m, const uint32_t* __restrict__ delta, uint32_t n, LR lab, SigParams p,
     uint32_t world, uint32_t nb, uint32_t cs, uint32_t* __restrict__ scur, uint4* __restrict__ send,
-    uint4* __restrict__ ovf, uint32_t* __restrict__ ovf_cnt) {
+    uint4* __restrict__ ovf, uint32_t* __restrict__ ovf_cnt, const uint64_t* __restrict__ part) {
     const unsigned lane = threadIdx.x & 31u, lt = (1u << lane) - 1u;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t q = list ? list[i] : p.q0 + (uint32_t)i;
-        const uint64_t key = tuple_key<LR, DFAKIT_SIGB_CH>(q, lab[q], delta, n, lab, p);
+        const uint64_t key = part ? key_of_part(p, __ldcs(part + i))
+                                  : tuple_key<LR, DFAKIT_SIGB_CH>(q, lab[q], delta, n, lab, p);
         const unsigned long long hk = p.kind == kKeyPacked ? mix64(key) : key;
         const uint32_t o = owner_of(hk, world);
         const uint32_t g = o * nb + ((uint32_t)(hk >> kBucketShift) & (nb - 1));
@@ -2654,10 +2830,13 @@ void shard_sig_owner(Ctx* ctx, const DevDfa& d, const void* keylab, const PassPl
     if (m) {
         SigParams p = sig_params(plan, d.k, salt);
         p.q0 = list_base;
-        with_lab_type(KeyLab{keylab, plan.keylab_bytes ? (int)plan.keylab_bytes : 4}, [&](auto lab) {
-            DK_LAUNCH_BU(ctx, (double)m * (4.0 * d.k + 16.0), (double)m * d.k, sig_owner_kernel,
-                         grid_for(m, kThreads, (unsigned)ctx->num_sms * 8u), kThreads, 0, s, list, m, d.delta, d.n,
-                         lab, p, W, nb, cs, ws.scur.get(), ws.send.get(), ws.ovf.get(), ws.ovf_cnt.get());
+        const KeyLab kl{keylab, plan.keylab_bytes ? (int)plan.keylab_bytes : 4};
+        const uint64_t* part = sliced_parts(ctx, kl, list, m, d, p, ws.part, s);
+        with_lab_type(kl, [&](auto lab) {
+            DK_LAUNCH_BU(ctx, part ? (double)m * 24.0 : (double)m * (4.0 * d.k + 16.0), part ? 0.0 : (double)m * d.k,
+                         sig_owner_kernel, grid_for(m, kThreads, (unsigned)ctx->num_sms * 8u), kThreads, 0, s, list,
+                         m, d.delta, d.n, lab, p, W, nb, cs, ws.scur.get(), ws.send.get(), ws.ovf.get(),
+                         ws.ovf_cnt.get(), part);
         });
     }
     DK_LAUNCH(ctx, owner_counts_kernel, grid_for((uint64_t)W * (nb + 1)), kThreads, 0, s, ws.scur.get(),

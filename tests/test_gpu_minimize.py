@@ -329,3 +329,24 @@ def test_arbitrary_replay_path(dk, oracle, monkeypatch):
     monkeypatch.delenv("DFAKIT_TEST_ARB_REPLAY")
     got = dk.naive_pr(mkdfa(dk, t), dk.ElectionPolicy.arbitrary(3))
     assert same(got, oracle.minimize("naive", t[0], t[1], policy=1, seed=3))
+
+
+def test_sliced_signature_passes(dk, oracle, monkeypatch):
+    """Passes whose key labels exceed the L2 gather their labels in sweeps
+    over slices of the label array and add partial keys (packed fields ORed,
+    fingerprint terms summed).  A tiny slice size forces that path (up to 64
+    slices) on small automata: partitions and pass counts stay the oracle's,
+    through fingerprints, packed keys, forced collisions and heavy
+    duplication."""
+    monkeypatch.setenv("DFAKIT_TEST_SLICE_BYTES", "2048")
+    g = random.Random(77)
+    for i in range(6):
+        n, k, s = g.randint(3000, 30000), g.randint(3, 12), g.getrandbits(64)
+        t = oracle.gen_random(n, k, 0.5 if i % 2 else 0.95, s)
+        want = oracle.minimize("moore", t[0], t[1])
+        dfa = mkdfa(dk, t)
+        for kw in ({}, {"fingerprint_bits": 6}, {"force_exact": True}):
+            assert same(dk.sort_pr(dfa, **kw), want), (i, kw)
+    for n0, c, k in ((2000, 50, 8), (20, 6000, 8)):
+        t = copies(oracle.gen_random(n0, k, 0.5, n0 * 7 + c), c)
+        assert same(dk.sort_pr(mkdfa(dk, t)), oracle.minimize("moore", t[0], t[1])), (n0, c)

@@ -157,7 +157,7 @@ def test_sharded_world2_one_gpu(dk):
         check(res[r])
 
 
-@pytest.mark.parametrize("layout", ["owner", "staged"])
+@pytest.mark.parametrize("layout", ["owner", "staged", "owner-sliced"])
 def test_native_driver_multirank_local_hub(dk, layout, monkeypatch):
     """The native C++ pass loop with world sizes 2 and 3: ranks are threads of
     this process, each with its own context on the one GPU, collectives
@@ -166,6 +166,8 @@ def test_native_driver_multirank_local_hub(dk, layout, monkeypatch):
     owner-bucket layout (the default) and the staged-entries protocol."""
     if layout == "staged":
         monkeypatch.setenv("DFAKIT_SHARD_STAGED", "1")
+    if layout == "owner-sliced":  # signature passes gathered in label slices
+        monkeypatch.setenv("DFAKIT_TEST_SLICE_BYTES", "4096")
     import ctypes as C
     import threading
     from paper_2508_20735_b200 import _native as nat
