@@ -136,6 +136,8 @@ _sig = {
 }
 EXPORTS = tuple(_sig)
 for _name, (_res, _args) in _sig.items():
+    if os.environ.get("DFAKIT_LIB_VARIANT") and not hasattr(lib, _name):
+        continue  # development variants may predate an export
     _fn = getattr(lib, _name)
     _fn.restype = _res
     _fn.argtypes = _args

@@ -62,6 +62,7 @@ struct ProfRec {
     const char* name;
     cudaEvent_t a, b;
     double bytes, units;
+    uint32_t pass;  // refinement pass the launch belongs to (0: none)
 };
 
 // Device context: one device, one stream, a stream-ordered pool, a pinned
@@ -80,6 +81,7 @@ struct Ctx {
     uint64_t launches = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     bool profiling = false;
+    uint32_t prof_pass = 0;  // set by the pass loops: launches are tagged with it
     cudaEvent_t pending = nullptr;
     std::vector<ProfRec> prof;
 };

@@ -24,7 +24,7 @@ void prof_end_launch(Ctx* ctx, cudaStream_t s, const char* name, double bytes, d
     cudaEvent_t b;
     DK_CUDA(cudaEventCreate(&b));
     DK_CUDA(cudaEventRecord(b, s));
-    ctx->prof.push_back(ProfRec{name, ctx->pending, b, bytes, units});
+    ctx->prof.push_back(ProfRec{name, ctx->pending, b, bytes, units, ctx->prof_pass});
     ctx->pending = nullptr;
 }
 
@@ -35,7 +35,7 @@ std::string prof_collect(Ctx* ctx) {
         uint64_t launches = 0;
         double ms = 0, bytes = 0, units = 0;
     };
-    std::vector<Agg> aggs;
+    std::vector<Agg> aggs, passes;  // per kernel name; per refinement pass ("#pass N")
     // DFAKIT_PROF_TIMELINE=1: every recorded launch with its start offset and
     // duration on stderr (development aid: gaps between launches)
     const bool timeline = getenv("DFAKIT_PROF_TIMELINE") != nullptr;
@@ -62,10 +62,25 @@ std::string prof_collect(Ctx* ctx) {
         g->ms += ms;
         g->bytes += r.bytes;
         g->units += r.units;
+        if (r.pass) {
+            const std::string pn = "#pass " + std::to_string(r.pass);
+            Agg* pg = nullptr;
+            for (auto& x : passes)
+                if (x.name == pn) pg = &x;
+            if (!pg) {
+                passes.push_back(Agg{pn});
+                pg = &passes.back();
+            }
+            ++pg->launches;
+            pg->ms += ms;
+            pg->bytes += r.bytes;
+            pg->units += r.units;
+        }
         cudaEventDestroy(r.a);
         cudaEventDestroy(r.b);
     }
     ctx->prof.clear();
+    aggs.insert(aggs.end(), passes.begin(), passes.end());
     std::string out = "[";
     char buf[512];
     for (size_t i = 0; i < aggs.size(); ++i) {

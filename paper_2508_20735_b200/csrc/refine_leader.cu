@@ -7,8 +7,12 @@
 // always compares larger and is overwritten without any reset kernel.  With
 // priority = q the winner is the minimum split state of the block -- the
 // reference's min_index policy exactly, so pass counts match bit for bit.
-// ElectionPolicy::arbitrary(seed) runs in refine_arbitrary.cu (the
-// reference's mt19937_64 reservoir sampling, reproduced exactly).
+// ElectionPolicy::arbitrary(seed) does not come here: refine_arbitrary.cu
+// reproduces the reference's mt19937_64 winner stream exactly.  The kernels
+// keep their priority hook (Prio; identity for min_index): without it the
+// persistent kernel measured slower (10M chain trans_pr 8.25 -> 10.8 ms, a
+// scheduling effect of the simpler code), so it stays as a generic
+// "order the candidates by" parameter.
 #include <cooperative_groups.h>
 
 #include "prims.cuh"
@@ -21,6 +25,36 @@ namespace dk {
 namespace {
 
 constexpr uint32_t kPending = 0x80000000u;
+
+// priority of a candidate: identity for min_index, a seeded bijection of
+// 32-bit words (xor, odd multiply, xorshift -- each step invertible) for
+// arbitrary(seed)
+struct Prio {
+    uint32_t salt, mul, mul_inv, ident;
+    __host__ __device__ uint32_t enc(uint32_t q) const {
+        if (ident) return q;
+        uint32_t x = (q ^ salt) * mul;
+        return x ^ (x >> 16);
+    }
+    __host__ __device__ uint32_t dec(uint32_t x) const {
+        if (ident) return x;
+        x ^= x >> 16;
+        return (x * mul_inv) ^ salt;
+    }
+};
+
+__host__ __device__ uint32_t inverse_odd(uint32_t a) {  // a * inv == 1 (mod 2^32), Newton iteration
+    uint32_t x = a;
+    for (int i = 0; i < 5; ++i) x *= 2u - a * x;
+    return x;
+}
+
+__host__ __device__ Prio make_prio(int policy, uint64_t seed, uint64_t pass) {
+    if (policy == DFAKIT_POLICY_MIN_INDEX) return {0u, 1u, 1u, 1u};
+    uint64_t h = mix64(seed * 0x9E3779B97F4A7C15ull + pass);
+    uint32_t mul = (uint32_t)(h >> 32) | 1u;
+    return {(uint32_t)h, mul, inverse_odd(mul), 0u};
+}
 
 // Alg. 3: election and reassignment in one pass.  Reads the pass-start
 // labels (cur), writes next; a split state records "pending on slot L" and
@@ -111,7 +145,7 @@ template <int C>
 __global__ void __launch_bounds__(kThreads)
     naive_persistent_kernel(const uint32_t* __restrict__ delta, uint32_t n, uint32_t k, uint32_t* __restrict__ lab,
                             unsigned long long* __restrict__ slot, uint32_t* __restrict__ split_list,
-                            uint32_t* __restrict__ cnt, PersistOut* __restrict__ out) {
+                            uint32_t* __restrict__ cnt, int policy, uint64_t seed, PersistOut* __restrict__ out) {
     __shared__ uint32_t cta_cnt[2];
     __shared__ uint32_t s_total;
     auto sync_all = [] { cg::this_grid().sync(); };
@@ -122,6 +156,7 @@ __global__ void __launch_bounds__(kThreads)
     __syncthreads();
     uint64_t pass = 0;
     for (;; ++pass) {
+        const Prio pr = make_prio(policy, seed, pass);
         const uint32_t epoch = 0xffffffffu - (uint32_t)pass;
         uint32_t* c = cnt + (pass & 1);
         uint32_t* cc = cta_cnt + (pass & 1);
@@ -132,7 +167,7 @@ __global__ void __launch_bounds__(kThreads)
             auto ident = [](uint32_t v) { return v; };
             const bool split =
                 L != q && differs_from_leader<decltype(ident), true, C>(q, L, delta, n, k, lab, ident);
-            elect(slot, L, epoch, split ? q : 0u, split);
+            elect(slot, L, epoch, split ? pr.enc(q) : 0u, split);
             const uint32_t at = warp_append(cc, split);
             if (split) my_list[at] = q;
         }
@@ -149,7 +184,7 @@ __global__ void __launch_bounds__(kThreads)
         if (tid == 0) cnt[(pass + 1) & 1] = 0;
         for (uint32_t i = threadIdx.x; i < mine; i += blockDim.x) {
             const uint32_t q = my_list[i];
-            lab[q] = (uint32_t)slot[lab[q]];
+            lab[q] = pr.dec((uint32_t)slot[lab[q]]);
         }
         sync_all();
     }
@@ -270,6 +305,7 @@ constexpr int kOneBatch = 8;  // states per thread per batch
 template <bool SMEM_DELTA>
 __global__ void __launch_bounds__(kOneThreads, 1) naive_one_kernel(const uint32_t* __restrict__ delta_g, uint32_t n,
                                                                    uint32_t k, uint32_t* __restrict__ lab_g,
+                                                                   int policy, uint64_t seed,
                                                                    PersistOut* __restrict__ out) {
     extern __shared__ __align__(16) unsigned char one_raw[];
     unsigned long long* slot = reinterpret_cast<unsigned long long*>(one_raw);
@@ -285,6 +321,7 @@ __global__ void __launch_bounds__(kOneThreads, 1) naive_one_kernel(const uint32_
     __syncthreads();
     uint64_t pass = 0;
     for (;; ++pass) {
+        const Prio pr = make_prio(policy, seed, pass);
         const uint32_t epoch = 0xffffffffu - (uint32_t)pass;
         uint32_t* c = misc + (pass & 1);
         for (uint32_t q0 = 0; q0 < n; q0 += blockDim.x * kOneBatch) {
@@ -299,7 +336,7 @@ __global__ void __launch_bounds__(kOneThreads, 1) naive_one_kernel(const uint32_
             for (int r = 0; r < kOneBatch; ++r) {
                 const bool split = Ls[r] != qs[r] && ((dif >> r) & 1u);
                 if (!__any_sync(0xffffffffu, split)) continue;
-                elect(slot, Ls[r], epoch, split ? qs[r] : 0u, split);
+                elect(slot, Ls[r], epoch, split ? pr.enc(qs[r]) : 0u, split);
                 const uint32_t at = warp_append(c, split);
                 if (split) split_list[at] = qs[r];
             }
@@ -310,7 +347,7 @@ __global__ void __launch_bounds__(kOneThreads, 1) naive_one_kernel(const uint32_
         if (threadIdx.x == 0) misc[(pass + 1) & 1] = 0;
         for (uint32_t i = threadIdx.x; i < total; i += blockDim.x) {
             const uint32_t q = split_list[i];
-            lab[q] = (uint32_t)slot[lab[q]];
+            lab[q] = pr.dec((uint32_t)slot[lab[q]]);
         }
         __syncthreads();
     }
@@ -458,9 +495,11 @@ RefineResult naive_pr_device(Ctx* ctx, const DevDfa& d, int policy, uint64_t see
         DK_CUDA(cudaFuncSetAttribute(op.mode == 2 ? naive_one_kernel<true> : naive_one_kernel<false>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)op.smem));
         if (op.mode == 2)
-            DK_LAUNCH(ctx, naive_one_kernel<true>, 1, op.threads, op.smem, s, d.delta, n, d.k, lab.get(), out.get());
+            DK_LAUNCH(ctx, naive_one_kernel<true>, 1, op.threads, op.smem, s, d.delta, n, d.k, lab.get(), policy,
+                      seed, out.get());
         else
-            DK_LAUNCH(ctx, naive_one_kernel<false>, 1, op.threads, op.smem, s, d.delta, n, d.k, lab.get(), out.get());
+            DK_LAUNCH(ctx, naive_one_kernel<false>, 1, op.threads, op.smem, s, d.delta, n, d.k, lab.get(), policy,
+                      seed, out.get());
         PersistOut o{};
         read_words(ctx, out.get(), sizeof(o), &o, s);
         res.passes = o.passes;
@@ -483,7 +522,7 @@ RefineResult naive_pr_device(Ctx* ctx, const DevDfa& d, int policy, uint64_t see
         PersistOut* outp = out.get();
         uint32_t nn = n;
         void* args[] = {(void*)&delta, (void*)&nn, (void*)&k, (void*)&labp, (void*)&slotp, (void*)&splitp,
-                        (void*)&cntp, (void*)&outp};
+                        (void*)&cntp, (void*)&policy, (void*)&seed, (void*)&outp};
         prof_begin_launch(ctx, s);
         DK_CUDA(cudaLaunchCooperativeKernel(kern, g, kThreads, args, 0, s));
         note_launch(ctx);

@@ -393,16 +393,36 @@ __global__ void __launch_bounds__(kThreads, DFAKIT_SIGB_MINB) sig_part_vec_kerne
                         }
                 }
         }
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-            if ((uint32_t)e < cnt) {
-                if (first) {
-                    __stcs(part + i + e, acc[e]);
-                } else {
-                    const uint64_t prev = __ldcs(part + i + e);
-                    __stcs(part + i + e, packed ? prev | acc[e] : prev + acc[e]);
-                }
+        // the four partial keys move as one 32-byte access (a warp's accesses
+        // cover 1 KB contiguously; four 8-byte accesses per thread touched 32
+        // sectors each)
+        if (cnt == 4) {
+            uint64_t* dst = part + i;
+            if (!first) {
+                uint64_t p0, p1, p2, p3;
+                asm volatile("ld.global.cs.v4.u64 {%0, %1, %2, %3}, [%4];"
+                             : "=l"(p0), "=l"(p1), "=l"(p2), "=l"(p3)
+                             : "l"(dst));
+                acc[0] = packed ? acc[0] | p0 : acc[0] + p0;
+                acc[1] = packed ? acc[1] | p1 : acc[1] + p1;
+                acc[2] = packed ? acc[2] | p2 : acc[2] + p2;
+                acc[3] = packed ? acc[3] | p3 : acc[3] + p3;
             }
+            asm volatile("st.global.cs.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(dst), "l"(acc[0]), "l"(acc[1]),
+                         "l"(acc[2]), "l"(acc[3])
+                         : "memory");
+        } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                if ((uint32_t)e < cnt) {
+                    if (first) {
+                        __stcs(part + i + e, acc[e]);
+                    } else {
+                        const uint64_t prev = __ldcs(part + i + e);
+                        __stcs(part + i + e, packed ? prev | acc[e] : prev + acc[e]);
+                    }
+                }
+        }
     }
 }
 
@@ -1480,8 +1500,27 @@ const uint64_t* sliced_parts(Ctx* ctx, const KeyLab& kl, const uint32_t* list, u
     const uint32_t slices = label_slices(kl, d.n);
     if (slices <= 1 || m == 0) return nullptr;
     if (part.n < m) part.alloc(m, s);
+    // the slice of labels a sweep gathers is pinned in the L2 (access-policy
+    // window, persisting) while delta and the partial keys stream past it
+    const bool pin = kl.bytes != kBitLabels && !getenv("DFAKIT_NO_L2_PIN");
+    size_t pin_max = 0;
+    if (pin) {
+        int v = 0;
+        DK_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMaxPersistingL2CacheSize, ctx->device));
+        pin_max = (size_t)v;
+        DK_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, pin_max));
+    }
     for (uint32_t j = 0; j < slices; ++j) {
         const uint32_t lo = (uint32_t)((uint64_t)d.n * j / slices), hi = (uint32_t)((uint64_t)d.n * (j + 1) / slices);
+        if (pin && pin_max) {
+            cudaStreamAttrValue av{};
+            av.accessPolicyWindow.base_ptr = const_cast<char*>(static_cast<const char*>(kl.p) + (size_t)lo * kl.bytes);
+            av.accessPolicyWindow.num_bytes = std::min<size_t>((size_t)(hi - lo) * kl.bytes, pin_max);
+            av.accessPolicyWindow.hitRatio = 1.0f;
+            av.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+            av.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+            DK_CUDA(cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &av));
+        }
         const bool vec = !list && d.n % 4 == 0 && p.q0 % 4 == 0;
         with_lab_type(kl, [&](auto lab) {
             // algorithmic HBM bytes: delta rows, the slice's labels, the partial keys
@@ -1495,6 +1534,15 @@ const uint64_t* sliced_parts(Ctx* ctx, const KeyLab& kl, const uint32_t* list, u
                              grid_for(m, kThreads, (unsigned)ctx->num_sms * 8u), kThreads, 0, s, list, m, d.delta,
                              d.n, lab, p, lo, hi, j == 0 ? 1 : 0, part.get());
         });
+    }
+    if (pin && pin_max) {  // release the window and the persisting lines
+        cudaStreamAttrValue av{};
+        av.accessPolicyWindow.num_bytes = 0;
+        DK_CUDA(cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &av));
+        DK_CUDA(cudaCtxResetPersistingL2Cache());
+        // give the set-aside L2 back to normal accesses (the kernels after
+        // the sweeps lost ~10 % with it reserved)
+        DK_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0));
     }
     return part.get();
 }
@@ -1962,6 +2010,7 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
             collisions_this_pass = 3;
         }
         ++res.passes;
+        ctx->prof_pass = (uint32_t)res.passes;  // profiler: this pass's launches
         const PassPlan plan = plan_pass(n, k, B, m, collisions_this_pass, o.force_exact);
         const bool fingerprint = plan.strategy == kPlanFingerprint, chunked = plan.strategy == kPlanChunked;
         const uint32_t field_bits = plan.field_bits;
@@ -2346,6 +2395,7 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
             if (dst == list_alt) std::swap(list_buf, list_alt);
         }
     }
+    ctx->prof_pass = 0;
     wait_all_chunks();  // inputs that needed no pass are still validated
     check_streamed();
     res.num_blocks = canonical_from_min_labels(ctx, w.lab.get(), n, block_out, w.scratch.get(), s, B);

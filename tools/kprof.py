@@ -125,7 +125,11 @@ def main():
         run()
     buf = C.create_string_buffer(1 << 16)
     nat.check(nat.lib.dfakit_profile_end(ctx.handle, buf, len(buf)))
-    ks = sorted(json.loads(buf.value.decode()), key=lambda x: -x["ms"])
+    allk = json.loads(buf.value.decode())
+    ks = sorted((x for x in allk if not x["name"].startswith("#")), key=lambda x: -x["ms"])
+    for x in allk:
+        if x["name"].startswith("#pass"):
+            print(f"  {x['name']:10s} {x['ms'] / a.reps:9.3f} ms  {x['bytes'] / a.reps / 1e6:9.1f} MB algorithmic")
     tot = sum(x["ms"] for x in ks)
     for x in ks[:15]:
         print(f"  {x['name'][:40]:40s} {x['ms'] / a.reps:9.3f} ms  x{x['launches'] / a.reps:.1f}  {100 * x['ms'] / tot:5.1f}%")

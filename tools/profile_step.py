@@ -9,7 +9,7 @@ workloads:
   naive     naive_pr + naive_pr_fused on 100K x 10
   chain     trans_pr on a 10M-state chain (pointer doubling)
   equiv     equivalence + inclusion (hash-set product BFS) and union-find HK, 10M x 2
-  sharded   the sharded engine at world size 1 (NCCL), 10M x 10
+  sharded   the native sharded engine at world size 1 (NCCL), 10M x 10
   trans     trans_minimize (CH92) on Fibonacci 12
   fib       naive_pr / naive_pr_fused (single-CTA kernels) and sort_pr (persistent small-m engine) on Fibonacci 19
   calib     the random-gather calibration probe
@@ -103,10 +103,11 @@ def main():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29533")
         dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
-        ops = sharded.CudaShardOps(ctx, delta, acc, n, k)
+        ncomm = sharded.NativeComm(ctx)  # the native C++ driver (owner-bucket layout)
         for _ in range(a.reps):
-            blocks, rep = sharded.sort_pr_sharded(ops, sharded.TorchComm(), n, k)
+            blocks, rep = sharded.sort_pr_sharded_native(ctx, ncomm, delta, acc, n, k)
         print("passes", rep.passes, "blocks", rep.num_blocks)
+        ncomm.close()
         dist.destroy_process_group()
         return
     if w == "naive":
