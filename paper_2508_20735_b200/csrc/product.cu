@@ -264,7 +264,9 @@ __device__ void solo_levels(const BfsArgs& A, SoloOut& o) {
             const uint32_t sl = tile_find_or_insert(tile, valid, key, A.table, mask);
             if (valid) {
                 const unsigned long long old = atomicMin(&A.table[sl].disc, disc);
-                A.item_slot[t] = (old >= ((unsigned long long)(wb + 1) << 32)) ? sl : kNone;
+                // a candidate winner only if the slot is new this level AND no
+                // smaller discoverer got there first (a loser needs no re-check)
+                A.item_slot[t] = (old >= ((unsigned long long)(wb + 1) << 32) && old > disc) ? sl : kNone;
                 A.item_key[t] = key;
             }
         }
@@ -395,7 +397,9 @@ __global__ void __launch_bounds__(kThreads) bfs_persistent_kernel(BfsArgs A) {
             const uint32_t sl = tile_find_or_insert(tile, valid, key, A.table, mask);
             if (valid) {
                 const unsigned long long old = atomicMin(&A.table[sl].disc, disc);
-                A.item_slot[t] = (old >= ((unsigned long long)(wb + 1) << 32)) ? sl : kNone;
+                // a candidate winner only if the slot is new this level AND no
+                // smaller discoverer got there first (a loser needs no re-check)
+                A.item_slot[t] = (old >= ((unsigned long long)(wb + 1) << 32) && old > disc) ? sl : kNone;
                 A.item_key[t] = key;
             }
         }
