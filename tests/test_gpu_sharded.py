@@ -157,56 +157,76 @@ def test_sharded_world2_one_gpu(dk):
         check(res[r])
 
 
+def run_hub(dk, world, d, a):
+    """The native driver at `world` ranks as threads of this process (each
+    with its own context on the one GPU, collectives through the in-process
+    hub); returns every rank's (block_of, refining_iterations, num_blocks)."""
+    import ctypes as C
+    import threading
+    from paper_2508_20735_b200 import _native as nat
+    k, n = d.shape
+    hub = C.c_void_p()
+    nat.check(nat.lib.dfakit_local_hub_create(world, C.byref(hub)))
+    out, errs = [None] * world, []
+
+    def rank_main(r):
+        try:
+            ctx = dk.Context(0)
+            comm = C.c_void_p()
+            nat.check(nat.lib.dfakit_comm_init_local(hub, r, C.byref(comm)))
+            delta = torch.from_numpy(np.ascontiguousarray(d).view(np.int32).reshape(-1)).cuda()
+            acc = torch.from_numpy(np.ascontiguousarray(a)).cuda()
+            blocks = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+            torch.cuda.synchronize()
+            view = nat.CDfa(n, k, delta.data_ptr() if k else None, acc.data_ptr(), -1)
+            rep = nat.CReport()
+            nat.check(nat.lib.dfakit_sort_pr_sharded(ctx.handle, comm, C.byref(view), blocks.data_ptr(),
+                                                     C.byref(rep), None, None))
+            out[r] = (blocks[:n].cpu().numpy().view(np.uint32), int(rep.refining_iterations), int(rep.num_blocks))
+            nat.lib.dfakit_comm_destroy(comm)
+        except Exception as e:  # pragma: no cover - reported below
+            errs.append((r, repr(e)))
+
+    threads = [threading.Thread(target=rank_main, args=(r,), daemon=True) for r in range(world)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(timeout=600)
+    nat.lib.dfakit_local_hub_destroy(hub)
+    assert not errs, (world, errs)
+    return out
+
+
+def check_hub(out, want, tag):
+    for r, (blocks, iters, nb) in enumerate(out):
+        assert np.array_equal(blocks, want.blocks) and nb == want.num_blocks, (tag, r)
+        assert iters == want.refine_iters, (tag, r, iters, want.refine_iters)
+
+
 @pytest.mark.parametrize("layout", ["owner", "staged", "owner-sliced"])
 def test_native_driver_multirank_local_hub(dk, layout, monkeypatch):
-    """The native C++ pass loop with world sizes 2 and 3: ranks are threads of
-    this process, each with its own context on the one GPU, collectives
-    through the in-process hub (NCCL refuses two ranks on one device).  Every
-    rank must return the oracle's partition and pass count -- through the
-    owner-bucket layout (the default) and the staged-entries protocol."""
+    """The native C++ pass loop with world sizes 2 and 3 (ranks as threads on
+    the one GPU; NCCL refuses two ranks on one device).  Every rank must
+    return the oracle's partition and pass count -- through the owner-bucket
+    layout (the default), the staged-entries protocol, and sliced passes."""
     if layout == "staged":
         monkeypatch.setenv("DFAKIT_SHARD_STAGED", "1")
     if layout == "owner-sliced":  # signature passes gathered in label slices
         monkeypatch.setenv("DFAKIT_TEST_SLICE_BYTES", "4096")
-    import ctypes as C
-    import threading
-    from paper_2508_20735_b200 import _native as nat
     cases = [c for c in CASES if c[0] != "synth"] + [("synth", 300_000, 10, 0.0, 5)]
     for world in (2, 3):
         for case in cases:
             d, a, want = make_case(case)
-            k, n = d.shape
-            hub = C.c_void_p()
-            nat.check(nat.lib.dfakit_local_hub_create(world, C.byref(hub)))
-            out, errs = [None] * world, []
+            check_hub(run_hub(dk, world, d, a), want, (layout, world, case))
 
-            def rank_main(r):
-                try:
-                    ctx = dk.Context(0)
-                    comm = C.c_void_p()
-                    nat.check(nat.lib.dfakit_comm_init_local(hub, r, C.byref(comm)))
-                    delta = torch.from_numpy(np.ascontiguousarray(d).view(np.int32).reshape(-1)).cuda()
-                    acc = torch.from_numpy(np.ascontiguousarray(a)).cuda()
-                    blocks = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
-                    torch.cuda.synchronize()
-                    view = nat.CDfa(n, k, delta.data_ptr() if k else None, acc.data_ptr(), -1)
-                    rep = nat.CReport()
-                    nat.check(nat.lib.dfakit_sort_pr_sharded(ctx.handle, comm, C.byref(view), blocks.data_ptr(),
-                                                             C.byref(rep), None, None))
-                    out[r] = (blocks[:n].cpu().numpy().view(np.uint32), int(rep.refining_iterations),
-                              int(rep.num_blocks))
-                    nat.lib.dfakit_comm_destroy(comm)
-                except Exception as e:  # pragma: no cover - reported below
-                    errs.append((r, repr(e)))
 
-            threads = [threading.Thread(target=rank_main, args=(r,), daemon=True) for r in range(world)]
-            for t in threads:
-                t.start()
-            for t in threads:
-                t.join(timeout=600)
-            nat.lib.dfakit_local_hub_destroy(hub)
-            assert not errs, (world, case, errs)
-            for r in range(world):
-                blocks, iters, nb = out[r]
-                assert np.array_equal(blocks, want.blocks) and nb == want.num_blocks, (world, case, r)
-                assert iters == want.refine_iters, (world, case, r, iters, want.refine_iters)
+def test_native_driver_wide_worlds(dk):
+    """World sizes 5 and 8 (the owner-bucket layout's largest: sub-buckets of
+    2048 / 8 = 256 slots, so heavy classes overflow into the fallback) and 9
+    (past it: the staged protocol)."""
+    cases = [("random", 20000, 10, 0.5, 14), ("bigcopies", 40, 8, 0.5, 17), ("copies", 400, 8, 0.5, 15),
+             ("family", 12, 0, 0.0, 1), ("synth", 200_000, 10, 0.0, 7)]
+    for world in (5, 8, 9):
+        for case in cases:
+            d, a, want = make_case(case)
+            check_hub(run_hub(dk, world, d, a), want, (world, case))
