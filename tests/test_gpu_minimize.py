@@ -246,6 +246,17 @@ def test_streamed_host_input(dk, oracle):
         dk.sort_pr(dk.Dfa(bad, t[1], 0))
 
 
+def test_streamed_host_input_sliced(dk, oracle, monkeypatch):
+    """The streamed host-buffer path with every wide pass sliced (the
+    1B-transition e2e shape, forced at 1.5M states)."""
+    monkeypatch.setenv("DFAKIT_TEST_SLICE_BYTES", "200000")
+    t = oracle.gen_synth(1_500_000, 10, 4)
+    want = oracle.minimize("moore", t[0], t[1])
+    assert same(dk.sort_pr(mkdfa(dk, t)), want)
+    t = copies(oracle.gen_random(3000, 6, 0.5, 9), 400)
+    assert same(dk.sort_pr(mkdfa(dk, t)), oracle.minimize("moore", t[0], t[1]))
+
+
 def test_naive_kernel_paths(dk, oracle):
     """Leader election through each of its kernels: single CTA with delta in
     shared memory (n * k small), single CTA with delta from L1 (shared arrays
