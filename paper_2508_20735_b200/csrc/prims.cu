@@ -407,7 +407,10 @@ uint32_t canonical_from_min_labels(Ctx* ctx, const uint32_t* lab, uint64_t n, ui
 
 constexpr int kRadixBits = 8;
 constexpr int kRadix = 1 << kRadixBits;
-constexpr int kSortThreads = 256;
+#ifndef DFAKIT_SORT_THREADS
+#define DFAKIT_SORT_THREADS 256
+#endif
+constexpr int kSortThreads = DFAKIT_SORT_THREADS;  // >= kRadix: threads d < 256 own digit d in the tile scan
 constexpr int kSortWarps = kSortThreads / 32;
 #ifndef DFAKIT_SORT_ITEMS
 #define DFAKIT_SORT_ITEMS 12
@@ -481,7 +484,7 @@ __global__ void __launch_bounds__(kSortThreads, DFAKIT_SORT_MINB) radix_onesweep
         (&sm.warp_hist[0][0])[i] = 0;
         (&sm.match[0][0])[i] = 0;
     }
-    sm.tile_hist[threadIdx.x] = 0;
+    if (threadIdx.x < kRadix) sm.tile_hist[threadIdx.x] = 0;
     __syncthreads();
     const uint32_t tile = sm.tile;
     const uint64_t seg = (uint64_t)tile * kSortTile + (uint64_t)wid * kWarpSpan;
@@ -503,7 +506,7 @@ __global__ void __launch_bounds__(kSortThreads, DFAKIT_SORT_MINB) radix_onesweep
     __syncthreads();
     volatile unsigned long long* lk = look;
     const unsigned long long hi = (unsigned long long)tag << 40;
-    {
+    if (threadIdx.x < kRadix) {
         const uint32_t d = threadIdx.x, c = sm.tile_hist[d];
         lk[(uint64_t)tile * kRadix + d] = hi | ((tile == 0 ? kFlagPre : kFlagAgg) << 32) | c;
     }
@@ -537,8 +540,9 @@ __global__ void __launch_bounds__(kSortThreads, DFAKIT_SORT_MINB) radix_onesweep
     __syncthreads();
     uint32_t tile_count = 0;
     {
-        const int d = threadIdx.x;  // kSortThreads == kRadix
+        const int d = threadIdx.x;  // digit d < kRadix; the other threads only join the scan
         uint32_t run = 0;
+        if (d < kRadix) {
 #pragma unroll
         for (int w = 0; w < kSortWarps; ++w) {
             const uint32_t c = sm.warp_hist[w][d];
@@ -570,7 +574,9 @@ __global__ void __launch_bounds__(kSortThreads, DFAKIT_SORT_MINB) radix_onesweep
             lk[(uint64_t)tile * kRadix + d] = hi | (kFlagPre << 32) | (excl + run);
             sm.global_base[d] = bins[d] + excl;
         }
-        sm.digit_start[d] = block_exclusive_scan<kSortThreads>(run, &tile_count, sm.ws);
+        }
+        const uint32_t ds = block_exclusive_scan<kSortThreads>(run, &tile_count, sm.ws);
+        if (d < kRadix) sm.digit_start[d] = ds;
     }
     __syncthreads();
 #pragma unroll
@@ -594,7 +600,7 @@ __global__ void __launch_bounds__(kSortThreads, DFAKIT_SORT_MINB) radix_onesweep
 
 bool radix_sort_pairs_range(Ctx* ctx, RadixBuffers b, uint64_t m, uint32_t bit_lo, uint32_t bit_hi,
                             cudaStream_t s) {
-    static_assert(kSortThreads == kRadix, "one thread per digit in the tile scan");
+    static_assert(kSortThreads >= kRadix && kSortThreads % 32 == 0, "one thread per digit in the tile scan");
     if (m <= 1 || bit_hi <= bit_lo) return false;
     if (m > 0xffffffffull) throw Error(DFAKIT_E_RESOURCE, "radix sort: more than 2^32 keys");
     DK_CUDA(cudaFuncSetAttribute(radix_onesweep_kernel<kLookWin>, cudaFuncAttributeMaxDynamicSharedMemorySize,
