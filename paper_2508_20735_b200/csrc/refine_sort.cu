@@ -1502,13 +1502,15 @@ const uint64_t* sliced_parts(Ctx* ctx, const KeyLab& kl, const uint32_t* list, u
     if (part.n < m) part.alloc(m, s);
     // the slice of labels a sweep gathers is pinned in the L2 (access-policy
     // window, persisting) while delta and the partial keys stream past it
-    const bool pin = kl.bytes != kBitLabels && !getenv("DFAKIT_NO_L2_PIN");
+    // (a performance hint only: where the device refuses it, the sweeps run unpinned)
+    bool pin = kl.bytes != kBitLabels && !getenv("DFAKIT_NO_L2_PIN");
     size_t pin_max = 0;
     if (pin) {
         int v = 0;
-        DK_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMaxPersistingL2CacheSize, ctx->device));
-        pin_max = (size_t)v;
-        DK_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, pin_max));
+        pin = cudaDeviceGetAttribute(&v, cudaDevAttrMaxPersistingL2CacheSize, ctx->device) == cudaSuccess && v > 0 &&
+              cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)v) == cudaSuccess;
+        pin_max = pin ? (size_t)v : 0;
+        if (!pin) (void)cudaGetLastError();
     }
     for (uint32_t j = 0; j < slices; ++j) {
         const uint32_t lo = (uint32_t)((uint64_t)d.n * j / slices), hi = (uint32_t)((uint64_t)d.n * (j + 1) / slices);
@@ -1519,7 +1521,8 @@ const uint64_t* sliced_parts(Ctx* ctx, const KeyLab& kl, const uint32_t* list, u
             av.accessPolicyWindow.hitRatio = 1.0f;
             av.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
             av.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-            DK_CUDA(cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &av));
+            if (cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &av) != cudaSuccess)
+                (void)cudaGetLastError();
         }
         const bool vec = !list && d.n % 4 == 0 && p.q0 % 4 == 0;
         with_lab_type(kl, [&](auto lab) {
@@ -1538,11 +1541,12 @@ const uint64_t* sliced_parts(Ctx* ctx, const KeyLab& kl, const uint32_t* list, u
     if (pin && pin_max) {  // release the window and the persisting lines
         cudaStreamAttrValue av{};
         av.accessPolicyWindow.num_bytes = 0;
-        DK_CUDA(cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &av));
-        DK_CUDA(cudaCtxResetPersistingL2Cache());
         // give the set-aside L2 back to normal accesses (the kernels after
         // the sweeps lost ~10 % with it reserved)
-        DK_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0));
+        if (cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &av) != cudaSuccess ||
+            cudaCtxResetPersistingL2Cache() != cudaSuccess ||
+            cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0) != cudaSuccess)
+            (void)cudaGetLastError();
     }
     return part.get();
 }
