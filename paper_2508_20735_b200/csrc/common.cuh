@@ -160,5 +160,9 @@ __device__ __forceinline__ uint32_t warp_append(uint32_t* counter, bool pred) {
 
 // Synchronous readback of `count` words from device memory through the pinned mailbox.
 void read_words(Ctx* ctx, const void* dsrc, size_t bytes, void* hdst, cudaStream_t s);
+// the same in two halves: the copy is queued by _begin, _end waits for it --
+// work queued in between runs while the host waits
+uint32_t read_words_begin(Ctx* ctx, const void* dsrc, size_t bytes, cudaStream_t s);
+void read_words_end(Ctx* ctx, uint32_t seq, size_t bytes, void* hdst, cudaStream_t s);
 
 }  // namespace dk

@@ -106,11 +106,19 @@ __global__ void mailbox_kernel(const uint8_t* __restrict__ src, uint32_t bytes, 
 }
 
 void read_words(Ctx* ctx, const void* dsrc, size_t bytes, void* hdst, cudaStream_t s) {
+    read_words_end(ctx, read_words_begin(ctx, dsrc, bytes, s), bytes, hdst, s);
+}
+
+uint32_t read_words_begin(Ctx* ctx, const void* dsrc, size_t bytes, cudaStream_t s) {
     if (bytes > 56 * sizeof(uint64_t)) throw Error(DFAKIT_E_INVALID, "read_words: too large");
     const uint32_t seq = ++ctx->fast_seq;
     mailbox_kernel<<<1, 128, 0, s>>>(static_cast<const uint8_t*>(dsrc), (uint32_t)bytes, ctx->fastbox, seq);
     DK_CUDA(cudaGetLastError());
     note_launch(ctx);
+    return seq;
+}
+
+void read_words_end(Ctx* ctx, uint32_t seq, size_t bytes, void* hdst, cudaStream_t s) {
     // spin for short waits (the pass loop's readbacks follow sub-millisecond
     // kernels); past ~200 us block in cudaStreamSynchronize instead of
     // burning a core behind a long kernel

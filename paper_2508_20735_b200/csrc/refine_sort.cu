@@ -54,6 +54,15 @@ namespace {
 constexpr uint32_t kTableBits = 20;
 constexpr uint32_t kSmemTableBits = 13;
 
+// layout of one bucket-strategy pass (see bucket_layout in sort_pr_device)
+struct BucketLayout {
+    uint32_t nb = 0;
+    uint64_t bspace = 0, espace = 0;
+    bool state_order = false, defer = false, direct = false;
+};
+// automata from this size on queue their second pass speculatively
+constexpr uint32_t kSpecMinStates = 1u << 22;
+
 struct IterCounters {
     uint32_t runs;
     uint32_t active_blocks;
@@ -1457,7 +1466,7 @@ struct Workspace {
     DBuf<uint4> bent;
     DBuf<unsigned long long> gkey;
     DBuf<uint8_t> keep_slot, gmul;
-    DBuf<IterCounters> ctr;
+    DBuf<IterCounters> ctr, ctr2;  // ctr2: the counters of a speculative second pass
 };
 
 // Key-label array of one pass: min-state labels, or dense block ids in the
@@ -1878,6 +1887,7 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
     w.scratch.alloc((uint64_t)n + 1, s);
     w.keep.alloc(n, s);
     w.ctr.alloc(1, s);
+    w.ctr2.alloc(1, s);
     DK_CUDA(cudaFuncSetAttribute(bucket_group_kernel<ArrLab<uint32_t>, OneSrc>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)sizeof(GroupSmem)));
     const int smem_table = (int)(2u << kSmemTableBits) * 4;
@@ -1950,6 +1960,88 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
     // compactions in state order, and order-preserving table compactions);
     // lists in bucket-slot or sorted order clear it
     bool list_inc = true;
+    // Speculative second pass: a first pass over every state with a counting
+    // table already wrote the next key labels (table ranks) and labels when
+    // its counters are still on their way to the host; the second pass -- a
+    // fingerprint bucket pass over every state, the plan every wide second
+    // pass can take -- is queued right behind it instead of after the
+    // readback (one host round trip less between the passes).  It defers its
+    // labels (nothing is applied before its counters are read), so a pass-1
+    // fixed point or survivors that make it moot just drop it.
+    bool spec_launched = false;
+    bool iota_out = false;  // block_out holds the identity numbering (queued speculatively)
+    PassPlan spec_plan{};
+    KeyLab spec_kl{nullptr, 0};
+    // DFAKIT_TEST_SPEC_MIN=<states> lowers the threshold (tests), DFAKIT_NO_SPEC=1 disables it
+    const char* spec_min_env = getenv("DFAKIT_TEST_SPEC_MIN");
+    const uint64_t spec_min = spec_min_env ? strtoull(spec_min_env, nullptr, 10) : kSpecMinStates;
+    const bool spec_ok = !(ds && ds->chunks) && o.grouping == 0 && !o.force_exact && n >= spec_min &&
+                         n < 0x80000000u && !getenv("DFAKIT_NO_SPEC");
+
+    // bucket strategy: 2^D buckets of 768..1536 expected keys (Poisson tail
+    // well inside the 2048 slots unless keys repeat).  Big passes flag
+    // survivors per state (the next list comes out sorted, so its delta
+    // reads stay coalesced) and write labels in place (exact keys); big
+    // fingerprint passes defer their labels: packed per-slot records
+    // (coalesced) applied after verification -- and not at all when every
+    // block came out a singleton (the usual last pass: 4-byte label stores to
+    // random states cost as much as the rest of the grouping); small passes
+    // keep per-slot outputs and apply fingerprint labels afterwards
+    auto bucket_layout = [&](bool fingerprint, uint64_t mm) {
+        BucketLayout L;
+        uint32_t D = 1;
+        while (D < 24 && ((uint64_t)1 << D) * (kGrpCap * 3 / 4) < mm) ++D;
+        L.nb = 1u << D;
+        L.bspace = (uint64_t)L.nb * kGrpCap;
+        L.espace = L.bspace + mm;
+        L.state_order = mm >= (uint64_t)n / 16;
+        L.defer = fingerprint && L.state_order && n < 0x80000000u;
+        L.direct = (!fingerprint || L.state_order) && !L.defer;
+        return L;
+    };
+    // allocations, the pass prologue's fills, signature + bucket append,
+    // grouping (counters into ctrx)
+    auto bucket_launch = [&](const PassPlan& pl, const KeyLab& klx, const SigParams& px, const uint32_t* lst,
+                             uint64_t mm, IterCounters* ctrx, Fills& fl) {
+        const bool fingerprint = pl.strategy == kPlanFingerprint;
+        const BucketLayout L = bucket_layout(fingerprint, mm);
+        if (w.bcnt.n < (uint64_t)L.nb * kCntStride) w.bcnt.alloc((uint64_t)L.nb * kCntStride, s);
+        if (w.bent.n < L.espace) {
+            w.bent.alloc(L.espace, s);
+            w.keep_slot.alloc(L.espace, s);
+        }
+        if (!L.direct && !L.defer && w.rep_slot.n < L.espace) w.rep_slot.alloc(L.espace, s);
+        if (L.defer && w.rec.n < L.espace) w.rec.alloc(L.espace, s);
+        if (L.state_order && !w.act.get()) w.act.alloc(n, s);
+        if (fingerprint && L.direct) {
+            if (!w.lab2.get()) w.lab2.alloc(n, s);
+            // a pass over every state writes every label of the copy
+            if (lst) DK_CUDA(cudaMemcpyAsync(w.lab2.get(), w.lab.get(), (size_t)n * 4, cudaMemcpyDeviceToDevice, s));
+        }
+        uint32_t* out_lab = fingerprint && L.direct ? w.lab2.get() : w.lab.get();
+        fl.add(w.bcnt.get(), (size_t)L.nb * kCntStride * 4, 0);
+        if (L.state_order) fl.add(w.act.get(), n, 0);
+        if (!L.state_order) fl.add(w.keep_slot.get(), L.espace, 0);
+        fl.flush(ctx, s);
+        const double lb = lst ? 4.0 : 0.0;
+        const uint64_t* part = sliced_parts(ctx, klx, lst, mm, d, px, w.part, s);
+        with_lab_type(klx, [&](auto lab) {
+            // algorithmic HBM bytes: delta rows (+ list), (hkey, state) out, the key-label array once
+            // (a sliced pass: the partial keys in, hkey out)
+            DK_LAUNCH_BU(ctx, part ? (double)mm * 24.0 : (double)mm * (4.0 * k + 16.0 + lb) + keylab_bytes_per_state(klx) * n,
+                         part ? 0.0 : (double)mm * k, sig_bucket_kernel,
+                         grid_for(mm, kThreads, (unsigned)ctx->num_sms * 8u), kThreads, 0, s, lst, mm, d.delta, n,
+                         lab, px, L.nb, w.bcnt.get(), w.bent.get(), ctrx, part);
+        });
+        GroupOut go{L.direct ? 1 : 0, L.state_order ? 1 : 0, out_lab, w.act.get(),
+                    L.direct || L.defer ? nullptr : w.rep_slot.get(), w.keep_slot.get(), nullptr,
+                    L.defer ? w.rec.get() : nullptr, 0};
+        const unsigned gg = (unsigned)std::min<uint64_t>(L.nb, (uint64_t)ctx->num_sms * kGrpCtasPerSm);
+        // algorithmic HBM bytes: (hkey, state) in, label + survivor flag out
+        DK_LAUNCH_B(ctx, (double)mm * (16.0 + 4.0 + 1.0 + (L.direct ? 0.0 : 4.0)), bucket_group_kernel, gg,
+                    kGrpThreads, sizeof(GroupSmem), s, OneSrc{w.bcnt.get(), w.bent.get()}, L.nb, fingerprint ? 1 : 0,
+                    d.delta, n, k, ArrLab<uint32_t>{w.lab.get()}, go, ctrx);
+    };
 
     auto dense_keylab = [&](int bytes) -> KeyLab {
         void* p;
@@ -2015,11 +2107,18 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
         }
         ++res.passes;
         ctx->prof_pass = (uint32_t)res.passes;  // profiler: this pass's launches
-        const PassPlan plan = plan_pass(n, k, B, m, collisions_this_pass, o.force_exact);
+        // a speculative pass launched behind the previous one is used when
+        // that pass left every state active (it then covered exactly this
+        // pass's states); otherwise its work is dropped (it applied nothing)
+        const bool use_spec = spec_launched && list == nullptr && m == n && collisions_this_pass == 0;
+        spec_launched = false;
+        const PassPlan plan = use_spec ? spec_plan : plan_pass(n, k, B, m, collisions_this_pass, o.force_exact);
         const bool fingerprint = plan.strategy == kPlanFingerprint, chunked = plan.strategy == kPlanChunked;
         const uint32_t field_bits = plan.field_bits;
         KeyLab kl{w.lab.get(), 4};
-        if (plan.keylab_bytes) {
+        if (use_spec) {
+            kl = spec_kl;
+        } else if (plan.keylab_bytes) {
             if (next_valid && plan.strategy != kPlanChunked) {
                 kl = w.next16.get() && prev_nbits <= 16 ? KeyLab{w.next16.get(), 2} : KeyLab{w.next32.get(), 4};
             } else if (B <= 2 && plan.strategy != kPlanChunked && n >= kBitLabelsMinStates) {
@@ -2151,6 +2250,27 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
                             full && nbits > 16 ? w.next32.get() : nullptr, 0u, dctr);
             next_valid = full;
             prev_nbits = nbits;
+            if (spec_ok && full && nbits <= 16 && res.passes == 1 && collisions_this_pass == 0) {
+                // the second pass, queued before this pass's readback: a
+                // fingerprint bucket pass over every state on the table ranks
+                spec_plan = PassPlan{};
+                spec_plan.strategy = kPlanFingerprint;
+                spec_plan.key_bits = 64;
+                spec_plan.keylab_bytes = 2;
+                spec_kl = KeyLab{w.next16.get(), 2};
+                SigParams sp{};
+                sp.kind = kKeyFingerprint;
+                sp.a0 = 0;
+                sp.a1 = k;
+                sp.salt = salt;
+                sp.fp_mask = fp_mask;
+                Fills sf;
+                sf.add(w.ctr2.get(), sizeof(IterCounters), 0);
+                ctx->prof_pass = (uint32_t)res.passes + 1;
+                bucket_launch(spec_plan, spec_kl, sp, nullptr, n, w.ctr2.get(), sf);
+                ctx->prof_pass = (uint32_t)res.passes;
+                spec_launched = true;
+            }
             // every state survives (the first pass of a random automaton):
             if (deferred_info && res.passes == 1) {  // the class sizes, read while the pass ran
                 li = leader_info_wait(ctx);
@@ -2166,62 +2286,28 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
         } else if (!chunked && o.grouping != 1) {
             wait_all_chunks();
             // ---- bucket strategy
-            // 2^D buckets of 768..1536 expected keys (Poisson tail well inside
-            // the 2048 slots unless keys repeat)
-            uint32_t D = 1;
-            while (D < 24 && ((uint64_t)1 << D) * (kGrpCap * 3 / 4) < m) ++D;
-            const uint32_t nb = 1u << D;
-            const uint64_t bspace = (uint64_t)nb * kGrpCap, espace = bspace + m;
-            if (w.bcnt.n < (uint64_t)nb * kCntStride) w.bcnt.alloc((uint64_t)nb * kCntStride, s);
-            if (w.bent.n < espace) {
-                w.bent.alloc(espace, s);
-                w.keep_slot.alloc(espace, s);
-            }
-            // big passes flag survivors per state (the next list comes out
-            // sorted, so its delta reads stay coalesced) and write labels in
-            // place (exact keys) or into the ping-pong copy (fingerprints:
-            // discarded if verification finds a collision); small passes
-            // keep per-slot outputs and apply fingerprint labels afterwards
-            const bool state_order = m >= (uint64_t)n / 16;
-            // big fingerprint passes defer their labels: packed per-slot
-            // records (coalesced) are applied after verification -- and not at
-            // all when every block came out a singleton (the usual last pass:
-            // 4-byte label stores to random states cost as much as the rest
-            // of the grouping)
-            const bool defer = fingerprint && state_order && n < 0x80000000u;
-            const bool direct = (!fingerprint || state_order) && !defer;
-            if (!direct && !defer && w.rep_slot.n < espace) w.rep_slot.alloc(espace, s);
-            if (defer && w.rec.n < espace) w.rec.alloc(espace, s);
-            if (state_order && !w.act.get()) w.act.alloc(n, s);
-            if (fingerprint && direct) {
-                if (!w.lab2.get()) w.lab2.alloc(n, s);
-                // a pass over every state writes every label of the copy
-                if (list) DK_CUDA(cudaMemcpyAsync(w.lab2.get(), w.lab.get(), (size_t)n * 4, cudaMemcpyDeviceToDevice, s));
-            }
+            const BucketLayout L = bucket_layout(fingerprint, m);
+            const uint32_t nb = L.nb;
+            const uint64_t bspace = L.bspace, espace = L.espace;
+            const bool state_order = L.state_order, defer = L.defer, direct = L.direct;
+            IterCounters* pctr = use_spec ? w.ctr2.get() : dctr;  // the counters this pass's kernels wrote
+            if (!use_spec) bucket_launch(plan, kl, p, list, m, dctr, fills);
             uint32_t* out_lab = fingerprint && direct ? w.lab2.get() : w.lab.get();
-            fills.add(w.bcnt.get(), (size_t)nb * kCntStride * 4, 0);
-            if (state_order) fills.add(w.act.get(), n, 0);
-            if (!state_order) fills.add(w.keep_slot.get(), espace, 0);
-            fills.flush(ctx, s);
-            const uint64_t* part = sliced_parts(ctx, kl, list, m, d, p, w.part, s);
-            with_lab_type(kl, [&](auto lab) {
-                // algorithmic HBM bytes: delta rows (+ list), (hkey, state) out, the key-label array once
-                // (a sliced pass: the partial keys in, hkey out)
-                DK_LAUNCH_BU(ctx, part ? (double)m * 24.0 : (double)m * (4.0 * k + 16.0 + list_b) + keylab_bytes_per_state(kl) * n,
-                             part ? 0.0 : (double)m * k, sig_bucket_kernel,
-                             grid_for(m, kThreads, (unsigned)ctx->num_sms * 8u), kThreads, 0, s, list, m, d.delta, n,
-                             lab, p, nb, w.bcnt.get(), w.bent.get(), dctr, part);
-            });
             GroupOut go{direct ? 1 : 0, state_order ? 1 : 0, out_lab, w.act.get(),
                         direct || defer ? nullptr : w.rep_slot.get(), w.keep_slot.get(), nullptr,
                         defer ? w.rec.get() : nullptr, 0};
-            const unsigned gg = (unsigned)std::min<uint64_t>(nb, (uint64_t)ctx->num_sms * kGrpCtasPerSm);
-            // algorithmic HBM bytes: (hkey, state) in, label + survivor flag out
-            DK_LAUNCH_B(ctx, (double)m * (16.0 + 4.0 + 1.0 + (direct ? 0.0 : 4.0)),
-                        bucket_group_kernel, gg, kGrpThreads, sizeof(GroupSmem), s,
-                        OneSrc{w.bcnt.get(), w.bent.get()}, nb, fingerprint ? 1 : 0, d.delta, n, k,
-                        ArrLab<uint32_t>{w.lab.get()}, go, dctr);
-            read_words(ctx, dctr, sizeof(c), &c, s);
+            {
+                const uint32_t seq = read_words_begin(ctx, pctr, sizeof(c), s);
+                // a deferred pass over every state is usually the last one,
+                // leaving every block a singleton: the identity numbering is
+                // queued while the host waits for the counters (the final
+                // numbering overwrites it otherwise)
+                if (defer && m == n && !iota_out) {
+                    iota_u32(ctx, block_out, n, s);
+                    iota_out = true;
+                }
+                read_words_end(ctx, seq, sizeof(c), &c, s);
+            }
             if (c.overflow) {
                 // heavy duplication: overflowed buckets through a global table
                 uint64_t T = 2;
@@ -2242,8 +2328,8 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
                           w.grep.get(), w.gslot.get(), w.gmul.get());
                 DK_LAUNCH(ctx, ghash_out_kernel, eg, kThreads, 0, s, w.bcnt.get(), nb, c.overflow, w.bent.get(),
                           w.grep.get(), w.gslot.get(), w.gmul.get(), fingerprint ? 1 : 0, d.delta, n, k,
-                          ArrLab<uint32_t>{w.lab.get()}, go, dctr);
-                read_words(ctx, dctr, sizeof(c), &c, s);
+                          ArrLab<uint32_t>{w.lab.get()}, go, pctr);
+                read_words(ctx, pctr, sizeof(c), &c, s);
             }
             res.sorted += m;
             check_streamed();
@@ -2268,13 +2354,13 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
                             w.lab.get(), state_order ? w.act.get() : nullptr);
             list_inc = state_order;
             if (c.active_states) {
-                if (state_order) compact_flags(ctx, nullptr, w.act.get(), n, dst, &dctr->listed, s);
+                if (state_order) compact_flags(ctx, nullptr, w.act.get(), n, dst, &pctr->listed, s);
                 else {
                     // survivors in slot order: states of the slot entries
                     if (w.eval.n < espace) w.eval.alloc(espace, s);
                     DK_LAUNCH(ctx, entry_state_kernel, grid_for(bspace + c.overflow), kThreads, 0, s, w.bent.get(),
                               w.keep_slot.get(), bspace + c.overflow, w.eval.get());
-                    compact_flags(ctx, w.eval.get(), w.keep_slot.get(), bspace + c.overflow, dst, &dctr->listed, s);
+                    compact_flags(ctx, w.eval.get(), w.keep_slot.get(), bspace + c.overflow, dst, &pctr->listed, s);
                 }
             }
         } else {
@@ -2402,7 +2488,8 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
     ctx->prof_pass = 0;
     wait_all_chunks();  // inputs that needed no pass are still validated
     check_streamed();
-    res.num_blocks = canonical_from_min_labels(ctx, w.lab.get(), n, block_out, w.scratch.get(), s, B);
+    if (B == n && iota_out) res.num_blocks = n;  // the identity numbering is in block_out already
+    else res.num_blocks = canonical_from_min_labels(ctx, w.lab.get(), n, block_out, w.scratch.get(), s, B);
     return res;
 }
 

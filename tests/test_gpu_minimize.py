@@ -361,3 +361,26 @@ def test_sliced_signature_passes(dk, oracle, monkeypatch):
     for n0, c, k in ((2000, 50, 8), (20, 6000, 8)):
         t = copies(oracle.gen_random(n0, k, 0.5, n0 * 7 + c), c)
         assert same(dk.sort_pr(mkdfa(dk, t)), oracle.minimize("moore", t[0], t[1])), (n0, c)
+
+
+def test_speculative_second_pass(dk, oracle, monkeypatch):
+    """Large automata queue their second pass (a fingerprint bucket pass over
+    every state) behind the first before its counters are read; it is used
+    when the first pass left every state active and dropped otherwise.  The
+    threshold is lowered so small automata take that path: pass-1 fixed
+    points, survivors that make it moot, collisions (6-bit fingerprints) and
+    duplicates -- partitions and pass counts stay the oracle's."""
+    monkeypatch.setenv("DFAKIT_TEST_SPEC_MIN", "1000")
+    g = random.Random(91)
+    for i in range(24):
+        n, k, s = g.randint(1000, 40000), g.randint(1, 12), g.getrandbits(64)
+        t = oracle.gen_random(n, k, [0.5, 0.9, 1.0, 0.0, 0.99][i % 5], s)
+        want = oracle.minimize("moore", t[0], t[1])
+        dfa = mkdfa(dk, t)
+        for kw in ({}, {"fingerprint_bits": 6}):
+            assert same(dk.sort_pr(dfa, **kw), want), (i, n, k, kw)
+    for n0, c, k in ((2000, 50, 8), (20, 6000, 8), (3000, 3, 12)):
+        t = copies(oracle.gen_random(n0, k, 0.5, n0 * 7 + c), c)
+        assert same(dk.sort_pr(mkdfa(dk, t)), oracle.minimize("moore", t[0], t[1])), (n0, c)
+    t = oracle.gen_synth(2_000_000, 10, 5)
+    assert same(dk.sort_pr(mkdfa(dk, t)), oracle.minimize("moore", t[0], t[1]))
