@@ -485,6 +485,7 @@ __global__ void __launch_bounds__(512, 3) sig_table_kernel(const uint32_t* __res
                                                         uint32_t* __restrict__ keys32, uint32_t* __restrict__ tmin,
                                                         uint32_t* __restrict__ tcnt, int inc) {
     extern __shared__ uint32_t st[];  // [tsize] minima, then [tsize] counts (shared mode only)
+    p.kind = kKeyPacked;  // table keys are packed: the compiler drops the fingerprint paths
     const bool local = nbits <= kSmemTableBits;
     const uint32_t tsize = 1u << nbits;
     uint32_t* smin = st;
@@ -848,7 +849,9 @@ __device__ __forceinline__ void bucket_append(unsigned long long hk, uint32_t q,
 // Signature + fused radix partition: (hkey, state) appended to bucket
 // hkey >> shift.  Slots b*cap .. b*cap+cap-1; the excess goes to the
 // overflow region at nb*cap (counted in ctr->overflow).
-template <typename LR>
+// MODE (compile time): 0 any key kind, 1 fingerprints, 2 finishing the
+// partial keys of a sliced pass
+template <typename LR, int MODE>
 __global__ void __launch_bounds__(kThreads, DFAKIT_SIGB_MINB) sig_bucket_kernel(const uint32_t* __restrict__ list, uint64_t m,
                                                               const uint32_t* __restrict__ delta, uint32_t n,
                                                               LR lab, SigParams p,
@@ -856,11 +859,12 @@ __global__ void __launch_bounds__(kThreads, DFAKIT_SIGB_MINB) sig_bucket_kernel(
                                                               uint4* __restrict__ bent,
                                                               IterCounters* __restrict__ ctr,
                                                               const uint64_t* __restrict__ part) {
+    if (MODE == 1) p.kind = kKeyFingerprint;  // lets the compiler drop the packed-key paths
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t q = list ? list[i] : p.q0 + (uint32_t)i;
         // part: the keys were gathered by a sliced pass (sig_part_kernel sweeps)
-        const uint64_t key = part ? key_of_part(p, __ldcs(part + i))
-                                  : tuple_key<LR, DFAKIT_SIGB_CH>(q, lab[q], delta, n, lab, p);
+        const uint64_t key = MODE == 2 ? key_of_part(p, __ldcs(part + i))
+                                       : tuple_key<LR, DFAKIT_SIGB_CH>(q, lab[q], delta, n, lab, p);
         const unsigned long long hk = p.kind == kKeyPacked ? mix64(key) : key;
         bucket_append(hk, q, 0u, nb, bcnt, bent, ctr);
     }
@@ -2026,12 +2030,21 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
         const double lb = lst ? 4.0 : 0.0;
         const uint64_t* part = sliced_parts(ctx, klx, lst, mm, d, px, w.part, s);
         with_lab_type(klx, [&](auto lab) {
+            using LR = decltype(lab);
             // algorithmic HBM bytes: delta rows (+ list), (hkey, state) out, the key-label array once
             // (a sliced pass: the partial keys in, hkey out)
-            DK_LAUNCH_BU(ctx, part ? (double)mm * 24.0 : (double)mm * (4.0 * k + 16.0 + lb) + keylab_bytes_per_state(klx) * n,
-                         part ? 0.0 : (double)mm * k, sig_bucket_kernel,
-                         grid_for(mm, kThreads, (unsigned)ctx->num_sms * 8u), kThreads, 0, s, lst, mm, d.delta, n,
-                         lab, px, L.nb, w.bcnt.get(), w.bent.get(), ctrx, part);
+            const double bytes = part ? (double)mm * 24.0
+                                      : (double)mm * (4.0 * k + 16.0 + lb) + keylab_bytes_per_state(klx) * n;
+            const unsigned grid = grid_for(mm, kThreads, (unsigned)ctx->num_sms * 8u);
+            if (part)
+                DK_LAUNCH_BU(ctx, bytes, 0.0, (sig_bucket_kernel<LR, 2>), grid, kThreads, 0, s, lst, mm, d.delta, n, lab, px,
+                             L.nb, w.bcnt.get(), w.bent.get(), ctrx, part);
+            else if (fingerprint)
+                DK_LAUNCH_BU(ctx, bytes, (double)mm * k, (sig_bucket_kernel<LR, 1>), grid, kThreads, 0, s, lst, mm, d.delta, n,
+                             lab, px, L.nb, w.bcnt.get(), w.bent.get(), ctrx, part);
+            else
+                DK_LAUNCH_BU(ctx, bytes, (double)mm * k, (sig_bucket_kernel<LR, 0>), grid, kThreads, 0, s, lst, mm, d.delta, n,
+                             lab, px, L.nb, w.bcnt.get(), w.bent.get(), ctrx, part);
         });
         GroupOut go{L.direct ? 1 : 0, L.state_order ? 1 : 0, out_lab, w.act.get(),
                     L.direct || L.defer ? nullptr : w.rep_slot.get(), w.keep_slot.get(), nullptr,
@@ -2626,16 +2639,17 @@ __global__ void init_act_range_kernel(const uint8_t* __restrict__ acc, uint32_t 
 // buckets -- so the owner groups what it receives as is (MultiSrc): no
 // staging pass, no partition pass, no re-bucketing at the owner.  Past cs a
 // sub-bucket's entries go to an overflow list {hk lo, hk hi, state, owner}.
-template <typename LR>
+template <typename LR, int MODE>  // as sig_bucket_kernel: 0 any kind, 1 fingerprints, 2 sliced partial keys
 __global__ void __launch_bounds__(kThreads, DFAKIT_SIGB_MINB) sig_owner_kernel(
     const uint32_t* __restrict__ list, uint64_t m, const uint32_t* __restrict__ delta, uint32_t n, LR lab, SigParams p,
     uint32_t world, uint32_t nb, uint32_t cs, uint32_t* __restrict__ scur, uint4* __restrict__ send,
     uint4* __restrict__ ovf, uint32_t* __restrict__ ovf_cnt, const uint64_t* __restrict__ part) {
     const unsigned lane = threadIdx.x & 31u, lt = (1u << lane) - 1u;
+    if (MODE == 1) p.kind = kKeyFingerprint;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t q = list ? list[i] : p.q0 + (uint32_t)i;
-        const uint64_t key = part ? key_of_part(p, __ldcs(part + i))
-                                  : tuple_key<LR, DFAKIT_SIGB_CH>(q, lab[q], delta, n, lab, p);
+        const uint64_t key = MODE == 2 ? key_of_part(p, __ldcs(part + i))
+                                       : tuple_key<LR, DFAKIT_SIGB_CH>(q, lab[q], delta, n, lab, p);
         const unsigned long long hk = p.kind == kKeyPacked ? mix64(key) : key;
         const uint32_t o = owner_of(hk, world);
         const uint32_t g = o * nb + ((uint32_t)(hk >> kBucketShift) & (nb - 1));
@@ -2974,10 +2988,20 @@ void shard_sig_owner(Ctx* ctx, const DevDfa& d, const void* keylab, const PassPl
         const KeyLab kl{keylab, plan.keylab_bytes ? (int)plan.keylab_bytes : 4};
         const uint64_t* part = sliced_parts(ctx, kl, list, m, d, p, ws.part, s);
         with_lab_type(kl, [&](auto lab) {
-            DK_LAUNCH_BU(ctx, part ? (double)m * 24.0 : (double)m * (4.0 * d.k + 16.0), part ? 0.0 : (double)m * d.k,
-                         sig_owner_kernel, grid_for(m, kThreads, (unsigned)ctx->num_sms * 8u), kThreads, 0, s, list,
-                         m, d.delta, d.n, lab, p, W, nb, cs, ws.scur.get(), ws.send.get(), ws.ovf.get(),
-                         ws.ovf_cnt.get(), part);
+            using LR = decltype(lab);
+            const double bytes = part ? (double)m * 24.0 : (double)m * (4.0 * d.k + 16.0);
+            const unsigned grid = grid_for(m, kThreads, (unsigned)ctx->num_sms * 8u);
+            if (part)
+                DK_LAUNCH_BU(ctx, bytes, 0.0, (sig_owner_kernel<LR, 2>), grid, kThreads, 0, s, list, m, d.delta, d.n,
+                             lab, p, W, nb, cs, ws.scur.get(), ws.send.get(), ws.ovf.get(), ws.ovf_cnt.get(), part);
+            else if (plan.strategy == kPlanFingerprint)
+                DK_LAUNCH_BU(ctx, bytes, (double)m * d.k, (sig_owner_kernel<LR, 1>), grid, kThreads, 0, s, list, m,
+                             d.delta, d.n, lab, p, W, nb, cs, ws.scur.get(), ws.send.get(), ws.ovf.get(),
+                             ws.ovf_cnt.get(), part);
+            else
+                DK_LAUNCH_BU(ctx, bytes, (double)m * d.k, (sig_owner_kernel<LR, 0>), grid, kThreads, 0, s, list, m,
+                             d.delta, d.n, lab, p, W, nb, cs, ws.scur.get(), ws.send.get(), ws.ovf.get(),
+                             ws.ovf_cnt.get(), part);
         });
     }
     DK_LAUNCH(ctx, owner_counts_kernel, grid_for((uint64_t)W * (nb + 1)), kThreads, 0, s, ws.scur.get(),
