@@ -910,6 +910,16 @@ __device__ __forceinline__ void emit(const GroupOut& o, uint64_t slot, uint32_t 
     }
 }
 
+// Emit with the output mode fixed at compile time (EM 1: deferred records by
+// state, EM 2: per-entry results; 0: decided at run time from o)
+template <int EM>
+__device__ __forceinline__ void emit_as(const GroupOut& o, uint64_t slot, uint32_t q, uint32_t r, bool multi,
+                                        uint32_t idx) {
+    if (EM == 1) o.rec[slot] = make_uint2(q, r | (multi ? 0x80000000u : 0u));
+    else if (EM == 2) o.res[idx] = r | (multi ? 0x80000000u : 0u);
+    else emit(o, slot, q, r, multi, idx);
+}
+
 // Bucket sources of the grouping kernel.  OneSrc: the single-GPU layout --
 // bucket b's entries at bent + b * kGrpCap, its count at bcnt[b * stride].
 // MultiSrc (sharded owners): bucket b is the concatenation of one sub-bucket
@@ -1026,11 +1036,13 @@ struct MultiSrc {
 
 // One CTA per bucket (persistent over buckets).  Buckets whose count
 // exceeds the capacity are left to the ghash fallback.
-template <typename LR, typename Src = OneSrc>
+// EM: the output mode at compile time (see emit_as); EM 1 implies fingerprints.
+template <typename LR, typename Src = OneSrc, int EM = 0>
 __global__ void __launch_bounds__(kGrpThreads, DFAKIT_GRP_MINB) bucket_group_kernel(
-    const __grid_constant__ Src src, uint32_t nb, int fingerprint, const uint32_t* __restrict__ delta, uint32_t n,
+    const __grid_constant__ Src src, uint32_t nb, int fingerprint_rt, const uint32_t* __restrict__ delta, uint32_t n,
     uint32_t k, LR lab_in,
     GroupOut o, IterCounters* __restrict__ ctr) {
+    const int fingerprint = EM == 1 ? 1 : fingerprint_rt;
     extern __shared__ __align__(16) unsigned char grp_raw[];
     GroupSmem& sm = *reinterpret_cast<GroupSmem*>(grp_raw);
     const unsigned tid = threadIdx.x;
@@ -1117,7 +1129,7 @@ __global__ void __launch_bounds__(kGrpThreads, DFAKIT_GRP_MINB) bucket_group_ker
                 ablk += head && multi;
                 surv += multi;
                 if (fingerprint && !head && !same_tuple(q[j], r, delta, n, k, lab_in)) clash = true;
-                emit(o, s0 + idx, q[j], r, multi, view.index(idx, ix[j]));
+                emit_as<EM>(o, s0 + idx, q[j], r, multi, view.index(idx, ix[j]));
             }
         }
         __syncthreads();
@@ -1894,6 +1906,8 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
     w.ctr2.alloc(1, s);
     DK_CUDA(cudaFuncSetAttribute(bucket_group_kernel<ArrLab<uint32_t>, OneSrc>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)sizeof(GroupSmem)));
+    DK_CUDA(cudaFuncSetAttribute(bucket_group_kernel<ArrLab<uint32_t>, OneSrc, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sizeof(GroupSmem)));
     const int smem_table = (int)(2u << kSmemTableBits) * 4;
     DK_CUDA(cudaFuncSetAttribute(sig_table_kernel<BitLab>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_table));
     DK_CUDA(cudaFuncSetAttribute(sig_table_kernel<ArrLab<uint8_t>>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2051,9 +2065,15 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
                     L.defer ? w.rec.get() : nullptr, 0};
         const unsigned gg = (unsigned)std::min<uint64_t>(L.nb, (uint64_t)ctx->num_sms * kGrpCtasPerSm);
         // algorithmic HBM bytes: (hkey, state) in, label + survivor flag out
-        DK_LAUNCH_B(ctx, (double)mm * (16.0 + 4.0 + 1.0 + (L.direct ? 0.0 : 4.0)), bucket_group_kernel, gg,
-                    kGrpThreads, sizeof(GroupSmem), s, OneSrc{w.bcnt.get(), w.bent.get()}, L.nb, fingerprint ? 1 : 0,
-                    d.delta, n, k, ArrLab<uint32_t>{w.lab.get()}, go, ctrx);
+        const double gbytes = (double)mm * (16.0 + 4.0 + 1.0 + (L.direct ? 0.0 : 4.0));
+        if (L.defer)  // deferred records (fingerprints): the output mode fixed at compile time
+            DK_LAUNCH_B(ctx, gbytes, (bucket_group_kernel<ArrLab<uint32_t>, OneSrc, 1>), gg, kGrpThreads,
+                        sizeof(GroupSmem), s, OneSrc{w.bcnt.get(), w.bent.get()}, L.nb, 1, d.delta, n, k,
+                        ArrLab<uint32_t>{w.lab.get()}, go, ctrx);
+        else
+            DK_LAUNCH_B(ctx, gbytes, bucket_group_kernel, gg, kGrpThreads, sizeof(GroupSmem), s,
+                        OneSrc{w.bcnt.get(), w.bent.get()}, L.nb, fingerprint ? 1 : 0, d.delta, n, k,
+                        ArrLab<uint32_t>{w.lab.get()}, go, ctrx);
     };
 
     auto dense_keylab = [&](int bytes) -> KeyLab {
@@ -3040,10 +3060,10 @@ void shard_group_owner(Ctx* ctx, const DevDfa& d, const void* verify_lab, uint32
     const KeyLab vl{verify_lab, (int)verify_bytes};
     with_lab_type(vl, [&](auto lab) {
         using LR = decltype(lab);
-        DK_CUDA(cudaFuncSetAttribute(bucket_group_kernel<LR, MultiSrc>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        DK_CUDA(cudaFuncSetAttribute(bucket_group_kernel<LR, MultiSrc, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)sizeof(GroupSmem)));
-        DK_LAUNCH_B(ctx, 20.0 * (double)op.nb * kGrpCap * 3 / 4, bucket_group_kernel, gg, kGrpThreads,
-                    sizeof(GroupSmem), s, src, op.nb, fp, d.delta, d.n, d.k, lab, go, dctr);
+        DK_LAUNCH_B(ctx, 20.0 * (double)op.nb * kGrpCap * 3 / 4, (bucket_group_kernel<LR, MultiSrc, 2>), gg,
+                    kGrpThreads, sizeof(GroupSmem), s, src, op.nb, fp, d.delta, d.n, d.k, lab, go, dctr);
     });
     if (ovf_total) {
         // some sub-bucket overflowed: its whole bucket (every sender's part)
