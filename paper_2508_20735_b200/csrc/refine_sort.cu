@@ -459,12 +459,14 @@ __global__ void __launch_bounds__(kThreads, DFAKIT_SIGB_MINB) sig_part_kernel(co
 
 // Plain signature kernel (radix-sort grouping and the exact chunked path):
 // one thread per active state, (key, state) written in list order.
-template <typename LR>
+// FP: fingerprint keys known at compile time (1) or the kind read from p (0)
+template <typename LR, int FP = 0>
 __global__ void __launch_bounds__(kThreads) signature_kernel(const uint32_t* __restrict__ list, uint64_t m,
                                                              const uint32_t* __restrict__ delta, uint32_t n,
                                                              LR lab,
                                                              const uint32_t* __restrict__ head, SigParams p,
                                                              uint64_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+    if (FP) p.kind = kKeyFingerprint;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t q = list ? list[i] : p.q0 + (uint32_t)i;
         keys[i] = tuple_key<LR>(q, head ? head[i] : lab[q], delta, n, lab, p);
@@ -2414,9 +2416,14 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
             uint32_t* svals = w.vals0.get();
             if (!chunked) {
                 with_lab_type(kl, [&](auto lab) {
-                    DK_LAUNCH_BU(ctx, (double)m * (12.0 + 4.0 * k + list_b) + keylab_bytes_per_state(kl) * n, (double)m * k,
-                                 signature_kernel, g, kThreads, 0, s, list, m, d.delta, n, lab, nullptr, p,
-                                w.keys0.get(), w.vals0.get());
+                    using LR = decltype(lab);
+                    const double bytes = (double)m * (12.0 + 4.0 * k + list_b) + keylab_bytes_per_state(kl) * n;
+                    if (fingerprint)
+                        DK_LAUNCH_BU(ctx, bytes, (double)m * k, (signature_kernel<LR, 1>), g, kThreads, 0, s, list, m,
+                                     d.delta, n, lab, nullptr, p, w.keys0.get(), w.vals0.get());
+                    else
+                        DK_LAUNCH_BU(ctx, bytes, (double)m * k, signature_kernel, g, kThreads, 0, s, list, m, d.delta,
+                                     n, lab, nullptr, p, w.keys0.get(), w.vals0.get());
                 });
                 if (radix_sort_pairs(ctx, rb, m, nbits, s)) {
                     skeys = w.keys1.get();
