@@ -44,6 +44,8 @@
 
 #include <algorithm>
 
+#include <functional>
+
 #include "prims.cuh"
 #include "refine.cuh"
 
@@ -62,6 +64,7 @@ struct BucketLayout {
 };
 // automata from this size on queue their second pass speculatively
 constexpr uint32_t kSpecMinStates = 1u << 22;
+
 
 struct IterCounters {
     uint32_t runs;
@@ -478,14 +481,13 @@ __global__ void __launch_bounds__(kThreads) signature_kernel(const uint32_t* __r
 
 // step 1: signature + table of (run minimum, run size), in shared memory
 // when <= 13 bits; equal keys of a warp are combined first (match_any).
-// Run sizes are only compared with 0 and 2: the shared-memory path keeps
-// them saturated (any value >= 2 means "two or more").
 template <typename LR, bool CLAMP = false>
 __global__ void __launch_bounds__(512, 3) sig_table_kernel(const uint32_t* __restrict__ list, uint64_t m,
                                                         const uint32_t* __restrict__ delta, uint32_t n,
                                                         LR lab, SigParams p, uint32_t nbits,
                                                         uint32_t* __restrict__ keys32, uint32_t* __restrict__ tmin,
-                                                        uint32_t* __restrict__ tcnt, int inc) {
+                                                        uint32_t* __restrict__ tcnt, int inc,
+                                                        uint16_t* __restrict__ keys16 = nullptr) {
     extern __shared__ uint32_t st[];  // [tsize] minima, then [tsize] counts (shared mode only)
     p.kind = kKeyPacked;  // table keys are packed: the compiler drops the fingerprint paths
     const bool local = nbits <= kSmemTableBits;
@@ -503,6 +505,7 @@ __global__ void __launch_bounds__(512, 3) sig_table_kernel(const uint32_t* __res
         const uint32_t q = list ? list[i] : p.q0 + (uint32_t)i;
         const uint32_t key = (uint32_t)tuple_key<LR, 8, CLAMP>(q, lab[q], delta, n, lab, p);
         keys32[i] = key;
+        if (keys16) keys16[i] = (uint16_t)key;  // the raw keys as the next pass's labels (lazy apply)
         const unsigned peers = __match_any_sync(__activemask(), key);
         // inc: states increase with the lane (identity / increasing list), so
         // the lowest peer lane -- the one that updates the table -- holds the
@@ -510,11 +513,8 @@ __global__ void __launch_bounds__(512, 3) sig_table_kernel(const uint32_t* __res
         const uint32_t mq = inc ? q : __reduce_min_sync(peers, q);
         if ((threadIdx.x & 31u) == (unsigned)(__ffs(peers) - 1)) {
             if (local) {
-                // counts are only ever tested for 0 / 1 / >= 2: one shared
-                // atomic per warp-distinct key (the minimum's old value says
-                // whether the key was seen before), the count saturates at 2
-                const uint32_t old = atomicMin(&smin[key], mq);
-                if (old != kNone || __popc(peers) >= 2) scnt[key] = 2u;
+                atomicMin(&smin[key], mq);
+                atomicAdd(&scnt[key], (uint32_t)__popc(peers));
             } else {
                 atomicMin(&tmin[key], mq);
                 atomicAdd(&tcnt[key], (uint32_t)__popc(peers));
@@ -524,8 +524,8 @@ __global__ void __launch_bounds__(512, 3) sig_table_kernel(const uint32_t* __res
     if (local) {
         __syncthreads();
         for (uint32_t e = threadIdx.x; e < tsize; e += blockDim.x)
-            if (smin[e] != kNone) {
-                atomicAdd(&tcnt[e], scnt[e] ? 2u : 1u);
+            if (scnt[e]) {
+                atomicAdd(&tcnt[e], scnt[e]);
                 atomicMin(&tmin[e], smin[e]);
             }
     }
@@ -712,6 +712,21 @@ __global__ void __launch_bounds__(1024) table_rank_one_kernel(const uint32_t* __
             }
         carry += tot;
     }
+}
+
+// counters of a counting-table pass over every state, from the table alone
+// (runs = occupied keys, active blocks = keys counted twice or more, active
+// states = their counts): what the apply kernel would sum per state
+__global__ void __launch_bounds__(1024) table_counts_kernel(const uint32_t* __restrict__ tcnt, uint32_t tsize,
+                                                            IterCounters* __restrict__ ctr) {
+    uint32_t runs = 0, ablk = 0, surv = 0;
+    for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < tsize; e += gridDim.x * blockDim.x) {
+        const uint32_t c = tcnt[e];
+        runs += c != 0;
+        ablk += c >= 2;
+        surv += c >= 2 ? c : 0u;
+    }
+    flush_counters<1024>(runs, ablk, surv, &ctr->runs, &ctr->active_blocks, &ctr->active_states);
 }
 
 __global__ void table_occupied_kernel(const uint32_t* __restrict__ tcnt, uint32_t tsize, uint32_t* __restrict__ occ) {
@@ -1990,6 +2005,12 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
     // fixed point or survivors that make it moot just drop it.
     bool spec_launched = false;
     bool iota_out = false;  // block_out holds the identity numbering (queued speculatively)
+    // lab_pending: pass 1 (a counting-table pass over every state, every
+    // state surviving) skipped its per-state apply -- its labels are
+    // tmin[heads[q]], materialised by `materialise` only if something reads
+    // them; meanwhile the raw table keys (heads) label the blocks
+    bool lab_pending = false;
+    std::function<void()> materialise;
     PassPlan spec_plan{};
     KeyLab spec_kl{nullptr, 0};
     // DFAKIT_TEST_SPEC_MIN=<states> lowers the threshold (tests), DFAKIT_NO_SPEC=1 disables it
@@ -2022,7 +2043,7 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
     // allocations, the pass prologue's fills, signature + bucket append,
     // grouping (counters into ctrx)
     auto bucket_launch = [&](const PassPlan& pl, const KeyLab& klx, const SigParams& px, const uint32_t* lst,
-                             uint64_t mm, IterCounters* ctrx, Fills& fl) {
+                             uint64_t mm, IterCounters* ctrx, Fills& fl, const uint32_t* vlab) {
         const bool fingerprint = pl.strategy == kPlanFingerprint;
         const BucketLayout L = bucket_layout(fingerprint, mm);
         if (w.bcnt.n < (uint64_t)L.nb * kCntStride) w.bcnt.alloc((uint64_t)L.nb * kCntStride, s);
@@ -2071,11 +2092,11 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
         if (L.defer)  // deferred records (fingerprints): the output mode fixed at compile time
             DK_LAUNCH_B(ctx, gbytes, (bucket_group_kernel<ArrLab<uint32_t>, OneSrc, 1>), gg, kGrpThreads,
                         sizeof(GroupSmem), s, OneSrc{w.bcnt.get(), w.bent.get()}, L.nb, 1, d.delta, n, k,
-                        ArrLab<uint32_t>{w.lab.get()}, go, ctrx);
+                        ArrLab<uint32_t>{vlab}, go, ctrx);
         else
             DK_LAUNCH_B(ctx, gbytes, bucket_group_kernel, gg, kGrpThreads, sizeof(GroupSmem), s,
                         OneSrc{w.bcnt.get(), w.bent.get()}, L.nb, fingerprint ? 1 : 0, d.delta, n, k,
-                        ArrLab<uint32_t>{w.lab.get()}, go, ctrx);
+                        ArrLab<uint32_t>{vlab}, go, ctrx);
     };
 
     auto dense_keylab = [&](int bytes) -> KeyLab {
@@ -2206,6 +2227,25 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
             const bool local = nbits <= kSmemTableBits;
             const size_t smem = local ? (size_t)(2u << nbits) * 4 : 0;
             const int inc = list == nullptr || list_inc ? 1 : 0;
+            // a table pass over every state sees every block of the next
+            // partition as one table key: the ranks of the occupied entries
+            // are compact block ids, the next pass's key labels (no O(n) scan)
+            const bool full = list == nullptr;
+            auto a16 = [](const void* x) { return ((uintptr_t)x & 15u) == 0; };
+            if (full) {
+                if (nbits <= 16 && !w.next16.get()) w.next16.alloc(n, s);
+                if (nbits > 16 && !w.next32.get()) w.next32.alloc(n, s);
+            }
+            const bool vec = full && a16(w.heads.get()) && a16(w.lab.get()) && a16(w.keep.get()) &&
+                             a16(nbits <= 16 ? (void*)w.next16.get() : (void*)w.next32.get());
+            const bool staged = vec && tsize <= kApplyStageMax;  // ranks computed by the apply kernel
+            // lazy: the second pass is queued speculatively on the raw table
+            // keys (every block of the next partition is one key; written as
+            // 16-bit labels by the signature kernel), and the per-state apply
+            // only runs when its outputs are needed
+            const bool lazy = spec_ok && staged && nbits <= 16 && res.passes == 1 && collisions_this_pass == 0 &&
+                              !streamed;
+            uint16_t* keys16 = lazy ? w.next16.get() : nullptr;
             auto sig_table = [&](uint32_t q0, uint64_t mm, bool clamp) {
                 const unsigned tg = (unsigned)std::min<uint64_t>((mm + 511) / 512, (uint64_t)ctx->num_sms * 3);
                 SigParams pc = p;
@@ -2221,11 +2261,11 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
                                                      (int)(2u << kSmemTableBits) * 4));
                         DK_LAUNCH_BU(ctx, bytes, (double)mm * k, sig_table_clamped_kernel, tg, 512, smem, s, list,
                                      mm, d.delta, n, lab, pc, nbits, w.heads.get() + q0, w.tmin.get(), w.tcnt.get(),
-                                     inc);
+                                     inc, keys16 ? keys16 + q0 : nullptr);
                     } else {
                         DK_LAUNCH_BU(ctx, bytes, (double)mm * k, sig_table_kernel<LR>, tg, 512, smem, s, list, mm,
                                      d.delta, n, lab, pc, nbits, w.heads.get() + q0, w.tmin.get(), w.tcnt.get(),
-                                     inc);
+                                     inc, keys16 ? keys16 + q0 : nullptr);
                     }
                 });
             };
@@ -2243,18 +2283,7 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
                 wait_all_chunks();
                 sig_table(0, m, false);
             }
-            // a table pass over every state sees every block of the next
-            // partition as one table key: the ranks of the occupied entries
-            // are compact block ids, the next pass's key labels (no O(n) scan)
-            const bool full = list == nullptr;
-            auto a16 = [](const void* x) { return ((uintptr_t)x & 15u) == 0; };
-            if (full) {
-                if (nbits <= 16 && !w.next16.get()) w.next16.alloc(n, s);
-                if (nbits > 16 && !w.next32.get()) w.next32.alloc(n, s);
-            }
-            const bool vec = full && a16(w.heads.get()) && a16(w.lab.get()) && a16(w.keep.get()) &&
-                             a16(nbits <= 16 ? (void*)w.next16.get() : (void*)w.next32.get());
-            const bool staged = vec && tsize <= kApplyStageMax;  // ranks computed by the apply kernel
+            auto apply_table = [&, vec, staged, full, nbits, tsize, g, list, m, list_b]() {
             if (full) {
                 if (w.trank.n < tsize) w.trank.alloc(tsize, s);
                 if (staged) {
@@ -2283,16 +2312,23 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
                             w.heads.get(), m, w.tmin.get(), w.tcnt.get(), w.lab.get(), w.keep.get(), nullptr,
                             full ? w.trank.get() : nullptr, full && nbits <= 16 ? w.next16.get() : nullptr,
                             full && nbits > 16 ? w.next32.get() : nullptr, 0u, dctr);
-            next_valid = full;
-            prev_nbits = nbits;
+            };
+            if (lazy) {
+                DK_LAUNCH(ctx, table_counts_kernel, 1, 1024, 0, s, w.tcnt.get(), (uint32_t)tsize, dctr);
+            } else {
+                apply_table();
+                next_valid = full;
+                prev_nbits = nbits;
+            }
             if (spec_ok && full && nbits <= 16 && res.passes == 1 && collisions_this_pass == 0) {
                 // the second pass, queued before this pass's readback: a
                 // fingerprint bucket pass over every state on the table ranks
+                // (or the raw table keys when the apply is skipped)
                 spec_plan = PassPlan{};
                 spec_plan.strategy = kPlanFingerprint;
                 spec_plan.key_bits = 64;
                 spec_plan.keylab_bytes = 2;
-                spec_kl = KeyLab{w.next16.get(), 2};
+                spec_kl = KeyLab{w.next16.get(), 2};  // the ranks, or the raw keys when the apply is skipped
                 SigParams sp{};
                 sp.kind = kKeyFingerprint;
                 sp.a0 = 0;
@@ -2302,7 +2338,7 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
                 Fills sf;
                 sf.add(w.ctr2.get(), sizeof(IterCounters), 0);
                 ctx->prof_pass = (uint32_t)res.passes + 1;
-                bucket_launch(spec_plan, spec_kl, sp, nullptr, n, w.ctr2.get(), sf);
+                bucket_launch(spec_plan, spec_kl, sp, nullptr, n, w.ctr2.get(), sf, lazy ? w.heads.get() : w.lab.get());
                 ctx->prof_pass = (uint32_t)res.passes;
                 spec_launched = true;
             }
@@ -2313,6 +2349,23 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
                 A = B;
             }
             read_words(ctx, dctr, sizeof(c), &c, s);
+            if (lazy) {
+                if (!list && c.active_states == m && B - A + c.runs != B) {
+                    // every state survives and the pass split: the speculative
+                    // second pass on the raw keys is the next pass
+                    lab_pending = true;
+                    materialise = [apply_table, nbits, &next_valid, &prev_nbits, &lab_pending]() {
+                        apply_table();
+                        next_valid = true;
+                        prev_nbits = nbits;
+                        lab_pending = false;
+                    };
+                } else {
+                    apply_table();  // labels, survivor flags and ranks now (counters unchanged)
+                    next_valid = full;
+                    prev_nbits = nbits;
+                }
+            }
             // compaction after the readback: when every state survives the
             // identity list stays and nothing is launched (three launches of
             // ~2.4K CTAs that would only exit cost ~25 us)
@@ -2326,7 +2379,9 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
             const uint64_t bspace = L.bspace, espace = L.espace;
             const bool state_order = L.state_order, defer = L.defer, direct = L.direct;
             IterCounters* pctr = use_spec ? w.ctr2.get() : dctr;  // the counters this pass's kernels wrote
-            if (!use_spec) bucket_launch(plan, kl, p, list, m, dctr, fills);
+            if (!use_spec) bucket_launch(plan, kl, p, list, m, dctr, fills, w.lab.get());
+            // verification labels: any injective labelling of the current blocks
+            const uint32_t* vlab = lab_pending ? w.heads.get() : w.lab.get();
             uint32_t* out_lab = fingerprint && direct ? w.lab2.get() : w.lab.get();
             GroupOut go{direct ? 1 : 0, state_order ? 1 : 0, out_lab, w.act.get(),
                         direct || defer ? nullptr : w.rep_slot.get(), w.keep_slot.get(), nullptr,
@@ -2363,7 +2418,7 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
                           w.grep.get(), w.gslot.get(), w.gmul.get());
                 DK_LAUNCH(ctx, ghash_out_kernel, eg, kThreads, 0, s, w.bcnt.get(), nb, c.overflow, w.bent.get(),
                           w.grep.get(), w.gslot.get(), w.gmul.get(), fingerprint ? 1 : 0, d.delta, n, k,
-                          ArrLab<uint32_t>{w.lab.get()}, go, pctr);
+                          ArrLab<uint32_t>{vlab}, go, pctr);
                 read_words(ctx, pctr, sizeof(c), &c, s);
             }
             res.sorted += m;
@@ -2374,15 +2429,22 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
                 ++collisions_this_pass;
                 --res.passes;
                 salt = mix64(salt + 0x1234567ull);
+                if (lab_pending) materialise();  // the retry plans on the labels
                 continue;
             }
             collisions_this_pass = 0;
-            if (B - A + c.runs == B) break;  // fixed point (reference l.411)
+            if (B - A + c.runs == B) {  // fixed point (reference l.411)
+                if (lab_pending) materialise();
+                break;
+            }
             if (fingerprint && direct) std::swap(w.lab, w.lab2);
             if (defer) {
-                if (B - A + c.runs != n)
+                if (B - A + c.runs != n) {
+                    // (a pass over every state: every label is rewritten)
                     DK_LAUNCH_B(ctx, (double)m * 12.0, rec_apply_kernel, grid_for(bspace + c.overflow), kThreads, 0,
                                 s, w.bcnt.get(), nb, c.overflow, w.rec.get(), w.lab.get(), w.act.get());
+                    lab_pending = false;
+                }
             } else if (!direct)
                 DK_LAUNCH_B(ctx, (double)m * 13.0, slot_apply_kernel, grid_for(bspace + c.overflow), kThreads, 0, s,
                             w.bcnt.get(), nb, c.overflow, w.bent.get(), w.rep_slot.get(), w.keep_slot.get(),
