@@ -98,20 +98,32 @@ __global__ void __launch_bounds__(kThreads) leader_info_kernel(const uint8_t* __
     const bool vec = ((uintptr_t)acc & 15u) == 0 && ((uintptr_t)dense2 & 15u) == 0;
     const uint32_t nv = vec ? n / 16 : 0;
     const uint32_t a0 = n ? acc[0] != 0 : 0u;
-    for (uint32_t v = tid; v < nv; v += stride) {
-        const uint4 w = __ldcs(reinterpret_cast<const uint4*>(acc) + v);
-        if (dense2)
-            reinterpret_cast<uint4*>(dense2)[v] =
-                make_uint4(flags4(w.x, a0), flags4(w.y, a0), flags4(w.z, a0), flags4(w.w, a0));
-        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+    constexpr int kU = 4;  // loads in flight per thread before any is used
+    for (uint32_t v0 = tid; v0 < nv; v0 += kU * stride) {
+        uint4 wv[kU];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {  // four flags per byte-SIMD compare
-            const uint32_t nz = __vcmpne4(ws[j], 0u), q0 = v * 16 + 4 * j;
-            const uint32_t c = __popc(nz) >> 3;
-            ca += c;
-            cr += 4 - c;
-            if (nz) mina = min(mina, q0 + ((__ffs(nz) - 1) >> 3));
-            if (~nz) minr = min(minr, q0 + ((__ffs(~nz) - 1) >> 3));
+        for (int u = 0; u < kU; ++u) {
+            const uint32_t v = v0 + u * stride;
+            wv[u] = v < nv ? __ldcs(reinterpret_cast<const uint4*>(acc) + v) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const uint32_t v = v0 + u * stride;
+            if (v >= nv) break;
+            const uint4 w = wv[u];
+            if (dense2)
+                reinterpret_cast<uint4*>(dense2)[v] =
+                    make_uint4(flags4(w.x, a0), flags4(w.y, a0), flags4(w.z, a0), flags4(w.w, a0));
+            const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {  // four flags per byte-SIMD compare
+                const uint32_t nz = __vcmpne4(ws[j], 0u), q0 = v * 16 + 4 * j;
+                const uint32_t c = __popc(nz) >> 3;
+                ca += c;
+                cr += 4 - c;
+                if (nz) mina = min(mina, q0 + ((__ffs(nz) - 1) >> 3));
+                if (~nz) minr = min(minr, q0 + ((__ffs(~nz) - 1) >> 3));
+            }
         }
     }
     for (uint32_t q = nv * 16 + tid; q < n; q += stride) {
@@ -165,7 +177,8 @@ __global__ void __launch_bounds__(kThreads) leader_info_kernel(const uint8_t* __
             vi[2] = 0;
             vi[3] = 0;
             vi[12] = 0;
-            __threadfence_system();
+            // (no system fence: the host reads `out` after the event recorded
+            // behind this kernel completes)
         }
     }
 }
@@ -1363,7 +1376,7 @@ __global__ void __launch_bounds__(kThreads) run_label_kernel(const uint64_t* __r
                                                              uint32_t* __restrict__ tile_ctr,
                                                              uint32_t* __restrict__ lab, uint8_t* __restrict__ keep,
                                                              uint8_t* __restrict__ act,
-                                                             IterCounters* __restrict__ ctr) {
+                                                             IterCounters* __restrict__ ctr, int multi_only) {
     __shared__ uint32_t s_tile, s_carry;
     __shared__ uint32_t s_has[kThreads / 32], s_val[kThreads / 32];
     const unsigned lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
@@ -1373,13 +1386,36 @@ __global__ void __launch_bounds__(kThreads) run_label_kernel(const uint64_t* __r
     const uint64_t i0 = (uint64_t)tile * kRunTile + (uint64_t)threadIdx.x * kRunItems;
     uint64_t key[kRunItems + 2];  // [0] = element i0 - 1, [kRunItems + 1] = element i0 + kRunItems
     uint32_t val[kRunItems];
+    if (i0 + kRunItems <= m) {  // a full run of items: 16-byte loads (i0 is a multiple of 8)
 #pragma unroll
-    for (int j = 0; j < kRunItems + 2; ++j) {
-        const uint64_t i = i0 + j - 1;
-        key[j] = (j == 0 && i0 == 0) || i >= m ? ~0ull : __ldcs(keys + i);
+        for (int j = 0; j < kRunItems; j += 2) {
+            const ulonglong2 v = __ldcs(reinterpret_cast<const ulonglong2*>(keys + i0 + j));
+            key[j + 1] = v.x;
+            key[j + 2] = v.y;
+        }
+#pragma unroll
+        for (int j = 0; j < kRunItems; j += 4) {
+            const uint4 v = __ldcs(reinterpret_cast<const uint4*>(vals + i0 + j));
+            val[j] = v.x;
+            val[j + 1] = v.y;
+            val[j + 2] = v.z;
+            val[j + 3] = v.w;
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < kRunItems; ++j) {
+            key[j + 1] = i0 + j < m ? __ldcs(keys + i0 + j) : ~0ull;
+            val[j] = i0 + j < m ? __ldcs(vals + i0 + j) : 0u;
+        }
     }
-#pragma unroll
-    for (int j = 0; j < kRunItems; ++j) val[j] = i0 + j < m ? __ldcs(vals + i0 + j) : 0u;
+    // the neighbours' elements: from the adjacent lanes, loaded at warp edges
+    {
+        const uint64_t up = __shfl_up_sync(0xffffffffu, key[kRunItems], 1);
+        const uint64_t dn = __shfl_down_sync(0xffffffffu, key[1], 1);
+        key[0] = lane > 0 ? up : (i0 == 0 ? ~0ull : keys[i0 - 1]);
+        key[kRunItems + 1] = lane < 31 && i0 + kRunItems < m ? dn
+                             : (i0 + kRunItems < m ? keys[i0 + kRunItems] : ~0ull);
+    }
     uint32_t head_mask = 0, multi_mask = 0, has = 0, last = 0;
 #pragma unroll
     for (int j = 0; j < kRunItems; ++j) {
@@ -1460,12 +1496,19 @@ __global__ void __launch_bounds__(kThreads) run_label_kernel(const uint64_t* __r
         if (i >= m) break;
         const bool head = (head_mask >> j) & 1u, multi = (multi_mask >> j) & 1u;
         if (head) hv = val[j];
-        lab[val[j]] = hv;
-        if (keep) keep[i] = multi;
+        if (!multi_only || multi) lab[val[j]] = hv;  // (multi_only: singletons hold their own id already)
+        if (keep && i0 + kRunItems > m) keep[i] = multi;
         if (act && multi) act[val[j]] = 1;  // act was zeroed
         nh += head;
         ab += head && multi;
         sv += multi;
+    }
+    if (keep && i0 + kRunItems <= m) {  // the eight flags in one store
+        static_assert(kRunItems == 8, "one 8-byte flag store");
+        uint64_t f = 0;
+#pragma unroll
+        for (int j = 0; j < kRunItems; ++j) f |= (uint64_t)((multi_mask >> j) & 1u) << (8 * j);
+        *reinterpret_cast<uint64_t*>(keep + i0) = f;
     }
     flush_counters<kThreads>(nh, ab, sv, &ctr->runs, &ctr->active_blocks, &ctr->active_states);
 }
@@ -1789,8 +1832,8 @@ __global__ void __launch_bounds__(kThreads) small_persistent_kernel(SmallArgs A)
 
 LeaderInfo leader_info(Ctx* ctx, const DevDfa& d, cudaStream_t s) {
     uint32_t* info = reinterpret_cast<uint32_t*>(ctx->dmailbox);
-    DK_LAUNCH(ctx, leader_info_kernel, grid_for(d.n, kThreads, (unsigned)ctx->num_sms * 8u), kThreads, 0, s, d.acc,
-              d.n, info, (uint8_t*)nullptr, info + 16);
+    DK_LAUNCH(ctx, leader_info_kernel, grid_for(d.n / 64 + 1, kThreads, (unsigned)ctx->num_sms * 8u), kThreads, 0, s,
+              d.acc, d.n, info, (uint8_t*)nullptr, info + 16);
     LeaderInfo li;
     read_words(ctx, info + 16, sizeof(li), &li, s);
     return li;
@@ -1798,8 +1841,10 @@ LeaderInfo leader_info(Ctx* ctx, const DevDfa& d, cudaStream_t s) {
 
 void leader_info_async(Ctx* ctx, const DevDfa& d, cudaStream_t s, uint8_t* dense2) {
     uint32_t* info = reinterpret_cast<uint32_t*>(ctx->dmailbox);
-    DK_LAUNCH(ctx, leader_info_kernel, grid_for(d.n, kThreads, (unsigned)ctx->num_sms * 8u), kThreads, 0, s, d.acc,
-              d.n, info, dense2, ctx->fastbox + 120);  // straight into mapped pinned memory
+    // ~4 16-byte loads in flight per thread, ~2 CTAs per SM: one round trip
+    // to HBM, and few CTAs in the atomic tail
+    DK_LAUNCH(ctx, leader_info_kernel, grid_for(d.n / 64 + 1, kThreads, (unsigned)ctx->num_sms * 8u), kThreads, 0, s,
+              d.acc, d.n, info, dense2, ctx->fastbox + 120);  // straight into mapped pinned memory
     DK_CUDA(cudaEventRecord(ctx->info_ev, s));
 }
 
@@ -2476,6 +2521,16 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
             RadixBuffers rb{w.keys0.get(), w.vals0.get(), w.keys1.get(), w.vals1.get()};
             uint64_t* skeys = w.keys0.get();
             uint32_t* svals = w.vals0.get();
+            uint32_t sort_bits = nbits;
+            if (!chunked && fingerprint) {
+                // the radix sort orders only the low 2 log2(m) + 8 fingerprint
+                // bits (a false merge stays ~2^-8 likely per pass and is caught
+                // by verify_runs_kernel): 7 digit passes instead of 8 at 10M
+                const uint32_t want = std::min(64u, std::max(32u, 2u * bits_for(m) + 8u));
+                const uint32_t have = 64u - (uint32_t)__builtin_clzll(fp_mask | 1ull);
+                sort_bits = std::min(want, have);
+                if (sort_bits < 64) p.fp_mask = fp_mask & ((1ull << sort_bits) - 1ull);
+            }
             if (!chunked) {
                 with_lab_type(kl, [&](auto lab) {
                     using LR = decltype(lab);
@@ -2487,7 +2542,7 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
                         DK_LAUNCH_BU(ctx, bytes, (double)m * k, signature_kernel, g, kThreads, 0, s, list, m, d.delta,
                                      n, lab, nullptr, p, w.keys0.get(), w.vals0.get());
                 });
-                if (radix_sort_pairs(ctx, rb, m, nbits, s)) {
+                if (radix_sort_pairs(ctx, rb, m, sort_bits, s)) {
                     skeys = w.keys1.get();
                     svals = w.vals1.get();
                 }
@@ -2551,9 +2606,15 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
                 const uint64_t tiles = (m + kRunTile - 1) / kRunTile;
                 DBuf<unsigned long long> look(tiles + 1, s);  // look-back words + the tile counter
                 DK_CUDA(cudaMemsetAsync(look.get(), 0, (tiles + 1) * 8, s));
+                // a pass over every state: the identity labels first (one
+                // coalesced write), then only the members of multi-state runs
+                // are scattered -- none once the partition is all singletons
+                const bool multi_only = m == n;
+                if (multi_only) iota_u32(ctx, w.lab.get(), n, s);
                 DK_LAUNCH_B(ctx, 17.0 * m, run_label_kernel, (unsigned)tiles, kThreads, 0, s, skeys, svals, m,
                             look.get(), reinterpret_cast<uint32_t*>(look.get() + tiles), w.lab.get(),
-                            state_order ? nullptr : w.keep.get(), state_order ? w.act.get() : nullptr, dctr);
+                            state_order ? nullptr : w.keep.get(), state_order ? w.act.get() : nullptr, dctr,
+                            multi_only ? 1 : 0);
             } else {
                 DK_LAUNCH(ctx, run_heads_kernel, g, kThreads, 0, s, skeys, m, w.heads.get());
                 exclusive_scan_u32(ctx, w.heads.get(), w.pos.get(), m, &dctr->runs, s);
@@ -2567,9 +2628,14 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
                             state_order ? w.act.get() : nullptr, dctr);
             }
             list_inc = state_order;
-            if (state_order) compact_flags(ctx, nullptr, w.act.get(), n, dst, &dctr->listed, s);
-            else compact_flags(ctx, svals, w.keep.get(), m, dst, &dctr->listed, s);
             read_words(ctx, dctr, sizeof(c), &c, s);
+            // compaction after the readback: nothing when no state survives
+            // or when every state does (the identity list stays)
+            if (state_order && c.active_states == n) all_survive = true;
+            else if (c.active_states && B - A + c.runs != B) {
+                if (state_order) compact_flags(ctx, nullptr, w.act.get(), n, dst, &dctr->listed, s);
+                else compact_flags(ctx, svals, w.keep.get(), m, dst, &dctr->listed, s);
+            }
         }
 
         check_streamed();

@@ -1,10 +1,9 @@
-#!/bin/bash
-# radix sort primitive: parity vs numpy + per-digit timing for each library variant
 cd "$GRAFT_REPO_ROOT"
-mkdir -p gpurun_out
-timeout -s KILL 600 python -m pytest tests/test_gpu_prims.py -q -m gpu -p no:cacheprovider --timeout 500 -x > gpurun_out/sort_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/sort_pytest.log
-for v in base ${VARIANTS}; do
+python -m pytest tests/test_gpu_minimize.py tests/test_gpu_prims.py -m gpu -x -q 2>&1 | tail -2
+python tools/kprof.py synth --reps 5 2>&1 | grep -E "wall|leader|#pass"
+for v in base m4 i8m4 t512; do
   if [ "$v" = base ]; then unset DFAKIT_LIB_VARIANT; else export DFAKIT_LIB_VARIANT=$v; fi
-  echo "== $v" >> gpurun_out/sortv.log
-  timeout -s KILL 300 python tools/sort_bench.py >> gpurun_out/sortv.log 2>&1
+  echo "== $v"; python tools/sort_bench.py 2>&1 | grep onesweep
 done
+unset DFAKIT_LIB_VARIANT
+python tools/kprof.py synth --grouping 1 --reps 5 2>&1 | tail -17

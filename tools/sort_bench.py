@@ -45,6 +45,18 @@ def main():
         per = x["ms"] / x["launches"]
         gbs = x["bytes"] / (x["ms"] / 1e3) / 1e9 if x["bytes"] else 0
         print(f"  {x['name'][:40]:40s} {per * 1000:8.1f} us/launch  x{x['launches'] / a.reps:.0f}  {gbs:7.0f} GB/s")
+    # calibration: torch.sort (CUB device radix sort, 64-bit keys + 64-bit
+    # indices) on the same keys, whole sort
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for stable in (True,):
+        torch.sort(src, stable=stable)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(a.reps):
+            torch.sort(src, stable=stable)
+        e1.record()
+        torch.cuda.synchronize()
+        print(f"  torch.sort(int64, stable={stable}) {e0.elapsed_time(e1) / a.reps * 1000:8.1f} us per sort")
 
 
 if __name__ == "__main__":
