@@ -919,6 +919,8 @@ struct GroupOut {
     uint32_t* res;     // sharded engine: res[entry index] = rep | multi << 31
     uint2* rec;        // deferred: rec[slot] = {state, rep | multi << 31}, applied once verified
     int rec_index;     // rec[slot].x = the entry index instead of the state (sharded owners)
+    uint8_t* bsingle;  // EM 1: per bucket, 1 = every key distinct (no records written: the
+                       // bucket's states keep their own ids)
 };
 
 __device__ __forceinline__ void emit(const GroupOut& o, uint64_t slot, uint32_t q, uint32_t r, bool multi,
@@ -1089,7 +1091,10 @@ __global__ void __launch_bounds__(kGrpThreads, DFAKIT_GRP_MINB) bucket_group_ker
             len_next = src.count(bn);
             src.prefetch(bn, len_next, tid, kGrpThreads);
         }
-        if (len == 0 || len > kGrpCap) continue;  // uniform across the CTA
+        if (len == 0 || len > kGrpCap) {  // uniform across the CTA
+            if (EM == 1 && tid == 0) o.bsingle[b] = 0;
+            continue;
+        }
         const uint32_t T = max(64u, pow2_at_least(2 * len));
         // rep needs no reset: every claimed slot's rep is written by its
         // claimer; keys and flags are reset with 16-byte stores (T >= 64)
@@ -1142,7 +1147,19 @@ __global__ void __launch_bounds__(kGrpThreads, DFAKIT_GRP_MINB) bucket_group_ker
                 }
             }
         }
-        if (__syncthreads_or(dup != 0)) {
+        const bool any_dup = __syncthreads_or(dup != 0);
+        if (EM == 1) {
+            if (tid == 0) o.bsingle[b] = any_dup ? 0 : 1;
+            if (!any_dup) {
+                // every key distinct: all singletons, nothing to verify and no
+                // records (rec_apply_kernel reads the states from the entries)
+#pragma unroll
+                for (int j = 0; j < kGrpItems; ++j) heads += j * kGrpThreads + tid < len;
+                __syncthreads();
+                continue;
+            }
+        }
+        if (any_dup) {
 #pragma unroll
             for (int j = 0; j < kGrpItems; ++j)
                 if (dup & (1u << j)) atomicMin(&sm.rep[slot[j]], q[j]);
@@ -1264,11 +1281,17 @@ __global__ void slot_apply_kernel(const uint32_t* __restrict__ bcnt, uint32_t nb
 // pass left every block a singleton (the numbering is then the identity)
 __global__ void rec_apply_kernel(const uint32_t* __restrict__ bcnt, uint32_t nb, uint32_t ovf,
                                  const uint2* __restrict__ rec, uint32_t* __restrict__ lab,
-                                 uint8_t* __restrict__ act) {
+                                 uint8_t* __restrict__ act, const uint8_t* __restrict__ bsingle,
+                                 const uint4* __restrict__ bent) {
     const uint64_t bspace = (uint64_t)nb * kGrpCap, total = bspace + ovf;
     for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
          e += (uint64_t)gridDim.x * blockDim.x) {
         if (e < bspace && (uint32_t)(e % kGrpCap) >= min(bcnt[(e / kGrpCap) * kCntStride], kGrpCap)) continue;
+        if (e < bspace && bsingle[e / kGrpCap]) {  // a bucket of distinct keys: singletons
+            const uint32_t q = __ldcs(bent + e).z;
+            lab[q] = q;
+            continue;
+        }
         const uint2 r = __ldcs(rec + e);
         lab[r.x] = r.y & 0x7fffffffu;
         if (r.y >> 31) act[r.x] = 1;
@@ -1538,6 +1561,7 @@ struct Workspace {
     // bucket strategy
     DBuf<uint32_t> bcnt, rep_slot, gslot, grep, eval;
     DBuf<uint2> rec;
+    DBuf<uint8_t> bsingle;
     DBuf<uint64_t> part;  // partial keys of a sliced pass
     DBuf<uint4> bent;
     DBuf<unsigned long long> gkey;
@@ -2098,6 +2122,7 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
         }
         if (!L.direct && !L.defer && w.rep_slot.n < L.espace) w.rep_slot.alloc(L.espace, s);
         if (L.defer && w.rec.n < L.espace) w.rec.alloc(L.espace, s);
+        if (L.defer && w.bsingle.n < L.nb) w.bsingle.alloc(L.nb, s);
         if (L.state_order && !w.act.get()) w.act.alloc(n, s);
         if (fingerprint && L.direct) {
             if (!w.lab2.get()) w.lab2.alloc(n, s);
@@ -2130,7 +2155,7 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
         });
         GroupOut go{L.direct ? 1 : 0, L.state_order ? 1 : 0, out_lab, w.act.get(),
                     L.direct || L.defer ? nullptr : w.rep_slot.get(), w.keep_slot.get(), nullptr,
-                    L.defer ? w.rec.get() : nullptr, 0};
+                    L.defer ? w.rec.get() : nullptr, 0, w.bsingle.get()};
         const unsigned gg = (unsigned)std::min<uint64_t>(L.nb, (uint64_t)ctx->num_sms * kGrpCtasPerSm);
         // algorithmic HBM bytes: (hkey, state) in, label + survivor flag out
         const double gbytes = (double)mm * (16.0 + 4.0 + 1.0 + (L.direct ? 0.0 : 4.0));
@@ -2487,7 +2512,8 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
                 if (B - A + c.runs != n) {
                     // (a pass over every state: every label is rewritten)
                     DK_LAUNCH_B(ctx, (double)m * 12.0, rec_apply_kernel, grid_for(bspace + c.overflow), kThreads, 0,
-                                s, w.bcnt.get(), nb, c.overflow, w.rec.get(), w.lab.get(), w.act.get());
+                                s, w.bcnt.get(), nb, c.overflow, w.rec.get(), w.lab.get(), w.act.get(),
+                                w.bsingle.get(), w.bent.get());
                     lab_pending = false;
                 }
             } else if (!direct)
