@@ -2131,7 +2131,9 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
         }
         uint32_t* out_lab = fingerprint && L.direct ? w.lab2.get() : w.lab.get();
         fl.add(w.bcnt.get(), (size_t)L.nb * kCntStride * 4, 0);
-        if (L.state_order) fl.add(w.act.get(), n, 0);
+        // (deferred passes flag survivors in rec_apply_kernel, which zeroes
+        // act itself when it runs -- not at all in the usual all-singleton pass)
+        if (L.state_order && !L.defer) fl.add(w.act.get(), n, 0);
         if (!L.state_order) fl.add(w.keep_slot.get(), L.espace, 0);
         fl.flush(ctx, s);
         const double lb = lst ? 4.0 : 0.0;
@@ -2511,6 +2513,7 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
             if (defer) {
                 if (B - A + c.runs != n) {
                     // (a pass over every state: every label is rewritten)
+                    DK_CUDA(cudaMemsetAsync(w.act.get(), 0, n, s));
                     DK_LAUNCH_B(ctx, (double)m * 12.0, rec_apply_kernel, grid_for(bspace + c.overflow), kThreads, 0,
                                 s, w.bcnt.get(), nb, c.overflow, w.rec.get(), w.lab.get(), w.act.get(),
                                 w.bsingle.get(), w.bent.get());
