@@ -2901,6 +2901,51 @@ __global__ void __launch_bounds__(kThreads, DFAKIT_SIGB_MINB) sig_owner_kernel(
     uint4* __restrict__ ovf, uint32_t* __restrict__ ovf_cnt, const uint64_t* __restrict__ part) {
     const unsigned lane = threadIdx.x & 31u, lt = (1u << lane) - 1u;
     if (MODE == 1) p.kind = kKeyFingerprint;
+    if constexpr (MODE == 2) {
+        // partial keys of a sliced pass (no gathers): the cursor atomic of one
+        // state in flight while the next state's key is read (as sig_bucket)
+        const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+        const uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x + (threadIdx.x & ~31u);
+        bool have = false, pvalid = false;
+        unsigned long long phk = 0;
+        uint32_t pq = 0, po = 0, pg = 0, pbase = 0, prank = 0, pleader = 0;
+        auto finish = [&]() {
+            const uint32_t pos = __shfl_sync(0xffffffffu, pbase, pleader) + prank;
+            if (!pvalid) return;
+            const uint4 e = make_uint4((uint32_t)phk, (uint32_t)(phk >> 32), pq, po);
+            if (pos < cs) {
+                send[(uint64_t)pg * cs + pos] = e;
+            } else {
+                ovf[atomicAdd(&ovf_cnt[world], 1u)] = e;
+                atomicAdd(&ovf_cnt[po], 1u);
+            }
+        };
+        for (uint64_t w = i0; w < m; w += stride) {
+            const uint64_t i = w + lane;
+            const bool valid = i < m;
+            unsigned long long hk = 0;
+            uint32_t q = 0;
+            if (valid) {
+                q = list ? list[i] : p.q0 + (uint32_t)i;
+                const uint64_t key = key_of_part(p, __ldcs(part + i));
+                hk = p.kind == kKeyPacked ? mix64(key) : key;
+            }
+            if (have) finish();
+            pvalid = valid;
+            phk = hk;
+            pq = q;
+            po = valid ? owner_of(hk, world) : 0u;
+            pg = valid ? po * nb + ((uint32_t)(hk >> kBucketShift) & (nb - 1)) : 0xffffffffu;
+            const unsigned peers = __match_any_sync(0xffffffffu, pg);
+            pleader = __ffs(peers) - 1;
+            prank = (uint32_t)__popc(peers & lt);
+            pbase = 0;
+            if (valid && lane == pleader) pbase = atomicAdd(&scur[pg * kCntStride], (uint32_t)__popc(peers));
+            have = true;
+        }
+        if (have) finish();
+        return;
+    }
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t q = list ? list[i] : p.q0 + (uint32_t)i;
         const uint64_t key = MODE == 2 ? key_of_part(p, __ldcs(part + i))
