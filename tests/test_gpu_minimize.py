@@ -384,3 +384,29 @@ def test_speculative_second_pass(dk, oracle, monkeypatch):
         assert same(dk.sort_pr(mkdfa(dk, t)), oracle.minimize("moore", t[0], t[1])), (n0, c)
     t = oracle.gen_synth(2_000_000, 10, 5)
     assert same(dk.sort_pr(mkdfa(dk, t)), oracle.minimize("moore", t[0], t[1]))
+
+
+def with_duplicates(t, d, seed):
+    """t plus d new states, each a duplicate (same row, same acceptance) of a
+    random existing state: d small classes among otherwise distinct states."""
+    delta, acc, _ = t
+    k, n = delta.shape
+    src = np.random.default_rng(seed).integers(0, n, d)
+    return np.concatenate([delta, delta[:, src]], axis=1), np.concatenate([acc, acc[src]]), 0
+
+
+@pytest.mark.parametrize("spec", [False, True], ids=["plain", "speculative"])
+def test_deferred_pass_mixed_buckets(dk, oracle, monkeypatch, spec):
+    """A big fingerprint pass whose buckets are mostly all-distinct (no
+    records written, states taken from the entries) with a few holding
+    equivalent states (records applied): random automata plus a few
+    thousand duplicated states, past the small-automaton kernel's size so the
+    bucket grouping defers its labels -- with the speculative second pass on
+    the first pass's raw table keys too."""
+    if spec:
+        monkeypatch.setenv("DFAKIT_TEST_SPEC_MIN", "1000")
+    for n0, d, k, s in ((400_000, 3000, 10, 5), (300_000, 40, 12, 6), (250_000, 20_000, 9, 7)):
+        t = with_duplicates(oracle.gen_synth(n0, k, s), d, s)
+        want = oracle.minimize("moore", t[0], t[1])
+        assert want.num_blocks < n0 + d
+        assert same(dk.sort_pr(mkdfa(dk, t)), want), (n0, d, k)
