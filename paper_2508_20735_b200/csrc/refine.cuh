@@ -105,9 +105,31 @@ struct OwnerSources {
     const uint4* base[8];
     const uint32_t* cnt[8];
 };
+// Where the sender's signature kernel puts owner o's sub-bucket entries
+// (nb * cs slots) and their counts (nb + 1 words): its own send regions,
+// exchanged afterwards, or -- peer mode -- this rank's region of owner o's
+// receive buffers, written over NVLink by the kernel itself.
+struct OwnerDst {
+    uint4* entries[8];
+    uint32_t* counts[8];
+};
+// Owners' label writes into the senders' label / survivor-flag arrays (peer mode)
+struct PeerLabels {
+    uint32_t* lab[8];
+    uint8_t* act[8];
+};
 void shard_sig_owner(Ctx* ctx, const DevDfa& d, const void* keylab, const PassPlan& plan, uint64_t salt,
                      const uint32_t* list, uint32_t list_base, uint64_t m, const OwnerPlan& op, OwnerSend& ws,
-                     cudaStream_t s);
+                     cudaStream_t s, const OwnerDst* dst = nullptr);
+// peer mode, owner side: every received region entry's result straight into
+// its sender's label (and survivor flag) -- the results' trip back and the
+// sender's apply in one kernel
+void shard_owner_scatter(Ctx* ctx, const OwnerPlan& op, const uint4* recv, const uint32_t* recv_cnt,
+                         const uint32_t* results, const PeerLabels& out, cudaStream_t s);
+// sender: the results of its overflow entries (peer mode: the region entries
+// were applied by their owners)
+void shard_apply_overflow(Ctx* ctx, const OwnerSend& ws, const uint32_t* back_ovf, uint32_t ovf_total, uint32_t* lab,
+                          uint8_t* act, cudaStream_t s);
 void shard_sort_overflow(Ctx* ctx, const OwnerPlan& op, OwnerSend& ws, uint32_t ovf_total, cudaStream_t s);
 void shard_owner_ovf_counts(Ctx* ctx, const OwnerPlan& op, const uint32_t* recv_msg, uint32_t* out, cudaStream_t s);
 void shard_group_owner(Ctx* ctx, const DevDfa& d, const void* verify_lab, uint32_t verify_bytes, const PassPlan& plan,

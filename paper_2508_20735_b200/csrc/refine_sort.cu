@@ -2897,7 +2897,7 @@ __global__ void init_act_range_kernel(const uint8_t* __restrict__ acc, uint32_t 
 template <typename LR, int MODE>  // as sig_bucket_kernel: 0 any kind, 1 fingerprints, 2 sliced partial keys
 __global__ void __launch_bounds__(kThreads, DFAKIT_SIGB_MINB) sig_owner_kernel(
     const uint32_t* __restrict__ list, uint64_t m, const uint32_t* __restrict__ delta, uint32_t n, LR lab, SigParams p,
-    uint32_t world, uint32_t nb, uint32_t cs, uint32_t* __restrict__ scur, uint4* __restrict__ send,
+    uint32_t world, uint32_t nb, uint32_t cs, uint32_t* __restrict__ scur, const __grid_constant__ OwnerDst dst,
     uint4* __restrict__ ovf, uint32_t* __restrict__ ovf_cnt, const uint64_t* __restrict__ part) {
     const unsigned lane = threadIdx.x & 31u, lt = (1u << lane) - 1u;
     if (MODE == 1) p.kind = kKeyFingerprint;
@@ -2914,7 +2914,7 @@ __global__ void __launch_bounds__(kThreads, DFAKIT_SIGB_MINB) sig_owner_kernel(
             if (!pvalid) return;
             const uint4 e = make_uint4((uint32_t)phk, (uint32_t)(phk >> 32), pq, po);
             if (pos < cs) {
-                send[(uint64_t)pg * cs + pos] = e;
+                dst.entries[po][(uint64_t)(pg - po * nb) * cs + pos] = e;
             } else {
                 ovf[atomicAdd(&ovf_cnt[world], 1u)] = e;
                 atomicAdd(&ovf_cnt[po], 1u);
@@ -2962,7 +2962,7 @@ __global__ void __launch_bounds__(kThreads, DFAKIT_SIGB_MINB) sig_owner_kernel(
         const uint32_t pos = base + (uint32_t)__popc(peers & lt);
         const uint4 e = make_uint4((uint32_t)hk, (uint32_t)(hk >> 32), q, o);
         if (pos < cs) {
-            send[(uint64_t)g * cs + pos] = e;
+            dst.entries[o][(uint64_t)(g - o * nb) * cs + pos] = e;  // (peer mode: a store over NVLink)
         } else {
             ovf[atomicAdd(&ovf_cnt[world], 1u)] = e;
             atomicAdd(&ovf_cnt[o], 1u);
@@ -2972,11 +2972,26 @@ __global__ void __launch_bounds__(kThreads, DFAKIT_SIGB_MINB) sig_owner_kernel(
 
 // per owner o: the nb sub-bucket counts then its overflow count (nb + 1 words)
 __global__ void owner_counts_kernel(const uint32_t* __restrict__ scur, const uint32_t* __restrict__ ovf_cnt,
-                                    uint32_t world, uint32_t nb, uint32_t* __restrict__ msg) {
+                                    uint32_t world, uint32_t nb, const __grid_constant__ OwnerDst dst) {
     const uint64_t total = (uint64_t)world * (nb + 1);
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t o = (uint32_t)(i / (nb + 1)), b = (uint32_t)(i % (nb + 1));
-        msg[i] = b < nb ? scur[((uint64_t)o * nb + b) * kCntStride] : ovf_cnt[o];
+        dst.counts[o][b] = b < nb ? scur[((uint64_t)o * nb + b) * kCntStride] : ovf_cnt[o];
+    }
+}
+
+// peer mode, owner side: region entry e of sender s = e / region gets its
+// result written straight into s's label / survivor-flag arrays
+__global__ void owner_scatter_kernel(const uint4* __restrict__ recv, const uint32_t* __restrict__ recv_cnt,
+                                     uint32_t world, uint32_t nb, uint32_t cs, const uint32_t* __restrict__ results,
+                                     const __grid_constant__ PeerLabels out) {
+    const uint64_t region = (uint64_t)nb * cs, total = region * world;
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total; e += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t s = (uint32_t)(e / region), r = (uint32_t)(e % region);
+        if (r % cs >= min(recv_cnt[(uint64_t)s * (nb + 1) + r / cs], cs)) continue;
+        const uint32_t q = __ldcs(recv + e).z, v = results[e];
+        out.lab[s][q] = v & 0x7fffffffu;
+        if (v >> 31) out.act[s][q] = 1;  // zeroed by the sender before the pass's counter exchange
     }
 }
 
@@ -3264,10 +3279,10 @@ OwnerPlan owner_plan(uint64_t m_total, uint32_t world) {
 
 void shard_sig_owner(Ctx* ctx, const DevDfa& d, const void* keylab, const PassPlan& plan, uint64_t salt,
                      const uint32_t* list, uint32_t list_base, uint64_t m, const OwnerPlan& op, OwnerSend& ws,
-                     cudaStream_t s) {
+                     cudaStream_t s, const OwnerDst* dst_in) {
     const uint32_t W = op.world, nb = op.nb, cs = op.cs;
     const uint64_t slots = (uint64_t)W * nb * cs;
-    if (ws.send.n < std::max<uint64_t>(1, slots)) ws.send.alloc(std::max<uint64_t>(1, slots), s);
+    if (!dst_in && ws.send.n < std::max<uint64_t>(1, slots)) ws.send.alloc(std::max<uint64_t>(1, slots), s);
     if (ws.scur.n < (uint64_t)W * nb * kCntStride) ws.scur.alloc((uint64_t)W * nb * kCntStride, s);
     if (ws.ovf.n < std::max<uint64_t>(1, m)) {
         ws.ovf.alloc(std::max<uint64_t>(1, m), s);
@@ -3277,7 +3292,16 @@ void shard_sig_owner(Ctx* ctx, const DevDfa& d, const void* keylab, const PassPl
         ws.ovf_cnt.alloc(W + 1, s);
         ws.ovf_cur.alloc(W, s);
     }
-    if (ws.msg.n < (uint64_t)W * (nb + 1)) ws.msg.alloc((uint64_t)W * (nb + 1), s);
+    if (!dst_in && ws.msg.n < (uint64_t)W * (nb + 1)) ws.msg.alloc((uint64_t)W * (nb + 1), s);
+    OwnerDst dst{};
+    if (dst_in) {
+        dst = *dst_in;
+    } else {
+        for (uint32_t o = 0; o < W; ++o) {
+            dst.entries[o] = ws.send.get() + (uint64_t)o * nb * cs;
+            dst.counts[o] = ws.msg.get() + (uint64_t)o * (nb + 1);
+        }
+    }
     Fills f;
     f.add(ws.scur.get(), (size_t)W * nb * kCntStride * 4, 0);
     f.add(ws.ovf_cnt.get(), (size_t)(W + 1) * 4, 0);
@@ -3293,19 +3317,19 @@ void shard_sig_owner(Ctx* ctx, const DevDfa& d, const void* keylab, const PassPl
             const unsigned grid = grid_for(m, kThreads, (unsigned)ctx->num_sms * 8u);
             if (part)
                 DK_LAUNCH_BU(ctx, bytes, 0.0, (sig_owner_kernel<LR, 2>), grid, kThreads, 0, s, list, m, d.delta, d.n,
-                             lab, p, W, nb, cs, ws.scur.get(), ws.send.get(), ws.ovf.get(), ws.ovf_cnt.get(), part);
+                             lab, p, W, nb, cs, ws.scur.get(), dst, ws.ovf.get(), ws.ovf_cnt.get(), part);
             else if (plan.strategy == kPlanFingerprint)
                 DK_LAUNCH_BU(ctx, bytes, (double)m * d.k, (sig_owner_kernel<LR, 1>), grid, kThreads, 0, s, list, m,
-                             d.delta, d.n, lab, p, W, nb, cs, ws.scur.get(), ws.send.get(), ws.ovf.get(),
+                             d.delta, d.n, lab, p, W, nb, cs, ws.scur.get(), dst, ws.ovf.get(),
                              ws.ovf_cnt.get(), part);
             else
                 DK_LAUNCH_BU(ctx, bytes, (double)m * d.k, (sig_owner_kernel<LR, 0>), grid, kThreads, 0, s, list, m,
-                             d.delta, d.n, lab, p, W, nb, cs, ws.scur.get(), ws.send.get(), ws.ovf.get(),
+                             d.delta, d.n, lab, p, W, nb, cs, ws.scur.get(), dst, ws.ovf.get(),
                              ws.ovf_cnt.get(), part);
         });
     }
     DK_LAUNCH(ctx, owner_counts_kernel, grid_for((uint64_t)W * (nb + 1)), kThreads, 0, s, ws.scur.get(),
-              ws.ovf_cnt.get(), W, nb, ws.msg.get());
+              ws.ovf_cnt.get(), W, nb, dst);
 }
 
 void shard_sort_overflow(Ctx* ctx, const OwnerPlan& op, OwnerSend& ws, uint32_t ovf_total, cudaStream_t s) {
@@ -3375,6 +3399,20 @@ void shard_group_owner(Ctx* ctx, const DevDfa& d, const void* verify_lab, uint32
         });
     }
     DK_CUDA(cudaMemcpyAsync(counters, dctr, 4 * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+}
+
+void shard_owner_scatter(Ctx* ctx, const OwnerPlan& op, const uint4* recv, const uint32_t* recv_cnt,
+                         const uint32_t* results, const PeerLabels& out, cudaStream_t s) {
+    const uint64_t total = (uint64_t)op.world * op.nb * op.cs;
+    DK_LAUNCH_B(ctx, 25.0 * total * 3 / 4, owner_scatter_kernel, grid_for(total), kThreads, 0, s, recv, recv_cnt,
+                op.world, op.nb, op.cs, results, out);
+}
+
+void shard_apply_overflow(Ctx* ctx, const OwnerSend& ws, const uint32_t* back_ovf, uint32_t ovf_total, uint32_t* lab,
+                          uint8_t* act, cudaStream_t s) {
+    if (ovf_total)
+        DK_LAUNCH(ctx, shard_apply_kernel, grid_for(ovf_total), kThreads, 0, s, ws.ovf_sorted.get(), back_ovf,
+                  (uint64_t)ovf_total, lab, act);
 }
 
 void shard_apply_owner(Ctx* ctx, const OwnerPlan& op, const OwnerSend& ws, uint32_t rank, const uint32_t* own_res,

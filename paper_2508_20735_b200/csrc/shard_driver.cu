@@ -20,6 +20,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <array>
 #include <cstdlib>
 #include <cstring>
 #include <condition_variable>
@@ -106,6 +107,21 @@ void grouped_all_to_all(const NcclApi& api, ncclComm_t comm, int world, const vo
 
 }  // namespace
 
+// Peer-memory workspace of a communicator (peer mode of the owner-bucket
+// passes): every rank's receive regions, received counts, block labels and
+// survivor flags, allocated with cudaMalloc (IPC-exportable) and mapped into
+// every other rank (CUDA IPC over NVLink / NVSwitch between processes; plain
+// pointers between the local hub's threads).  Kept across calls; grown
+// collectively (every rank asks for the same sizes: they follow from n).
+struct PeerSpace {
+    int state = 0;  // 0 untried, 1 enabled, -1 disabled (setup or self-test failed)
+    int device = 0;
+    uint64_t recv_slots = 0, cnt_words = 0, lab_words = 0, act_bytes = 0;
+    void* local[4] = {nullptr, nullptr, nullptr, nullptr};  // recv (uint4), cnt (u32), lab (u32), act (u8)
+    std::vector<std::array<void*, 4>> peer;                  // per rank; own entry = local
+    uint32_t* sync = nullptr;                                // barrier word
+};
+
 // Collectives of the pass loop on stream s.  NCCL in production; the local
 // hub runs several ranks as threads of one process sharing a device (each
 // with its own context), staging through host memory -- the way the
@@ -113,6 +129,13 @@ void grouped_all_to_all(const NcclApi& api, ncclComm_t comm, int world, const vo
 struct NcclComm {
     virtual ~NcclComm() = default;
     int world = 1, rank = 0;
+    PeerSpace peer;
+    // every rank's local[4] pointers, mapped into this process (collective)
+    virtual void exchange_peer_ptrs(cudaStream_t s) = 0;
+    virtual void release_peer_ptrs() = 0;
+    // stream-ordered barrier: this rank's prior work on s is complete, and
+    // work queued on s after it starts only once every rank's prior work is
+    virtual void barrier(cudaStream_t s) = 0;
     virtual void allreduce_u32(uint32_t* buf, size_t count, bool use_min, cudaStream_t s) = 0;
     // full holds world slices of `bytes`; this rank's slice is at rank * bytes
     virtual void allgather(void* full, size_t bytes, cudaStream_t s) = 0;
@@ -136,7 +159,44 @@ namespace {
 struct NcclImpl : NcclComm {
     ncclComm_t comm = nullptr;
     ~NcclImpl() override {
+        release_peer_ptrs();
         if (comm) nccl().CommDestroy(comm);
+    }
+    void barrier(cudaStream_t s) override {
+        nccl_check(nccl().AllReduce(peer.sync, peer.sync, 1, ncclUint32, ncclSum, comm, s), "barrier");
+    }
+    // CUDA IPC: every rank exports its four buffers, the 64-byte handles
+    // travel by one ncclAllGather, and the peers' buffers are opened with
+    // lazy peer access (NVLink / NVSwitch stores from this rank's kernels)
+    void exchange_peer_ptrs(cudaStream_t s) override {
+        constexpr size_t H = sizeof(cudaIpcMemHandle_t);
+        std::vector<unsigned char> mine(4 * H), all((size_t)world * 4 * H);
+        for (int i = 0; i < 4; ++i)
+            DK_CUDA(cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(mine.data() + i * H), peer.local[i]));
+        DBuf<unsigned char> dev((size_t)world * 4 * H, s);
+        DK_CUDA(cudaMemcpyAsync(dev.get() + (size_t)rank * 4 * H, mine.data(), 4 * H, cudaMemcpyHostToDevice, s));
+        nccl_check(nccl().AllGather(dev.get() + (size_t)rank * 4 * H, dev.get(), 4 * H, ncclUint8, comm, s),
+                   "allgather (ipc handles)");
+        DK_CUDA(cudaMemcpyAsync(all.data(), dev.get(), all.size(), cudaMemcpyDeviceToHost, s));
+        DK_CUDA(cudaStreamSynchronize(s));
+        peer.peer.assign(world, {nullptr, nullptr, nullptr, nullptr});
+        for (int r = 0; r < world; ++r)
+            for (int i = 0; i < 4; ++i) {
+                if (r == rank) {
+                    peer.peer[r][i] = peer.local[i];
+                    continue;
+                }
+                cudaIpcMemHandle_t h;
+                std::memcpy(&h, all.data() + ((size_t)r * 4 + i) * H, H);
+                DK_CUDA(cudaIpcOpenMemHandle(&peer.peer[r][i], h, cudaIpcMemLazyEnablePeerAccess));
+            }
+    }
+    void release_peer_ptrs() override {
+        for (int r = 0; r < (int)peer.peer.size(); ++r)
+            if (r != rank)
+                for (void* p : peer.peer[r])
+                    if (p) cudaIpcCloseMemHandle(p);
+        peer.peer.clear();
     }
     void allreduce_u32(uint32_t* buf, size_t count, bool use_min, cudaStream_t s) override {
         nccl_check(nccl().AllReduce(buf, buf, count, ncclUint32, use_min ? ncclMin : ncclSum, comm, s), "allreduce");
@@ -155,8 +215,9 @@ struct NcclImpl : NcclComm {
 }  // namespace
 
 struct LocalHub {
-    explicit LocalHub(int w) : world(w), host(w), counts(w) {}
+    explicit LocalHub(int w) : world(w), host(w), counts(w), ptrs(w) {}
     int world;
+    std::vector<std::array<void*, 4>> ptrs;  // peer mode: the ranks' buffers (one device, plain pointers)
     std::mutex mu;
     std::condition_variable cv;
     int arrived = 0;
@@ -180,6 +241,19 @@ namespace {
 
 struct LocalImpl : NcclComm {
     LocalHub* hub = nullptr;
+    ~LocalImpl() override { release_peer_ptrs(); }
+    void barrier(cudaStream_t s) override {
+        DK_CUDA(cudaStreamSynchronize(s));
+        hub->barrier();
+    }
+    void exchange_peer_ptrs(cudaStream_t s) override {
+        DK_CUDA(cudaStreamSynchronize(s));
+        for (int i = 0; i < 4; ++i) hub->ptrs[rank][i] = peer.local[i];
+        hub->barrier();
+        peer.peer = hub->ptrs;
+        hub->barrier();
+    }
+    void release_peer_ptrs() override { peer.peer.clear(); }
     void publish(const void* dev, size_t bytes, cudaStream_t s) {
         auto& h = hub->host[rank];
         h.resize(bytes);
@@ -285,7 +359,110 @@ NcclComm* local_comm_init(LocalHub* hub, int rank) {
     return c;
 }
 
-void nccl_comm_destroy(NcclComm* c) { delete c; }
+void peer_space_release(NcclComm* cm);
+
+void nccl_comm_destroy(NcclComm* c) {
+    if (!c) return;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    if (c->peer.state > 0) cudaSetDevice(c->peer.device);
+    peer_space_release(c);
+    cudaSetDevice(cur);
+    delete c;
+}
+
+namespace {
+
+__global__ void peer_probe_kernel(PeerLabels pl, int world, int rank) {
+    // every rank stamps its id into word `rank` of every rank's label buffer
+    const int r = threadIdx.x;
+    if (r < world) pl.lab[r][rank] = 0xC0DE0000u | (uint32_t)rank;
+}
+
+void peer_free_local(PeerSpace& p) {
+    for (void*& q : p.local)
+        if (q) {
+            cudaFree(q);
+            q = nullptr;
+        }
+    if (p.sync) cudaFree(p.sync);
+    p.sync = nullptr;
+}
+
+// Makes the peer workspace at least this large on every rank (collective:
+// every rank passes the same sizes) and, the first time, proves the mapping
+// with a stamp exchange; any failure turns peer mode off for the comm (the
+// NCCL region exchange takes over).  Returns whether peer mode is on.
+bool peer_ensure(Ctx* ctx, NcclComm* cm, uint64_t recv_slots, uint64_t cnt_words, uint64_t lab_words,
+                 uint64_t act_bytes, cudaStream_t s) {
+    PeerSpace& p = cm->peer;
+    if (p.state < 0) return false;
+    if (p.state > 0 && p.recv_slots >= recv_slots && p.cnt_words >= cnt_words && p.lab_words >= lab_words &&
+        p.act_bytes >= act_bytes)
+        return true;
+    const int world = cm->world, rank = cm->rank;
+    int ok = 1;
+    try {
+        DK_CUDA(cudaStreamSynchronize(s));
+        if (p.state > 0) cm->barrier(s);  // nobody still writes into the old buffers
+        DK_CUDA(cudaStreamSynchronize(s));
+        cm->release_peer_ptrs();
+        peer_free_local(p);
+        p.device = ctx->device;
+        p.recv_slots = std::max(p.recv_slots, recv_slots);
+        p.cnt_words = std::max(p.cnt_words, cnt_words);
+        p.lab_words = std::max(p.lab_words, std::max<uint64_t>(lab_words, (uint64_t)world));
+        p.act_bytes = std::max(p.act_bytes, act_bytes);
+        DK_CUDA(cudaMalloc(&p.local[0], std::max<uint64_t>(1, p.recv_slots) * sizeof(uint4)));
+        DK_CUDA(cudaMalloc(&p.local[1], std::max<uint64_t>(1, p.cnt_words) * sizeof(uint32_t)));
+        DK_CUDA(cudaMalloc(&p.local[2], p.lab_words * sizeof(uint32_t)));
+        DK_CUDA(cudaMalloc(&p.local[3], std::max<uint64_t>(1, p.act_bytes)));
+        DK_CUDA(cudaMalloc(reinterpret_cast<void**>(&p.sync), sizeof(uint32_t)));
+        DK_CUDA(cudaMemsetAsync(p.sync, 0, sizeof(uint32_t), s));
+        DK_CUDA(cudaMemsetAsync(p.local[2], 0, (size_t)world * sizeof(uint32_t), s));
+        cm->exchange_peer_ptrs(s);
+        if (p.state == 0) {
+            cm->barrier(s);  // every rank's stamp area is zeroed
+            PeerLabels pl{};
+            for (int r = 0; r < world; ++r) pl.lab[r] = static_cast<uint32_t*>(p.peer[r][2]);
+            peer_probe_kernel<<<1, 32, 0, s>>>(pl, world, rank);
+            DK_CUDA(cudaGetLastError());
+            cm->barrier(s);
+            std::vector<uint32_t> got(world);
+            DK_CUDA(cudaMemcpyAsync(got.data(), p.local[2], world * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+            DK_CUDA(cudaStreamSynchronize(s));
+            for (int r = 0; r < world; ++r) ok &= got[r] == (0xC0DE0000u | (uint32_t)r);
+        }
+    } catch (const Error&) {
+        ok = 0;
+        cudaGetLastError();
+    }
+    if (p.state == 0) {
+        // every rank learns whether every rank's mapping works
+        DBuf<uint32_t> v(1, s);
+        const uint32_t mine = (uint32_t)ok;
+        DK_CUDA(cudaMemcpyAsync(v.get(), &mine, 4, cudaMemcpyHostToDevice, s));
+        cm->allreduce_u32(v.get(), 1, true, s);
+        uint32_t all = 0;
+        DK_CUDA(cudaMemcpyAsync(&all, v.get(), 4, cudaMemcpyDeviceToHost, s));
+        DK_CUDA(cudaStreamSynchronize(s));
+        p.state = all ? 1 : -1;
+    } else if (!ok) {
+        throw Error(DFAKIT_E_CUDA, "sharded sort_pr: growing the peer workspace failed");
+    }
+    if (p.state < 0) {
+        cm->release_peer_ptrs();
+        peer_free_local(p);
+    }
+    return p.state > 0;
+}
+
+}  // namespace
+
+void peer_space_release(NcclComm* cm) {
+    cm->release_peer_ptrs();
+    peer_free_local(cm->peer);
+}
 
 RefineResult sort_pr_sharded_device(Ctx* ctx, NcclComm* cm, const DevDfa& d, uint32_t* block_out, cudaStream_t s,
                                     uint64_t* exchanged) {
@@ -298,17 +475,35 @@ RefineResult sort_pr_sharded_device(Ctx* ctx, NcclComm* cm, const DevDfa& d, uin
     const uint32_t shard = (uint32_t)((((uint64_t)n + world - 1) / world + 3) / 4 * 4);
     const uint32_t lo = std::min<uint64_t>(n, (uint64_t)rank * shard);
     const uint32_t hi = std::min<uint64_t>(n, (uint64_t)(rank + 1) * shard);
-    DBuf<uint32_t> lab((uint64_t)world * shard, s), list(std::max(1u, hi - lo), s), scratch((uint64_t)n + 1, s);
-    DBuf<uint8_t> act(n, s);
+    // owner-bucket layout (up to 8 ranks; DFAKIT_SHARD_STAGED=1 forces the
+    // staged entries + partition + owner re-bucketing protocol of sharded.py)
+    const bool owner_layout = world <= 8 && !getenv("DFAKIT_SHARD_STAGED");
+    // peer mode (owner layout; DFAKIT_SHARD_PEER=0 turns it off): the
+    // signature kernel stores each entry straight into its owner's receive
+    // region and the owners write the results straight into the senders'
+    // labels -- over NVLink between GPUs -- instead of two NCCL exchanges
+    const char* peer_env = getenv("DFAKIT_SHARD_PEER");
+    const OwnerPlan op_max = owner_plan(n, (uint32_t)world);
+    const bool peer_mode = owner_layout && !(peer_env && peer_env[0] == '0') &&
+                           peer_ensure(ctx, cm, (uint64_t)world * op_max.nb * op_max.cs,
+                                       (uint64_t)world * (op_max.nb + 1), (uint64_t)world * shard, n, s);
+    // DFAKIT_SHARD_PEER=2 (tests): peer mode required, its absence an error
+    if (owner_layout && peer_env && peer_env[0] == '2' && !peer_mode)
+        throw Error(DFAKIT_E_RESOURCE, "sharded sort_pr: peer mode required but unavailable");
+    DBuf<uint32_t> lab_own, list(std::max(1u, hi - lo), s), scratch((uint64_t)n + 1, s);
+    DBuf<uint8_t> act_own;
+    if (!peer_mode) {
+        lab_own.alloc((uint64_t)world * shard, s);
+        act_own.alloc(n, s);
+    }
+    uint32_t* const LAB = peer_mode ? static_cast<uint32_t*>(cm->peer.local[2]) : lab_own.get();
+    uint8_t* const ACT = peer_mode ? static_cast<uint8_t*>(cm->peer.local[3]) : act_own.get();
     DBuf<uint32_t> dctr(8, s), counts(2 * (uint64_t)world, s), keys32;  // [send counts | receive counts]
     DBuf<uint8_t> kl8;
     DBuf<uint16_t> kl16, next16;
     DBuf<uint32_t> kl32, next32, tmin, tcnt, results, back, bits;
     DBuf<uint4> send, recv;
     ShardGroupWs gws;  // owner-side grouping workspace (slot-ordered records)
-    // owner-bucket layout (up to 8 ranks; DFAKIT_SHARD_STAGED=1 forces the
-    // staged entries + partition + owner re-bucketing protocol of sharded.py)
-    const bool owner_layout = world <= 8 && !getenv("DFAKIT_SHARD_STAGED");
     OwnerSend ows;
     DBuf<uint32_t> rmsg, small(2 * (uint64_t)world + 2, s);
     DBuf<uint4> rreg, rovf_buf;
@@ -318,12 +513,12 @@ RefineResult sort_pr_sharded_device(Ctx* ctx, NcclComm* cm, const DevDfa& d, uin
             read_words(ctx, p + i, std::min<size_t>(112, count - i) * sizeof(uint32_t), out + i, s);
     };
 
-    const ShardInit si = shard_init(ctx, d, lo, hi, lab.get(), act.get(), s, /*lazy=*/true);
+    const ShardInit si = shard_init(ctx, d, lo, hi, LAB, ACT, s, /*lazy=*/true);
     uint32_t B = si.num_blocks, A = si.active_blocks;
     uint64_t m_total = si.active_states;
     uint32_t m = 0;
     auto compact = [&] {
-        shard_compact(ctx, act.get(), lo, hi, list.get(), dctr.get() + 4, s);
+        shard_compact(ctx, ACT, lo, hi, list.get(), dctr.get() + 4, s);
         read_u32(dctr.get() + 4, 1, &m);
     };
     if (m_total == n) m = hi - lo;  // every state active: the identity range
@@ -347,10 +542,10 @@ RefineResult sort_pr_sharded_device(Ctx* ctx, NcclComm* cm, const DevDfa& d, uin
         // the other ranks' min-state labels are needed unless the pass
         // gathers carried key labels
         if (lab_stale && !(plan.keylab_bytes && carried)) {
-            cm->allgather(lab.get(), (size_t)shard * sizeof(uint32_t), s);
+            cm->allgather(LAB, (size_t)shard * sizeof(uint32_t), s);
             lab_stale = false;
         }
-        const void* keylab = lab.get();
+        const void* keylab = LAB;
         if (plan.keylab_bytes) {
             if (carried) {
                 keylab = carried;
@@ -371,7 +566,7 @@ RefineResult sort_pr_sharded_device(Ctx* ctx, NcclComm* cm, const DevDfa& d, uin
                     if (!kl32.get()) kl32.alloc(n, s);
                     out = kl32.get();
                 }
-                shard_keylab(ctx, lab.get(), n, B, plan, out, scratch.get(), s, res.iters == 0 ? d.acc : nullptr);
+                shard_keylab(ctx, LAB, n, B, plan, out, scratch.get(), s, res.iters == 0 ? d.acc : nullptr);
                 keylab = out;
             }
         }
@@ -388,7 +583,7 @@ RefineResult sort_pr_sharded_device(Ctx* ctx, NcclComm* cm, const DevDfa& d, uin
             shard_table_signature(ctx, d, keylab, plan, lst, lo, m, keys32.get(), tmin.get(), tcnt.get(), s);
             cm->allreduce_u32(tmin.get(), tsize, true, s);
             cm->allreduce_u32(tcnt.get(), tsize, false, s);
-            if (hi > lo) DK_CUDA(cudaMemsetAsync(act.get() + lo, 0, hi - lo, s));
+            if (hi > lo) DK_CUDA(cudaMemsetAsync(ACT + lo, 0, hi - lo, s));
             if (m_total == n) {
                 // every block of the next partition is one table key
                 if (plan.key_bits <= 16) {
@@ -399,7 +594,7 @@ RefineResult sort_pr_sharded_device(Ctx* ctx, NcclComm* cm, const DevDfa& d, uin
                     next_kl = next32.get();
                 }
             }
-            shard_table_apply(ctx, plan, lst, lo, keys32.get(), m, tmin.get(), tcnt.get(), lab.get(), act.get(),
+            shard_table_apply(ctx, plan, lst, lo, keys32.get(), m, tmin.get(), tcnt.get(), LAB, ACT,
                               next_kl, dctr.get(), s);
             // only this rank's slice of `lab` was written (after a lazy
             // shard_init the other slices were never initialised): a fixed
@@ -411,13 +606,27 @@ RefineResult sort_pr_sharded_device(Ctx* ctx, NcclComm* cm, const DevDfa& d, uin
             // wide pass, owner-bucket layout: the signature kernel fills
             // (owner, bucket) sub-buckets that travel as they are
             const OwnerPlan op = owner_plan(m_total, (uint32_t)world);
-            shard_sig_owner(ctx, d, keylab, plan, salt, lst, lo, m, op, ows, s);
             const uint64_t msgw = op.nb + 1, region = (uint64_t)op.nb * op.cs;
-            if (rmsg.n < world * msgw) rmsg.alloc(world * msgw, s);
-            const std::vector<uint64_t> mcount(world, msgw);
-            cm->all_to_all_v(ows.msg.get(), mcount, rmsg.get(), mcount, sizeof(uint32_t), s);
+            uint4* const precv = peer_mode ? static_cast<uint4*>(cm->peer.local[0]) : nullptr;
+            uint32_t* const pcnt = peer_mode ? static_cast<uint32_t*>(cm->peer.local[1]) : nullptr;
+            if (peer_mode) {
+                // this rank's region of every owner's receive buffer
+                OwnerDst dst{};
+                for (int o = 0; o < world; ++o) {
+                    dst.entries[o] = static_cast<uint4*>(cm->peer.peer[o][0]) + (uint64_t)rank * region;
+                    dst.counts[o] = static_cast<uint32_t*>(cm->peer.peer[o][1]) + (uint64_t)rank * msgw;
+                }
+                shard_sig_owner(ctx, d, keylab, plan, salt, lst, lo, m, op, ows, s, &dst);
+                cm->barrier(s);  // every sender's entries and counts have landed
+            } else {
+                shard_sig_owner(ctx, d, keylab, plan, salt, lst, lo, m, op, ows, s);
+                if (rmsg.n < world * msgw) rmsg.alloc(world * msgw, s);
+                const std::vector<uint64_t> mcount(world, msgw);
+                cm->all_to_all_v(ows.msg.get(), mcount, rmsg.get(), mcount, sizeof(uint32_t), s);
+            }
+            const uint32_t* const rcnt_all = peer_mode ? pcnt : rmsg.get();
             // overflow counts: received per sender, own per owner, own total
-            shard_owner_ovf_counts(ctx, op, rmsg.get(), small.get(), s);
+            shard_owner_ovf_counts(ctx, op, rcnt_all, small.get(), s);
             DK_CUDA(cudaMemcpyAsync(small.get() + world, ows.ovf_cnt.get(), (world + 1) * sizeof(uint32_t),
                                     cudaMemcpyDeviceToDevice, s));
             std::vector<uint32_t> w32(2 * (size_t)world + 1);
@@ -437,7 +646,7 @@ RefineResult sort_pr_sharded_device(Ctx* ctx, NcclComm* cm, const DevDfa& d, uin
                 scnt[r] = rcnt[r] = r == rank ? 0 : region;
                 roff[r] = r == rank ? 0 : (uint64_t)(r - (r > rank)) * region;
             }
-            const uint64_t peers_slots = (uint64_t)(world - 1) * region;
+            const uint64_t peers_slots = peer_mode ? 0 : (uint64_t)(world - 1) * region;
             if (peers_slots && rreg.n < peers_slots) rreg.alloc(peers_slots, s);
             if (peers_slots) cm->all_to_all_off(ows.send.get(), soff, scnt, rreg.get(), roff, rcnt, sizeof(uint4), s);
             if (rovf_buf.n < std::max<uint64_t>(1, rovf_total)) rovf_buf.alloc(std::max<uint64_t>(1, rovf_total), s);
@@ -445,8 +654,9 @@ RefineResult sort_pr_sharded_device(Ctx* ctx, NcclComm* cm, const DevDfa& d, uin
             sent += m;
             OwnerSources in{};
             for (int r = 0; r < world; ++r) {
-                in.base[r] = r == rank ? ows.send.get() + (uint64_t)rank * region : rreg.get() + roff[r];
-                in.cnt[r] = rmsg.get() + (uint64_t)r * msgw;
+                in.base[r] = peer_mode ? precv + (uint64_t)r * region
+                                       : (r == rank ? ows.send.get() + (uint64_t)rank * region : rreg.get() + roff[r]);
+                in.cnt[r] = rcnt_all + (uint64_t)r * msgw;
             }
             const uint64_t rslots = (uint64_t)world * region + rovf_total;
             if (results.n < rslots) results.alloc(rslots, s);
@@ -454,8 +664,11 @@ RefineResult sort_pr_sharded_device(Ctx* ctx, NcclComm* cm, const DevDfa& d, uin
                 shard_group_owner(ctx, d, keylab, plan.keylab_bytes ? plan.keylab_bytes : 4, plan, op, in,
                                   rovf_buf.get(), (uint32_t)rovf_total, results.get(), dctr.get(), s);
             else
-                shard_group_owner(ctx, d, lab.get(), 4, plan, op, in, rovf_buf.get(), (uint32_t)rovf_total,
+                shard_group_owner(ctx, d, LAB, 4, plan, op, in, rovf_buf.get(), (uint32_t)rovf_total,
                                   results.get(), dctr.get(), s);
+            // peer mode: the owners will write this rank's flags; zeroed before
+            // the counter exchange, which every owner passes before writing
+            if (peer_mode && hi > lo) DK_CUDA(cudaMemsetAsync(ACT + lo, 0, hi - lo, s));
             cm->allreduce_u32(dctr.get(), 4, false, s);
             read_u32(dctr.get(), 4, ctr);
             if (ctr[3]) {
@@ -471,6 +684,22 @@ RefineResult sort_pr_sharded_device(Ctx* ctx, NcclComm* cm, const DevDfa& d, uin
                 B = n;
                 break;
             }
+            if (peer_mode) {
+                // owners: region results straight into the senders' labels and
+                // flags; the overflow results travel back as before
+                PeerLabels pl{};
+                for (int r = 0; r < world; ++r) {
+                    pl.lab[r] = static_cast<uint32_t*>(cm->peer.peer[r][2]);
+                    pl.act[r] = static_cast<uint8_t*>(cm->peer.peer[r][3]);
+                }
+                shard_owner_scatter(ctx, op, precv, pcnt, results.get(), pl, s);
+                if (back_ovf.n < std::max<uint32_t>(1, own_ovf)) back_ovf.alloc(std::max<uint32_t>(1, own_ovf), s);
+                cm->all_to_all_v(results.get() + (uint64_t)world * region, rovf, back_ovf.get(), sovf,
+                                 sizeof(uint32_t), s);
+                shard_apply_overflow(ctx, ows, back_ovf.get(), own_ovf, LAB, ACT, s);
+                cm->barrier(s);  // every owner's label writes into this rank have landed
+                goto pass_done;
+            }
             // results back: each sender's padded part of every region, then the overflow results
             if (peers_slots && back.n < peers_slots) back.alloc(peers_slots, s);
             if (peers_slots)
@@ -478,9 +707,9 @@ RefineResult sort_pr_sharded_device(Ctx* ctx, NcclComm* cm, const DevDfa& d, uin
             if (back_ovf.n < std::max<uint32_t>(1, own_ovf)) back_ovf.alloc(std::max<uint32_t>(1, own_ovf), s);
             cm->all_to_all_v(results.get() + (uint64_t)world * region, rovf, back_ovf.get(), sovf, sizeof(uint32_t),
                              s);
-            if (hi > lo) DK_CUDA(cudaMemsetAsync(act.get() + lo, 0, hi - lo, s));
+            if (hi > lo) DK_CUDA(cudaMemsetAsync(ACT + lo, 0, hi - lo, s));
             shard_apply_owner(ctx, op, ows, (uint32_t)rank, results.get() + (uint64_t)rank * region, back.get(),
-                              back_ovf.get(), own_ovf, lab.get(), act.get(), s);
+                              back_ovf.get(), own_ovf, LAB, ACT, s);
         } else {
             if (send.n < std::max(1u, m)) send.alloc(std::max(1u, hi - lo), s);
             shard_sig_partition(ctx, d, keylab, plan, salt, lst, lo, m, (uint32_t)world, send.get(), counts.get(), s);
@@ -504,7 +733,7 @@ RefineResult sort_pr_sharded_device(Ctx* ctx, NcclComm* cm, const DevDfa& d, uin
                 shard_group_deferred(ctx, d, keylab, plan.keylab_bytes ? plan.keylab_bytes : 4, plan, recv.get(),
                                      rtotal, gws, dctr.get(), s);
             else
-                shard_group_deferred(ctx, d, lab.get(), 4, plan, recv.get(), rtotal, gws, dctr.get(), s);
+                shard_group_deferred(ctx, d, LAB, 4, plan, recv.get(), rtotal, gws, dctr.get(), s);
             cm->allreduce_u32(dctr.get(), 4, false, s);
             read_u32(dctr.get(), 4, ctr);
             if (ctr[3]) {
@@ -527,9 +756,10 @@ RefineResult sort_pr_sharded_device(Ctx* ctx, NcclComm* cm, const DevDfa& d, uin
             shard_group_results(ctx, gws, results.get(), s);
             if (back.n < std::max(1u, m)) back.alloc(std::max(1u, hi - lo), s);
             cm->all_to_all_v(results.get(), rcount, back.get(), scount, sizeof(uint32_t), s);
-            if (hi > lo) DK_CUDA(cudaMemsetAsync(act.get() + lo, 0, hi - lo, s));
-            shard_apply(ctx, send.get(), back.get(), m, lab.get(), act.get(), s);
+            if (hi > lo) DK_CUDA(cudaMemsetAsync(ACT + lo, 0, hi - lo, s));
+            shard_apply(ctx, send.get(), back.get(), m, LAB, ACT, s);
         }
+    pass_done:
         strikes = 0;
         const uint32_t newB = B - A + ctr[0];
         if (newB == B) break;  // fixed point
@@ -547,7 +777,7 @@ RefineResult sort_pr_sharded_device(Ctx* ctx, NcclComm* cm, const DevDfa& d, uin
             carried_bytes = (uint32_t)es;
             lab_stale = true;
         } else if (B < n) {
-            cm->allgather(lab.get(), (size_t)shard * sizeof(uint32_t), s);
+            cm->allgather(LAB, (size_t)shard * sizeof(uint32_t), s);
             lab_stale = false;
         } else {
             lab_stale = true;  // all singletons: the numbering needs no labels
@@ -556,8 +786,8 @@ RefineResult sort_pr_sharded_device(Ctx* ctx, NcclComm* cm, const DevDfa& d, uin
         else if (m_total) compact();     // (none left: the loop ends, nothing to compact)
     }
     // an all-singleton partition is numbered by identity (no label exchange)
-    if (lab_stale && B < n) cm->allgather(lab.get(), (size_t)shard * sizeof(uint32_t), s);
-    res.num_blocks = canonical_from_min_labels(ctx, lab.get(), n, block_out, scratch.get(), s, B);
+    if (lab_stale && B < n) cm->allgather(LAB, (size_t)shard * sizeof(uint32_t), s);
+    res.num_blocks = canonical_from_min_labels(ctx, LAB, n, block_out, scratch.get(), s, B);
     if (exchanged) *exchanged = sent;
     return res;
 }

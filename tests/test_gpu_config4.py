@@ -18,7 +18,7 @@ over-splits (separates copies) or under-splits fails the comparison.
 Checked: the single-GPU engine (default grouping and the literal radix-sort
 grouping), the native sharded engine at world size 1 over NCCL, and at world
 sizes 2 and 4 with the ranks as threads sharing the one GPU (collectives
-through the in-process hub)."""
+through the in-process hub, entries and results through peer memory)."""
 import ctypes as C
 import os
 import socket
@@ -109,11 +109,12 @@ def test_config4_sharded_native_world1_nccl_exact(dk, instance):
 
 
 @pytest.mark.parametrize("world", [2, 4])
-def test_config4_sharded_native_hub_exact(dk, instance, world):
+def test_config4_sharded_native_hub_exact(dk, instance, world, monkeypatch):
     """World sizes 2 and 4 of the native driver: ranks are threads of this
     process sharing the GPU (and the read-only automaton), each with its own
     context; every rank must return the whole exact partition."""
     from paper_2508_20735_b200 import _native as nat
+    monkeypatch.setenv("DFAKIT_SHARD_PEER", "2")  # the peer-memory exchange, required
     delta, acc, expect, nb, iters = instance
     n = expect.numel()
     hub = C.c_void_p()

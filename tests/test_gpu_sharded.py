@@ -103,9 +103,13 @@ def test_sharded_world1_nccl(dk):
         dist.destroy_process_group()
 
 
-def test_sharded_native_driver_world1(dk):
-    """The C++ pass loop over NCCL (dfakit_sort_pr_sharded), world size 1."""
+@pytest.mark.parametrize("peer", ["2", "0"], ids=["peer", "collectives"])
+def test_sharded_native_driver_world1(dk, monkeypatch, peer):
+    """The C++ pass loop over NCCL (dfakit_sort_pr_sharded), world size 1:
+    peer mode (the comm's own buffers as the one peer) and the collective
+    exchanges."""
     from paper_2508_20735_b200 import sharded
+    monkeypatch.setenv("DFAKIT_SHARD_PEER", peer)
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
     os.environ["MASTER_PORT"] = str(free_port())
     dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
@@ -203,12 +207,18 @@ def check_hub(out, want, tag):
         assert iters == want.refine_iters, (tag, r, iters, want.refine_iters)
 
 
-@pytest.mark.parametrize("layout", ["owner", "staged", "owner-sliced"])
+@pytest.mark.parametrize("layout", ["owner", "owner-nccl", "staged", "owner-sliced"])
 def test_native_driver_multirank_local_hub(dk, layout, monkeypatch):
     """The native C++ pass loop with world sizes 2 and 3 (ranks as threads on
     the one GPU; NCCL refuses two ranks on one device).  Every rank must
     return the oracle's partition and pass count -- through the owner-bucket
-    layout (the default), the staged-entries protocol, and sliced passes."""
+    layout in peer mode (the default: entries stored into the owners' receive
+    regions and results into the senders' labels by the kernels themselves,
+    here required), the owner layout with both exchanges as collectives, the
+    staged-entries protocol, and sliced passes."""
+    monkeypatch.setenv("DFAKIT_SHARD_PEER", "2")
+    if layout == "owner-nccl":
+        monkeypatch.setenv("DFAKIT_SHARD_PEER", "0")
     if layout == "staged":
         monkeypatch.setenv("DFAKIT_SHARD_STAGED", "1")
     if layout == "owner-sliced":  # signature passes gathered in label slices
@@ -220,13 +230,31 @@ def test_native_driver_multirank_local_hub(dk, layout, monkeypatch):
             check_hub(run_hub(dk, world, d, a), want, (layout, world, case))
 
 
-def test_native_driver_wide_worlds(dk):
+def test_native_driver_wide_worlds(dk, monkeypatch):
     """World sizes 5 and 8 (the owner-bucket layout's largest: sub-buckets of
-    2048 / 8 = 256 slots, so heavy classes overflow into the fallback) and 9
-    (past it: the staged protocol)."""
+    2048 / 8 = 256 slots, so heavy classes overflow into the fallback; peer
+    mode required) and 9 (past it: the staged protocol)."""
+    monkeypatch.setenv("DFAKIT_SHARD_PEER", "2")
     cases = [("random", 20000, 10, 0.5, 14), ("bigcopies", 40, 8, 0.5, 17), ("copies", 400, 8, 0.5, 15),
              ("family", 12, 0, 0.0, 1), ("synth", 200_000, 10, 0.0, 7)]
     for world in (5, 8, 9):
         for case in cases:
             d, a, want = make_case(case)
             check_hub(run_hub(dk, world, d, a), want, (world, case))
+
+
+def test_cuda_ipc_mapping_two_processes(tmp_path):
+    """The CUDA IPC calls of peer mode between two processes (on the one GPU
+    here; between GPUs the same mapping rides NVLink): a buffer exported by
+    one process is written by a kernel of the other through
+    cudaIpcOpenMemHandle(..., cudaIpcMemLazyEnablePeerAccess)."""
+    import subprocess
+    exe = str(tmp_path / "ipc_check")
+    subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O2", "-o", exe,
+                    os.path.join(ROOT, "tests", "cpp", "ipc_check.cu")], check=True)
+    f = str(tmp_path / "handle")
+    server = subprocess.Popen([exe, "serve", f], stdout=subprocess.PIPE, text=True)
+    writer = subprocess.run([exe, "write", f], capture_output=True, text=True, timeout=180)
+    out, _ = server.communicate(timeout=180)
+    assert writer.returncode == 0 and writer.stdout.startswith("OK"), writer.stdout + writer.stderr
+    assert server.returncode == 0 and out.startswith("OK"), out
