@@ -130,8 +130,9 @@ struct NcclComm {
     virtual ~NcclComm() = default;
     int world = 1, rank = 0;
     PeerSpace peer;
-    // every rank's local[4] pointers, mapped into this process (collective)
-    virtual void exchange_peer_ptrs(cudaStream_t s) = 0;
+    // every rank's local[4] pointers, mapped into this process (collective:
+    // every rank calls it, valid or not; false when any mapping is missing)
+    virtual bool exchange_peer_ptrs(cudaStream_t s, bool valid) = 0;
     virtual void release_peer_ptrs() = 0;
     // stream-ordered barrier: this rank's prior work on s is complete, and
     // work queued on s after it starts only once every rank's prior work is
@@ -168,28 +169,47 @@ struct NcclImpl : NcclComm {
     // CUDA IPC: every rank exports its four buffers, the 64-byte handles
     // travel by one ncclAllGather, and the peers' buffers are opened with
     // lazy peer access (NVLink / NVSwitch stores from this rank's kernels)
-    void exchange_peer_ptrs(cudaStream_t s) override {
-        constexpr size_t H = sizeof(cudaIpcMemHandle_t);
-        std::vector<unsigned char> mine(4 * H), all((size_t)world * 4 * H);
-        for (int i = 0; i < 4; ++i)
-            DK_CUDA(cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(mine.data() + i * H), peer.local[i]));
-        DBuf<unsigned char> dev((size_t)world * 4 * H, s);
-        DK_CUDA(cudaMemcpyAsync(dev.get() + (size_t)rank * 4 * H, mine.data(), 4 * H, cudaMemcpyHostToDevice, s));
-        nccl_check(nccl().AllGather(dev.get() + (size_t)rank * 4 * H, dev.get(), 4 * H, ncclUint8, comm, s),
+    bool exchange_peer_ptrs(cudaStream_t s, bool valid) override {
+        // one extra byte per buffer flags a handle that could not be made
+        constexpr size_t H = sizeof(cudaIpcMemHandle_t), E = H + 1;
+        std::vector<unsigned char> mine(4 * E, 0), all((size_t)world * 4 * E);
+        for (int i = 0; i < 4 && valid && world > 1; ++i) {
+            const cudaError_t e =
+                cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(mine.data() + i * E), peer.local[i]);
+            if (e != cudaSuccess) {
+                cudaGetLastError();
+                valid = false;
+            }
+        }
+        for (int i = 0; i < 4; ++i) mine[i * E + H] = valid ? 1 : 0;
+        DBuf<unsigned char> dev((size_t)world * 4 * E, s);
+        DK_CUDA(cudaMemcpyAsync(dev.get() + (size_t)rank * 4 * E, mine.data(), 4 * E, cudaMemcpyHostToDevice, s));
+        nccl_check(nccl().AllGather(dev.get() + (size_t)rank * 4 * E, dev.get(), 4 * E, ncclUint8, comm, s),
                    "allgather (ipc handles)");
         DK_CUDA(cudaMemcpyAsync(all.data(), dev.get(), all.size(), cudaMemcpyDeviceToHost, s));
         DK_CUDA(cudaStreamSynchronize(s));
         peer.peer.assign(world, {nullptr, nullptr, nullptr, nullptr});
+        bool ok = valid;
         for (int r = 0; r < world; ++r)
             for (int i = 0; i < 4; ++i) {
                 if (r == rank) {
-                    peer.peer[r][i] = peer.local[i];
+                    peer.peer[r][i] = valid ? peer.local[i] : nullptr;
+                    continue;
+                }
+                const unsigned char* rec = all.data() + ((size_t)r * 4 + i) * E;
+                if (!rec[H] || !valid) {
+                    ok = false;
                     continue;
                 }
                 cudaIpcMemHandle_t h;
-                std::memcpy(&h, all.data() + ((size_t)r * 4 + i) * H, H);
-                DK_CUDA(cudaIpcOpenMemHandle(&peer.peer[r][i], h, cudaIpcMemLazyEnablePeerAccess));
+                std::memcpy(&h, rec, H);
+                if (cudaIpcOpenMemHandle(&peer.peer[r][i], h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+                    cudaGetLastError();
+                    peer.peer[r][i] = nullptr;
+                    ok = false;
+                }
             }
+        return ok;
     }
     void release_peer_ptrs() override {
         for (int r = 0; r < (int)peer.peer.size(); ++r)
@@ -246,12 +266,16 @@ struct LocalImpl : NcclComm {
         DK_CUDA(cudaStreamSynchronize(s));
         hub->barrier();
     }
-    void exchange_peer_ptrs(cudaStream_t s) override {
+    bool exchange_peer_ptrs(cudaStream_t s, bool valid) override {
         DK_CUDA(cudaStreamSynchronize(s));
-        for (int i = 0; i < 4; ++i) hub->ptrs[rank][i] = peer.local[i];
+        for (int i = 0; i < 4; ++i) hub->ptrs[rank][i] = valid ? peer.local[i] : nullptr;
         hub->barrier();
         peer.peer = hub->ptrs;
         hub->barrier();
+        bool ok = true;
+        for (const auto& a : peer.peer)
+            for (void* p : a) ok &= p != nullptr;
+        return ok;
     }
     void release_peer_ptrs() override { peer.peer.clear(); }
     void publish(const void* dev, size_t bytes, cudaStream_t s) {
@@ -400,61 +424,68 @@ bool peer_ensure(Ctx* ctx, NcclComm* cm, uint64_t recv_slots, uint64_t cnt_words
     if (p.state > 0 && p.recv_slots >= recv_slots && p.cnt_words >= cnt_words && p.lab_words >= lab_words &&
         p.act_bytes >= act_bytes)
         return true;
+    // every step below is taken by every rank, whatever failed locally, so
+    // the collectives inside line up; the verdict is allreduced at the end
     const int world = cm->world, rank = cm->rank;
-    int ok = 1;
-    try {
-        DK_CUDA(cudaStreamSynchronize(s));
-        if (p.state > 0) cm->barrier(s);  // nobody still writes into the old buffers
-        DK_CUDA(cudaStreamSynchronize(s));
-        cm->release_peer_ptrs();
-        peer_free_local(p);
-        p.device = ctx->device;
-        p.recv_slots = std::max(p.recv_slots, recv_slots);
-        p.cnt_words = std::max(p.cnt_words, cnt_words);
-        p.lab_words = std::max(p.lab_words, std::max<uint64_t>(lab_words, (uint64_t)world));
-        p.act_bytes = std::max(p.act_bytes, act_bytes);
-        DK_CUDA(cudaMalloc(&p.local[0], std::max<uint64_t>(1, p.recv_slots) * sizeof(uint4)));
-        DK_CUDA(cudaMalloc(&p.local[1], std::max<uint64_t>(1, p.cnt_words) * sizeof(uint32_t)));
-        DK_CUDA(cudaMalloc(&p.local[2], p.lab_words * sizeof(uint32_t)));
-        DK_CUDA(cudaMalloc(&p.local[3], std::max<uint64_t>(1, p.act_bytes)));
-        DK_CUDA(cudaMalloc(reinterpret_cast<void**>(&p.sync), sizeof(uint32_t)));
-        DK_CUDA(cudaMemsetAsync(p.sync, 0, sizeof(uint32_t), s));
-        DK_CUDA(cudaMemsetAsync(p.local[2], 0, (size_t)world * sizeof(uint32_t), s));
-        cm->exchange_peer_ptrs(s);
-        if (p.state == 0) {
-            cm->barrier(s);  // every rank's stamp area is zeroed
+    const bool first = p.state == 0;
+    DK_CUDA(cudaStreamSynchronize(s));
+    if (!first) cm->barrier(s);  // nobody still writes into the old buffers
+    DK_CUDA(cudaStreamSynchronize(s));
+    cm->release_peer_ptrs();
+    peer_free_local(p);
+    p.device = ctx->device;
+    p.recv_slots = std::max(p.recv_slots, recv_slots);
+    p.cnt_words = std::max(p.cnt_words, cnt_words);
+    p.lab_words = std::max(p.lab_words, std::max<uint64_t>(lab_words, (uint64_t)world));
+    p.act_bytes = std::max(p.act_bytes, act_bytes);
+    bool ok = true;
+    const size_t bytes[4] = {std::max<uint64_t>(1, p.recv_slots) * sizeof(uint4),
+                             std::max<uint64_t>(1, p.cnt_words) * sizeof(uint32_t), p.lab_words * sizeof(uint32_t),
+                             std::max<uint64_t>(1, p.act_bytes)};
+    for (int i = 0; i < 4 && ok; ++i)
+        if (cudaMalloc(&p.local[i], bytes[i]) != cudaSuccess) {
+            cudaGetLastError();
+            p.local[i] = nullptr;
+            ok = false;
+        }
+    DK_CUDA(cudaMalloc(reinterpret_cast<void**>(&p.sync), sizeof(uint32_t)));
+    DK_CUDA(cudaMemsetAsync(p.sync, 0, sizeof(uint32_t), s));
+    if (ok) DK_CUDA(cudaMemsetAsync(p.local[2], 0, (size_t)world * sizeof(uint32_t), s));
+    ok = cm->exchange_peer_ptrs(s, ok);
+    if (first) {
+        // stamp exchange: every rank writes its id into word `rank` of every
+        // rank's label buffer through the mapping, then checks its own
+        cm->barrier(s);
+        if (ok) {
             PeerLabels pl{};
             for (int r = 0; r < world; ++r) pl.lab[r] = static_cast<uint32_t*>(p.peer[r][2]);
             peer_probe_kernel<<<1, 32, 0, s>>>(pl, world, rank);
-            DK_CUDA(cudaGetLastError());
-            cm->barrier(s);
+            if (cudaGetLastError() != cudaSuccess) ok = false;
+        }
+        cm->barrier(s);
+        if (ok) {
             std::vector<uint32_t> got(world);
             DK_CUDA(cudaMemcpyAsync(got.data(), p.local[2], world * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
             DK_CUDA(cudaStreamSynchronize(s));
             for (int r = 0; r < world; ++r) ok &= got[r] == (0xC0DE0000u | (uint32_t)r);
         }
-    } catch (const Error&) {
-        ok = 0;
-        cudaGetLastError();
     }
-    if (p.state == 0) {
-        // every rank learns whether every rank's mapping works
-        DBuf<uint32_t> v(1, s);
-        const uint32_t mine = (uint32_t)ok;
-        DK_CUDA(cudaMemcpyAsync(v.get(), &mine, 4, cudaMemcpyHostToDevice, s));
-        cm->allreduce_u32(v.get(), 1, true, s);
-        uint32_t all = 0;
-        DK_CUDA(cudaMemcpyAsync(&all, v.get(), 4, cudaMemcpyDeviceToHost, s));
-        DK_CUDA(cudaStreamSynchronize(s));
-        p.state = all ? 1 : -1;
-    } else if (!ok) {
-        throw Error(DFAKIT_E_CUDA, "sharded sort_pr: growing the peer workspace failed");
+    DBuf<uint32_t> v(1, s);
+    const uint32_t mine = ok ? 1u : 0u;
+    DK_CUDA(cudaMemcpyAsync(v.get(), &mine, 4, cudaMemcpyHostToDevice, s));
+    cm->allreduce_u32(v.get(), 1, true, s);
+    uint32_t all = 0;
+    DK_CUDA(cudaMemcpyAsync(&all, v.get(), 4, cudaMemcpyDeviceToHost, s));
+    DK_CUDA(cudaStreamSynchronize(s));
+    if (all) {
+        p.state = 1;
+        return true;
     }
-    if (p.state < 0) {
-        cm->release_peer_ptrs();
-        peer_free_local(p);
-    }
-    return p.state > 0;
+    cm->release_peer_ptrs();
+    peer_free_local(p);
+    if (!first) throw Error(DFAKIT_E_RESOURCE, "sharded sort_pr: growing the peer workspace failed");
+    p.state = -1;
+    return false;
 }
 
 }  // namespace
