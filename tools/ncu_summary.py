@@ -144,6 +144,8 @@ def main():
                           f"{sspr:.2f} | {d['l1_pct'] or 0:.0f} | {d['lts_pct'] or 0:.0f} | {d['l2_hit'] or 0:.1f} | "
                           f"{d['warps'] or 0:.1f} | {int(d['regs'] or 0)} |")
                 s_ = summary.setdefault(d["kernel"], {"launches": 0, "dram_bytes": 0.0, "us": 0.0, "workload": name})
+                if s_["workload"] != name:
+                    continue  # per-launch figures of the first workload that runs the kernel, not a blend
                 s_["launches"] += 1
                 s_["dram_bytes"] += byts
                 s_["us"] += d["dur_us"] or 0
