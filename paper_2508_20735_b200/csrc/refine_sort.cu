@@ -451,6 +451,96 @@ __global__ void __launch_bounds__(kThreads, DFAKIT_SIGB_MINB) sig_part_vec_kerne
     }
 }
 
+// One sweep over every state (identity range), S states per thread, the
+// key kind fixed at compile time: the delta loads of all (up to 16) letters
+// are issued before any label is gathered and every in-slice gather before
+// any term is formed -- one HBM round trip and one L2 round trip per S
+// states (the chunked vec kernel paid both per 4 letters).
+#ifndef DFAKIT_PART_MINB
+#define DFAKIT_PART_MINB 4
+#endif
+template <typename LR, bool FP, int S>
+__global__ void __launch_bounds__(kThreads, DFAKIT_PART_MINB) sig_part_all_kernel(
+    uint64_t m, const uint32_t* __restrict__ delta, uint32_t n, LR lab, SigParams p, uint32_t lo, uint32_t hi,
+    int first, uint64_t* __restrict__ part) {
+    constexpr int C = 16;
+    const uint32_t nl = p.a1 - p.a0;
+    for (uint64_t iS = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; iS * S < m;
+         iS += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t i = iS * S;
+        const uint32_t q = p.q0 + (uint32_t)i;
+        const bool full = i + S <= m;
+        uint64_t acc[S];
+#pragma unroll
+        for (int e = 0; e < S; ++e) acc[e] = 0;
+        if (first)
+#pragma unroll
+            for (int e = 0; e < S; ++e)
+                if (full || i + e < m) {
+                    const uint32_t lead = lab[q + e];
+                    acc[e] = FP ? fp_term(p.salt, 0, lead) : packed_field(lead, p.field_bits * nl);
+                }
+        for (uint32_t a = p.a0; a < p.a1; a += C) {
+            uint32_t t[C][S];
+#pragma unroll
+            for (int j = 0; j < C; ++j)
+                if (a + j < p.a1) {
+                    const uint32_t* row = delta + (uint64_t)(a + j) * n + q;
+                    if (S == 2 && full) {
+                        const uint2 v = __ldcs(reinterpret_cast<const uint2*>(row));
+                        t[j][0] = v.x;
+                        t[j][S - 1] = v.y;
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < S; ++e) t[j][e] = (full || i + e < m) ? __ldcs(row + e) : lo - 1;
+                    }
+                }
+            uint32_t in = 0;  // bit j * S + e: successor in the slice
+#pragma unroll
+            for (int j = 0; j < C; ++j)
+                if (a + j < p.a1)
+#pragma unroll
+                    for (int e = 0; e < S; ++e)
+                        if (t[j][e] - lo < hi - lo) {
+                            in |= 1u << (j * S + e);
+                            t[j][e] = lab[t[j][e]];
+                        }
+#pragma unroll
+            for (int j = 0; j < C; ++j)
+                if (a + j < p.a1) {
+                    const uint32_t r = a + j - p.a0;
+#pragma unroll
+                    for (int e = 0; e < S; ++e)
+                        if ((in >> (j * S + e)) & 1u) {
+                            if (FP) acc[e] += fp_term(p.salt, r + 1, t[j][e]);
+                            else acc[e] |= packed_field(t[j][e], p.field_bits * (nl - 1 - r));
+                        }
+                }
+        }
+        // streaming accesses: the partial keys must not push the slice's labels out of the L2
+        if (S == 2 && full) {
+            ulonglong2* dst = reinterpret_cast<ulonglong2*>(part + i);
+            if (!first) {
+                const ulonglong2 pv = __ldcs(dst);
+                acc[0] = FP ? acc[0] + pv.x : acc[0] | pv.x;
+                acc[S - 1] = FP ? acc[S - 1] + pv.y : acc[S - 1] | pv.y;
+            }
+            __stcs(dst, make_ulonglong2(acc[0], acc[S - 1]));
+        } else {
+#pragma unroll
+            for (int e = 0; e < S; ++e)
+                if (full || i + e < m) {
+                    if (first) {
+                        __stcs(part + i + e, acc[e]);
+                    } else {
+                        const uint64_t prev = __ldcs(part + i + e);
+                        __stcs(part + i + e, FP ? prev + acc[e] : prev | acc[e]);
+                    }
+                }
+        }
+    }
+}
+
 // One sweep of a sliced signature pass: the partial keys of the active
 // states over successors in [lo, hi) (the lead in the first sweep), added
 // into part[] (written by the first sweep).
@@ -1705,10 +1795,25 @@ const uint64_t* sliced_parts(Ctx* ctx, const KeyLab& kl, const uint32_t* list, u
                 (void)cudaGetLastError();
         }
         const bool vec = !list && d.n % 4 == 0 && p.q0 % 4 == 0;
+        // all-letters kernel, one state per thread (1B transitions: 8.87 -> 8.64 ms
+        // for the three sweeps; two states per thread 9.20); DFAKIT_PART_KERNEL=0
+        // selects the chunked four-state kernel
+        static const int part_kernel = getenv("DFAKIT_PART_KERNEL") ? atoi(getenv("DFAKIT_PART_KERNEL")) : 1;
+        const bool all_letters = part_kernel > 0 && !list && d.k <= 16;
         with_lab_type(kl, [&](auto lab) {
+            using LR = decltype(lab);
             // algorithmic HBM bytes: delta rows, the slice's labels, the partial keys
             const double bytes = (double)m * (4.0 * d.k + (j ? 16.0 : 8.0)) + keylab_bytes_per_state(kl) * (hi - lo);
-            if (vec)
+            const bool fp = p.kind != kKeyPacked;
+            if (all_letters) {
+                const unsigned grid = grid_for(m, kThreads, (unsigned)ctx->num_sms * 8u);
+                if (fp)
+                    DK_LAUNCH_BU(ctx, bytes, (double)m * d.k / slices, (sig_part_all_kernel<LR, true, 1>), grid,
+                                 kThreads, 0, s, m, d.delta, d.n, lab, p, lo, hi, j == 0 ? 1 : 0, part.get());
+                else
+                    DK_LAUNCH_BU(ctx, bytes, (double)m * d.k / slices, (sig_part_all_kernel<LR, false, 1>), grid,
+                                 kThreads, 0, s, m, d.delta, d.n, lab, p, lo, hi, j == 0 ? 1 : 0, part.get());
+            } else if (vec)
                 DK_LAUNCH_BU(ctx, bytes, (double)m * d.k / slices, sig_part_vec_kernel,
                              grid_for((m + 3) / 4, kThreads, (unsigned)ctx->num_sms * 5u), kThreads, 0, s, m, d.delta,
                              d.n, lab, p, lo, hi, j == 0 ? 1 : 0, part.get());
