@@ -1755,7 +1755,11 @@ double keylab_bytes_per_state(const KeyLab& kl) { return kl.bytes == kBitLabels 
 // (each L2-resident while its sweep runs), adding partial keys (tuple_part);
 // the bucket kernel then only finishes the keys.  DFAKIT_TEST_SLICE_BYTES
 // overrides the slice size (tests force slicing on small automata).
-constexpr double kSliceBytes = 72.0 * 1024 * 1024;  // 200 MB of labels: 3 slices (2: same time, 4: +10 %)
+// Measured (16-bit labels, 10 letters, no L2 pin): 80 MB unsliced 4.5 ms vs
+// 5.3 in 2 slices; 100 MB 6.6 either way; 120 MB 9.1 vs 8.2; 200 MB 19.1
+// unsliced, 15.3 in 2 slices, 16.3 in 3, 18.9 in 4 -- a sweep re-reads all
+// of delta, so the fewest slices that still mostly hit the L2 win.
+constexpr double kSliceBytes = 100.0 * 1024 * 1024;
 
 uint32_t label_slices(const KeyLab& kl, uint32_t n) {
     double slice = kSliceBytes;
@@ -1770,10 +1774,11 @@ const uint64_t* sliced_parts(Ctx* ctx, const KeyLab& kl, const uint32_t* list, u
     const uint32_t slices = label_slices(kl, d.n);
     if (slices <= 1 || m == 0) return nullptr;
     if (part.n < m) part.alloc(m, s);
-    // the slice of labels a sweep gathers is pinned in the L2 (access-policy
-    // window, persisting) while delta and the partial keys stream past it
-    // (a performance hint only: where the device refuses it, the sweeps run unpinned)
-    bool pin = kl.bytes != kBitLabels && !getenv("DFAKIT_NO_L2_PIN");
+    // DFAKIT_L2_PIN=1: the slice of labels a sweep gathers is pinned in the
+    // L2 (access-policy window, persisting) while delta and the partial keys
+    // stream past it -- off by default: no gain at 72 MB slices (8.64 vs 8.68
+    // ms for 1B transitions), a loss at 100 MB ones (10.6 vs 7.6 ms)
+    bool pin = kl.bytes != kBitLabels && getenv("DFAKIT_L2_PIN") && getenv("DFAKIT_L2_PIN")[0] == '1';
     size_t pin_max = 0;
     if (pin) {
         int v = 0;
