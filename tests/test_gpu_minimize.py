@@ -361,6 +361,12 @@ def test_sliced_signature_passes(dk, oracle, monkeypatch):
     for n0, c, k in ((2000, 50, 8), (20, 6000, 8)):
         t = copies(oracle.gen_random(n0, k, 0.5, n0 * 7 + c), c)
         assert same(dk.sort_pr(mkdfa(dk, t)), oracle.minimize("moore", t[0], t[1])), (n0, c)
+    # more than 16 letters: the chunked sweep kernel instead of the all-letters one
+    for n, k, s in ((9000, 20, 3), (12001, 17, 4)):
+        t = oracle.gen_random(n, k, 0.5, s)
+        want = oracle.minimize("moore", t[0], t[1])
+        for kw in ({}, {"fingerprint_bits": 6}):
+            assert same(dk.sort_pr(mkdfa(dk, t), **kw), want), (n, k, kw)
 
 
 def test_speculative_second_pass(dk, oracle, monkeypatch):
