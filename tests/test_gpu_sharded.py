@@ -258,3 +258,15 @@ def test_cuda_ipc_mapping_two_processes(tmp_path):
     out, _ = server.communicate(timeout=180)
     assert writer.returncode == 0 and writer.stdout.startswith("OK"), writer.stdout + writer.stderr
     assert server.returncode == 0 and out.startswith("OK"), out
+
+
+def test_native_driver_tiny_automata_odd_worlds(dk, monkeypatch):
+    """Peer mode at world sizes 4, 6 and 7 on automata smaller than the world
+    (empty shards on some ranks) and on a few small odd shapes."""
+    monkeypatch.setenv("DFAKIT_SHARD_PEER", "2")
+    cases = [("random", 1, 1, 1.0, 21), ("random", 3, 2, 0.5, 22), ("random", 50, 3, 0.5, 23),
+             ("copies", 5, 2, 0.5, 24), ("random", 3001, 7, 0.7, 25)]
+    for world in (4, 6, 7):
+        for case in cases:
+            d, a, want = make_case(case)
+            check_hub(run_hub(dk, world, d, a), want, (world, case))
