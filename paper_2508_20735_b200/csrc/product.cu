@@ -107,18 +107,33 @@ __device__ uint32_t tile_find_or_insert(cg::thread_block_tile<kTile> tile, bool 
     return mine;
 }
 
+// Records into a fresh table, discovered before any current wave.  Primary
+// mode (pb_of): a record takes its first state's primary slot when free (the
+// initial pair) or already holds it (keeps its discoverer); the others go
+// back into the (grown) hash table, counted as its reservations.
 __global__ void reinsert_kernel(const unsigned long long* __restrict__ keys, uint64_t count, Slot* __restrict__ table,
-                                uint64_t mask) {
+                                uint64_t mask, uint32_t* __restrict__ pb_of, unsigned long long* __restrict__ disc_of,
+                                unsigned long long* __restrict__ hkeys) {
     auto tile = cg::tiled_partition<kTile>(cg::this_thread_block());
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     const uint64_t first = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     const uint64_t trips = (count + stride - 1) / stride;
     for (uint64_t it = 0; it < trips; ++it) {
         const uint64_t t = first + it * stride;
-        const bool valid = t < count;
-        const unsigned long long key = valid ? keys[t] : 0ull;
+        const unsigned long long key = t < count ? keys[t] : 0ull;
+        bool valid = t < count;
+        if (valid && pb_of) {
+            const uint32_t pa = (uint32_t)(key >> 32), pb = (uint32_t)key;
+            uint32_t e = pb_of[pa];
+            if (e == kNone) e = atomicCAS(pb_of + pa, kNone, pb);
+            if (e == kNone) disc_of[pa] = 0ull;
+            valid = e != kNone && e != pb;
+        }
         const uint32_t s = tile_find_or_insert(tile, valid, key, table, mask);
-        if (valid) table[s].disc = 0ull;  // discovered before any current wave
+        if (valid) {
+            table[s].disc = 0ull;
+            if (hkeys) atomicAdd(hkeys, 1ull);
+        }
     }
 }
 
@@ -185,8 +200,10 @@ struct BfsState {
     unsigned long long first_fail_all;  // FULL mode: first failing record (~0 if none)
     uint32_t levels, status;
     uint32_t fail_rec;                  // failing record (kBfsFail)
-    uint32_t pad;
+    uint32_t need_grow;                 // primary mode: a hash-table insertion found no room (level re-run)
     uint32_t fail[3];                   // per level (mod 3): first failing emit position
+    uint32_t pad;
+    unsigned long long hkeys;           // primary mode: hash-table reservations (>= keys in it)
 };
 
 struct BfsArgs {
@@ -205,14 +222,47 @@ struct BfsArgs {
     int mode;
     uint64_t max_visited;
     BfsState* st;
+    // primary mode: pair (pa, pb) lives in slot pa of a direct-mapped table
+    // (pb_of / disc_of, L2-sized) unless another pb holds it -- then in the
+    // hash table, whose insertions reserve room first
+    uint32_t* pb_of;
+    unsigned long long* disc_of;
 };
 
-__device__ __forceinline__ bool item_wins(const Slot* __restrict__ table, const uint32_t* __restrict__ item_slot,
-                                          uint64_t wb, uint64_t t, uint32_t k) {
-    const uint32_t s = item_slot[t];
+constexpr uint32_t kPrim = 0x80000000u;  // item slot: primary slot pa (pa < 2^31)
+
+__device__ __forceinline__ unsigned long long* disc_at(const BfsArgs& A, uint32_t sl) {
+    return (sl & kPrim) ? A.disc_of + (sl & ~kPrim) : &A.table[sl].disc;
+}
+
+// find-or-insert of every lane's pair: its primary slot when free or its
+// own, else the hash table (all lanes of the tile call; a lane whose hash
+// insertion finds no reserved room gets kNone and flags the level for a re-run)
+__device__ __forceinline__ uint32_t pair_find_or_insert(cg::thread_block_tile<kTile> tile, bool valid,
+                                                        unsigned long long key, const BfsArgs& A, uint64_t mask) {
+    bool hash = valid;
+    uint32_t mine = kNone;
+    if (valid && A.pb_of) {
+        const uint32_t pa = (uint32_t)(key >> 32), pb = (uint32_t)key;
+        uint32_t e = __ldcg(A.pb_of + pa);
+        if (e == kNone) e = atomicCAS(A.pb_of + pa, kNone, pb);
+        if (e == kNone || e == pb) {
+            mine = kPrim | pa;
+            hash = false;
+        } else if (atomicAdd(&A.st->hkeys, 1ull) >= A.cap / 2) {
+            atomicExch(&A.st->need_grow, 1u);
+            hash = false;
+        }
+    }
+    const uint32_t h = tile_find_or_insert(tile, hash, key, A.table, mask);
+    return hash ? h : mine;
+}
+
+__device__ __forceinline__ bool item_wins(const BfsArgs& A, uint64_t wb, uint64_t t, uint32_t k) {
+    const uint32_t s = A.item_slot[t];
     if (s == kNone) return false;
     const unsigned long long disc = ((unsigned long long)(wb + t / k + 1) << 32) | (uint32_t)(t % k);
-    return __ldcg(&table[s].disc) == disc;
+    return __ldcg(disc_at(A, s)) == disc;
 }
 
 // Levels of at most kSoloItems (frontier records x letters) run on CTA 0
@@ -243,7 +293,7 @@ __device__ void solo_levels(const BfsArgs& A, SoloOut& o) {
     while (wb < we) {
         const uint64_t items = (we - wb) * A.k;
         if (items > kSoloItems) break;  // back to the whole grid
-        if (items > A.item_cap || we + items > A.rec_cap || 2 * (we + items) + 64 > A.cap) {
+        if (items > A.item_cap || we + items > A.rec_cap || (!A.pb_of && 2 * (we + items) + 64 > A.cap)) {
             status = kBfsGrow;
             break;
         }
@@ -261,20 +311,26 @@ __device__ void solo_levels(const BfsArgs& A, SoloOut& o) {
                 key = ((unsigned long long)pa << 32) | pb;
                 disc = ((unsigned long long)(i + 1) << 32) | la;
             }
-            const uint32_t sl = tile_find_or_insert(tile, valid, key, A.table, mask);
-            if (valid) {
-                const unsigned long long old = atomicMin(&A.table[sl].disc, disc);
+            const uint32_t sl = pair_find_or_insert(tile, valid, key, A, mask);
+            if (valid && sl != kNone) {
+                const unsigned long long old = atomicMin(disc_at(A, sl), disc);
                 // a candidate winner only if the slot is new this level AND no
-                // smaller discoverer got there first (a loser needs no re-check)
-                A.item_slot[t] = (old >= ((unsigned long long)(wb + 1) << 32) && old > disc) ? sl : kNone;
+                // smaller discoverer got there first (a loser needs no re-check;
+                // old == disc: this item's own discoverer from an aborted run
+                // of the level -- the level is re-run after the table grows)
+                A.item_slot[t] = (old >= ((unsigned long long)(wb + 1) << 32) && old >= disc) ? sl : kNone;
                 A.item_key[t] = key;
             }
         }
         __syncthreads();
+        if (A.pb_of && *(volatile uint32_t*)&A.st->need_grow) {  // re-run this level once the hash table grew
+            status = kBfsGrow;
+            break;
+        }
         uint32_t run = 0;
         for (uint64_t base = 0; base < items; base += blockDim.x) {
             const uint64_t t = base + threadIdx.x;
-            const bool win = t < items && item_wins(A.table, A.item_slot, wb, t, A.k);
+            const bool win = t < items && item_wins(A, wb, t, A.k);
             uint32_t tot;
             const uint32_t e = block_exclusive_scan<kThreads>(win ? 1u : 0u, &tot, ws);
             if (win) {
@@ -368,7 +424,7 @@ __global__ void __launch_bounds__(kThreads) bfs_persistent_kernel(BfsArgs A) {
             }
             continue;
         }
-        if (items > A.item_cap || we + items > A.rec_cap || 2 * (we + items) + 64 > A.cap) {
+        if (items > A.item_cap || we + items > A.rec_cap || (!A.pb_of && 2 * (we + items) + 64 > A.cap)) {
             status = kBfsGrow;
             break;
         }
@@ -394,22 +450,33 @@ __global__ void __launch_bounds__(kThreads) bfs_persistent_kernel(BfsArgs A) {
                 key = ((unsigned long long)pa << 32) | pb;
                 disc = ((unsigned long long)(i + 1) << 32) | la;
             }
-            const uint32_t sl = tile_find_or_insert(tile, valid, key, A.table, mask);
-            if (valid) {
-                const unsigned long long old = atomicMin(&A.table[sl].disc, disc);
+            const uint32_t sl = pair_find_or_insert(tile, valid, key, A, mask);
+            if (valid && sl != kNone) {
+                const unsigned long long old = atomicMin(disc_at(A, sl), disc);
                 // a candidate winner only if the slot is new this level AND no
-                // smaller discoverer got there first (a loser needs no re-check)
-                A.item_slot[t] = (old >= ((unsigned long long)(wb + 1) << 32) && old > disc) ? sl : kNone;
+                // smaller discoverer got there first (a loser needs no re-check;
+                // old == disc only on a re-run of the level, see solo_levels)
+                A.item_slot[t] = (old >= ((unsigned long long)(wb + 1) << 32) && old >= disc) ? sl : kNone;
                 A.item_key[t] = key;
             }
         }
         grid.sync();
+        if (A.pb_of) {  // some insertion found no room: grow the hash table and re-run the level
+            if (threadIdx.x == 0) red[0] = *(volatile uint32_t*)&A.st->need_grow;
+            __syncthreads();
+            const uint32_t ng = red[0];
+            __syncthreads();
+            if (ng) {
+                status = kBfsGrow;
+                break;
+            }
+        }
         // winner counts per contiguous chunk
         const uint64_t chunk = (items + gridDim.x - 1) / gridDim.x;
         const uint64_t c0 = min(items, blockIdx.x * chunk), c1 = min(items, c0 + chunk);
         uint32_t c = 0;
         for (uint64_t t = c0 + threadIdx.x; t < c1; t += blockDim.x) {
-            const bool w = item_wins(A.table, A.item_slot, wb, t, A.k);
+            const bool w = item_wins(A, wb, t, A.k);
             A.item_win[t] = w;
             c += w;
         }
@@ -672,28 +739,53 @@ ProductOut explore_product_device(Ctx* ctx, const DevDfa& a, const DevDfa& b, in
         min_slots = 1ull << std::min(30, std::max(4, atoi(t)));
         tiny = true;
     }
+    // primary mode (first automaton below 2^31 states; DFAKIT_BFS_NO_PRIMARY=1
+    // turns it off): pair (pa, pb) is kept in slot pa of a direct-mapped
+    // table -- pb and the discoverer, 12 B per state of A, sized for the L2
+    // rather than 16-byte slots for max(nA, nB) pairs at load 1/2 -- unless
+    // another pb already holds slot pa; only those pairs go to the hash
+    // table, which then starts small and grows (x4) when its reservations
+    // run out, re-running the level that ran out
+    const bool prim = a.n < 0x80000000u && !getenv("DFAKIT_BFS_NO_PRIMARY");
+    DBuf<uint32_t> pb_of;
+    DBuf<unsigned long long> disc_of;
+    if (prim) {
+        pb_of.alloc(std::max<uint64_t>(1, a.n), s);
+        disc_of.alloc(std::max<uint64_t>(1, a.n), s);
+        DK_CUDA(cudaMemsetAsync(pb_of.get(), 0xff, (size_t)a.n * 4, s));
+        DK_CUDA(cudaMemsetAsync(disc_of.get(), 0xff, (size_t)a.n * 8, s));
+    }
+    const uint64_t pairs_guess = tiny ? 0 : std::min<uint64_t>(max_visited, std::max(a.n, b.n)) + 64;
     for (;;) {
         // room for the next level: table at load <= 1/2; the record store and
         // the item buffers are sized with the table (cap / 2 each), so the
         // kernel comes back only when the table must grow (4x from 2^20)
         const uint64_t items = (we - wb) * k;
-        const uint64_t need = next_pow2(2 * (we + items) + 64);
+        const uint64_t need = prim ? (hs.need_grow ? cap * 4 : (cap ? cap : min_slots))
+                                   : next_pow2(2 * (we + items) + 64);
         if (need > cap) {
             // first allocation sized for max(nA, nB) pairs at load 1/2 (the
             // usual size of an equivalence product; bounded by the visited
             // budget), so most explorations run in one launch without
             // re-insertion, and the table initialisation stays small
-            const uint64_t guess =
-                tiny ? 0 : next_pow2(2 * std::min<uint64_t>(max_visited, std::max(a.n, b.n)) + 64);
+            const uint64_t guess = tiny || prim ? 0 : next_pow2(2 * pairs_guess);
             const uint64_t nc = cap ? std::max<uint64_t>(need, cap * 4)
                                     : std::max<uint64_t>(need, std::max<uint64_t>(min_slots, guess));
             table.alloc(nc, s);
             cap = nc;
             DK_CUDA(cudaMemsetAsync(table.get(), 0xff, cap * sizeof(Slot), s));
-            DK_LAUNCH(ctx, reinsert_kernel, grid_for(we), kThreads, 0, s, rs.key.get(), we, table.get(), cap - 1);
+            if (prim) {  // reservations restart from the records actually in the hash table
+                DK_CUDA(cudaMemsetAsync(&dst.get()->hkeys, 0, sizeof(unsigned long long), s));
+                DK_CUDA(cudaMemsetAsync(&dst.get()->need_grow, 0, sizeof(uint32_t), s));
+                hs.need_grow = 0;
+            }
+            DK_LAUNCH(ctx, reinsert_kernel, grid_for(we), kThreads, 0, s, rs.key.get(), we, table.get(), cap - 1,
+                      prim ? pb_of.get() : nullptr, prim ? disc_of.get() : nullptr,
+                      prim ? &dst.get()->hkeys : nullptr);
         }
-        rs.ensure(std::max<uint64_t>(cap / 2, we + items), we, s);
-        const uint64_t icap = std::max<uint64_t>(cap / 2, items);
+        const uint64_t base_cap = prim ? pairs_guess : cap / 2;
+        rs.ensure(std::max<uint64_t>(base_cap, we + items), we, s);
+        const uint64_t icap = std::max<uint64_t>(base_cap, items);
         if (icap > item_slot.n) {
             item_slot.alloc(icap, s);
             item_win.alloc(icap, s);
@@ -701,7 +793,8 @@ ProductOut explore_product_device(Ctx* ctx, const DevDfa& a, const DevDfa& b, in
         }
         BfsArgs A{rs.view(), rs.cap, table.get(), cap, item_slot.get(), item_win.get(), item_key.get(), item_slot.n,
                   cta_cnt.get(), a.delta, b.delta,
-                  to_b.get(), a.n, b.n, k, a.acc, b.acc, mode, max_visited, dst.get()};
+                  to_b.get(), a.n, b.n, k, a.acc, b.acc, mode, max_visited, dst.get(),
+                  prim ? pb_of.get() : nullptr, prim ? disc_of.get() : nullptr};
         void* args[] = {(void*)&A};
         prof_begin_launch(ctx, s);
         DK_CUDA(cudaLaunchCooperativeKernel((const void*)bfs_persistent_kernel, grid_n, kThreads, args, 0, s));

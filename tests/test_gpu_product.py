@@ -55,21 +55,28 @@ def test_random_products_vs_oracle(dk, oracle):
             assert accepts(A, u.counterexample) != accepts(B, u.counterexample)
 
 
-def test_products_through_table_collisions(dk, oracle, monkeypatch):
-    """A 64-slot first table (test hook): explorations run at load up to 1/2,
-    so keys collide on their home slots and go through the tile-cooperative
-    windows, and the table grows and re-inserts the records; results must
-    not change."""
+@pytest.mark.parametrize("table", ["hash", "primary"])
+def test_products_through_table_collisions(dk, oracle, monkeypatch, table):
+    """A 64-slot first hash table (test hook): explorations run at load up to
+    1/2, so keys collide on their home slots and go through the
+    tile-cooperative windows, and the table grows and re-inserts the
+    records; results must not change.  `hash`: every pair in the hash table
+    (the primary table off); `primary` (the default): pairs whose first
+    state's direct-mapped slot is taken go to the hash table, whose
+    reservations run out mid-level -- the table grows and the level re-runs."""
+    if table == "hash":
+        monkeypatch.setenv("DFAKIT_BFS_NO_PRIMARY", "1")
     ctx = dk.default_context()
     A = oracle.gen_random(3000, 2, 0.5, 1)
-    da = mkdfa(dk, A)
+    B = A if table == "hash" else oracle.gen_random(2500, 2, 0.5, 2)
+    da, db = mkdfa(dk, A), mkdfa(dk, B)
     l0 = ctx.kernel_launches
-    dk.explore_product(da, da, dk.ExploreMode["full"])
+    dk.explore_product(da, db, dk.ExploreMode["full"])
     plain = ctx.kernel_launches - l0
     monkeypatch.setenv("DFAKIT_TEST_TABLE_LOG2", "6")
     l0 = ctx.kernel_launches
-    r = dk.explore_product(da, da, dk.ExploreMode["full"])
-    assert same(r, oracle.explore("full", A, A))
+    r = dk.explore_product(da, db, dk.ExploreMode["full"])
+    assert same(r, oracle.explore("full", A, B))
     assert ctx.kernel_launches - l0 > plain + 2  # the 64-slot table grew: re-insertions, relaunches
     g = random.Random(77)
     for i in range(40):
