@@ -41,6 +41,13 @@ struct Slot {
     unsigned long long disc;
 };
 
+// primary slot of first-automaton state pa: the pair's second state and its
+// discoverer in one 16-byte record (one sector per pair, not two)
+struct PrimSlot {
+    uint32_t pb, pad;
+    unsigned long long disc;
+};
+
 struct Rec {
     unsigned long long* key;
     uint32_t* parent;
@@ -108,12 +115,11 @@ __device__ uint32_t tile_find_or_insert(cg::thread_block_tile<kTile> tile, bool 
 }
 
 // Records into a fresh table, discovered before any current wave.  Primary
-// mode (pb_of): a record takes its first state's primary slot when free (the
+// mode (prim): a record takes its first state's primary slot when free (the
 // initial pair) or already holds it (keeps its discoverer); the others go
 // back into the (grown) hash table, counted as its reservations.
 __global__ void reinsert_kernel(const unsigned long long* __restrict__ keys, uint64_t count, Slot* __restrict__ table,
-                                uint64_t mask, uint32_t* __restrict__ pb_of, unsigned long long* __restrict__ disc_of,
-                                unsigned long long* __restrict__ hkeys) {
+                                uint64_t mask, PrimSlot* __restrict__ prim, unsigned long long* __restrict__ hkeys) {
     auto tile = cg::tiled_partition<kTile>(cg::this_thread_block());
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     const uint64_t first = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
@@ -122,11 +128,11 @@ __global__ void reinsert_kernel(const unsigned long long* __restrict__ keys, uin
         const uint64_t t = first + it * stride;
         const unsigned long long key = t < count ? keys[t] : 0ull;
         bool valid = t < count;
-        if (valid && pb_of) {
+        if (valid && prim) {
             const uint32_t pa = (uint32_t)(key >> 32), pb = (uint32_t)key;
-            uint32_t e = pb_of[pa];
-            if (e == kNone) e = atomicCAS(pb_of + pa, kNone, pb);
-            if (e == kNone) disc_of[pa] = 0ull;
+            uint32_t e = prim[pa].pb;
+            if (e == kNone) e = atomicCAS(&prim[pa].pb, kNone, pb);
+            if (e == kNone) prim[pa].disc = 0ull;
             valid = e != kNone && e != pb;
         }
         const uint32_t s = tile_find_or_insert(tile, valid, key, table, mask);
@@ -223,16 +229,15 @@ struct BfsArgs {
     uint64_t max_visited;
     BfsState* st;
     // primary mode: pair (pa, pb) lives in slot pa of a direct-mapped table
-    // (pb_of / disc_of, L2-sized) unless another pb holds it -- then in the
+    // (prim: {pb, discoverer} per state of A) unless another pb holds it -- then in the
     // hash table, whose insertions reserve room first
-    uint32_t* pb_of;
-    unsigned long long* disc_of;
+    PrimSlot* prim;
 };
 
 constexpr uint32_t kPrim = 0x80000000u;  // item slot: primary slot pa (pa < 2^31)
 
 __device__ __forceinline__ unsigned long long* disc_at(const BfsArgs& A, uint32_t sl) {
-    return (sl & kPrim) ? A.disc_of + (sl & ~kPrim) : &A.table[sl].disc;
+    return (sl & kPrim) ? &A.prim[sl & ~kPrim].disc : &A.table[sl].disc;
 }
 
 // find-or-insert of every lane's pair: its primary slot when free or its
@@ -242,10 +247,10 @@ __device__ __forceinline__ uint32_t pair_find_or_insert(cg::thread_block_tile<kT
                                                         unsigned long long key, const BfsArgs& A, uint64_t mask) {
     bool hash = valid;
     uint32_t mine = kNone;
-    if (valid && A.pb_of) {
+    if (valid && A.prim) {
         const uint32_t pa = (uint32_t)(key >> 32), pb = (uint32_t)key;
-        uint32_t e = __ldcg(A.pb_of + pa);
-        if (e == kNone) e = atomicCAS(A.pb_of + pa, kNone, pb);
+        uint32_t e = __ldcg(&A.prim[pa].pb);
+        if (e == kNone) e = atomicCAS(&A.prim[pa].pb, kNone, pb);
         if (e == kNone || e == pb) {
             mine = kPrim | pa;
             hash = false;
@@ -293,7 +298,7 @@ __device__ void solo_levels(const BfsArgs& A, SoloOut& o) {
     while (wb < we) {
         const uint64_t items = (we - wb) * A.k;
         if (items > kSoloItems) break;  // back to the whole grid
-        if (items > A.item_cap || we + items > A.rec_cap || (!A.pb_of && 2 * (we + items) + 64 > A.cap)) {
+        if (items > A.item_cap || we + items > A.rec_cap || (!A.prim && 2 * (we + items) + 64 > A.cap)) {
             status = kBfsGrow;
             break;
         }
@@ -323,7 +328,7 @@ __device__ void solo_levels(const BfsArgs& A, SoloOut& o) {
             }
         }
         __syncthreads();
-        if (A.pb_of && *(volatile uint32_t*)&A.st->need_grow) {  // re-run this level once the hash table grew
+        if (A.prim && *(volatile uint32_t*)&A.st->need_grow) {  // re-run this level once the hash table grew
             status = kBfsGrow;
             break;
         }
@@ -424,7 +429,7 @@ __global__ void __launch_bounds__(kThreads) bfs_persistent_kernel(BfsArgs A) {
             }
             continue;
         }
-        if (items > A.item_cap || we + items > A.rec_cap || (!A.pb_of && 2 * (we + items) + 64 > A.cap)) {
+        if (items > A.item_cap || we + items > A.rec_cap || (!A.prim && 2 * (we + items) + 64 > A.cap)) {
             status = kBfsGrow;
             break;
         }
@@ -461,7 +466,7 @@ __global__ void __launch_bounds__(kThreads) bfs_persistent_kernel(BfsArgs A) {
             }
         }
         grid.sync();
-        if (A.pb_of) {  // some insertion found no room: grow the hash table and re-run the level
+        if (A.prim) {  // some insertion found no room: grow the hash table and re-run the level
             if (threadIdx.x == 0) red[0] = *(volatile uint32_t*)&A.st->need_grow;
             __syncthreads();
             const uint32_t ng = red[0];
@@ -741,19 +746,16 @@ ProductOut explore_product_device(Ctx* ctx, const DevDfa& a, const DevDfa& b, in
     }
     // primary mode (first automaton below 2^31 states; DFAKIT_BFS_NO_PRIMARY=1
     // turns it off): pair (pa, pb) is kept in slot pa of a direct-mapped
-    // table -- pb and the discoverer, 12 B per state of A, sized for the L2
+    // table -- pb and the discoverer, 16 B per state of A, nearer the L2's size
     // rather than 16-byte slots for max(nA, nB) pairs at load 1/2 -- unless
     // another pb already holds slot pa; only those pairs go to the hash
     // table, which then starts small and grows (x4) when its reservations
     // run out, re-running the level that ran out
     const bool prim = a.n < 0x80000000u && !getenv("DFAKIT_BFS_NO_PRIMARY");
-    DBuf<uint32_t> pb_of;
-    DBuf<unsigned long long> disc_of;
+    DBuf<PrimSlot> prim_tab;
     if (prim) {
-        pb_of.alloc(std::max<uint64_t>(1, a.n), s);
-        disc_of.alloc(std::max<uint64_t>(1, a.n), s);
-        DK_CUDA(cudaMemsetAsync(pb_of.get(), 0xff, (size_t)a.n * 4, s));
-        DK_CUDA(cudaMemsetAsync(disc_of.get(), 0xff, (size_t)a.n * 8, s));
+        prim_tab.alloc(std::max<uint64_t>(1, a.n), s);
+        DK_CUDA(cudaMemsetAsync(prim_tab.get(), 0xff, (size_t)a.n * sizeof(PrimSlot), s));
     }
     const uint64_t pairs_guess = tiny ? 0 : std::min<uint64_t>(max_visited, std::max(a.n, b.n)) + 64;
     for (;;) {
@@ -780,8 +782,7 @@ ProductOut explore_product_device(Ctx* ctx, const DevDfa& a, const DevDfa& b, in
                 hs.need_grow = 0;
             }
             DK_LAUNCH(ctx, reinsert_kernel, grid_for(we), kThreads, 0, s, rs.key.get(), we, table.get(), cap - 1,
-                      prim ? pb_of.get() : nullptr, prim ? disc_of.get() : nullptr,
-                      prim ? &dst.get()->hkeys : nullptr);
+                      prim ? prim_tab.get() : nullptr, prim ? &dst.get()->hkeys : nullptr);
         }
         const uint64_t base_cap = prim ? pairs_guess : cap / 2;
         rs.ensure(std::max<uint64_t>(base_cap, we + items), we, s);
@@ -794,7 +795,7 @@ ProductOut explore_product_device(Ctx* ctx, const DevDfa& a, const DevDfa& b, in
         BfsArgs A{rs.view(), rs.cap, table.get(), cap, item_slot.get(), item_win.get(), item_key.get(), item_slot.n,
                   cta_cnt.get(), a.delta, b.delta,
                   to_b.get(), a.n, b.n, k, a.acc, b.acc, mode, max_visited, dst.get(),
-                  prim ? pb_of.get() : nullptr, prim ? disc_of.get() : nullptr};
+                  prim ? prim_tab.get() : nullptr};
         void* args[] = {(void*)&A};
         prof_begin_launch(ctx, s);
         DK_CUDA(cudaLaunchCooperativeKernel((const void*)bfs_persistent_kernel, grid_n, kThreads, args, 0, s));
