@@ -380,7 +380,22 @@ __device__ void solo_levels(const BfsArgs& A, SoloOut& o) {
     o.status = status;
 }
 
+// the initial pair (record 0) fails the check: a counterexample at once
+// (the empty word, one explored pair), or -- FULL mode -- the first failure
+__global__ void bfs_init_kernel(const uint8_t* __restrict__ acc_a, const uint8_t* __restrict__ acc_b, uint32_t ia,
+                                uint32_t ib, int mode, BfsState* st) {
+    const bool fa = acc_a[ia] != 0, fb = acc_b[ib] != 0;
+    if (!(mode == DFAKIT_MODE_INCLUSION ? (fa && !fb) : (fa != fb))) return;
+    if (mode == DFAKIT_MODE_FULL) {
+        st->first_fail_all = 0;
+    } else {
+        st->status = kBfsFail;
+        st->fail_rec = 0;
+    }
+}
+
 __global__ void __launch_bounds__(kThreads) bfs_persistent_kernel(BfsArgs A) {
+    if (*(volatile uint32_t*)&A.st->status == kBfsFail) return;  // decided by bfs_init_kernel (uniform)
     cg::grid_group grid = cg::this_grid();
     auto tile = cg::tiled_partition<kTile>(cg::this_thread_block());
     __shared__ uint32_t ws[kThreads / 32];
@@ -685,26 +700,17 @@ ProductOut explore_product_device(Ctx* ctx, const DevDfa& a, const DevDfa& b, in
     const uint32_t k = a.k;
     if (max_visited > 0xfffffffeull) max_visited = 0xfffffffeull;  // record indices are 32-bit
     ProductOut out;
-    std::vector<uint8_t> acc0(2);
-    DK_CUDA(cudaMemcpyAsync(&acc0[0], a.acc + a.initial, 1, cudaMemcpyDeviceToHost, s));
-    DK_CUDA(cudaMemcpyAsync(&acc0[1], b.acc + b.initial, 1, cudaMemcpyDeviceToHost, s));
-    DK_CUDA(cudaStreamSynchronize(s));
     if (max_visited == 0) throw Error(DFAKIT_E_RESOURCE, "product exploration exceeded the visited-set budget of 0 pairs");
-    const bool fa = acc0[0], fb = acc0[1];
-    const bool init_fails = mode == DFAKIT_MODE_INCLUSION ? (fa && !fb) : (fa != fb);
-    if (init_fails && mode != DFAKIT_MODE_FULL) {
-        out.verdict = DFAKIT_COUNTEREXAMPLE;
-        out.explored = 1;
-        return out;
-    }
-    uint64_t first_fail_all = init_fails ? 0 : ~0ull;
+    // the initial pair's check runs on the device (bfs_init_kernel) ahead of
+    // the exploration: no host round trip before the first launch
+    uint64_t first_fail_all = ~0ull;
 
     DBuf<uint32_t> to_b(k ? k : 1, s);
     {
         std::vector<uint32_t> m(k);
         for (uint32_t i = 0; i < k; ++i) m[i] = letter_map ? letter_map[i] : i;
+        // (pageable source: the copy is staged before the call returns)
         if (k) DK_CUDA(cudaMemcpyAsync(to_b.get(), m.data(), k * 4ull, cudaMemcpyHostToDevice, s));
-        DK_CUDA(cudaStreamSynchronize(s));
     }
     RecStore rs;
     rs.ensure(1024, 0, s);
@@ -731,6 +737,8 @@ ProductOut explore_product_device(Ctx* ctx, const DevDfa& a, const DevDfa& b, in
     hs.status = kBfsRunning;
     hs.fail[0] = hs.fail[1] = hs.fail[2] = kNone;
     DK_CUDA(cudaMemcpyAsync(dst.get(), &hs, sizeof(hs), cudaMemcpyHostToDevice, s));
+    DK_LAUNCH(ctx, bfs_init_kernel, 1, 1, 0, s, a.acc, b.acc, (uint32_t)a.initial, (uint32_t)b.initial, mode,
+              dst.get());
     uint64_t wb = 0, we = 1;
     DBuf<uint8_t> item_win;
     DBuf<unsigned long long> item_key;
