@@ -54,6 +54,8 @@ def main():
     torch.cuda.synchronize()
     view = nat.CDfa(n, k, delta.data_ptr(), accd.data_ptr(), 0)
     algo = a.algo or {"chain": "trans_pr", "naive": "naive_pr"}.get(w, "sort_pr")
+    if algo == "uf":
+        algo = "sort_pr"  # (report label only; the equiv workload reads a.algo)
 
     def run():
         rep = nat.CReport()
@@ -106,6 +108,10 @@ def main():
         def run():  # noqa: F811
             r = nat.CProduct()
             cex = (C.c_uint32 * 4096)()
+            if a.algo == "uf":  # union-find Hopcroft-Karp
+                nat.check(nat.lib.dfakit_check_equiv_uf_device(ctx.handle, C.byref(view), C.byref(v2), cex, 4096,
+                                                               C.byref(r), ctx.stream))
+                return r
             nat.check(nat.lib.dfakit_explore_product_device(ctx.handle, C.byref(view), C.byref(v2), 0, None,
                                                             1 << 40, cex, 4096, C.byref(r), ctx.stream))
             return r
