@@ -584,8 +584,19 @@ __global__ void __launch_bounds__(kThreads) signature_kernel(const uint32_t* __r
 
 // step 1: signature + table of (run minimum, run size), in shared memory
 // when <= 13 bits; equal keys of a warp are combined first (match_any).
+// 1024-thread CTAs, two per SM (32 registers, no spills): 0.400 -> 0.387 ms
+// on the bench pass, 3.92 -> 3.80 ms at 1B (512 x 3 / 4, 256 x 6, 768 x 2,
+// 1024 x 1 measured: 0.393 -- 0.408 ms)
+#ifndef DFAKIT_SIGT_THREADS
+#define DFAKIT_SIGT_THREADS 1024
+#endif
+#ifndef DFAKIT_SIGT_MINB
+#define DFAKIT_SIGT_MINB 2
+#endif
+constexpr int kSigtThreads = DFAKIT_SIGT_THREADS;
+constexpr int kSigtCtas = DFAKIT_SIGT_MINB;
 template <typename LR, bool CLAMP = false>
-__global__ void __launch_bounds__(512, 3) sig_table_kernel(const uint32_t* __restrict__ list, uint64_t m,
+__global__ void __launch_bounds__(kSigtThreads, kSigtCtas) sig_table_kernel(const uint32_t* __restrict__ list, uint64_t m,
                                                         const uint32_t* __restrict__ delta, uint32_t n,
                                                         LR lab, SigParams p, uint32_t nbits,
                                                         uint32_t* __restrict__ keys32, uint32_t* __restrict__ tmin,
@@ -2500,7 +2511,8 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
                               !streamed;
             uint16_t* keys16 = lazy ? w.next16.get() : nullptr;
             auto sig_table = [&](uint32_t q0, uint64_t mm, bool clamp) {
-                const unsigned tg = (unsigned)std::min<uint64_t>((mm + 511) / 512, (uint64_t)ctx->num_sms * 3);
+                const unsigned tg = (unsigned)std::min<uint64_t>((mm + kSigtThreads - 1) / kSigtThreads,
+                                                                 (uint64_t)ctx->num_sms * kSigtCtas);
                 SigParams pc = p;
                 pc.q0 = q0;
                 with_lab_type(kl, [&](auto lab) {
@@ -2512,11 +2524,11 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
                         DK_CUDA(cudaFuncSetAttribute(sig_table_clamped_kernel,
                                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                      (int)(2u << kSmemTableBits) * 4));
-                        DK_LAUNCH_BU(ctx, bytes, (double)mm * k, sig_table_clamped_kernel, tg, 512, smem, s, list,
+                        DK_LAUNCH_BU(ctx, bytes, (double)mm * k, sig_table_clamped_kernel, tg, kSigtThreads, smem, s, list,
                                      mm, d.delta, n, lab, pc, nbits, w.heads.get() + q0, w.tmin.get(), w.tcnt.get(),
                                      inc, keys16 ? keys16 + q0 : nullptr);
                     } else {
-                        DK_LAUNCH_BU(ctx, bytes, (double)mm * k, sig_table_kernel<LR>, tg, 512, smem, s, list, mm,
+                        DK_LAUNCH_BU(ctx, bytes, (double)mm * k, sig_table_kernel<LR>, tg, kSigtThreads, smem, s, list, mm,
                                      d.delta, n, lab, pc, nbits, w.heads.get() + q0, w.tmin.get(), w.tcnt.get(),
                                      inc, keys16 ? keys16 + q0 : nullptr);
                     }
@@ -3217,13 +3229,13 @@ void shard_table_signature(Ctx* ctx, const DevDfa& d, const void* keylab, const 
     const bool local = nbits <= kSmemTableBits;
     const size_t smem = local ? (size_t)(2u << nbits) * 4 : 0;
     const int smem_table = (int)(2u << kSmemTableBits) * 4;
-    const unsigned tg = (unsigned)std::min<uint64_t>((m + 511) / 512, (uint64_t)ctx->num_sms * 3);
+    const unsigned tg = (unsigned)std::min<uint64_t>((m + kSigtThreads - 1) / kSigtThreads, (uint64_t)ctx->num_sms * kSigtCtas);
     SigParams p = sig_params(plan, d.k, 0);
     p.q0 = list_base;
     with_lab_type(KeyLab{keylab, plan.keylab_bytes ? (int)plan.keylab_bytes : 4}, [&](auto lab) {
         using LR = decltype(lab);
         DK_CUDA(cudaFuncSetAttribute(sig_table_kernel<LR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_table));
-        DK_LAUNCH_BU(ctx, (double)m * (8.0 + 4.0 * d.k), (double)m * d.k, sig_table_kernel<LR>, tg, 512, smem, s, list, m, d.delta,
+        DK_LAUNCH_BU(ctx, (double)m * (8.0 + 4.0 * d.k), (double)m * d.k, sig_table_kernel<LR>, tg, kSigtThreads, smem, s, list, m, d.delta,
                     d.n, lab, p, nbits, keys32, tmin, tcnt, 1 /* local lists are compacted in state order */);
     });
 }
