@@ -239,6 +239,13 @@ struct SigParams {
     uint32_t q0;          // list == nullptr: the active states are q0, q0 + 1, ...
 };
 
+#ifndef DFAKIT_SIGB_THREADS
+#define DFAKIT_SIGB_THREADS 256
+#endif
+#ifndef DFAKIT_SIGB_GRID
+#define DFAKIT_SIGB_GRID 8
+#endif
+constexpr int kSigbThreads = DFAKIT_SIGB_THREADS;
 #ifndef DFAKIT_SIGB_MINB
 #define DFAKIT_SIGB_MINB 5
 #endif
@@ -1026,7 +1033,7 @@ __device__ __forceinline__ void append_finish(const PendingAppend& a, uint32_t n
 
 
 template <typename LR, int MODE>
-__global__ void __launch_bounds__(kThreads, DFAKIT_SIGB_MINB) sig_bucket_kernel(const uint32_t* __restrict__ list, uint64_t m,
+__global__ void __launch_bounds__(kSigbThreads, DFAKIT_SIGB_MINB) sig_bucket_kernel(const uint32_t* __restrict__ list, uint64_t m,
                                                               const uint32_t* __restrict__ delta, uint32_t n,
                                                               LR lab, SigParams p,
                                                               uint32_t nb, uint32_t* __restrict__ bcnt,
@@ -2336,15 +2343,15 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
             // (a sliced pass: the partial keys in, hkey out)
             const double bytes = part ? (double)mm * 24.0
                                       : (double)mm * (4.0 * k + 16.0 + lb) + keylab_bytes_per_state(klx) * n;
-            const unsigned grid = grid_for(mm, kThreads, (unsigned)ctx->num_sms * 8u);
+            const unsigned grid = grid_for(mm, kSigbThreads, (unsigned)ctx->num_sms * DFAKIT_SIGB_GRID);
             if (part)
-                DK_LAUNCH_BU(ctx, bytes, 0.0, (sig_bucket_kernel<LR, 2>), grid, kThreads, 0, s, lst, mm, d.delta, n, lab, px,
+                DK_LAUNCH_BU(ctx, bytes, 0.0, (sig_bucket_kernel<LR, 2>), grid, kSigbThreads, 0, s, lst, mm, d.delta, n, lab, px,
                              L.nb, w.bcnt.get(), w.bent.get(), ctrx, part);
             else if (fingerprint)
-                DK_LAUNCH_BU(ctx, bytes, (double)mm * k, (sig_bucket_kernel<LR, 1>), grid, kThreads, 0, s, lst, mm, d.delta, n,
+                DK_LAUNCH_BU(ctx, bytes, (double)mm * k, (sig_bucket_kernel<LR, 1>), grid, kSigbThreads, 0, s, lst, mm, d.delta, n,
                              lab, px, L.nb, w.bcnt.get(), w.bent.get(), ctrx, part);
             else
-                DK_LAUNCH_BU(ctx, bytes, (double)mm * k, (sig_bucket_kernel<LR, 0>), grid, kThreads, 0, s, lst, mm, d.delta, n,
+                DK_LAUNCH_BU(ctx, bytes, (double)mm * k, (sig_bucket_kernel<LR, 0>), grid, kSigbThreads, 0, s, lst, mm, d.delta, n,
                              lab, px, L.nb, w.bcnt.get(), w.bent.get(), ctrx, part);
         });
         GroupOut go{L.direct ? 1 : 0, L.state_order ? 1 : 0, out_lab, w.act.get(),
