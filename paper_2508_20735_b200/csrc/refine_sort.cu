@@ -573,8 +573,18 @@ __global__ void __launch_bounds__(kThreads, DFAKIT_SIGB_MINB) sig_part_kernel(co
 // Plain signature kernel (radix-sort grouping and the exact chunked path):
 // one thread per active state, (key, state) written in list order.
 // FP: fingerprint keys known at compile time (1) or the kind read from p (0)
+// 512-thread CTAs, three per SM (the radix-sort grouping's signature passes
+// 0.41 -> 0.39 ms at 10M; 1024 x 2 spills, no minimum let ptxas take ~90
+// registers and ran at 0.48 -- 0.72 ms)
+#ifndef DFAKIT_SIG_THREADS
+#define DFAKIT_SIG_THREADS 512
+#endif
+#ifndef DFAKIT_SIG_MINB
+#define DFAKIT_SIG_MINB 3
+#endif
+constexpr int kSigThreads = DFAKIT_SIG_THREADS, kSigCtas = DFAKIT_SIG_MINB;
 template <typename LR, int FP = 0>
-__global__ void __launch_bounds__(kThreads) signature_kernel(const uint32_t* __restrict__ list, uint64_t m,
+__global__ void __launch_bounds__(kSigThreads, kSigCtas) signature_kernel(const uint32_t* __restrict__ list, uint64_t m,
                                                              const uint32_t* __restrict__ delta, uint32_t n,
                                                              LR lab,
                                                              const uint32_t* __restrict__ head, SigParams p,
@@ -2761,14 +2771,15 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
                 if (sort_bits < 64) p.fp_mask = fp_mask & ((1ull << sort_bits) - 1ull);
             }
             if (!chunked) {
+                const unsigned gs = grid_for(m, kSigThreads);
                 with_lab_type(kl, [&](auto lab) {
                     using LR = decltype(lab);
                     const double bytes = (double)m * (12.0 + 4.0 * k + list_b) + keylab_bytes_per_state(kl) * n;
                     if (fingerprint)
-                        DK_LAUNCH_BU(ctx, bytes, (double)m * k, (signature_kernel<LR, 1>), g, kThreads, 0, s, list, m,
+                        DK_LAUNCH_BU(ctx, bytes, (double)m * k, (signature_kernel<LR, 1>), gs, kSigThreads, 0, s, list, m,
                                      d.delta, n, lab, nullptr, p, w.keys0.get(), w.vals0.get());
                     else
-                        DK_LAUNCH_BU(ctx, bytes, (double)m * k, signature_kernel, g, kThreads, 0, s, list, m, d.delta,
+                        DK_LAUNCH_BU(ctx, bytes, (double)m * k, signature_kernel, gs, kSigThreads, 0, s, list, m, d.delta,
                                      n, lab, nullptr, p, w.keys0.get(), w.vals0.get());
                 });
                 if (radix_sort_pairs(ctx, rb, m, sort_bits, s)) {
