@@ -112,6 +112,7 @@ struct OwnerSources {
 struct OwnerDst {
     uint4* entries[8];
     uint32_t* counts[8];
+    int peer;  // some destinations are other GPUs' memory: system-scope fence before the kernel ends
 };
 // Owners' label writes into the senders' label / survivor-flag arrays (peer mode)
 struct PeerLabels {

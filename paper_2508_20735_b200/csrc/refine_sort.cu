@@ -3084,6 +3084,7 @@ __global__ void __launch_bounds__(kThreads, DFAKIT_SIGB_MINB) sig_owner_kernel(
             have = true;
         }
         if (have) finish();
+        if (dst.peer) __threadfence_system();  // the stores into other GPUs are complete before the barrier
         return;
     }
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
@@ -3108,6 +3109,7 @@ __global__ void __launch_bounds__(kThreads, DFAKIT_SIGB_MINB) sig_owner_kernel(
             atomicAdd(&ovf_cnt[o], 1u);
         }
     }
+    if (dst.peer) __threadfence_system();  // the stores into other GPUs are complete before the barrier
 }
 
 // per owner o: the nb sub-bucket counts then its overflow count (nb + 1 words)
@@ -3118,6 +3120,7 @@ __global__ void owner_counts_kernel(const uint32_t* __restrict__ scur, const uin
         const uint32_t o = (uint32_t)(i / (nb + 1)), b = (uint32_t)(i % (nb + 1));
         dst.counts[o][b] = b < nb ? scur[((uint64_t)o * nb + b) * kCntStride] : ovf_cnt[o];
     }
+    if (dst.peer) __threadfence_system();
 }
 
 // peer mode, owner side: region entry e of sender s = e / region gets its
@@ -3133,6 +3136,7 @@ __global__ void owner_scatter_kernel(const uint4* __restrict__ recv, const uint3
         out.lab[s][q] = v & 0x7fffffffu;
         if (v >> 31) out.act[s][q] = 1;  // zeroed by the sender before the pass's counter exchange
     }
+    __threadfence_system();  // the label stores into other GPUs are complete before the barrier
 }
 
 // received overflow counts of every sender (for the host readback)

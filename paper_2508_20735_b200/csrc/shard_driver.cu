@@ -643,6 +643,7 @@ RefineResult sort_pr_sharded_device(Ctx* ctx, NcclComm* cm, const DevDfa& d, uin
             if (peer_mode) {
                 // this rank's region of every owner's receive buffer
                 OwnerDst dst{};
+                dst.peer = world > 1;
                 for (int o = 0; o < world; ++o) {
                     dst.entries[o] = static_cast<uint4*>(cm->peer.peer[o][0]) + (uint64_t)rank * region;
                     dst.counts[o] = static_cast<uint32_t*>(cm->peer.peer[o][1]) + (uint64_t)rank * msgw;
