@@ -126,7 +126,7 @@ void shard_sig_owner(Ctx* ctx, const DevDfa& d, const void* keylab, const PassPl
 // its sender's label (and survivor flag) -- the results' trip back and the
 // sender's apply in one kernel
 void shard_owner_scatter(Ctx* ctx, const OwnerPlan& op, const uint4* recv, const uint32_t* recv_cnt,
-                         const uint32_t* results, const PeerLabels& out, cudaStream_t s);
+                         const uint32_t* results, const uint8_t* bsingle, const PeerLabels& out, cudaStream_t s);
 // sender: the results of its overflow entries (peer mode: the region entries
 // were applied by their owners)
 void shard_apply_overflow(Ctx* ctx, const OwnerSend& ws, const uint32_t* back_ovf, uint32_t ovf_total, uint32_t* lab,
@@ -135,7 +135,7 @@ void shard_sort_overflow(Ctx* ctx, const OwnerPlan& op, OwnerSend& ws, uint32_t 
 void shard_owner_ovf_counts(Ctx* ctx, const OwnerPlan& op, const uint32_t* recv_msg, uint32_t* out, cudaStream_t s);
 void shard_group_owner(Ctx* ctx, const DevDfa& d, const void* verify_lab, uint32_t verify_bytes, const PassPlan& plan,
                        const OwnerPlan& op, const OwnerSources& in, const uint4* ovf_in, uint32_t ovf_total,
-                       uint32_t* results, uint32_t* counters, cudaStream_t s);
+                       uint32_t* results, uint32_t* counters, cudaStream_t s, uint8_t* bsingle = nullptr);
 void shard_apply_owner(Ctx* ctx, const OwnerPlan& op, const OwnerSend& ws, uint32_t rank, const uint32_t* own_res,
                        const uint32_t* back, const uint32_t* back_ovf, uint32_t ovf_total, uint32_t* lab,
                        uint8_t* act, cudaStream_t s);

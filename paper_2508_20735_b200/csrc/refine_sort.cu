@@ -1281,7 +1281,7 @@ __global__ void __launch_bounds__(kGrpThreads, DFAKIT_GRP_MINB) bucket_group_ker
             src.prefetch(bn, len_next, tid, kGrpThreads);
         }
         if (len == 0 || len > kGrpCap) {  // uniform across the CTA
-            if (EM == 1 && tid == 0) o.bsingle[b] = 0;
+            if ((EM == 1 || EM == 2) && o.bsingle && tid == 0) o.bsingle[b] = 0;
             continue;
         }
         const uint32_t T = max(64u, pow2_at_least(2 * len));
@@ -1337,11 +1337,12 @@ __global__ void __launch_bounds__(kGrpThreads, DFAKIT_GRP_MINB) bucket_group_ker
             }
         }
         const bool any_dup = __syncthreads_or(dup != 0);
-        if (EM == 1) {
+        if (EM == 1 || (EM == 2 && o.bsingle)) {
             if (tid == 0) o.bsingle[b] = any_dup ? 0 : 1;
             if (!any_dup) {
                 // every key distinct: all singletons, nothing to verify and no
-                // records (rec_apply_kernel reads the states from the entries)
+                // records / results (rec_apply_kernel, owner_scatter_kernel
+                // read the states from the entries)
 #pragma unroll
                 for (int j = 0; j < kGrpItems; ++j) heads += j * kGrpThreads + tid < len;
                 __syncthreads();
@@ -3127,12 +3128,13 @@ __global__ void owner_counts_kernel(const uint32_t* __restrict__ scur, const uin
 // result written straight into s's label / survivor-flag arrays
 __global__ void owner_scatter_kernel(const uint4* __restrict__ recv, const uint32_t* __restrict__ recv_cnt,
                                      uint32_t world, uint32_t nb, uint32_t cs, const uint32_t* __restrict__ results,
-                                     const __grid_constant__ PeerLabels out) {
+                                     const uint8_t* __restrict__ bsingle, const __grid_constant__ PeerLabels out) {
     const uint64_t region = (uint64_t)nb * cs, total = region * world;
     for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total; e += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t s = (uint32_t)(e / region), r = (uint32_t)(e % region);
         if (r % cs >= min(recv_cnt[(uint64_t)s * (nb + 1) + r / cs], cs)) continue;
-        const uint32_t q = __ldcs(recv + e).z, v = results[e];
+        const uint32_t q = __ldcs(recv + e).z;
+        const uint32_t v = bsingle && bsingle[r / cs] ? q : results[e];  // (a bucket of distinct keys: singletons)
         out.lab[s][q] = v & 0x7fffffffu;
         if (v >> 31) out.act[s][q] = 1;  // zeroed by the sender before the pass's counter exchange
     }
@@ -3490,7 +3492,7 @@ void shard_owner_ovf_counts(Ctx* ctx, const OwnerPlan& op, const uint32_t* recv_
 
 void shard_group_owner(Ctx* ctx, const DevDfa& d, const void* verify_lab, uint32_t verify_bytes, const PassPlan& plan,
                        const OwnerPlan& op, const OwnerSources& in, const uint4* ovf_in, uint32_t ovf_total,
-                       uint32_t* results, uint32_t* counters, cudaStream_t s) {
+                       uint32_t* results, uint32_t* counters, cudaStream_t s, uint8_t* bsingle) {
     if (op.world > (uint32_t)kMaxSrc) throw Error(DFAKIT_E_INVALID, "owner buckets: at most 8 ranks");
     IterCounters* dctr = reinterpret_cast<IterCounters*>(ctx->dmailbox) + 4;
     DK_CUDA(cudaMemsetAsync(dctr, 0, sizeof(IterCounters), s));
@@ -3503,7 +3505,7 @@ void shard_group_owner(Ctx* ctx, const DevDfa& d, const void* verify_lab, uint32
     src.nb = op.nb;
     src.cs = op.cs;
     const int fp = plan.strategy == kPlanFingerprint ? 1 : 0;
-    GroupOut go{0, 0, nullptr, nullptr, nullptr, nullptr, results, nullptr, 0};
+    GroupOut go{0, 0, nullptr, nullptr, nullptr, nullptr, results, nullptr, 0, bsingle};
     const unsigned gg = (unsigned)std::min<uint64_t>(op.nb, (uint64_t)ctx->num_sms * kGrpCtasPerSm);
     const KeyLab vl{verify_lab, (int)verify_bytes};
     with_lab_type(vl, [&](auto lab) {
@@ -3546,10 +3548,10 @@ void shard_group_owner(Ctx* ctx, const DevDfa& d, const void* verify_lab, uint32
 }
 
 void shard_owner_scatter(Ctx* ctx, const OwnerPlan& op, const uint4* recv, const uint32_t* recv_cnt,
-                         const uint32_t* results, const PeerLabels& out, cudaStream_t s) {
+                         const uint32_t* results, const uint8_t* bsingle, const PeerLabels& out, cudaStream_t s) {
     const uint64_t total = (uint64_t)op.world * op.nb * op.cs;
     DK_LAUNCH_B(ctx, 25.0 * total * 3 / 4, owner_scatter_kernel, grid_for(total), kThreads, 0, s, recv, recv_cnt,
-                op.world, op.nb, op.cs, results, out);
+                op.world, op.nb, op.cs, results, bsingle, out);
 }
 
 void shard_apply_overflow(Ctx* ctx, const OwnerSend& ws, const uint32_t* back_ovf, uint32_t ovf_total, uint32_t* lab,

@@ -539,6 +539,7 @@ RefineResult sort_pr_sharded_device(Ctx* ctx, NcclComm* cm, const DevDfa& d, uin
     DBuf<uint32_t> rmsg, small(2 * (uint64_t)world + 2, s);
     DBuf<uint4> rreg, rovf_buf;
     DBuf<uint32_t> back_ovf;
+    DBuf<uint8_t> bsingle;  // peer mode: per owner bucket, 1 = every key distinct (no results written)
     auto read_u32 = [&](const uint32_t* p, size_t count, uint32_t* out) {
         for (size_t i = 0; i < count; i += 112)  // read_words moves at most 112 words
             read_words(ctx, p + i, std::min<size_t>(112, count - i) * sizeof(uint32_t), out + i, s);
@@ -692,12 +693,16 @@ RefineResult sort_pr_sharded_device(Ctx* ctx, NcclComm* cm, const DevDfa& d, uin
             }
             const uint64_t rslots = (uint64_t)world * region + rovf_total;
             if (results.n < rslots) results.alloc(rslots, s);
+            // peer mode: buckets of distinct keys write no results (the owner's
+            // scatter takes their states from the entries)
+            if (peer_mode && bsingle.n < op.nb) bsingle.alloc(op.nb, s);
+            uint8_t* const bs = peer_mode ? bsingle.get() : nullptr;
             if (lab_stale)
                 shard_group_owner(ctx, d, keylab, plan.keylab_bytes ? plan.keylab_bytes : 4, plan, op, in,
-                                  rovf_buf.get(), (uint32_t)rovf_total, results.get(), dctr.get(), s);
+                                  rovf_buf.get(), (uint32_t)rovf_total, results.get(), dctr.get(), s, bs);
             else
                 shard_group_owner(ctx, d, LAB, 4, plan, op, in, rovf_buf.get(), (uint32_t)rovf_total,
-                                  results.get(), dctr.get(), s);
+                                  results.get(), dctr.get(), s, bs);
             // peer mode: the owners will write this rank's flags; zeroed before
             // the counter exchange, which every owner passes before writing
             if (peer_mode && hi > lo) DK_CUDA(cudaMemsetAsync(ACT + lo, 0, hi - lo, s));
@@ -724,7 +729,7 @@ RefineResult sort_pr_sharded_device(Ctx* ctx, NcclComm* cm, const DevDfa& d, uin
                     pl.lab[r] = static_cast<uint32_t*>(cm->peer.peer[r][2]);
                     pl.act[r] = static_cast<uint8_t*>(cm->peer.peer[r][3]);
                 }
-                shard_owner_scatter(ctx, op, precv, pcnt, results.get(), pl, s);
+                shard_owner_scatter(ctx, op, precv, pcnt, results.get(), bs, pl, s);
                 if (back_ovf.n < std::max<uint32_t>(1, own_ovf)) back_ovf.alloc(std::max<uint32_t>(1, own_ovf), s);
                 cm->all_to_all_v(results.get() + (uint64_t)world * region, rovf, back_ovf.get(), sovf,
                                  sizeof(uint32_t), s);
