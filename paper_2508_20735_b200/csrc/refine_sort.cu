@@ -3042,6 +3042,11 @@ __global__ void __launch_bounds__(kThreads, DFAKIT_SIGB_MINB) sig_owner_kernel(
     uint4* __restrict__ ovf, uint32_t* __restrict__ ovf_cnt, const uint64_t* __restrict__ part) {
     const unsigned lane = threadIdx.x & 31u, lt = (1u << lane) - 1u;
     if (MODE == 1) p.kind = kKeyFingerprint;
+    // the owners' region pointers in shared memory (a runtime-indexed kernel
+    // parameter is a local-memory copy per thread)
+    __shared__ uint4* s_dst[8];
+    if (threadIdx.x < 8) s_dst[threadIdx.x] = threadIdx.x < world ? dst.entries[threadIdx.x] : nullptr;
+    __syncthreads();
     if constexpr (MODE == 2) {
         // partial keys of a sliced pass (no gathers): the cursor atomic of one
         // state in flight while the next state's key is read (as sig_bucket)
@@ -3055,7 +3060,7 @@ __global__ void __launch_bounds__(kThreads, DFAKIT_SIGB_MINB) sig_owner_kernel(
             if (!pvalid) return;
             const uint4 e = make_uint4((uint32_t)phk, (uint32_t)(phk >> 32), pq, po);
             if (pos < cs) {
-                dst.entries[po][(uint64_t)(pg - po * nb) * cs + pos] = e;
+                s_dst[po][(uint64_t)(pg - po * nb) * cs + pos] = e;
             } else {
                 ovf[atomicAdd(&ovf_cnt[world], 1u)] = e;
                 atomicAdd(&ovf_cnt[po], 1u);
@@ -3104,7 +3109,7 @@ __global__ void __launch_bounds__(kThreads, DFAKIT_SIGB_MINB) sig_owner_kernel(
         const uint32_t pos = base + (uint32_t)__popc(peers & lt);
         const uint4 e = make_uint4((uint32_t)hk, (uint32_t)(hk >> 32), q, o);
         if (pos < cs) {
-            dst.entries[o][(uint64_t)(g - o * nb) * cs + pos] = e;  // (peer mode: a store over NVLink)
+            s_dst[o][(uint64_t)(g - o * nb) * cs + pos] = e;  // (peer mode: a store over NVLink)
         } else {
             ovf[atomicAdd(&ovf_cnt[world], 1u)] = e;
             atomicAdd(&ovf_cnt[o], 1u);
