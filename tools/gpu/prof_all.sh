@@ -18,7 +18,7 @@ run chain 'double_kernel|naive_persistent_kernel' 6 0 --workload chain --reps 1
 cp /tmp/prof/chain.ncu-rep gpurun_out/prof_chain.ncu-rep
 run equiv 'bfs_persistent_kernel|uf_persistent_kernel|reinsert_kernel' 8 0 --workload equiv
 run sharded 'sig_owner_kernel|owner_apply_kernel|bucket_group_kernel|owner_counts_kernel' 10 0 --workload sharded --reps 1
-run sliced 'sig_part_vec_kernel|sig_bucket_kernel|bucket_group_kernel|sig_table_kernel' 6 0 --workload synth --states 100000000 --reps 1
+run sliced 'sig_part_all_kernel|sig_part_vec_kernel|sig_bucket_kernel|bucket_group_kernel|sig_table_kernel' 6 0 --workload synth --states 100000000 --reps 1
 run trans 'trans_' 6 0 --workload trans --reps 1
 run fib 'naive_one_kernel|fused_one_kernel|small_persistent_kernel' 3 0 --workload fib
 run calib 'gather_probe_kernel' 2 0 --workload calib
