@@ -277,6 +277,30 @@ struct BitLab {
     const uint32_t* w;
     __device__ __forceinline__ uint32_t operator[](uint32_t i) const { return (__ldg(w + (i >> 5)) >> (i & 31u)) & 1u; }
 };
+// 12-bit labels, five per 64-bit word (1.6 bytes per state, no field spans
+// two words): the raw table keys of a first pass whose second pass is sliced
+// -- 100M states' labels are 160 MB instead of 200, two L2-friendlier slices
+struct Pack12Lab {
+    static constexpr int kBits = 12;
+    const unsigned long long* w;
+    __device__ __forceinline__ uint32_t operator[](uint32_t i) const {
+        const uint32_t word = i / 5u, slot = i - word * 5u;
+        return (uint32_t)(__ldg(w + word) >> (12u * slot)) & 0xFFFu;
+    }
+};
+
+__global__ void pack12_kernel(const uint16_t* __restrict__ keys16, uint32_t n, unsigned long long* __restrict__ out) {
+    const uint32_t words = (n + 4) / 5;
+    for (uint32_t wi = blockIdx.x * blockDim.x + threadIdx.x; wi < words; wi += gridDim.x * blockDim.x) {
+        unsigned long long v = 0;
+#pragma unroll
+        for (int j = 0; j < 5; ++j) {
+            const uint32_t q = wi * 5u + j;
+            if (q < n) v |= (unsigned long long)(__ldcs(keys16 + q) & 0xFFFu) << (12 * j);
+        }
+        out[wi] = v;
+    }
+}
 
 // Key of q's (block, signature) tuple.  CLAMP: successor ids are clamped to
 // n - 1 -- streamed host-buffer calls validate delta while pass 1 already
@@ -1752,6 +1776,7 @@ struct Workspace {
     DBuf<uint32_t> bcnt, rep_slot, gslot, grep, eval;
     DBuf<uint2> rec;
     DBuf<uint8_t> bsingle;
+    DBuf<unsigned long long> pack12;  // packed 12-bit key labels of a sliced speculative pass
     DBuf<uint64_t> part;  // partial keys of a sliced pass
     DBuf<uint4> bent;
     DBuf<unsigned long long> gkey;
@@ -1776,7 +1801,18 @@ void with_lab_type(const KeyLab& kl, F&& f) {
     else f(ArrLab<uint32_t>{static_cast<const uint32_t*>(kl.p)});
 }
 
-double keylab_bytes_per_state(const KeyLab& kl) { return kl.bytes == kBitLabels ? 0.125 : (double)kl.bytes; }
+constexpr int kPack12Labels = 254;  // KeyLab::bytes tag: Pack12Lab (sliced signature passes only)
+
+double keylab_bytes_per_state(const KeyLab& kl) {
+    return kl.bytes == kBitLabels ? 0.125 : kl.bytes == kPack12Labels ? 1.6 : (double)kl.bytes;
+}
+
+// with_lab_type plus the packed 12-bit labels (the paths a sliced pass takes)
+template <typename F>
+void with_lab_type_p12(const KeyLab& kl, F&& f) {
+    if (kl.bytes == kPack12Labels) f(Pack12Lab{static_cast<const unsigned long long*>(kl.p)});
+    else with_lab_type(kl, f);
+}
 
 // Label arrays past the L2 (100M states' 16-bit key labels are 200 MB against
 // 126 MB of L2) make every gather of a signature pass a DRAM sector read.
@@ -1807,7 +1843,8 @@ const uint64_t* sliced_parts(Ctx* ctx, const KeyLab& kl, const uint32_t* list, u
     // L2 (access-policy window, persisting) while delta and the partial keys
     // stream past it -- off by default: no gain at 72 MB slices (8.64 vs 8.68
     // ms for 1B transitions), a loss at 100 MB ones (10.6 vs 7.6 ms)
-    bool pin = kl.bytes != kBitLabels && getenv("DFAKIT_L2_PIN") && getenv("DFAKIT_L2_PIN")[0] == '1';
+    bool pin = (kl.bytes == 1 || kl.bytes == 2 || kl.bytes == 4) && getenv("DFAKIT_L2_PIN") &&
+               getenv("DFAKIT_L2_PIN")[0] == '1';
     size_t pin_max = 0;
     if (pin) {
         int v = 0;
@@ -1834,7 +1871,9 @@ const uint64_t* sliced_parts(Ctx* ctx, const KeyLab& kl, const uint32_t* list, u
         // selects the chunked four-state kernel
         static const int part_kernel = getenv("DFAKIT_PART_KERNEL") ? atoi(getenv("DFAKIT_PART_KERNEL")) : 1;
         const bool all_letters = part_kernel > 0 && !list && d.k <= 16;
-        with_lab_type(kl, [&](auto lab) {
+        if (kl.bytes == kPack12Labels && !all_letters)
+            throw Error(DFAKIT_E_INVALID, "packed 12-bit labels need the all-letters sweep kernel");
+        with_lab_type_p12(kl, [&](auto lab) {
             using LR = decltype(lab);
             // algorithmic HBM bytes: delta rows, the slice's labels, the partial keys
             const double bytes = (double)m * (4.0 * d.k + (j ? 16.0 : 8.0)) + keylab_bytes_per_state(kl) * (hi - lo);
@@ -2348,7 +2387,8 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
         fl.flush(ctx, s);
         const double lb = lst ? 4.0 : 0.0;
         const uint64_t* part = sliced_parts(ctx, klx, lst, mm, d, px, w.part, s);
-        with_lab_type(klx, [&](auto lab) {
+        if (klx.bytes == kPack12Labels && !part) throw Error(DFAKIT_E_INVALID, "packed 12-bit labels outside a sliced pass");
+        with_lab_type_p12(klx, [&](auto lab) {
             using LR = decltype(lab);
             // algorithmic HBM bytes: delta rows (+ list), (hkey, state) out, the key-label array once
             // (a sliced pass: the partial keys in, hkey out)
@@ -2612,6 +2652,14 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
                 spec_plan.key_bits = 64;
                 spec_plan.keylab_bytes = 2;
                 spec_kl = KeyLab{w.next16.get(), 2};  // the ranks, or the raw keys when the apply is skipped
+                // raw keys of at most 12 bits for a sliced second pass: packed
+                // five per 64-bit word (fewer label bytes per slice in the L2)
+                if (lazy && nbits <= 12 && k <= 16 && label_slices(spec_kl, n) > 1 && !getenv("DFAKIT_NO_PACK12")) {
+                    if (w.pack12.n < ((uint64_t)n + 4) / 5) w.pack12.alloc(((uint64_t)n + 4) / 5, s);
+                    DK_LAUNCH_B(ctx, (double)n * 2.0 + (double)n * 1.6, pack12_kernel,
+                                grid_for(((uint64_t)n + 4) / 5), kThreads, 0, s, w.next16.get(), n, w.pack12.get());
+                    spec_kl = KeyLab{w.pack12.get(), kPack12Labels};
+                }
                 SigParams sp{};
                 sp.kind = kKeyFingerprint;
                 sp.a0 = 0;

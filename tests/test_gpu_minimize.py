@@ -416,3 +416,27 @@ def test_deferred_pass_mixed_buckets(dk, oracle, monkeypatch, spec):
         want = oracle.minimize("moore", t[0], t[1])
         assert want.num_blocks < n0 + d
         assert same(dk.sort_pr(mkdfa(dk, t)), want), (n0, d, k)
+
+
+def test_speculative_sliced_packed_labels(dk, oracle, monkeypatch):
+    """The speculative second pass sliced (tiny slice size) on the first
+    pass's raw table keys packed 12 bits apiece, five per 64-bit word:
+    random automata, duplicates, forced collisions -- partitions and pass
+    counts stay the oracle's (and the packing can be switched off)."""
+    monkeypatch.setenv("DFAKIT_TEST_SPEC_MIN", "1000")
+    monkeypatch.setenv("DFAKIT_TEST_SLICE_BYTES", "4096")
+    g = random.Random(123)
+    for i in range(10):
+        n, k, s = g.randint(3000, 60000), g.randint(2, 12), g.getrandbits(64)
+        t = oracle.gen_random(n, k, [0.5, 0.9, 0.3][i % 3], s)
+        if i % 4 == 3:
+            t = with_duplicates(t, 300, s)
+        want = oracle.minimize("moore", t[0], t[1])
+        dfa = mkdfa(dk, t)
+        for kw in ({}, {"fingerprint_bits": 6}):
+            assert same(dk.sort_pr(dfa, **kw), want), (i, n, k, kw)
+    t = oracle.gen_synth(200_001, 10, 9)
+    want = oracle.minimize("moore", t[0], t[1])
+    assert same(dk.sort_pr(mkdfa(dk, t)), want)
+    monkeypatch.setenv("DFAKIT_NO_PACK12", "1")
+    assert same(dk.sort_pr(mkdfa(dk, t)), want)
