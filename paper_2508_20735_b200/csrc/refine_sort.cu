@@ -2387,7 +2387,6 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
         fl.flush(ctx, s);
         const double lb = lst ? 4.0 : 0.0;
         const uint64_t* part = sliced_parts(ctx, klx, lst, mm, d, px, w.part, s);
-        if (klx.bytes == kPack12Labels && !part) throw Error(DFAKIT_E_INVALID, "packed 12-bit labels outside a sliced pass");
         with_lab_type_p12(klx, [&](auto lab) {
             using LR = decltype(lab);
             // algorithmic HBM bytes: delta rows (+ list), (hkey, state) out, the key-label array once
@@ -2654,7 +2653,11 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
                 spec_kl = KeyLab{w.next16.get(), 2};  // the ranks, or the raw keys when the apply is skipped
                 // raw keys of at most 12 bits for a sliced second pass: packed
                 // five per 64-bit word (fewer label bytes per slice in the L2)
-                if (lazy && nbits <= 12 && k <= 16 && label_slices(spec_kl, n) > 1 && !getenv("DFAKIT_NO_PACK12")) {
+                // (measured, 16-bit labels vs packed: 60 MB 3.21 vs 3.50 ms,
+                // 80 MB 4.51 vs 4.60, 100 MB 6.63 vs 6.17 unsliced, 200 MB
+                // sliced 7.91 vs 7.48 ms of sweeps: packing pays past ~90 MiB)
+                static const double pack_min = getenv("DFAKIT_PACK12_MIN_MB") ? atof(getenv("DFAKIT_PACK12_MIN_MB")) : 90.0;
+                if (lazy && nbits <= 12 && k <= 16 && 2.0 * n > pack_min * 1048576.0 && !getenv("DFAKIT_NO_PACK12")) {
                     if (w.pack12.n < ((uint64_t)n + 4) / 5) w.pack12.alloc(((uint64_t)n + 4) / 5, s);
                     DK_LAUNCH_B(ctx, (double)n * 2.0 + (double)n * 1.6, pack12_kernel,
                                 grid_for(((uint64_t)n + 4) / 5), kThreads, 0, s, w.next16.get(), n, w.pack12.get());

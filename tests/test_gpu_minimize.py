@@ -425,6 +425,7 @@ def test_speculative_sliced_packed_labels(dk, oracle, monkeypatch):
     counts stay the oracle's (and the packing can be switched off)."""
     monkeypatch.setenv("DFAKIT_TEST_SPEC_MIN", "1000")
     monkeypatch.setenv("DFAKIT_TEST_SLICE_BYTES", "4096")
+    monkeypatch.setenv("DFAKIT_PACK12_MIN_MB", "0")
     g = random.Random(123)
     for i in range(10):
         n, k, s = g.randint(3000, 60000), g.randint(2, 12), g.getrandbits(64)
@@ -437,6 +438,8 @@ def test_speculative_sliced_packed_labels(dk, oracle, monkeypatch):
             assert same(dk.sort_pr(dfa, **kw), want), (i, n, k, kw)
     t = oracle.gen_synth(200_001, 10, 9)
     want = oracle.minimize("moore", t[0], t[1])
+    assert same(dk.sort_pr(mkdfa(dk, t)), want)
+    monkeypatch.delenv("DFAKIT_TEST_SLICE_BYTES")  # packed labels in an unsliced pass
     assert same(dk.sort_pr(mkdfa(dk, t)), want)
     monkeypatch.setenv("DFAKIT_NO_PACK12", "1")
     assert same(dk.sort_pr(mkdfa(dk, t)), want)
