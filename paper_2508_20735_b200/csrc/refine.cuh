@@ -119,6 +119,9 @@ struct PeerLabels {
     uint32_t* lab[8];
     uint8_t* act[8];
 };
+// 16-bit labels below 4096 packed 12 bits apiece, five per 64-bit word;
+// returns the KeyLab::bytes tag of the packed array (signature passes only)
+uint32_t pack12_labels(Ctx* ctx, const uint16_t* keys16, uint32_t n, unsigned long long* out, cudaStream_t s);
 void shard_sig_owner(Ctx* ctx, const DevDfa& d, const void* keylab, const PassPlan& plan, uint64_t salt,
                      const uint32_t* list, uint32_t list_base, uint64_t m, const OwnerPlan& op, OwnerSend& ws,
                      cudaStream_t s, const OwnerDst* dst = nullptr);

@@ -3483,6 +3483,11 @@ OwnerPlan owner_plan(uint64_t m_total, uint32_t world) {
     return op;
 }
 
+uint32_t pack12_labels(Ctx* ctx, const uint16_t* keys16, uint32_t n, unsigned long long* out, cudaStream_t s) {
+    DK_LAUNCH_B(ctx, (double)n * 3.6, pack12_kernel, grid_for(((uint64_t)n + 4) / 5), kThreads, 0, s, keys16, n, out);
+    return (uint32_t)kPack12Labels;
+}
+
 void shard_sig_owner(Ctx* ctx, const DevDfa& d, const void* keylab, const PassPlan& plan, uint64_t salt,
                      const uint32_t* list, uint32_t list_base, uint64_t m, const OwnerPlan& op, OwnerSend& ws,
                      cudaStream_t s, const OwnerDst* dst_in) {
@@ -3517,7 +3522,7 @@ void shard_sig_owner(Ctx* ctx, const DevDfa& d, const void* keylab, const PassPl
         p.q0 = list_base;
         const KeyLab kl{keylab, plan.keylab_bytes ? (int)plan.keylab_bytes : 4};
         const uint64_t* part = sliced_parts(ctx, kl, list, m, d, p, ws.part, s);
-        with_lab_type(kl, [&](auto lab) {
+        with_lab_type_p12(kl, [&](auto lab) {
             using LR = decltype(lab);
             const double bytes = part ? (double)m * 24.0 : (double)m * (4.0 * d.k + 16.0);
             const unsigned grid = grid_for(m, kThreads, (unsigned)ctx->num_sms * 8u);

@@ -540,6 +540,7 @@ RefineResult sort_pr_sharded_device(Ctx* ctx, NcclComm* cm, const DevDfa& d, uin
     DBuf<uint4> rreg, rovf_buf;
     DBuf<uint32_t> back_ovf;
     DBuf<uint8_t> bsingle;  // peer mode: per owner bucket, 1 = every key distinct (no results written)
+    DBuf<unsigned long long> pack12;  // packed 12-bit copy of the carried key labels
     auto read_u32 = [&](const uint32_t* p, size_t count, uint32_t* out) {
         for (size_t i = 0; i < count; i += 112)  // read_words moves at most 112 words
             read_words(ctx, p + i, std::min<size_t>(112, count - i) * sizeof(uint32_t), out + i, s);
@@ -639,6 +640,18 @@ RefineResult sort_pr_sharded_device(Ctx* ctx, NcclComm* cm, const DevDfa& d, uin
             // (owner, bucket) sub-buckets that travel as they are
             const OwnerPlan op = owner_plan(m_total, (uint32_t)world);
             const uint64_t msgw = op.nb + 1, region = (uint64_t)op.nb * op.cs;
+            // carried 16-bit ranks below 4096 over a large automaton: the
+            // signature gathers them packed 12 bits apiece (fewer label bytes
+            // in the L2; the verification keeps the 16-bit array)
+            const void* sig_keylab = keylab;
+            PassPlan sig_plan = plan;
+            static const double pack_min = getenv("DFAKIT_PACK12_MIN_MB") ? atof(getenv("DFAKIT_PACK12_MIN_MB")) : 90.0;
+            if (plan.keylab_bytes == 2 && keylab != LAB && B <= 4096 && k <= 16 &&
+                2.0 * n > pack_min * 1048576.0 && !getenv("DFAKIT_NO_PACK12")) {
+                if (pack12.n < ((uint64_t)n + 4) / 5) pack12.alloc(((uint64_t)n + 4) / 5, s);
+                sig_plan.keylab_bytes = pack12_labels(ctx, static_cast<const uint16_t*>(keylab), n, pack12.get(), s);
+                sig_keylab = pack12.get();
+            }
             uint4* const precv = peer_mode ? static_cast<uint4*>(cm->peer.local[0]) : nullptr;
             uint32_t* const pcnt = peer_mode ? static_cast<uint32_t*>(cm->peer.local[1]) : nullptr;
             if (peer_mode) {
@@ -649,10 +662,10 @@ RefineResult sort_pr_sharded_device(Ctx* ctx, NcclComm* cm, const DevDfa& d, uin
                     dst.entries[o] = static_cast<uint4*>(cm->peer.peer[o][0]) + (uint64_t)rank * region;
                     dst.counts[o] = static_cast<uint32_t*>(cm->peer.peer[o][1]) + (uint64_t)rank * msgw;
                 }
-                shard_sig_owner(ctx, d, keylab, plan, salt, lst, lo, m, op, ows, s, &dst);
+                shard_sig_owner(ctx, d, sig_keylab, sig_plan, salt, lst, lo, m, op, ows, s, &dst);
                 cm->barrier(s);  // every sender's entries and counts have landed
             } else {
-                shard_sig_owner(ctx, d, keylab, plan, salt, lst, lo, m, op, ows, s);
+                shard_sig_owner(ctx, d, sig_keylab, sig_plan, salt, lst, lo, m, op, ows, s);
                 if (rmsg.n < world * msgw) rmsg.alloc(world * msgw, s);
                 const std::vector<uint64_t> mcount(world, msgw);
                 cm->all_to_all_v(ows.msg.get(), mcount, rmsg.get(), mcount, sizeof(uint32_t), s);

@@ -270,3 +270,20 @@ def test_native_driver_tiny_automata_odd_worlds(dk, monkeypatch):
         for case in cases:
             d, a, want = make_case(case)
             check_hub(run_hub(dk, world, d, a), want, (world, case))
+
+
+def test_native_driver_packed_labels(dk, monkeypatch):
+    """Wide passes gathering the carried 16-bit ranks packed 12 bits apiece
+    (forced on small automata; sliced too): peer mode at worlds 1, 2 and 3."""
+    monkeypatch.setenv("DFAKIT_SHARD_PEER", "2")
+    monkeypatch.setenv("DFAKIT_PACK12_MIN_MB", "0")
+    cases = [("random", 5000, 3, 0.5, 12), ("random", 20000, 10, 0.5, 14), ("copies", 400, 8, 0.5, 15),
+             ("synth", 300_000, 10, 0.0, 5)]
+    for world in (1, 2, 3):
+        for case in cases:
+            d, a, want = make_case(case)
+            check_hub(run_hub(dk, world, d, a), want, (world, case))
+    monkeypatch.setenv("DFAKIT_TEST_SLICE_BYTES", "4096")
+    for case in cases[1:]:
+        d, a, want = make_case(case)
+        check_hub(run_hub(dk, 2, d, a), want, ("sliced", case))
