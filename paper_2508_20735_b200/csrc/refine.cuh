@@ -121,7 +121,12 @@ struct PeerLabels {
 };
 // 16-bit labels below 4096 packed 12 bits apiece, five per 64-bit word;
 // returns the KeyLab::bytes tag of the packed array (signature passes only)
-uint32_t pack12_labels(Ctx* ctx, const uint16_t* keys16, uint32_t n, unsigned long long* out, cudaStream_t s);
+// (eleven: 11-bit labels packed back to back instead; values below 2048)
+uint32_t pack12_labels(Ctx* ctx, const uint16_t* keys16, uint32_t n, unsigned long long* out, cudaStream_t s,
+                       bool eleven = false);
+uint64_t pack_words(uint32_t n);  // words of the packed array (either layout)
+bool pack11_unsliced(uint32_t n);  // 11-bit packed labels of n states need no slicing
+int pack_choice(uint32_t n, uint32_t bits);  // 0 (16-bit labels), 11 or 12 (packed) for a big pass
 void shard_sig_owner(Ctx* ctx, const DevDfa& d, const void* keylab, const PassPlan& plan, uint64_t salt,
                      const uint32_t* list, uint32_t list_base, uint64_t m, const OwnerPlan& op, OwnerSend& ws,
                      cudaStream_t s, const OwnerDst* dst = nullptr);

@@ -289,6 +289,38 @@ struct Pack12Lab {
     }
 };
 
+// 11-bit labels packed back to back (1.375 bytes per state; a field that
+// crosses a 64-bit word boundary -- 10 of every 64 -- takes a second load)
+struct Pack11Lab {
+    static constexpr int kBits = 11;
+    const unsigned long long* w;
+    __device__ __forceinline__ uint32_t operator[](uint32_t i) const {
+        const uint64_t bit = (uint64_t)i * 11u;
+        const uint64_t word = bit >> 6;
+        const uint32_t sh = (uint32_t)(bit & 63u);
+        unsigned long long v = __ldg(w + word) >> sh;
+        if (sh > 53) v |= __ldg(w + word + 1) << (64u - sh);
+        return (uint32_t)v & 0x7FFu;
+    }
+};
+
+// word wi of the 11-bit packing: the fields overlapping bits [64 wi, 64 wi + 64)
+__global__ void pack11_kernel(const uint16_t* __restrict__ keys16, uint32_t n, unsigned long long* __restrict__ out,
+                              uint64_t words) {
+    for (uint64_t wi = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; wi < words;
+         wi += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t b0 = wi * 64u;
+        uint64_t i = b0 / 11u;
+        unsigned long long v = 0;
+        for (; i * 11u < b0 + 64u && i < n; ++i) {
+            const unsigned long long f = (unsigned long long)(__ldg(keys16 + i) & 0x7FFu);
+            const int64_t off = (int64_t)(i * 11u) - (int64_t)b0;  // field start relative to the word
+            v |= off >= 0 ? f << off : f >> (-off);
+        }
+        out[wi] = v;
+    }
+}
+
 __global__ void pack12_kernel(const uint16_t* __restrict__ keys16, uint32_t n, unsigned long long* __restrict__ out) {
     const uint32_t words = (n + 4) / 5;
     for (uint32_t wi = blockIdx.x * blockDim.x + threadIdx.x; wi < words; wi += gridDim.x * blockDim.x) {
@@ -1801,16 +1833,21 @@ void with_lab_type(const KeyLab& kl, F&& f) {
     else f(ArrLab<uint32_t>{static_cast<const uint32_t*>(kl.p)});
 }
 
-constexpr int kPack12Labels = 254;  // KeyLab::bytes tag: Pack12Lab (sliced signature passes only)
+constexpr int kPack12Labels = 254;  // KeyLab::bytes tags: Pack12Lab / Pack11Lab (signature passes only)
+constexpr int kPack11Labels = 253;
 
 double keylab_bytes_per_state(const KeyLab& kl) {
-    return kl.bytes == kBitLabels ? 0.125 : kl.bytes == kPack12Labels ? 1.6 : (double)kl.bytes;
+    return kl.bytes == kBitLabels      ? 0.125
+           : kl.bytes == kPack12Labels ? 1.6
+           : kl.bytes == kPack11Labels ? 1.375
+                                       : (double)kl.bytes;
 }
 
-// with_lab_type plus the packed 12-bit labels (the paths a sliced pass takes)
+// with_lab_type plus the packed labels (the signature paths of big passes)
 template <typename F>
 void with_lab_type_p12(const KeyLab& kl, F&& f) {
     if (kl.bytes == kPack12Labels) f(Pack12Lab{static_cast<const unsigned long long*>(kl.p)});
+    else if (kl.bytes == kPack11Labels) f(Pack11Lab{static_cast<const unsigned long long*>(kl.p)});
     else with_lab_type(kl, f);
 }
 
@@ -2651,17 +2688,13 @@ RefineResult sort_pr_device(Ctx* ctx, const DevDfa& d, const SortOptions& o, uin
                 spec_plan.key_bits = 64;
                 spec_plan.keylab_bytes = 2;
                 spec_kl = KeyLab{w.next16.get(), 2};  // the ranks, or the raw keys when the apply is skipped
-                // raw keys of at most 12 bits for a sliced second pass: packed
-                // five per 64-bit word (fewer label bytes per slice in the L2)
-                // (measured, 16-bit labels vs packed: 60 MB 3.21 vs 3.50 ms,
-                // 80 MB 4.51 vs 4.60, 100 MB 6.63 vs 6.17 unsliced, 200 MB
-                // sliced 7.91 vs 7.48 ms of sweeps: packing pays past ~90 MiB)
-                static const double pack_min = getenv("DFAKIT_PACK12_MIN_MB") ? atof(getenv("DFAKIT_PACK12_MIN_MB")) : 90.0;
-                if (lazy && nbits <= 12 && k <= 16 && 2.0 * n > pack_min * 1048576.0 && !getenv("DFAKIT_NO_PACK12")) {
-                    if (w.pack12.n < ((uint64_t)n + 4) / 5) w.pack12.alloc(((uint64_t)n + 4) / 5, s);
-                    DK_LAUNCH_B(ctx, (double)n * 2.0 + (double)n * 1.6, pack12_kernel,
-                                grid_for(((uint64_t)n + 4) / 5), kThreads, 0, s, w.next16.get(), n, w.pack12.get());
-                    spec_kl = KeyLab{w.pack12.get(), kPack12Labels};
+                // raw keys of at most 12 bits for a big second pass: packed
+                // when that keeps its labels L2-friendlier (see pack_choice)
+                const int pack = lazy && k <= 16 ? pack_choice(n, nbits) : 0;
+                if (pack) {
+                    if (w.pack12.n < pack_words(n)) w.pack12.alloc(pack_words(n), s);
+                    const uint32_t tag = pack12_labels(ctx, w.next16.get(), n, w.pack12.get(), s, pack == 11);
+                    spec_kl = KeyLab{w.pack12.get(), (int)tag};
                 }
                 SigParams sp{};
                 sp.kind = kKeyFingerprint;
@@ -3483,10 +3516,40 @@ OwnerPlan owner_plan(uint64_t m_total, uint32_t world) {
     return op;
 }
 
-uint32_t pack12_labels(Ctx* ctx, const uint16_t* keys16, uint32_t n, unsigned long long* out, cudaStream_t s) {
+uint32_t pack12_labels(Ctx* ctx, const uint16_t* keys16, uint32_t n, unsigned long long* out, cudaStream_t s,
+                       bool eleven) {
+    if (eleven) {
+        const uint64_t words = ((uint64_t)n * 11u + 63u) / 64u + 1;  // + 1: the reader's straddle load stays inside
+        DK_LAUNCH_B(ctx, (double)n * 3.4, pack11_kernel, grid_for(words), kThreads, 0, s, keys16, n, out, words);
+        return (uint32_t)kPack11Labels;
+    }
     DK_LAUNCH_B(ctx, (double)n * 3.6, pack12_kernel, grid_for(((uint64_t)n + 4) / 5), kThreads, 0, s, keys16, n, out);
     return (uint32_t)kPack12Labels;
 }
+
+bool pack11_unsliced(uint32_t n) { return label_slices(KeyLab{nullptr, kPack11Labels}, n) == 1; }
+
+// Label layout of a big signature pass over 16-bit labels below 2^bits (0:
+// keep 16 bits, 11 / 12: packed).  Measured on random n x 10 automata (wall
+// ms, 16-bit / 12-bit / 11-bit): 50M 6.63 / 6.17 / 5.88 (11-bit unsliced
+// best), 60M 8.22 / 8.65 / 8.12, 70M 9.37 / 10.01 / 10.07, 80M 10.78 /
+// 11.60 / --, 100M 15.45 / 15.00 / 17.3: 16-bit labels win while their
+// slices stay under ~90 MiB; packing pays for an unsliced pass just past the
+// unsliced limit and for slices the 16-bit layout would make too big.
+int pack_choice(uint32_t n, uint32_t bits) {
+    const double pack_min = getenv("DFAKIT_PACK12_MIN_MB") ? atof(getenv("DFAKIT_PACK12_MIN_MB")) : 90.0;
+    if (getenv("DFAKIT_NO_PACK12") || bits > 12) return 0;
+    const double mib = 1048576.0, u16 = 2.0 * n;
+    if (u16 <= pack_min * mib) return 0;
+    const bool forced = pack_min < 90.0;  // (tests: pack whatever the size)
+    if (bits <= 11 && !getenv("DFAKIT_NO_PACK11") && (1.375 * n <= 80.0 * mib || forced) && pack11_unsliced(n))
+        return 11;
+    const uint32_t slices = label_slices(KeyLab{nullptr, 2}, n);
+    if (!forced && u16 / slices <= 90.0 * mib) return 0;
+    return 12;
+}
+
+uint64_t pack_words(uint32_t n) { return std::max<uint64_t>(((uint64_t)n + 4) / 5, ((uint64_t)n * 11u + 63u) / 64u + 1); }
 
 void shard_sig_owner(Ctx* ctx, const DevDfa& d, const void* keylab, const PassPlan& plan, uint64_t salt,
                      const uint32_t* list, uint32_t list_base, uint64_t m, const OwnerPlan& op, OwnerSend& ws,

@@ -645,11 +645,14 @@ RefineResult sort_pr_sharded_device(Ctx* ctx, NcclComm* cm, const DevDfa& d, uin
             // in the L2; the verification keeps the 16-bit array)
             const void* sig_keylab = keylab;
             PassPlan sig_plan = plan;
-            static const double pack_min = getenv("DFAKIT_PACK12_MIN_MB") ? atof(getenv("DFAKIT_PACK12_MIN_MB")) : 90.0;
-            if (plan.keylab_bytes == 2 && keylab != LAB && B <= 4096 && k <= 16 &&
-                2.0 * n > pack_min * 1048576.0 && !getenv("DFAKIT_NO_PACK12")) {
-                if (pack12.n < ((uint64_t)n + 4) / 5) pack12.alloc(((uint64_t)n + 4) / 5, s);
-                sig_plan.keylab_bytes = pack12_labels(ctx, static_cast<const uint16_t*>(keylab), n, pack12.get(), s);
+            // (identity ranges only: the packed layouts' sliced sweeps take no state list)
+            const int pack = plan.keylab_bytes == 2 && keylab != LAB && k <= 16 && lst == nullptr
+                                 ? pack_choice(n, B <= 2048 ? 11u : B <= 4096 ? 12u : 16u)
+                                 : 0;
+            if (pack) {
+                if (pack12.n < pack_words(n)) pack12.alloc(pack_words(n), s);
+                sig_plan.keylab_bytes =
+                    pack12_labels(ctx, static_cast<const uint16_t*>(keylab), n, pack12.get(), s, pack == 11);
                 sig_keylab = pack12.get();
             }
             uint4* const precv = peer_mode ? static_cast<uint4*>(cm->peer.local[0]) : nullptr;

@@ -419,10 +419,11 @@ def test_deferred_pass_mixed_buckets(dk, oracle, monkeypatch, spec):
 
 
 def test_speculative_sliced_packed_labels(dk, oracle, monkeypatch):
-    """The speculative second pass sliced (tiny slice size) on the first
-    pass's raw table keys packed 12 bits apiece, five per 64-bit word:
-    random automata, duplicates, forced collisions -- partitions and pass
-    counts stay the oracle's (and the packing can be switched off)."""
+    """The speculative second pass on the first pass's raw table keys packed
+    12 bits apiece five per 64-bit word (sliced -- tiny slice size) or 11
+    bits back to back (unsliced): random automata, duplicates, forced
+    collisions -- partitions and pass counts stay the oracle's, the packing
+    kernels demonstrably ran, and the packing can be switched off."""
     monkeypatch.setenv("DFAKIT_TEST_SPEC_MIN", "1000")
     monkeypatch.setenv("DFAKIT_TEST_SLICE_BYTES", "4096")
     monkeypatch.setenv("DFAKIT_PACK12_MIN_MB", "0")
@@ -438,8 +439,24 @@ def test_speculative_sliced_packed_labels(dk, oracle, monkeypatch):
             assert same(dk.sort_pr(dfa, **kw), want), (i, n, k, kw)
     t = oracle.gen_synth(200_001, 10, 9)
     want = oracle.minimize("moore", t[0], t[1])
-    assert same(dk.sort_pr(mkdfa(dk, t)), want)
-    monkeypatch.delenv("DFAKIT_TEST_SLICE_BYTES")  # packed labels in an unsliced pass
-    assert same(dk.sort_pr(mkdfa(dk, t)), want)
+    dfa = mkdfa(dk, t)
+
+    def kernels_of_run():
+        import ctypes as C
+        import json
+        from paper_2508_20735_b200 import _native as nat
+        ctx = dk.Context(0)
+        nat.check(nat.lib.dfakit_profile_begin(ctx.handle))
+        rep = dk.sort_pr(dfa, ctx=ctx)
+        buf = C.create_string_buffer(1 << 16)
+        nat.check(nat.lib.dfakit_profile_end(ctx.handle, buf, len(buf)))
+        return rep, {x["name"] for x in json.loads(buf.value.decode())}
+
+    rep, names = kernels_of_run()  # sliced: 12-bit fields
+    assert same(rep, want) and "pack12_kernel" in names, names
+    monkeypatch.delenv("DFAKIT_TEST_SLICE_BYTES")  # unsliced: 11-bit fields
+    rep, names = kernels_of_run()
+    assert same(rep, want) and "pack11_kernel" in names, names
     monkeypatch.setenv("DFAKIT_NO_PACK12", "1")
-    assert same(dk.sort_pr(mkdfa(dk, t)), want)
+    rep, names = kernels_of_run()
+    assert same(rep, want) and not any(x.startswith("pack1") for x in names), names
