@@ -426,7 +426,10 @@ constexpr unsigned long long kFlagAgg = 1ull, kFlagPre = 2ull;
 // look-back window (predecessors per round trip): 1 / 4 / 8 measured
 // 138 / 135 / 139 us per digit pass on 10M keys -- the ranking, not the
 // look-back, bounds the pass once counts are published before it
-constexpr int kLookWin = 4;
+#ifndef DFAKIT_SORT_LOOKWIN
+#define DFAKIT_SORT_LOOKWIN 4
+#endif
+constexpr int kLookWin = DFAKIT_SORT_LOOKWIN;
 
 __device__ __forceinline__ uint32_t digit_of(uint64_t key, uint32_t shift) {
     return (uint32_t)(key >> shift) & (kRadix - 1);
