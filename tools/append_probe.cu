@@ -25,7 +25,10 @@
         }                                                                                  \
     } while (0)
 
-constexpr uint32_t kCap = 2048, kStride = 8, kShift = 20;
+__constant__ uint32_t kCapDev;
+static uint32_t kCapHost = 2048;
+#define kCap (kCapDev)
+constexpr uint32_t kStride = 8, kShift = 20;
 
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
     z += 0x9e3779b97f4a7c15ull;
@@ -170,7 +173,7 @@ float run(const uint32_t* delta, const uint16_t* lab, uint32_t n, uint32_t k, ui
 }
 
 int main(int argc, char** argv) {
-    // append_probe [states] [buckets]: the bench's pass-2 shape by default
+    // append_probe [states] [buckets] [capacity]: the bench's pass-2 shape by default
     const uint32_t n = argc > 1 ? (uint32_t)atoll(argv[1]) : 10000000u, k = 10,
                    nb = argc > 2 ? (uint32_t)atoll(argv[2]) : 8192u;
     int sms;
@@ -182,7 +185,9 @@ int main(int argc, char** argv) {
     CK(cudaMalloc(&delta, (size_t)n * k * 4));
     CK(cudaMalloc(&lab, (size_t)n * 2));
     CK(cudaMalloc(&bcnt, (size_t)nb * kStride * 4));
-    CK(cudaMalloc(&bent, (size_t)nb * kCap * 32));
+    kCapHost = argc > 3 ? (uint32_t)atoll(argv[3]) : 2048u;  // bucket capacity (slots)
+    CK(cudaMemcpyToSymbol(kCapDev, &kCapHost, sizeof(kCapHost)));
+    CK(cudaMalloc(&bent, (size_t)nb * kCapHost * 32));
     CK(cudaMalloc(&gtab, (size_t)8 << 25));
     CK(cudaMalloc(&sink, 4));
     init_kernel<<<sms * 8, 256>>>(delta, lab, n, k);
