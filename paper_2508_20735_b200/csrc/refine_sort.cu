@@ -45,6 +45,7 @@
 #include <algorithm>
 
 #include <functional>
+#include <type_traits>
 
 #include "prims.cuh"
 #include "refine.cuh"
@@ -248,6 +249,9 @@ struct SigParams {
 constexpr int kSigbThreads = DFAKIT_SIGB_THREADS;
 #ifndef DFAKIT_SIGB_MINB
 #define DFAKIT_SIGB_MINB 5
+#endif
+#ifndef DFAKIT_SIGT_CH
+#define DFAKIT_SIGT_CH 8
 #endif
 #ifndef DFAKIT_SIGB_CH
 #define DFAKIT_SIGB_CH 16
@@ -522,11 +526,15 @@ __global__ void __launch_bounds__(kThreads, DFAKIT_SIGB_MINB) sig_part_vec_kerne
 #ifndef DFAKIT_PART_MINB
 #define DFAKIT_PART_MINB 4
 #endif
-template <typename LR, bool FP, int S>
+
+// C: letters per load chunk, the smallest of 8 / 10 / 12 / 16 covering the
+// alphabet (predicated-off letters still cost registers and issue slots:
+// 1B transitions, k = 10: C = 16 7.56 ms of sweeps, C = 10 6.07, C = 8 --
+// two chunks -- 8.93)
+template <typename LR, bool FP, int S, int C = 16>
 __global__ void __launch_bounds__(kThreads, DFAKIT_PART_MINB) sig_part_all_kernel(
     uint64_t m, const uint32_t* __restrict__ delta, uint32_t n, LR lab, SigParams p, uint32_t lo, uint32_t hi,
     int first, uint64_t* __restrict__ part) {
-    constexpr int C = 16;
     const uint32_t nl = p.a1 - p.a0;
     for (uint64_t iS = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; iS * S < m;
          iS += (uint64_t)gridDim.x * blockDim.x) {
@@ -690,7 +698,7 @@ __global__ void __launch_bounds__(kSigtThreads, kSigtCtas) sig_table_kernel(cons
     }
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t q = list ? list[i] : p.q0 + (uint32_t)i;
-        const uint32_t key = (uint32_t)tuple_key<LR, 8, CLAMP>(q, lab[q], delta, n, lab, p);
+        const uint32_t key = (uint32_t)tuple_key<LR, DFAKIT_SIGT_CH, CLAMP>(q, lab[q], delta, n, lab, p);
         keys32[i] = key;
         if (keys16) keys16[i] = (uint16_t)key;  // the raw keys as the next pass's labels (lazy apply)
         const unsigned peers = __match_any_sync(__activemask(), key);
@@ -1917,12 +1925,20 @@ const uint64_t* sliced_parts(Ctx* ctx, const KeyLab& kl, const uint32_t* list, u
             const bool fp = p.kind != kKeyPacked;
             if (all_letters) {
                 const unsigned grid = grid_for(m, kThreads, (unsigned)ctx->num_sms * 8u);
-                if (fp)
-                    DK_LAUNCH_BU(ctx, bytes, (double)m * d.k / slices, (sig_part_all_kernel<LR, true, 1>), grid,
+                auto sweep = [&](auto fpc, auto cc) {
+                    constexpr bool FPV = decltype(fpc)::value;
+                    constexpr int CV = decltype(cc)::value;
+                    DK_LAUNCH_BU(ctx, bytes, (double)m * d.k / slices, (sig_part_all_kernel<LR, FPV, 1, CV>), grid,
                                  kThreads, 0, s, m, d.delta, d.n, lab, p, lo, hi, j == 0 ? 1 : 0, part.get());
-                else
-                    DK_LAUNCH_BU(ctx, bytes, (double)m * d.k / slices, (sig_part_all_kernel<LR, false, 1>), grid,
-                                 kThreads, 0, s, m, d.delta, d.n, lab, p, lo, hi, j == 0 ? 1 : 0, part.get());
+                };
+                auto by_c = [&](auto fpc) {
+                    if (d.k <= 8) sweep(fpc, std::integral_constant<int, 8>{});
+                    else if (d.k <= 10) sweep(fpc, std::integral_constant<int, 10>{});
+                    else if (d.k <= 12) sweep(fpc, std::integral_constant<int, 12>{});
+                    else sweep(fpc, std::integral_constant<int, 16>{});
+                };
+                if (fp) by_c(std::true_type{});
+                else by_c(std::false_type{});
             } else if (vec)
                 DK_LAUNCH_BU(ctx, bytes, (double)m * d.k / slices, sig_part_vec_kernel,
                              grid_for((m + 3) / 4, kThreads, (unsigned)ctx->num_sms * 5u), kThreads, 0, s, m, d.delta,
