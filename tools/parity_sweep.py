@@ -23,18 +23,24 @@ def main():
     p.add_argument("--cases", type=int, default=300)
     p.add_argument("--seed", type=int, default=1)
     a = p.parse_args()
+    bad = sweep(a.cases, a.seed)
+    sys.exit(1 if bad else 0)
+
+
+def sweep(cases, seed, log=print):
+    """Returns the number of mismatches (each also logged)."""
     import numpy as np
     import paper_2508_20735_b200 as dk
     import pyoracle
     from conftest import mkdfa
     o = pyoracle.COracle()
-    g = random.Random(a.seed)
+    g = random.Random(seed)
     envs = [{}, {"DFAKIT_TEST_SPEC_MIN": "500"},
             {"DFAKIT_TEST_SPEC_MIN": "500", "DFAKIT_PACK12_MIN_MB": "0"},
             {"DFAKIT_TEST_SPEC_MIN": "500", "DFAKIT_PACK12_MIN_MB": "0", "DFAKIT_TEST_SLICE_BYTES": "2048"},
             {"DFAKIT_TEST_SLICE_BYTES": "2048"}]
     bad = 0
-    for i in range(a.cases):
+    for i in range(cases):
         n, k = g.randint(2, 40000), g.randint(1, 14)
         frac = g.choice([0.0, 0.1, 0.5, 0.9, 1.0])
         t = o.gen_random(n, k, frac, g.getrandbits(64))
@@ -44,16 +50,18 @@ def main():
             t = (np.concatenate([d, d[:, src]], axis=1), np.concatenate([acc, acc[src]]), 0)
         want = o.minimize("moore", t[0], t[1])
         env = envs[i % len(envs)]
-        for key, val in env.items():
-            os.environ[key] = val
         fp = {"fingerprint_bits": 6} if g.random() < 0.2 else {}
-        r = dk.sort_pr(mkdfa(dk, t), **fp)
-        for key in env:
-            del os.environ[key]
+        try:
+            for key, val in env.items():
+                os.environ[key] = val
+            r = dk.sort_pr(mkdfa(dk, t), **fp)
+        finally:
+            for key in env:
+                os.environ.pop(key, None)
         ok = (np.array_equal(r.partition.block_of, want.blocks) and r.refining_iterations == want.refine_iters)
         if not ok:
             bad += 1
-            print("MISMATCH sort_pr", i, n, k, frac, env, fp, flush=True)
+            log(f"MISMATCH sort_pr {i} {n} {k} {frac} {env} {fp}")
         if i % 3 == 0:  # product exploration against the oracle
             A = t
             if g.random() < 0.5:  # a different pair: small, so the product stays within the pair budget
@@ -61,18 +69,21 @@ def main():
                 B = o.gen_random(g.randint(2, 3000), k, frac, g.getrandbits(64))
             else:
                 B = t
-            if g.random() < 0.3:
-                os.environ["DFAKIT_TEST_TABLE_LOG2"] = "6"
+            tiny = g.random() < 0.3
             mode = g.choice(["equivalence", "inclusion", "full"])
-            rr = dk.explore_product(mkdfa(dk, A), mkdfa(dk, B), dk.ExploreMode[mode])
-            os.environ.pop("DFAKIT_TEST_TABLE_LOG2", None)
+            try:
+                if tiny:
+                    os.environ["DFAKIT_TEST_TABLE_LOG2"] = "6"
+                rr = dk.explore_product(mkdfa(dk, A), mkdfa(dk, B), dk.ExploreMode[mode])
+            finally:
+                os.environ.pop("DFAKIT_TEST_TABLE_LOG2", None)
             oo = o.explore(mode, A, B)
             if (rr.verdict.name, rr.explored_states, rr.levels, rr.counterexample) != \
                     (oo.verdict, oo.explored, oo.levels, oo.counterexample):
                 bad += 1
-                print("MISMATCH explore", i, mode, flush=True)
-    print(f"parity sweep: {a.cases} cases, {bad} mismatches", flush=True)
-    sys.exit(1 if bad else 0)
+                log(f"MISMATCH explore {i} {mode}")
+    log(f"parity sweep: {cases} cases, {bad} mismatches")
+    return bad
 
 
 if __name__ == "__main__":
