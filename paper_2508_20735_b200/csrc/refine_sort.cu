@@ -1249,7 +1249,10 @@ struct MultiSrc {
         __device__ __forceinline__ uint32_t source(uint32_t idx) const {
             uint32_t s = 0;
 #pragma unroll
-            for (int t = 1; t < kMaxSrc; ++t) s += (uint32_t)t < nsrc && idx >= pre[t];
+            for (int t = 1; t < kMaxSrc; ++t) {
+                if ((uint32_t)t >= nsrc) break;  // (one sender: no prefix to read)
+                s += idx >= pre[t];
+            }
             return s;
         }
         __device__ __forceinline__ uint4 load(uint32_t idx) const {
