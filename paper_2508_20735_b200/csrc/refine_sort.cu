@@ -1246,13 +1246,14 @@ struct MultiSrc {
         const uint32_t* pre;       // kMaxSrc + 1 prefix sums
         const uint4* const* ptr;   // kMaxSrc chunk bases
         uint32_t nsrc, b, nb, cs;
+        // the last sender whose prefix is <= idx: a binary search over the 8
+        // prefixes (those of absent senders equal the total, never <= idx)
         __device__ __forceinline__ uint32_t source(uint32_t idx) const {
-            uint32_t s = 0;
-#pragma unroll
-            for (int t = 1; t < kMaxSrc; ++t) {
-                if ((uint32_t)t >= nsrc) break;  // (one sender: no prefix to read)
-                s += idx >= pre[t];
-            }
+            static_assert(kMaxSrc == 8, "three halving steps");
+            if (nsrc == 1) return 0;
+            uint32_t s = idx >= pre[4] ? 4u : 0u;
+            s += idx >= pre[s + 2] ? 2u : 0u;
+            s += idx >= pre[s + 1] ? 1u : 0u;
             return s;
         }
         __device__ __forceinline__ uint4 load(uint32_t idx) const {
